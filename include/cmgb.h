@@ -1,0 +1,226 @@
+/*
+ * cmgb.h — C ABI of the B200-native batched contact-manifold path.
+ *
+ * Drop-in boundary for the reference C++ collision API of arXiv 2602.20304
+ * (/root/reference/proj, namespace cmg). The reference exposes header-only
+ * templates and has no FFI of its own; every entry point below names the
+ * reference interface it replaces (file:line, relative to
+ * /root/reference/proj). Plain pointers and sizes only; no C++ or torch types
+ * cross this boundary, and no exception escapes it: every call returns a
+ * cmgb_status and cmgb_last_error() holds the message (thread-local).
+ *
+ * Memory conventions
+ *   - Descriptor inputs (meshes, SDF programs, configs) are HOST memory and are
+ *     copied at create time; handles are immutable afterwards and may be shared
+ *     between host threads (reference: SurfaceModel value semantics,
+ *     include/cmg/surface.hpp:16-33; sdf.cpp:52-67 deep copy).
+ *   - Batch entry points named *_batch take DEVICE pointers and a cudaStream_t
+ *     passed as void*; they are stream-ordered and allocate nothing on the hot
+ *     call. *_batch_host variants take HOST pointers and perform the H2D/D2H
+ *     copies inside the call (the end-to-end path).
+ *   - Scalars follow the reference: poses and witness inputs are FP64 exactly
+ *     as the reference receives them; contact outputs are FP32.
+ */
+#ifndef CMGB_H_
+#define CMGB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMGB_ABI_VERSION 1
+
+typedef enum cmgb_status {
+  CMGB_OK = 0,
+  CMGB_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  CMGB_ERR_PARSE = 2,            /* reference: MeshParseError (mesh.hpp:19-23) */
+  CMGB_ERR_CUDA = 3,             /* launch / runtime failure on the device */
+  CMGB_ERR_NO_DEVICE = 4,        /* no CUDA device: there is no CPU fallback */
+  CMGB_ERR_UNSUPPORTED = 5       /* valid in the reference, not supported here (message says why) */
+} cmgb_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* cmgb_last_error(void);
+int32_t cmgb_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Smoothing configuration — mirrors cmg::SmoothingConfig
+ * (include/cmg/config.hpp:17-46) field for field.
+ * ------------------------------------------------------------------------- */
+typedef enum cmgb_mode {
+  CMGB_MODE_FULL = 0,      /* ContactMode::kFull     (config.hpp:9)  */
+  CMGB_MODE_NO_EE = 1,     /* ContactMode::kNoEe     (config.hpp:10) */
+  CMGB_MODE_ONE_SIDED = 2  /* ContactMode::kOneSided (config.hpp:11) */
+} cmgb_mode;
+
+typedef struct cmgb_config {
+  double lambda, tau_clip, tau_min, tau_comp;          /* witness solver     */
+  double tau_sign, tau_pen, tau_nn, tau_clash, tau_cont; /* contact indicators */
+  double tau_topk_verts, tau_topk_edges, tau_normal, tau_union;
+  int32_t hard_ops;               /* bool */
+  int32_t sphere_trace;           /* bool */
+  int32_t sphere_trace_iters;
+  int32_t containment_safeguard;  /* bool */
+  int32_t mode;                   /* cmgb_mode */
+  int32_t reserved;
+} cmgb_config;
+
+/* SmoothingConfig{} defaults (config.hpp:17-46). */
+void cmgb_config_default(cmgb_config* out);
+/* SmoothingConfig::no_smoothing() (config.hpp:48-53). */
+void cmgb_config_no_smoothing(cmgb_config* out);
+/* SmoothingConfig::validate() (config.hpp:55-73). */
+int cmgb_config_validate(const cmgb_config* cfg);
+/* config_for_variant(): ours | ours_ns | ours_ne | ours_ne_s (src/batch.cpp:131-150). */
+int cmgb_config_for_variant(const char* variant, const cmgb_config* base, cmgb_config* out);
+
+/* ---------------------------------------------------------------------------
+ * SDF program — public, flattened form of the private cmg::SmoothSdf tree
+ * (include/cmg/sdf.hpp:138-202). Nodes are listed in POSTFIX order: a UNION
+ * node with `count` children pops the `count` most recent subtrees (in
+ * order), a SUBTRACTION pops (positive, negative). The last node is the root.
+ * ------------------------------------------------------------------------- */
+typedef enum cmgb_sdf_op {
+  CMGB_SDF_SUPERQUADRIC = 0,        /* SuperquadricParams        sdf.hpp:35-47  */
+  CMGB_SDF_CONVEX_POLYHEDRON = 1,   /* ConvexPolyhedronParams    sdf.hpp:49-62  */
+  CMGB_SDF_ORIENTED_POINTCLOUD = 2, /* OrientedPointcloudParams  sdf.hpp:64-79  */
+  CMGB_SDF_UNION = 3,               /* SdfUnion                  sdf.hpp:143-146 */
+  CMGB_SDF_SUBTRACTION = 4          /* SdfSubtraction            sdf.hpp:148-152 */
+} cmgb_sdf_op;
+
+typedef struct cmgb_sdf_node {
+  int32_t op;                 /* cmgb_sdf_op */
+  int32_t count;              /* CP planes | OPC points | UNION children | SUB: 2 */
+  double tau;                 /* CP logsumexp tau (default 1e-3) | UNION/SUB tau */
+  double eps1, eps2;          /* SQ boxiness, (0, 2] */
+  double axes[3];             /* SQ axis lengths > 0 */
+  double pose[6];             /* SQ primitive pose in the body frame [t; axis-angle] */
+  const double* normals;      /* CP / OPC: count x 3, unit */
+  const double* points;       /* CP / OPC: count x 3 */
+  const double* lengthscales; /* OPC: count, > 0 */
+} cmgb_sdf_node;
+
+/* ---------------------------------------------------------------------------
+ * Collision mesh — cmg::CollisionMesh (include/cmg/mesh.hpp:25-34).
+ * Vertex order and (lexicographic, lo<hi) edge order are preserved exactly:
+ * they define the candidate indices src_a / src_b of every contact.
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_mesh_s* cmgb_mesh;
+
+/* make_box_mesh(half, subdivisions, quad_edges) (src/mesh.cpp:123-173). */
+int cmgb_mesh_box(const double half_extents[3], int32_t subdivisions, int32_t quad_edges,
+                  cmgb_mesh* out);
+/* parse_obj(istream) on an in-memory OBJ text (src/mesh.cpp:60-115). On
+ * CMGB_ERR_PARSE, *error_line receives the OBJ line number (MeshParseError). */
+int cmgb_mesh_parse_obj(const char* text, size_t length, cmgb_mesh* out, int32_t* error_line);
+/* Raw arrays (faces/edges as given; edges must be unique lo<hi pairs). */
+int cmgb_mesh_from_arrays(const double* vertices, int32_t n_vertices, const int32_t* faces,
+                          int32_t n_faces, const int32_t* edges, int32_t n_edges, cmgb_mesh* out);
+int cmgb_mesh_sizes(cmgb_mesh mesh, int32_t* n_vertices, int32_t* n_faces, int32_t* n_edges,
+                    int32_t* n_warnings);
+int cmgb_mesh_read(cmgb_mesh mesh, double* vertices, int32_t* faces, int32_t* edges);
+const char* cmgb_mesh_warning(cmgb_mesh mesh, int32_t index);
+void cmgb_mesh_destroy(cmgb_mesh mesh);
+
+/* ---------------------------------------------------------------------------
+ * Surface — cmg::SurfaceModel + build_surface (include/cmg/surface.hpp:16-40,
+ * src/surface.cpp:9-44): mesh + SDF program + top-K budgets, validated at
+ * create time with the reference's messages; the mesh/SDF discrepancy check is
+ * a warning. Device copies are made lazily, once per device.
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_surface_s* cmgb_surface;
+
+int cmgb_surface_create(cmgb_mesh mesh, const cmgb_sdf_node* sdf_postfix, int32_t n_nodes,
+                        int32_t vertex_topk, int32_t edge_topk, double tolerance_fraction,
+                        cmgb_surface* out);
+void cmgb_surface_destroy(cmgb_surface surface);
+
+typedef struct cmgb_surface_info {
+  int32_t n_vertices, n_edges, n_faces, leaf_count;
+  int32_t vertex_topk, edge_topk;                     /* as given (0 = default) */
+  int32_t effective_vertex_topk, effective_edge_topk; /* surface.hpp:24-32 */
+  int32_t n_warnings;
+  int32_t n_nodes;
+} cmgb_surface_info;
+int cmgb_surface_get_info(cmgb_surface surface, cmgb_surface_info* out);
+const char* cmgb_surface_warning(cmgb_surface surface, int32_t index);
+
+/* ---------------------------------------------------------------------------
+ * Manifold layout — ContactManifold::expected_size and the fixed ordering
+ * (include/cmg/manifold.hpp:14-17, 62-72): [V-S side 1: n1][V-S side 2: n2]
+ * [E-E (k,l) row-major; side 1 then side 2].
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_layout {
+  int32_t n1, n2, m1, m2;
+  int32_t mode;
+  int32_t n_contacts;     /* expected_size() */
+  int32_t dynamic_src;    /* 1 if top-K selection is active on any side (src is data-dependent) */
+  int32_t reserved;
+} cmgb_layout;
+
+int cmgb_layout_query(cmgb_surface s1, cmgb_surface s2, const cmgb_config* cfg, cmgb_layout* out);
+/* Static per-contact metadata, each array n_contacts long (host memory):
+ * kind (0 = VS, 1 = EE), side (1|2), src_a, src_b. For selected (top-K) slots
+ * src_* hold -1 here; the batch call writes the data-dependent provenance. */
+int cmgb_layout_metadata(cmgb_surface s1, cmgb_surface s2, const cmgb_config* cfg,
+                         int32_t* kind, int32_t* side, int32_t* src_a, int32_t* src_b);
+
+/* ---------------------------------------------------------------------------
+ * Batched manifold generation — replaces the per-env loop body of
+ * bench_manifold (src/batch.cpp:207-215): generate_manifold<double>
+ * (include/cmg/manifold.hpp:336-377) + mean_contact_distance (379-384) for
+ * every env, in one launch sequence.
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_manifold_out {
+  float* contacts;   /* required: [n_env][n_contacts][8] = px,py,pz,dist,nx,ny,nz,activity */
+  int32_t* src;      /* optional: [n_env][n_contacts][2] = src_a, src_b (provenance)       */
+  float* ee;         /* optional: [n_env][9][m1*m2] dist,con,pen1,pen2,nn1,nn2,clash,act1,act2
+                        (EeIndicatorMatrices, manifold.hpp:41-52); full mode only          */
+  float* mean_dist;  /* optional: [n_env] mean_contact_distance (manifold.hpp:379-384)      */
+} cmgb_manifold_out;
+
+/* poses*: DEVICE [n][6] FP64 (Pose6d = [t; axis-angle], pose.hpp:16-18).
+ * pose1_stride / pose2_stride: 1 = one pose per env, 0 = the same pose for
+ * every env (bench_manifold keeps body 1 fixed, batch.cpp:196-203). */
+int cmgb_manifold_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1,
+                        int32_t pose1_stride, const double* poses2, int32_t pose2_stride,
+                        int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_out* out,
+                        void* cuda_stream);
+
+/* End-to-end variant: HOST poses in, HOST mean distances (and optionally HOST
+ * contacts) out; copies happen inside the call on the given stream, which is
+ * synchronised before returning. Device scratch is cached per surface pair. */
+int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                             int32_t pose1_stride, const double* poses2_host,
+                             int32_t pose2_stride, int64_t n_env, const cmgb_config* cfg,
+                             float* mean_dist_host, float* contacts_host, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * Witness batches — run_ee_batch / run_vf_batch (src/batch.cpp:53-98) over
+ * ee_witness / vf_witness (include/cmg/witness.hpp:137-158, 163-227).
+ * pairs: DEVICE [n][12] (e1a,e1b,e2a,e2b | v,t0,t1,t2), FP64 if pairs_fp64
+ * else FP32. out: DEVICE FP32 [n][6] (p1,p2) | [n][3] (closest point).
+ * alpha_gamma (optional, E-E): [n][3] = alpha1, alpha2, gamma_con.
+ * labels (optional): active-set label per pair = argmax candidate weight
+ * (0..3 E-E, 0..2 V-F) | (inside-indicator >= 0.5) << 2.
+ * ------------------------------------------------------------------------- */
+int cmgb_ee_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
+                          const cmgb_config* cfg, float* out, float* alpha_gamma,
+                          int32_t* labels, void* cuda_stream);
+int cmgb_vf_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
+                          const cmgb_config* cfg, float* out, int32_t* labels,
+                          void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * Device info (SM count etc. queried, never hard-coded).
+ * ------------------------------------------------------------------------- */
+int cmgb_device_count(int32_t* count);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* CMGB_H_ */

@@ -1,0 +1,180 @@
+"""ctypes mirror of include/cmgb.h and the loader for the native library.
+
+The product path is the in-tree shared library ``libcmgb.so`` (host C++ +
+sm_100a CUDA kernels). There is no CPU fallback: if the library is missing,
+``load()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcmgb.so")
+
+CMGB_OK = 0
+STATUS_NAMES = {
+    0: "CMGB_OK",
+    1: "CMGB_ERR_INVALID_ARGUMENT",
+    2: "CMGB_ERR_PARSE",
+    3: "CMGB_ERR_CUDA",
+    4: "CMGB_ERR_NO_DEVICE",
+    5: "CMGB_ERR_UNSUPPORTED",
+}
+
+MODE_FULL, MODE_NO_EE, MODE_ONE_SIDED = 0, 1, 2
+SDF_SUPERQUADRIC, SDF_CONVEX_POLYHEDRON, SDF_ORIENTED_POINTCLOUD, SDF_UNION, SDF_SUBTRACTION = range(5)
+
+
+class CmgbConfig(C.Structure):
+    """cmgb_config == cmg::SmoothingConfig (config.hpp:17-46)."""
+
+    _fields_ = [
+        ("lambda_", C.c_double),
+        ("tau_clip", C.c_double),
+        ("tau_min", C.c_double),
+        ("tau_comp", C.c_double),
+        ("tau_sign", C.c_double),
+        ("tau_pen", C.c_double),
+        ("tau_nn", C.c_double),
+        ("tau_clash", C.c_double),
+        ("tau_cont", C.c_double),
+        ("tau_topk_verts", C.c_double),
+        ("tau_topk_edges", C.c_double),
+        ("tau_normal", C.c_double),
+        ("tau_union", C.c_double),
+        ("hard_ops", C.c_int32),
+        ("sphere_trace", C.c_int32),
+        ("sphere_trace_iters", C.c_int32),
+        ("containment_safeguard", C.c_int32),
+        ("mode", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class CmgbSdfNode(C.Structure):
+    _fields_ = [
+        ("op", C.c_int32),
+        ("count", C.c_int32),
+        ("tau", C.c_double),
+        ("eps1", C.c_double),
+        ("eps2", C.c_double),
+        ("axes", C.c_double * 3),
+        ("pose", C.c_double * 6),
+        ("normals", C.POINTER(C.c_double)),
+        ("points", C.POINTER(C.c_double)),
+        ("lengthscales", C.POINTER(C.c_double)),
+    ]
+
+
+class CmgbSurfaceInfo(C.Structure):
+    _fields_ = [
+        (n, C.c_int32)
+        for n in (
+            "n_vertices", "n_edges", "n_faces", "leaf_count", "vertex_topk", "edge_topk",
+            "effective_vertex_topk", "effective_edge_topk", "n_warnings", "n_nodes",
+        )
+    ]
+
+
+class CmgbLayout(C.Structure):
+    _fields_ = [
+        (n, C.c_int32)
+        for n in ("n1", "n2", "m1", "m2", "mode", "n_contacts", "dynamic_src", "reserved")
+    ]
+
+
+class CmgbManifoldOut(C.Structure):
+    _fields_ = [
+        ("contacts", C.c_void_p),
+        ("src", C.c_void_p),
+        ("ee", C.c_void_p),
+        ("mean_dist", C.c_void_p),
+    ]
+
+
+# Every exported symbol of include/cmgb.h with its ctypes signature.
+_P = C.c_void_p
+_I = C.c_int
+SIGNATURES = {
+    "cmgb_last_error": (C.c_char_p, []),
+    "cmgb_abi_version": (C.c_int32, []),
+    "cmgb_config_default": (None, [C.POINTER(CmgbConfig)]),
+    "cmgb_config_no_smoothing": (None, [C.POINTER(CmgbConfig)]),
+    "cmgb_config_validate": (_I, [C.POINTER(CmgbConfig)]),
+    "cmgb_config_for_variant": (_I, [C.c_char_p, C.POINTER(CmgbConfig), C.POINTER(CmgbConfig)]),
+    "cmgb_mesh_box": (_I, [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "cmgb_mesh_parse_obj": (_I, [C.c_char_p, C.c_size_t, C.POINTER(_P), C.POINTER(C.c_int32)]),
+    "cmgb_mesh_from_arrays": (
+        _I,
+        [_P, C.c_int32, _P, C.c_int32, _P, C.c_int32, C.POINTER(_P)],
+    ),
+    "cmgb_mesh_sizes": (
+        _I,
+        [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
+    ),
+    "cmgb_mesh_read": (_I, [_P, _P, _P, _P]),
+    "cmgb_mesh_warning": (C.c_char_p, [_P, C.c_int32]),
+    "cmgb_mesh_destroy": (None, [_P]),
+    "cmgb_surface_create": (
+        _I,
+        [_P, C.POINTER(CmgbSdfNode), C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_P)],
+    ),
+    "cmgb_surface_destroy": (None, [_P]),
+    "cmgb_surface_get_info": (_I, [_P, C.POINTER(CmgbSurfaceInfo)]),
+    "cmgb_surface_warning": (C.c_char_p, [_P, C.c_int32]),
+    "cmgb_layout_query": (_I, [_P, _P, C.POINTER(CmgbConfig), C.POINTER(CmgbLayout)]),
+    "cmgb_layout_metadata": (_I, [_P, _P, C.POINTER(CmgbConfig), _P, _P, _P, _P]),
+    "cmgb_manifold_batch": (
+        _I,
+        [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig),
+         C.POINTER(CmgbManifoldOut), _P],
+    ),
+    "cmgb_manifold_batch_host": (
+        _I,
+        [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P],
+    ),
+    "cmgb_ee_witness_batch": (
+        _I,
+        [_P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P, _P],
+    ),
+    "cmgb_vf_witness_batch": (
+        _I,
+        [_P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P],
+    ),
+    "cmgb_device_count": (_I, [C.POINTER(C.c_int32)]),
+}
+
+_lib = None
+
+
+class CmgbError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+def load() -> C.CDLL:
+    """Load libcmgb.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the contact-manifold path)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != CMGB_OK:
+        msg = load().cmgb_last_error()
+        raise CmgbError(status, msg.decode() if msg else "")
