@@ -259,7 +259,7 @@ static sample eval_node(const orc_surface* s, int idx, v3 p, int flavor) {
       break;
     }
     case CMGB_SDF_CONVEX_POLYHEDRON: { /* cp_sdf (sdf.hpp:110-117) */
-      double d[256], w[256];
+      double d[256] = {0}, w[256];
       for (int i = 0; i < nd->count; ++i)
         d[i] = dot(ld3(nd->normals + 3 * i), sub(p, ld3(nd->points + 3 * i)));
       out.v = lse_max_w(d, nd->count, nd->tau, flavor ? w : NULL);
@@ -289,7 +289,7 @@ static sample eval_node(const orc_surface* s, int idx, v3 p, int flavor) {
     }
     case CMGB_SDF_UNION: { /* sdf.hpp:222-227, 260-277 */
       const int n = nd->n_children;
-      double neg[64], w[64];
+      double neg[64] = {0}, w[64];
       sample ch[64];
       for (int i = 0; i < n; ++i) {
         ch[i] = eval_node(s, nd->children[i], p, flavor);

@@ -1,0 +1,280 @@
+"""Python mirror of the reference C++ collision API over the C ABI (libcmgb.so).
+
+Reference interface -> this module:
+  make_box_mesh / parse_obj (src/mesh.cpp)          -> Mesh.box / Mesh.parse_obj
+  build_surface (src/surface.cpp:9-44)               -> Surface(...)
+  generate_manifold<double> (manifold.hpp:336-377)   -> generate_manifold (one env)
+  bench_manifold's per-env loop (batch.cpp:207-215)  -> generate_manifold_batch (device tensors)
+  run_ee_batch / run_vf_batch (batch.cpp:53-98)      -> run_ee_batch / run_vf_batch
+Errors mirror the reference's exceptions: ValueError for std::invalid_argument,
+MeshParseError for cmg::MeshParseError.
+
+Device memory and streams come from PyTorch; every compute call goes through
+the native library (no CPU path exists).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import abi
+from .scene import SdfNode, SdfProgram, SmoothingConfig
+
+
+class MeshParseError(ValueError):
+    def __init__(self, message: str, line: int):
+        super().__init__(message)
+        self.line_number = line
+
+
+def _raise(status: int):
+    lib = abi.load()
+    msg = (lib.cmgb_last_error() or b"").decode()
+    if status == 1:
+        raise ValueError(msg)
+    raise abi.CmgbError(status, msg)
+
+
+def _ok(status: int):
+    if status != abi.CMGB_OK:
+        _raise(status)
+
+
+def _cfg(cfg) -> abi.CmgbConfig:
+    if cfg is None:
+        cfg = SmoothingConfig()
+    return cfg.to_c() if isinstance(cfg, SmoothingConfig) else cfg
+
+
+class Mesh:
+    """cmg::CollisionMesh (include/cmg/mesh.hpp:25-34)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        lib = abi.load()
+        nv, nf, ne, nw = (C.c_int32() for _ in range(4))
+        _ok(lib.cmgb_mesh_sizes(handle, C.byref(nv), C.byref(nf), C.byref(ne), C.byref(nw)))
+        self.vertices = np.zeros((nv.value, 3))
+        self.faces = np.zeros((nf.value, 3), np.int32)
+        self.edges = np.zeros((ne.value, 2), np.int32)
+        _ok(lib.cmgb_mesh_read(handle, self.vertices.ctypes.data, self.faces.ctypes.data,
+                               self.edges.ctypes.data))
+        self.warnings = [lib.cmgb_mesh_warning(handle, i).decode() for i in range(nw.value)]
+
+    @staticmethod
+    def box(half_extents, subdivisions: int = 1, quad_edges: bool = True) -> "Mesh":
+        lib = abi.load()
+        h = (C.c_double * 3)(*[float(x) for x in half_extents])
+        out = C.c_void_p()
+        _ok(lib.cmgb_mesh_box(h, int(subdivisions), int(bool(quad_edges)), C.byref(out)))
+        return Mesh(out)
+
+    @staticmethod
+    def parse_obj(text: str) -> "Mesh":
+        lib = abi.load()
+        b = text.encode()
+        out = C.c_void_p()
+        line = C.c_int32(0)
+        st = lib.cmgb_mesh_parse_obj(b, len(b), C.byref(out), C.byref(line))
+        if st == 2:
+            raise MeshParseError(lib.cmgb_last_error().decode(), line.value)
+        _ok(st)
+        return Mesh(out)
+
+    @staticmethod
+    def from_arrays(vertices, faces, edges) -> "Mesh":
+        lib = abi.load()
+        v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        f = np.ascontiguousarray(faces, dtype=np.int32).reshape(-1, 3)
+        e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+        out = C.c_void_p()
+        _ok(lib.cmgb_mesh_from_arrays(v.ctypes.data, len(v), f.ctypes.data, len(f), e.ctypes.data,
+                                      len(e), C.byref(out)))
+        return Mesh(out)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            abi.load().cmgb_mesh_destroy(self._h)
+            self._h = None
+
+
+class Surface:
+    """cmg::SurfaceModel via build_surface (src/surface.cpp:9-44)."""
+
+    def __init__(self, mesh: Mesh, sdf: SdfNode, vertex_topk: int = 0, edge_topk: int = 0,
+                 tolerance_fraction: float = 1e-2):
+        lib = abi.load()
+        self.mesh = mesh
+        self.sdf = sdf
+        self._prog = SdfProgram(sdf)
+        out = C.c_void_p()
+        _ok(lib.cmgb_surface_create(mesh._h, self._prog.array, self._prog.n, int(vertex_topk),
+                                    int(edge_topk), float(tolerance_fraction), C.byref(out)))
+        self._h = out
+        info = abi.CmgbSurfaceInfo()
+        _ok(lib.cmgb_surface_get_info(out, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in abi.CmgbSurfaceInfo._fields_}
+        self.build_warnings = [lib.cmgb_surface_warning(out, i).decode()
+                               for i in range(info.n_warnings)]
+
+    def effective_vertex_topk(self) -> int:
+        return self.info["effective_vertex_topk"]
+
+    def effective_edge_topk(self) -> int:
+        return self.info["effective_edge_topk"]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            abi.load().cmgb_surface_destroy(self._h)
+            self._h = None
+
+
+def layout(s1: Surface, s2: Surface, cfg=None) -> dict:
+    """ContactManifold sizes (manifold.hpp:62-72)."""
+    L = abi.CmgbLayout()
+    _ok(abi.load().cmgb_layout_query(s1._h, s2._h, C.byref(_cfg(cfg)), C.byref(L)))
+    return {f: getattr(L, f) for f, _ in abi.CmgbLayout._fields_}
+
+
+def layout_metadata(s1: Surface, s2: Surface, cfg=None) -> np.ndarray:
+    """Per-contact (kind, side, src_a, src_b); src = -1 where top-K decides it."""
+    n = layout(s1, s2, cfg)["n_contacts"]
+    meta = np.zeros((4, n), np.int32)
+    _ok(abi.load().cmgb_layout_metadata(s1._h, s2._h, C.byref(_cfg(cfg)), meta[0].ctypes.data,
+                                        meta[1].ctypes.data, meta[2].ctypes.data,
+                                        meta[3].ctypes.data))
+    return meta.T.copy()
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, *,
+                            want_src: bool = False, want_ee: bool = False,
+                            want_mean: bool = True, out: Optional[dict] = None, stream=None) -> dict:
+    """Batched generate_manifold over envs: poses* are CUDA float64 tensors
+    [n, 6] (or [1, 6] / [6] for a pose shared by every env). Returns CUDA
+    tensors: contacts [n, C, 8] (px,py,pz,dist,nx,ny,nz,activity), and
+    optionally src [n, C, 2], ee [n, 9, m1*m2], mean_dist [n]."""
+    import torch
+
+    c = _cfg(cfg)
+    p1 = poses1.reshape(-1, 6)
+    p2 = poses2.reshape(-1, 6)
+    if p1.dtype != torch.float64 or p2.dtype != torch.float64 or not p1.is_cuda or not p2.is_cuda:
+        raise ValueError("poses must be CUDA float64 tensors")
+    p1 = p1.contiguous()
+    p2 = p2.contiguous()
+    n = max(p1.shape[0], p2.shape[0])
+    st1 = 1 if (p1.shape[0] == n and n > 1) else 0
+    st2 = 1 if (p2.shape[0] == n and n > 1) else 0
+    if n == 1:
+        st1 = st2 = 1
+    L = layout(s1, s2, c)
+    Cn = L["n_contacts"]
+    P = L["m1"] * L["m2"]
+    dev = p2.device
+    res = out if out is not None else {}
+    if "contacts" not in res:
+        res["contacts"] = torch.empty((n, Cn, 8), dtype=torch.float32, device=dev)
+    if want_src and "src" not in res:
+        res["src"] = torch.empty((n, Cn, 2), dtype=torch.int32, device=dev)
+    if want_ee and P > 0 and "ee" not in res:
+        res["ee"] = torch.empty((n, 9, P), dtype=torch.float32, device=dev)
+    if want_mean and "mean_dist" not in res:
+        res["mean_dist"] = torch.empty((n,), dtype=torch.float32, device=dev)
+    o = abi.CmgbManifoldOut()
+    o.contacts = res["contacts"].data_ptr()
+    o.src = res["src"].data_ptr() if "src" in res else None
+    o.ee = res["ee"].data_ptr() if "ee" in res else None
+    o.mean_dist = res["mean_dist"].data_ptr() if "mean_dist" in res else None
+    with torch.cuda.device(dev):
+        _ok(abi.load().cmgb_manifold_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
+                                           C.byref(c), C.byref(o), _stream_ptr(stream)))
+    return res
+
+
+def generate_manifold_batch_host(s1: Surface, s2: Surface, poses1: np.ndarray, poses2: np.ndarray,
+                                 cfg=None, mean_out: Optional[np.ndarray] = None,
+                                 contacts_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+    """End-to-end C-ABI path: HOST poses in, HOST mean distances out (copies inside)."""
+    c = _cfg(cfg)
+    p1 = np.ascontiguousarray(poses1, dtype=np.float64).reshape(-1, 6)
+    p2 = np.ascontiguousarray(poses2, dtype=np.float64).reshape(-1, 6)
+    n = max(len(p1), len(p2))
+    st1 = 1 if len(p1) == n and n > 1 else (1 if n == 1 else 0)
+    st2 = 1 if len(p2) == n and n > 1 else (1 if n == 1 else 0)
+    mean = mean_out if mean_out is not None else np.empty(n, np.float32)
+    _ok(abi.load().cmgb_manifold_batch_host(
+        s1._h, s2._h, p1.ctypes.data, st1, p2.ctypes.data, st2, n, C.byref(c), mean.ctypes.data,
+        contacts_out.ctypes.data if contacts_out is not None else None, _stream_ptr(stream)))
+    return mean
+
+
+def generate_manifold(s1: Surface, s2: Surface, pose1, pose2, cfg=None) -> dict:
+    """One env, reference-shaped result (numpy): contacts [C, 8], meta [C, 4]
+    (kind, side, src_a, src_b), ee [9, m1*m2], layout."""
+    import torch
+
+    p1 = torch.as_tensor(np.asarray(pose1, dtype=np.float64).reshape(1, 6), device="cuda")
+    p2 = torch.as_tensor(np.asarray(pose2, dtype=np.float64).reshape(1, 6), device="cuda")
+    r = generate_manifold_batch(s1, s2, p1, p2, cfg, want_src=True, want_ee=True)
+    torch.cuda.synchronize()
+    meta = layout_metadata(s1, s2, cfg)
+    meta[:, 2:] = r["src"][0].cpu().numpy()
+    out = {"contacts": r["contacts"][0].cpu().numpy(), "meta": meta, "layout": layout(s1, s2, cfg),
+           "mean_dist": float(r["mean_dist"][0].item())}
+    out["ee"] = r["ee"][0].cpu().numpy() if "ee" in r else np.zeros((9, 0), np.float32)
+    return out
+
+
+def run_ee_batch(pairs, cfg=None, *, want_alpha: bool = False, want_labels: bool = False,
+                 stream=None) -> dict:
+    """run_ee_batch (batch.cpp:53-76) on a CUDA [n, 12] float64/float32 tensor."""
+    import torch
+
+    c = _cfg(cfg)
+    pr = pairs.reshape(-1, 12).contiguous()
+    n = pr.shape[0]
+    res = {"out": torch.empty((n, 6), dtype=torch.float32, device=pr.device)}
+    if want_alpha:
+        res["alpha_gamma"] = torch.empty((n, 3), dtype=torch.float32, device=pr.device)
+    if want_labels:
+        res["labels"] = torch.empty((n,), dtype=torch.int32, device=pr.device)
+    with torch.cuda.device(pr.device):
+        _ok(abi.load().cmgb_ee_witness_batch(
+            pr.data_ptr(), int(pr.dtype == torch.float64), n, C.byref(c), res["out"].data_ptr(),
+            res["alpha_gamma"].data_ptr() if want_alpha else None,
+            res["labels"].data_ptr() if want_labels else None, _stream_ptr(stream)))
+    return res
+
+
+def run_vf_batch(pairs, cfg=None, *, want_labels: bool = False, stream=None) -> dict:
+    """run_vf_batch (batch.cpp:78-98) on a CUDA [n, 12] tensor."""
+    import torch
+
+    c = _cfg(cfg)
+    pr = pairs.reshape(-1, 12).contiguous()
+    n = pr.shape[0]
+    res = {"out": torch.empty((n, 3), dtype=torch.float32, device=pr.device)}
+    if want_labels:
+        res["labels"] = torch.empty((n,), dtype=torch.int32, device=pr.device)
+    with torch.cuda.device(pr.device):
+        _ok(abi.load().cmgb_vf_witness_batch(
+            pr.data_ptr(), int(pr.dtype == torch.float64), n, C.byref(c), res["out"].data_ptr(),
+            res["labels"].data_ptr() if want_labels else None, _stream_ptr(stream)))
+    return res
+
+
+def surface_from_spec(body) -> Surface:
+    """Build a Surface from a workloads.BodySpec."""
+    m = body.mesh
+    mesh = Mesh.box(m.box_half, m.subdivisions, m.quad_edges) if m.box_half is not None \
+        else Mesh.parse_obj(m.obj_text)
+    return Surface(mesh, body.sdf, body.vertex_topk, body.edge_topk)

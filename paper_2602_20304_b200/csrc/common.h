@@ -1,0 +1,129 @@
+// Structures shared by the host C++ layer and the sm_100a kernels.
+//
+// Device layout: geometry is FP64 in HBM (a few hundred bytes
+// per surface, read through L1/L2), SDF programs are packed into the kernel's
+// __grid_constant__ parameter block (constant bank: warp-uniform broadcast
+// loads), large primitive tables (CP planes, OPC points) live in a float4 pool
+// in HBM. Poses are FP64 [n_env][6]; contacts are FP32 [n_env][C][8].
+#pragma once
+
+#include <cstdint>
+
+#include <vector_types.h>  // float4 (CUDA toolkit header, host-safe)
+
+namespace cmgb {
+
+constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param block
+constexpr int kMaxStack = 8;    // generic interpreter stack depth
+constexpr int kPairRec = 20;    // floats per E-E pair record in shared memory
+
+enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2 };
+enum PowKind : int32_t { kPowGeneral = 0, kPowRsqrt = 1, kPowRcp = 2, kPowOne = 3 };
+enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
+
+// Superquadric leaf, pre-digested on the host (sdf.hpp:85-108):
+//   f = (x2^p1 + y2^p1)^p2 + z2^p3, phi = (1 - f^p4) / |x~|.
+// n1..n3 > 0 when the exponent is an exact small integer in double precision
+// (then powers are repeated products: no SFU work).
+struct DevSq {
+  float inv_ax[3];
+  float p1, p2, p3, p4;  // 1/e2, e2/e1, 1/e1, -e1/2
+  int32_t n1, n2, n3;    // integer exponents (1..64) or 0
+  int32_t p4kind;        // PowKind for f^p4
+  int32_t has_frame;     // primitive pose != identity
+  float R[9], t[3];      // body_from_prim (sdf.cpp:9)
+};
+
+struct DevNode {
+  int32_t op;      // cmgb_sdf_op
+  int32_t count;   // planes | points | children
+  int32_t offset;  // into the float4 pool (CP: 1 float4/plane, OPC: 2 float4/point)
+  int32_t pad;
+  float tau, inv_tau;
+  DevSq sq;
+};
+
+struct DevSdf {
+  int32_t n_nodes;
+  int32_t kind;        // SdfKind
+  int32_t leaf_count;
+  int32_t max_stack;
+  DevNode nodes[kMaxNodes];
+  const float4* pool;
+};
+
+// One side of a surface pair as the kernel sees it.
+struct DevSide {
+  const double* verts;  // [nv][3] body frame
+  const int32_t* edges; // [ne][2]
+  int32_t nv, ne;
+  int32_t n_sel;        // V-S contacts of this side (effective vertex top-K, or 0)
+  int32_t m_sel;        // selected edges of this side (effective edge top-K, or 0)
+  int32_t topk_v;       // 1: soft top-K over vertices active (n_sel < nv)
+  int32_t topk_e;       // 1: soft top-K over edges active (m_sel < ne)
+  DevSdf sdf;
+};
+
+// SmoothingConfig on the device (config.hpp:17-46). Temperatures are used as
+// reciprocals in FP32; lambda stays FP64 for the QP.
+struct DevCfg {
+  double lambda;
+  float tau_clip, inv_tau_clip;
+  float tau_min, inv_tau_min;
+  float tau_comp, inv_tau_comp;
+  float inv_tau_sign, inv_tau_pen, inv_tau_nn, inv_tau_clash, inv_tau_cont;
+  float tau_topk_v, inv_tau_topk_v, inv_tau_topk_e;
+  float tau_normal;
+  int32_t hard_ops, trace_iters, containment, mode;
+};
+
+// Per-env shared-memory carve-up (bytes from the env's base), host-computed.
+struct SmemLayout {
+  int32_t frames;    // 2 x (R[9], t[3]) doubles
+  int32_t vslots;    // (n1+n2) x 3 doubles: selected vertex payload, WORLD frame
+  int32_t eslots;    // (m1+m2) x 12 doubles: a_world, b_world, a_body, b_body
+  int32_t prov;      // (n1+n2+m1+m2) int32 provenance
+  int32_t scores;    // (V1+V2+E1+E2) floats: top-K scores (-penetration), top-K only
+  int32_t sorted;    // (V1+V2+E1+E2) floats: scores sorted descending
+  int32_t pairs;     // P x kPairRec floats: per E-E pair record
+  int32_t vsdist;    // (n1+n2) floats
+  int32_t nnstat;    // (m1+m2) x 2 floats: min, 1/sum
+  int32_t bytes;     // per env, 16-byte aligned
+};
+
+struct ManifoldParams {
+  DevSide side[2];
+  DevCfg cfg;
+  const double* poses1;
+  const double* poses2;
+  int32_t stride1, stride2;
+  int64_t n_env;
+  int32_t n1, n2, m1, m2, n_contacts;
+  int32_t envs_per_block;
+  SmemLayout smem;
+  float* contacts;
+  int32_t* src;
+  float* ee;
+  float* mean_dist;
+};
+
+struct WitnessParams {
+  const void* pairs;
+  int32_t fp64;
+  int64_t n;
+  DevCfg cfg;
+  float* out;
+  float* alpha_gamma;
+  int32_t* labels;
+};
+
+}  // namespace cmgb
+
+// Launchers implemented in the .cu files (host-callable, stream-ordered).
+namespace cmgb {
+int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
+                    void* stream);
+int launch_ee_witness(const WitnessParams& p, void* stream);
+int launch_vf_witness(const WitnessParams& p, void* stream);
+const char* last_cuda_error_string();
+}  // namespace cmgb

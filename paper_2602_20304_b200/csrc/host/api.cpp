@@ -1,0 +1,576 @@
+// extern "C" ABI of libcmgb (include/cmgb.h).
+//
+// Host responsibilities (all C++, none of them on the hot path): config
+// validation, mesh ingest, SDF program validation/packing, surface build
+// checks (src/surface.cpp:9-44), per-device geometry upload, manifold layout,
+// kernel-parameter assembly and launch. No exception crosses the boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "host.h"
+
+namespace cmgb {
+int manifold_max_threads();
+}
+
+using namespace cmgb;
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int status, const std::string& msg) {
+  g_error = msg;
+  return status;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return CMGB_OK;
+  } catch (const Error& e) {
+    return set_error(e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_error(CMGB_ERR_INVALID_ARGUMENT, "out of host memory");
+  } catch (const std::exception& e) {
+    return set_error(CMGB_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? CMGB_ERR_NO_DEVICE
+                                                                          : CMGB_ERR_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void validate_config(const cmgb_config* c) {
+  if (!c) invalid("config: null pointer");
+  auto positive = [](double v, const char* name) {
+    if (!(v > 0.0)) invalid(std::string("smoothing: ") + name + " must be > 0");
+  };
+  positive(c->lambda, "lambda");
+  positive(c->tau_clip, "tau_clip");
+  positive(c->tau_min, "tau_min");
+  positive(c->tau_comp, "tau_comp");
+  positive(c->tau_sign, "tau_sign");
+  positive(c->tau_pen, "tau_pen");
+  positive(c->tau_nn, "tau_nn");
+  positive(c->tau_clash, "tau_clash");
+  positive(c->tau_cont, "tau_cont");
+  positive(c->tau_topk_verts, "tau_topk_verts");
+  positive(c->tau_topk_edges, "tau_topk_edges");
+  positive(c->tau_normal, "tau_normal");
+  positive(c->tau_union, "tau_union");
+  if (c->sphere_trace_iters < 0) invalid("smoothing: sphere_trace_iters >= 0");
+  if (c->mode < CMGB_MODE_FULL || c->mode > CMGB_MODE_ONE_SIDED) invalid("config: unknown mode");
+}
+
+DevCfg device_config(const cmgb_config* c) {
+  DevCfg d{};
+  d.lambda = c->lambda;
+  d.tau_clip = (float)c->tau_clip;
+  d.inv_tau_clip = (float)(1.0 / c->tau_clip);
+  d.tau_min = (float)c->tau_min;
+  d.inv_tau_min = (float)(1.0 / c->tau_min);
+  d.tau_comp = (float)c->tau_comp;
+  d.inv_tau_comp = (float)(1.0 / c->tau_comp);
+  d.inv_tau_sign = (float)(1.0 / c->tau_sign);
+  d.inv_tau_pen = (float)(1.0 / c->tau_pen);
+  d.inv_tau_nn = (float)(1.0 / c->tau_nn);
+  d.inv_tau_clash = (float)(1.0 / c->tau_clash);
+  d.inv_tau_cont = (float)(1.0 / c->tau_cont);
+  d.tau_topk_v = (float)c->tau_topk_verts;
+  d.inv_tau_topk_v = (float)(1.0 / c->tau_topk_verts);
+  d.inv_tau_topk_e = (float)(1.0 / c->tau_topk_edges);
+  d.tau_normal = (float)c->tau_normal;
+  d.hard_ops = c->hard_ops ? 1 : 0;
+  d.trace_iters = (c->sphere_trace && c->sphere_trace_iters > 0) ? c->sphere_trace_iters : 0;
+  d.containment = c->containment_safeguard ? 1 : 0;
+  d.mode = c->mode;
+  return d;
+}
+
+cmgb_layout layout_of(const cmgb_surface_s* s1, const cmgb_surface_s* s2, const cmgb_config* c) {
+  cmgb_layout L{};
+  L.mode = c->mode;
+  L.n1 = s1->effective_vertex_topk();
+  const bool two = c->mode != CMGB_MODE_ONE_SIDED;
+  const bool full = c->mode == CMGB_MODE_FULL;
+  L.n2 = two ? s2->effective_vertex_topk() : 0;
+  L.m1 = full ? s1->effective_edge_topk() : 0;
+  L.m2 = full ? s2->effective_edge_topk() : 0;
+  L.n_contacts = L.n1 + L.n2 + 2 * L.m1 * L.m2;
+  L.dynamic_src = (L.n1 < s1->mesh.nv()) || (two && L.n2 < s2->mesh.nv()) ||
+                  (full && (L.m1 < s1->mesh.ne() || L.m2 < s2->mesh.ne()));
+  return L;
+}
+
+DeviceSurface& device_image(cmgb_surface_s* s) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(s->mu);
+  auto it = s->device.find(dev);
+  if (it != s->device.end()) return it->second;
+  DeviceSurface d;
+  std::vector<float4> pool;
+  d.sdf = pack_program(s->program, &pool);
+  cuda_check(cudaMalloc(&d.verts, sizeof(double) * s->mesh.vertices.size()), "cudaMalloc");
+  cuda_check(cudaMemcpy(d.verts, s->mesh.vertices.data(), sizeof(double) * s->mesh.vertices.size(),
+                        cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMalloc(&d.edges, sizeof(int32_t) * s->mesh.edges.size()), "cudaMalloc");
+  cuda_check(cudaMemcpy(d.edges, s->mesh.edges.data(), sizeof(int32_t) * s->mesh.edges.size(),
+                        cudaMemcpyHostToDevice), "cudaMemcpy");
+  if (!pool.empty()) {
+    cuda_check(cudaMalloc(&d.pool, sizeof(float4) * pool.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(d.pool, pool.data(), sizeof(float4) * pool.size(), cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+  }
+  d.sdf.pool = d.pool;
+  return s->device.emplace(dev, d).first->second;
+}
+
+int align16(int x) { return (x + 15) & ~15; }
+
+struct LaunchPlan {
+  ManifoldParams p{};
+  int threads = 0, grid = 0;
+  size_t smem = 0;
+};
+
+LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* poses1, int st1,
+                         const double* poses2, int st2, int64_t n_env, const cmgb_config* cfg,
+                         const cmgb_manifold_out* out) {
+  validate_config(cfg);
+  if (!s1 || !s2) invalid("manifold: null surface");
+  if (n_env < 0) invalid("manifold: n_env >= 0");
+  if (!out || !out->contacts) invalid("manifold: contacts output is required");
+  if (!poses1 || !poses2) invalid("manifold: null poses");
+  if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
+  const cmgb_layout L = layout_of(s1, s2, cfg);
+  LaunchPlan plan;
+  ManifoldParams& p = plan.p;
+  cmgb_surface_s* ss[2] = {s1, s2};
+  const int nsel[2] = {L.n1, L.mode == CMGB_MODE_ONE_SIDED ? 0 : L.n2};
+  const int msel[2] = {L.m1, L.m2};
+  for (int k = 0; k < 2; ++k) {
+    DeviceSurface& d = device_image(ss[k]);
+    DevSide& side = p.side[k];
+    side.verts = d.verts;
+    side.edges = d.edges;
+    side.nv = ss[k]->mesh.nv();
+    side.ne = ss[k]->mesh.ne();
+    side.n_sel = nsel[k];
+    side.m_sel = msel[k];
+    // Selection stages only run for slots that are actually emitted.
+    side.topk_v = (nsel[k] > 0 && nsel[k] < side.nv) ? 1 : 0;
+    side.topk_e = (msel[k] > 0 && msel[k] < side.ne) ? 1 : 0;
+    side.sdf = d.sdf;
+  }
+  p.cfg = device_config(cfg);
+  p.poses1 = poses1;
+  p.poses2 = poses2;
+  p.stride1 = st1;
+  p.stride2 = st2;
+  p.n_env = n_env;
+  p.n1 = L.n1;
+  p.n2 = nsel[1];
+  p.m1 = L.m1;
+  p.m2 = L.m2;
+  p.n_contacts = L.n_contacts;
+  p.contacts = out->contacts;
+  p.src = out->src;
+  p.ee = (L.m1 > 0 && L.m2 > 0) ? out->ee : nullptr;
+  p.mean_dist = out->mean_dist;
+
+  // Shared-memory carve-up per env.
+  const int P = L.m1 * L.m2;
+  const int nslot_v = p.n1 + p.n2, nslot_e = L.m1 + L.m2;
+  const bool topk = p.side[0].topk_v || p.side[1].topk_v || p.side[0].topk_e || p.side[1].topk_e;
+  const int nscore = topk ? (p.side[0].nv + p.side[1].nv + p.side[0].ne + p.side[1].ne) : 0;
+  SmemLayout& S = p.smem;
+  int off = 0;
+  S.frames = off; off = align16(off + 24 * 8);
+  S.vslots = off; off = align16(off + nslot_v * 3 * 8);
+  S.eslots = off; off = align16(off + nslot_e * 12 * 8);
+  S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
+  S.scores = off; off = align16(off + nscore * 4);
+  S.sorted = off; off = align16(off + nscore * 4);
+  S.pairs = off; off = align16(off + P * kPairRec * 4);
+  S.vsdist = off; off = align16(off + nslot_v * 4);
+  S.nnstat = off; off = align16(off + nslot_e * 2 * 4);
+  S.bytes = off;
+
+  // Envs per block: ~288 threads of E-E work per CTA (2 box-box envs = 9 warps).
+  const int per_env = std::max({P, nslot_v, 1});
+  int epb = std::max(1, 288 / per_env);
+  const size_t smem_cap = 96 * 1024;
+  while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
+  if ((size_t)S.bytes > 200 * 1024)
+    throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
+  const int maxt = manifold_max_threads();
+  int threads = ((epb * per_env + 31) / 32) * 32;
+  threads = std::min(std::max(threads, 32), maxt);
+  p.envs_per_block = epb;
+  plan.threads = threads;
+  plan.grid = static_cast<int>((n_env + epb - 1) / epb);
+  plan.smem = (size_t)epb * S.bytes;
+  return plan;
+}
+
+// Scratch for the end-to-end host API, per (device, thread) reuse.
+struct HostScratch {
+  double* poses1 = nullptr;
+  double* poses2 = nullptr;
+  float* contacts = nullptr;
+  float* mean = nullptr;
+  size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0;
+};
+
+template <class T>
+void ensure(T** ptr, size_t* cap, size_t n) {
+  if (*cap >= n) return;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  cuda_check(cudaMalloc(ptr, sizeof(T) * std::max<size_t>(n, 1)), "cudaMalloc");
+  *cap = n;
+}
+
+std::mutex g_scratch_mu;
+std::unordered_map<int, HostScratch> g_scratch;
+
+}  // namespace
+
+int cmgb_surface_s::effective_vertex_topk() const {
+  const int v = mesh.nv();
+  return vertex_topk <= 0 ? v : std::min(vertex_topk, v);
+}
+
+int cmgb_surface_s::effective_edge_topk() const {
+  const int e = mesh.ne();
+  return edge_topk <= 0 ? std::min(program.leaf_count, e) : std::min(edge_topk, e);
+}
+
+extern "C" {
+
+const char* cmgb_last_error(void) { return g_error.c_str(); }
+int32_t cmgb_abi_version(void) { return CMGB_ABI_VERSION; }
+
+void cmgb_config_default(cmgb_config* c) {
+  if (!c) return;
+  *c = cmgb_config{};
+  c->lambda = 0.01;
+  c->tau_clip = c->tau_min = c->tau_comp = 0.1;
+  c->tau_sign = 0.1;
+  c->tau_pen = 0.01;
+  c->tau_nn = 0.01;
+  c->tau_clash = 0.1;
+  c->tau_cont = 0.01;
+  c->tau_topk_verts = c->tau_topk_edges = 0.01;
+  c->tau_normal = 1e-9;
+  c->tau_union = 0.01;
+  c->hard_ops = 0;
+  c->sphere_trace = 1;
+  c->sphere_trace_iters = 5;
+  c->containment_safeguard = 0;
+  c->mode = CMGB_MODE_FULL;
+}
+
+void cmgb_config_no_smoothing(cmgb_config* c) {
+  cmgb_config_default(c);
+  if (!c) return;
+  c->lambda = 1e-6;
+  c->hard_ops = 1;
+}
+
+int cmgb_config_validate(const cmgb_config* c) {
+  return guarded([&] { validate_config(c); });
+}
+
+int cmgb_config_for_variant(const char* variant, const cmgb_config* base, cmgb_config* out) {
+  return guarded([&] {
+    if (!variant || !base || !out) invalid("config_for_variant: null argument");
+    cmgb_config c = *base;
+    const std::string v(variant);
+    if (v == "ours") {
+      c.hard_ops = 0;
+      c.mode = CMGB_MODE_FULL;
+    } else if (v == "ours_ns") {
+      c.hard_ops = 1;
+      c.lambda = 1e-6;
+      c.mode = CMGB_MODE_FULL;
+    } else if (v == "ours_ne") {
+      c.hard_ops = 0;
+      c.mode = CMGB_MODE_NO_EE;
+    } else if (v == "ours_ne_s") {
+      c.hard_ops = 0;
+      c.mode = CMGB_MODE_ONE_SIDED;
+    } else {
+      invalid("unknown variant: " + v + " (expected ours|ours_ns|ours_ne|ours_ne_s)");
+    }
+    *out = c;
+  });
+}
+
+// ---- meshes ---------------------------------------------------------------
+int cmgb_mesh_box(const double half[3], int32_t subdivisions, int32_t quad_edges, cmgb_mesh* out) {
+  return guarded([&] {
+    if (!half || !out) invalid("mesh_box: null argument");
+    auto* m = new cmgb_mesh_s{make_box_mesh(half, subdivisions, quad_edges != 0)};
+    *out = m;
+  });
+}
+
+int cmgb_mesh_parse_obj(const char* text, size_t length, cmgb_mesh* out, int32_t* error_line) {
+  return guarded([&] {
+    if (!text || !out) invalid("parse_obj: null argument");
+    try {
+      auto* m = new cmgb_mesh_s{parse_obj_text(std::string(text, length))};
+      *out = m;
+    } catch (const Error& e) {
+      if (error_line) *error_line = e.line;
+      throw;
+    }
+  });
+}
+
+int cmgb_mesh_from_arrays(const double* vertices, int32_t n_vertices, const int32_t* faces,
+                          int32_t n_faces, const int32_t* edges, int32_t n_edges, cmgb_mesh* out) {
+  return guarded([&] {
+    if (!out || n_vertices < 0 || n_faces < 0 || n_edges < 0) invalid("mesh_from_arrays: bad argument");
+    if ((n_vertices && !vertices) || (n_faces && !faces) || (n_edges && !edges))
+      invalid("mesh_from_arrays: null array");
+    auto* m = new cmgb_mesh_s;
+    m->mesh.vertices.assign(vertices, vertices + 3 * (size_t)n_vertices);
+    if (n_faces) m->mesh.faces.assign(faces, faces + 3 * (size_t)n_faces);
+    if (n_edges) m->mesh.edges.assign(edges, edges + 2 * (size_t)n_edges);
+    *out = m;
+  });
+}
+
+int cmgb_mesh_sizes(cmgb_mesh mesh, int32_t* nv, int32_t* nf, int32_t* ne, int32_t* nw) {
+  return guarded([&] {
+    if (!mesh) invalid("mesh_sizes: null mesh");
+    if (nv) *nv = mesh->mesh.nv();
+    if (nf) *nf = mesh->mesh.nf();
+    if (ne) *ne = mesh->mesh.ne();
+    if (nw) *nw = static_cast<int32_t>(mesh->mesh.warnings.size());
+  });
+}
+
+int cmgb_mesh_read(cmgb_mesh mesh, double* vertices, int32_t* faces, int32_t* edges) {
+  return guarded([&] {
+    if (!mesh) invalid("mesh_read: null mesh");
+    const Mesh& m = mesh->mesh;
+    if (vertices) std::memcpy(vertices, m.vertices.data(), sizeof(double) * m.vertices.size());
+    if (faces) std::memcpy(faces, m.faces.data(), sizeof(int32_t) * m.faces.size());
+    if (edges) std::memcpy(edges, m.edges.data(), sizeof(int32_t) * m.edges.size());
+  });
+}
+
+const char* cmgb_mesh_warning(cmgb_mesh mesh, int32_t i) {
+  if (!mesh || i < 0 || i >= (int32_t)mesh->mesh.warnings.size()) return nullptr;
+  return mesh->mesh.warnings[i].c_str();
+}
+
+void cmgb_mesh_destroy(cmgb_mesh mesh) { delete mesh; }
+
+// ---- surfaces ---------------------------------------------------------------
+int cmgb_surface_create(cmgb_mesh mesh, const cmgb_sdf_node* sdf, int32_t n_nodes,
+                        int32_t vertex_topk, int32_t edge_topk, double tolerance_fraction,
+                        cmgb_surface* out) {
+  return guarded([&] {
+    if (!mesh || !out) invalid("surface_create: null argument");
+    Program prog = make_program(sdf, n_nodes);
+    const Mesh& m = mesh->mesh;
+    // build_surface validation (src/surface.cpp:11-24), same messages.
+    if (m.nv() == 0 || m.ne() == 0) invalid("surface: mesh needs vertices and edges");
+    if (vertex_topk < 0 || vertex_topk > m.nv())
+      invalid("surface: vertex_topk must lie in [1, V] (or 0 for all)");
+    if (edge_topk < 0 || edge_topk > m.ne())
+      invalid("surface: edge_topk must lie in [1, E] (or 0 for default)");
+    for (int32_t idx : m.edges)
+      if (idx < 0 || idx >= m.nv()) invalid("surface: edge index out of range");
+    for (int32_t idx : m.faces)
+      if (idx < 0 || idx >= m.nv()) invalid("surface: face index out of range");
+    auto* s = new cmgb_surface_s;
+    s->mesh = m;
+    s->program = std::move(prog);
+    s->vertex_topk = vertex_topk;
+    s->edge_topk = edge_topk;
+    s->warnings = m.warnings;
+    // Mesh/SDF discrepancy is a warning (src/surface.cpp:31-42).
+    double worst = 0.0;
+    for (int i = 0; i < m.nv(); ++i) worst = std::max(worst, std::abs(s->program.value(&m.vertices[3 * i])));
+    const double tol = tolerance_fraction * m.bounding_diagonal();
+    if (worst > tol)
+      s->warnings.push_back("mesh/SDF discrepancy: max |phi(vertex)| = " + std::to_string(worst) +
+                            " exceeds tolerance " + std::to_string(tol) +
+                            "; witness projection and activity indicators may drift");
+    *out = s;
+  });
+}
+
+void cmgb_surface_destroy(cmgb_surface s) {
+  if (!s) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto& [dev, d] : s->device) {
+    cudaSetDevice(dev);
+    cudaFree(d.verts);
+    cudaFree(d.edges);
+    if (d.pool) cudaFree(d.pool);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  delete s;
+}
+
+int cmgb_surface_get_info(cmgb_surface s, cmgb_surface_info* out) {
+  return guarded([&] {
+    if (!s || !out) invalid("surface_get_info: null argument");
+    out->n_vertices = s->mesh.nv();
+    out->n_edges = s->mesh.ne();
+    out->n_faces = s->mesh.nf();
+    out->leaf_count = s->program.leaf_count;
+    out->vertex_topk = s->vertex_topk;
+    out->edge_topk = s->edge_topk;
+    out->effective_vertex_topk = s->effective_vertex_topk();
+    out->effective_edge_topk = s->effective_edge_topk();
+    out->n_warnings = static_cast<int32_t>(s->warnings.size());
+    out->n_nodes = static_cast<int32_t>(s->program.nodes.size());
+  });
+}
+
+const char* cmgb_surface_warning(cmgb_surface s, int32_t i) {
+  if (!s || i < 0 || i >= (int32_t)s->warnings.size()) return nullptr;
+  return s->warnings[i].c_str();
+}
+
+// ---- layout -------------------------------------------------------------------
+int cmgb_layout_query(cmgb_surface s1, cmgb_surface s2, const cmgb_config* cfg, cmgb_layout* out) {
+  return guarded([&] {
+    if (!s1 || !s2 || !out) invalid("layout_query: null argument");
+    validate_config(cfg);
+    *out = layout_of(s1, s2, cfg);
+  });
+}
+
+int cmgb_layout_metadata(cmgb_surface s1, cmgb_surface s2, const cmgb_config* cfg, int32_t* kind,
+                         int32_t* side, int32_t* src_a, int32_t* src_b) {
+  return guarded([&] {
+    if (!s1 || !s2) invalid("layout_metadata: null surface");
+    validate_config(cfg);
+    const cmgb_layout L = layout_of(s1, s2, cfg);
+    const bool sel_v1 = L.n1 < s1->mesh.nv(), sel_v2 = L.n2 < s2->mesh.nv();
+    const bool sel_e1 = L.m1 < s1->mesh.ne(), sel_e2 = L.m2 < s2->mesh.ne();
+    int q = 0;
+    auto put = [&](int k, int sd, int a, int b) {
+      if (kind) kind[q] = k;
+      if (side) side[q] = sd;
+      if (src_a) src_a[q] = a;
+      if (src_b) src_b[q] = b;
+      ++q;
+    };
+    for (int i = 0; i < L.n1; ++i) put(0, 1, sel_v1 ? -1 : i, -1);
+    for (int i = 0; i < L.n2; ++i) put(0, 2, sel_v2 ? -1 : i, -1);
+    for (int k = 0; k < L.m1; ++k)
+      for (int l = 0; l < L.m2; ++l) {
+        put(1, 1, sel_e1 ? -1 : k, sel_e2 ? -1 : l);
+        put(1, 2, sel_e1 ? -1 : k, sel_e2 ? -1 : l);
+      }
+  });
+}
+
+// ---- batched manifold ------------------------------------------------------------
+int cmgb_manifold_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1, int32_t st1,
+                        const double* poses2, int32_t st2, int64_t n_env, const cmgb_config* cfg,
+                        const cmgb_manifold_out* out, void* stream) {
+  return guarded([&] {
+    LaunchPlan plan = plan_manifold(s1, s2, poses1, st1, poses2, st2, n_env, cfg, out);
+    if (n_env == 0 || plan.p.n_contacts == 0) return;
+    if (launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                             int32_t st1, const double* poses2_host, int32_t st2, int64_t n_env,
+                             const cmgb_config* cfg, float* mean_dist_host, float* contacts_host,
+                             void* stream) {
+  return guarded([&] {
+    if (!s1 || !s2) invalid("manifold_batch_host: null surface");
+    validate_config(cfg);
+    if (!poses1_host || !poses2_host) invalid("manifold_batch_host: null poses");
+    if (n_env == 0) return;
+    const cmgb_layout L = layout_of(s1, s2, cfg);
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    HostScratch& sc = g_scratch[dev];
+    const size_t np1 = (st1 ? n_env : 1) * 6, np2 = (st2 ? n_env : 1) * 6;
+    ensure(&sc.poses1, &sc.cap_poses1, np1);
+    ensure(&sc.poses2, &sc.cap_poses2, np2);
+    ensure(&sc.contacts, &sc.cap_contacts, (size_t)n_env * L.n_contacts * 8);
+    ensure(&sc.mean, &sc.cap_mean, (size_t)n_env);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaMemcpyAsync(sc.poses1, poses1_host, sizeof(double) * np1, cudaMemcpyHostToDevice, s),
+               "H2D poses1");
+    cuda_check(cudaMemcpyAsync(sc.poses2, poses2_host, sizeof(double) * np2, cudaMemcpyHostToDevice, s),
+               "H2D poses2");
+    cmgb_manifold_out out{sc.contacts, nullptr, nullptr, sc.mean};
+    LaunchPlan plan = plan_manifold(s1, s2, sc.poses1, st1, sc.poses2, st2, n_env, cfg, &out);
+    if (launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
+    if (mean_dist_host)
+      cuda_check(cudaMemcpyAsync(mean_dist_host, sc.mean, sizeof(float) * n_env, cudaMemcpyDeviceToHost, s),
+                 "D2H mean");
+    if (contacts_host)
+      cuda_check(cudaMemcpyAsync(contacts_host, sc.contacts, sizeof(float) * n_env * L.n_contacts * 8,
+                                 cudaMemcpyDeviceToHost, s),
+                 "D2H contacts");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+// ---- witness batches --------------------------------------------------------------
+int cmgb_ee_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb_config* cfg,
+                          float* out, float* alpha_gamma, int32_t* labels, void* stream) {
+  return guarded([&] {
+    validate_config(cfg);
+    if (n < 0) invalid("ee_witness_batch: n >= 0");
+    if (n == 0) return;
+    if (!pairs || !out) invalid("ee_witness_batch: null buffer");
+    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, alpha_gamma, labels};
+    if (launch_ee_witness(p, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("ee_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_vf_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb_config* cfg,
+                          float* out, int32_t* labels, void* stream) {
+  return guarded([&] {
+    validate_config(cfg);
+    if (n < 0) invalid("vf_witness_batch: n >= 0");
+    if (n == 0) return;
+    if (!pairs || !out) invalid("vf_witness_batch: null buffer");
+    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, nullptr, labels};
+    if (launch_vf_witness(p, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_device_count(int32_t* count) {
+  return guarded([&] {
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (count) *count = n;
+  });
+}
+
+}  // extern "C"
