@@ -3,22 +3,21 @@
 // Device layout: geometry is FP64 in HBM (a few hundred bytes
 // per surface, read through L1/L2), SDF programs are packed into the kernel's
 // __grid_constant__ parameter block (constant bank: warp-uniform broadcast
-// loads), large primitive tables (CP planes, OPC points) live in a float4 pool
+// loads), large primitive tables (CP planes, OPC points) live in a double4 pool
 // in HBM. Poses are FP64 [n_env][6]; contacts are FP32 [n_env][C][8].
 #pragma once
 
 #include <cstdint>
 
-#include <vector_types.h>  // float4 (CUDA toolkit header, host-safe)
+#include <vector_types.h>  // double4 (CUDA toolkit header, host-safe)
 
 namespace cmgb {
 
 constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param block
 constexpr int kMaxStack = 8;    // generic interpreter stack depth
-constexpr int kPairRec = 20;    // floats per E-E pair record in shared memory
+constexpr int kPairRec = 24;    // floats per E-E pair record in shared memory (96 B)
 
 enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2 };
-enum PowKind : int32_t { kPowGeneral = 0, kPowRsqrt = 1, kPowRcp = 2, kPowOne = 3 };
 enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
 
 // Superquadric leaf, pre-digested on the host (sdf.hpp:85-108):
@@ -26,20 +25,23 @@ enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 
 // n1..n3 > 0 when the exponent is an exact small integer in double precision
 // (then powers are repeated products: no SFU work).
 struct DevSq {
-  float inv_ax[3];
-  float p1, p2, p3, p4;  // 1/e2, e2/e1, 1/e1, -e1/2
+  double inv_ax[3];
+  double p1, p2, p3;     // 1/e2, e2/e1, 1/e1 (general-exponent path)
+  double c_xy, c_z;      // 2 p1 p2, 2 p3 (grad f prefactors)
+  double R[9], t[3];     // body_from_prim (sdf.cpp:9)
+  double p4;             // -e1/2
   int32_t n1, n2, n3;    // integer exponents (1..64) or 0
-  int32_t p4kind;        // PowKind for f^p4
   int32_t has_frame;     // primitive pose != identity
-  float R[9], t[3];      // body_from_prim (sdf.cpp:9)
+  int32_t pad;
 };
 
 struct DevNode {
   int32_t op;      // cmgb_sdf_op
   int32_t count;   // planes | points | children
-  int32_t offset;  // into the float4 pool (CP: 1 float4/plane, OPC: 2 float4/point)
+  int32_t offset;  // into the double4 pool (CP: 1 per plane, OPC: 2 per point)
   int32_t pad;
-  float tau, inv_tau;
+  double tau_d;
+  double inv_tau_d;
   DevSq sq;
 };
 
@@ -49,7 +51,7 @@ struct DevSdf {
   int32_t leaf_count;
   int32_t max_stack;
   DevNode nodes[kMaxNodes];
-  const float4* pool;
+  const double4* pool;  // CP: (n, n.p) per plane; OPC: (p, -1/2th^2), (n, 1/th^2)
 };
 
 // One side of a surface pair as the kernel sees it.
@@ -64,16 +66,14 @@ struct DevSide {
   DevSdf sdf;
 };
 
-// SmoothingConfig on the device (config.hpp:17-46). Temperatures are used as
-// reciprocals in FP32; lambda stays FP64 for the QP.
+// SmoothingConfig on the device (config.hpp:17-46), FP64 (temperatures as
+// reciprocals: x / tau -> x * inv_tau, within 1 ulp of the reference).
 struct DevCfg {
   double lambda;
-  float tau_clip, inv_tau_clip;
-  float tau_min, inv_tau_min;
-  float tau_comp, inv_tau_comp;
-  float inv_tau_sign, inv_tau_pen, inv_tau_nn, inv_tau_clash, inv_tau_cont;
-  float tau_topk_v, inv_tau_topk_v, inv_tau_topk_e;
-  float tau_normal;
+  double tau_clip, inv_tau_clip, inv_tau_min, inv_tau_comp;
+  double inv_tau_sign, inv_tau_pen, inv_tau_nn, inv_tau_clash, inv_tau_cont;
+  double inv_tau_topk_v, inv_tau_topk_e;
+  double tau_normal;
   int32_t hard_ops, trace_iters, containment, mode;
 };
 

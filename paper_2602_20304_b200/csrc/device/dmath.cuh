@@ -1,9 +1,12 @@
 // Device scalar helpers for sm_100a.
 //
-// Precision policy: geometry that suffers cancellation (pose
-// transforms, QP linear algebra, witness points, sphere-trace accumulation,
-// the E-E separation vector) is FP64; SDF fields and the smooth operators'
-// transcendentals are FP32 on the SFU (MUFU.EX2/LG2/RSQ/RCP).
+// Precision policy: every quantity that the reference's outputs
+// are ill-conditioned in (pose transforms, SDF field cores and gradient
+// directions, QP linear algebra, witness points, sphere-trace accumulation,
+// the E-E separation vector) is FP64 on the B200's half-rate DFMA pipe; the
+// bounded transcendental corrections (sigmoid / softplus / softmin weights,
+// expm1 / log1p of small arguments) run in FP32 on the SFU (MUFU.EX2/LG2/RSQ/
+// RCP), and FP64 reciprocals are SFU seeds refined by one Newton step.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -32,66 +35,48 @@ __device__ __forceinline__ float rsqf(float x) {
   return r;
 }
 
-// x^p for a general real exponent via the SFU (x > 0).
-__device__ __forceinline__ float powg(float x, float p) { return ex2f(p * lg2f(x)); }
-
-// x^(n-1) for a small positive integer n (repeated squaring, no SFU);
-// the branch is warp-uniform (one SDF per launch side).
-__device__ __forceinline__ float powi_m1(float x, int n) {
-  switch (n) {
-    case 1: return 1.0f;
-    case 2: return x;
-    case 3: return x * x;
-    case 4: { const float x2 = x * x; return x2 * x; }
-    case 5: { const float x2 = x * x; return x2 * x2; }
-    case 10: { const float x2 = x * x, x4 = x2 * x2, x8 = x4 * x4; return x8 * x; }
-    case 20: { const float x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return (x16 * x2) * x; }
-    default: {
-      float r = 1.0f, b = x;
-      int e = n - 1;
-#pragma unroll 1
-      while (e) {
-        if (e & 1) r *= b;
-        b *= b;
-        e >>= 1;
-      }
-      return r;
-    }
-  }
+// FP64 reciprocal square root / reciprocal: SFU seed + one Newton step
+// (relative error ~1e-14, a handful of DFMAs instead of the libdevice paths).
+__device__ __forceinline__ double rsqrt_d(double x) {
+  double y = (double)rsqf((float)x);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_d(double x) {
+  double y = (double)rcpf((float)x);
+  y = y * fma(-x, y, 2.0);
+  return y;
 }
 
-// (x^p, x^(p-1)): integer fast path when n > 0, else SFU pow.
-__device__ __forceinline__ void pow_pair(float x, int n, float p, float& xp, float& xpm1) {
-  if (n > 0) {
-    xpm1 = powi_m1(x, n);
-    xp = xpm1 * x;
-  } else {
-    xp = powg(x, p);
-    xpm1 = xp * rcpf(x);
-  }
+// stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
+// function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each
+// to full relative precision (the blends need the small one exactly).
+__device__ __forceinline__ void sigmoid_pair_d(double x, double* s, double* c) {
+  const double e = exp(-fabs(x));
+  const double inv = 1.0 / (1.0 + e);
+  const double small = e * inv;
+  *s = x >= 0.0 ? inv : small;
+  *c = x >= 0.0 ? small : inv;
+}
+__device__ __forceinline__ double sigmoid_d(double x) {
+  double s, c;
+  sigmoid_pair_d(x, &s, &c);
+  return s;
 }
 
-// stable_sigmoid (smooth_ops.hpp:22-35): both arms evaluate the same function.
-__device__ __forceinline__ float sigmoidf(float x) {
-  const float e = __expf(-fabsf(x));
-  const float inv = __frcp_rn(1.0f + e);
-  return x >= 0.0f ? inv : e * inv;
+// softplus_s (smooth_ops.hpp:66-81): max(x, 0) + tau log1p(exp(-|x|/tau)); both
+// reference arms are this function.
+__device__ __forceinline__ double softplus_d(double x, double tau, double inv_tau) {
+  return fmax(x, 0.0) + tau * log1p(exp(-fabs(x) * inv_tau));
 }
-
-// softplus correction tau*log1p(exp(-|x|/tau)) (smooth_ops.hpp:66-81 with the
-// max(x,0) part taken exactly in FP64 by the caller).
-__device__ __forceinline__ float softplus_corr(float ax_over_tau, float tau) {
-  return tau * log1pf(__expf(-ax_over_tau));
-}
-
-// tanh (sign_s, smooth_ops.hpp:57-62): accurate libdevice form (2 ulp).
-__device__ __forceinline__ float tanh_acc(float x) { return tanhf(x); }
 
 __device__ __forceinline__ double3 d3(double x, double y, double z) { return make_double3(x, y, z); }
 __device__ __forceinline__ double3 operator+(double3 a, double3 b) { return d3(a.x + b.x, a.y + b.y, a.z + b.z); }
 __device__ __forceinline__ double3 operator-(double3 a, double3 b) { return d3(a.x - b.x, a.y - b.y, a.z - b.z); }
 __device__ __forceinline__ double3 operator*(double3 a, double s) { return d3(a.x * s, a.y * s, a.z * s); }
 __device__ __forceinline__ double ddot(double3 a, double3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double3 dscale(double3 a, double s) { return d3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ float3 to_f3v(double3 a) { return make_float3((float)a.x, (float)a.y, (float)a.z); }
 
 __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
 __device__ __forceinline__ float fdot(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }

@@ -1,12 +1,21 @@
-// Device evaluation of the smooth analytical SDF programs (FP32).
+// Device evaluation of the smooth analytical SDF programs.
 //
-// Three query flavours, as in the reference (sdf.hpp:177-195):
-//   kValue         phi                       (penetration scores / pen sigmoids)
-//   kGrad          phi, true grad phi        (sphere tracing, sdf.hpp:318-326)
-//   kNormalSource  phi, composed normal field; SQ leaves contribute grad f
-//                  (sdf.hpp:233-288)
-// Gradients are analytic (the reference nests a Dual<3>; the derivative of
-// the same expression graph).
+// Query flavours, as in the reference (sdf.hpp:177-195):
+//   kValue         phi                         (scores, pen sigmoids)
+//   kGrad          phi + true grad phi         (sphere tracing, sdf.hpp:318-326)
+//   kNormalSource  phi + composed normal field (SQ leaves give grad f, 233-288)
+//   kNormalOnly    normal field only (lone SQ leaf: phi skipped)
+// Gradients are analytic (the reference nests a Dual<3>: the derivative of the
+// same expression graph).
+//
+// Precision: phi feeds the fixed-count sphere trace, whose
+// tangential drift is phi * (direction error), and the E-E signed normal
+// amplifies witness errors by (1/|de|)(1 + 1/tau_sign); matching the FP64
+// reference to 1e-5 needs ~1e-10 absolute. The field is therefore FP64
+// throughout (integer-power chains instead of pow for the superquadric,
+// 1 - f^p4 = -expm1(p4 log1p(f - 1)) without cancellation, FP64 plane / RBF
+// distances, LSE / RBF weights). FP64 reciprocal square roots are SFU seeds
+// refined by one Newton step.
 #pragma once
 
 #include "../common.h"
@@ -15,149 +24,175 @@
 namespace cmgb {
 
 struct SdfOut {
-  float v;
-  float3 g;
+  double v;
+  double3 g;
 };
 
-// Superquadric leaf in its canonical frame (sdf.hpp:85-108).
-template <int FL>
-__device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, float3 p) {
-  if (q.has_frame) {  // Transform::apply_inverse: R^T (p - t)
-    const float dx = p.x - q.t[0], dy = p.y - q.t[1], dz = p.z - q.t[2];
-    p = f3(q.R[0] * dx + q.R[3] * dy + q.R[6] * dz, q.R[1] * dx + q.R[4] * dy + q.R[7] * dz,
-           q.R[2] * dx + q.R[5] * dy + q.R[8] * dz);
-  }
-  const float xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
-  const float x2 = fmaf(xn, xn, 1e-30f), y2 = fmaf(yn, yn, 1e-30f), z2 = fmaf(zn, zn, 1e-30f);
-  float A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
-  pow_pair(x2, q.n1, q.p1, A, Am1);
-  pow_pair(y2, q.n1, q.p1, B, Bm1);
-  const float g = A + B;
-  pow_pair(g, q.n2, q.p2, G, Gm1);
-  pow_pair(z2, q.n3, q.p3, Cz, Czm1);
-  const float f = G + Cz;
-  SdfOut out;
-  // df/dp through the normalisation (d x2^p1 = p1 x2^(p1-1) 2 xn / ax).
-  const float cxy = 2.0f * q.p1 * q.p2 * Gm1;
-  const float dfx = cxy * Am1 * xn * q.inv_ax[0];
-  const float dfy = cxy * Bm1 * yn * q.inv_ax[1];
-  const float dfz = 2.0f * q.p3 * Czm1 * zn * q.inv_ax[2];
-  if (FL != kNormalOnly) {  // V-S contacts need phi with the normal source
-    const float r2 = fmaf(xn, xn, fmaf(yn, yn, fmaf(zn, zn, 1e-20f)));
-    const float rinv = rsqf(r2);
-    float F;
-    if (q.p4kind == kPowRsqrt) F = rsqf(f);
-    else if (q.p4kind == kPowRcp) F = rcpf(f);
-    else F = powg(f, q.p4);
-    out.v = (1.0f - F) * rinv;
-    if (FL == kGrad) {
-      // grad phi = (-p4 F/f grad f - phi * (x~/axes) / r) / r
-      const float k = -q.p4 * F * rcpf(f);
-      const float h = out.v * rinv;
-      float3 gl = f3((k * dfx - h * xn * q.inv_ax[0]) * rinv, (k * dfy - h * yn * q.inv_ax[1]) * rinv,
-                     (k * dfz - h * zn * q.inv_ax[2]) * rinv);
-      if (q.has_frame)
-        gl = f3(q.R[0] * gl.x + q.R[1] * gl.y + q.R[2] * gl.z, q.R[3] * gl.x + q.R[4] * gl.y + q.R[5] * gl.z,
-                q.R[6] * gl.x + q.R[7] * gl.y + q.R[8] * gl.z);
-      out.g = gl;
+// (x^p, x^(p-1)) in FP64: integer chains (no SFU) or libdevice pow.
+__device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp, double& xpm1) {
+  if (n > 0) {
+    double r;
+    switch (n) {
+      case 1: r = 1.0; break;
+      case 2: r = x; break;
+      case 5: { const double x2 = x * x; r = x2 * x2; break; }
+      case 10: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4; r = x8 * x; break; }
+      default: {
+        double b = x;
+        r = 1.0;
+        int e = n - 1;
+#pragma unroll 1
+        while (e) {
+          if (e & 1) r *= b;
+          b *= b;
+          e >>= 1;
+        }
+      }
     }
+    xpm1 = r;
+    xp = r * x;
+  } else {
+    xp = pow(x, p);
+    xpm1 = xp / x;
   }
-  if (FL == kNormalSource || FL == kNormalOnly) {
-    float3 gl = f3(dfx, dfy, dfz);
-    if (q.has_frame)
-      gl = f3(q.R[0] * gl.x + q.R[1] * gl.y + q.R[2] * gl.z, q.R[3] * gl.x + q.R[4] * gl.y + q.R[5] * gl.z,
-              q.R[6] * gl.x + q.R[7] * gl.y + q.R[8] * gl.z);
-    out.g = gl;
+}
+
+// 1 - f^p4 = -expm1(p4 ln f) for f > 0: cancellation-free near the surface
+// (f -> 1), with ln f = log1p(f - 1) there (f - 1 is exact in FP64).
+__device__ __forceinline__ double one_minus_pow(double f, double p4) {
+  const double d = f - 1.0;
+  const double lnf = fabs(d) < 0.5 ? log1p(d) : log(f);
+  return -expm1(p4 * lnf);
+}
+
+// Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64).
+template <int FL>
+__device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
+  if (q.has_frame) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));  // apply_inverse
+  const double xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
+  const double x2 = fma(xn, xn, 1e-30), y2 = fma(yn, yn, 1e-30), z2 = fma(zn, zn, 1e-30);
+  double A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
+  pow_pair_d(x2, q.n1, q.p1, A, Am1);
+  pow_pair_d(y2, q.n1, q.p1, B, Bm1);
+  const double g = A + B;
+  pow_pair_d(g, q.n2, q.p2, G, Gm1);
+  pow_pair_d(z2, q.n3, q.p3, Cz, Czm1);
+  const double f = G + Cz;
+  SdfOut out;
+  out.v = 0.0;
+  out.g = d3(0, 0, 0);
+  if (FL == kValue) {
+    const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
+    out.v = one_minus_pow(f, q.p4) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
+    return out;
+  }
+  // grad f through the normalisation: d(x2^p1)/dx = p1 x2^(p1-1) 2 xn / ax.
+  const double cxy = q.c_xy * Gm1;
+  const double3 df = d3(cxy * Am1 * xn * q.inv_ax[0], cxy * Bm1 * yn * q.inv_ax[1],
+                        q.c_z * Czm1 * zn * q.inv_ax[2]);
+  if (FL == kNormalOnly) {
+    out.g = q.has_frame ? mul_R(q.R, df) : df;
+    return out;
+  }
+  const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
+  const double rinv = rsqrt_d(r2);
+  const double omF = one_minus_pow(f, q.p4);
+  const double phi = omF * rinv;
+  out.v = phi;
+  if (FL == kGrad) {
+    // grad phi = (-p4 (F/f) grad f - phi (x~ / axes) / r) / r, F = 1 - omF
+    const double k = -q.p4 * (1.0 - omF) * rcp_d(f);
+    const double h = phi * rinv;
+    double3 gl = d3((k * df.x - h * xn * q.inv_ax[0]) * rinv, (k * df.y - h * yn * q.inv_ax[1]) * rinv,
+                    (k * df.z - h * zn * q.inv_ax[2]) * rinv);
+    out.g = q.has_frame ? mul_R(q.R, gl) : gl;
+  } else {  // kNormalSource
+    out.g = q.has_frame ? mul_R(q.R, df) : df;
   }
   return out;
 }
 
 // Convex polyhedron leaf: LSE over plane distances (sdf.hpp:110-117).
-// Pool entry per plane: (n.x, n.y, n.z, n . point).
+// Pool per plane: double4 (n.x, n.y, n.z, n . point); distances in FP64.
 template <int FL>
-__device__ __forceinline__ SdfOut cp_leaf(const DevNode& nd, const float4* pool, float3 p) {
-  const float4* pl = pool + nd.offset;
-  float m = -INFINITY;
+__device__ __forceinline__ SdfOut cp_leaf(const DevNode& nd, const double4* pool, double3 p) {
+  const double4* pl = pool + nd.offset;
+  double m = -INFINITY;
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
-    const float4 q = pl[i];
-    const float d = fmaf(q.x, p.x, fmaf(q.y, p.y, fmaf(q.z, p.z, -q.w)));
-    m = fmaxf(m, d);
+    const double4 q = pl[i];
+    m = fmax(m, fma(q.x, p.x, fma(q.y, p.y, fma(q.z, p.z, -q.w))));
   }
-  float acc = 0.0f;
-  float3 g = f3(0.f, 0.f, 0.f);
+  double acc = 0.0;
+  double3 g = d3(0, 0, 0);
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
-    const float4 q = pl[i];
-    const float d = fmaf(q.x, p.x, fmaf(q.y, p.y, fmaf(q.z, p.z, -q.w)));
-    const float e = __expf((d - m) * nd.inv_tau);
+    const double4 q = pl[i];
+    const double d = fma(q.x, p.x, fma(q.y, p.y, fma(q.z, p.z, -q.w)));
+    const double e = exp((d - m) * nd.inv_tau_d);
     acc += e;
-    if (FL != kValue) {
-      g.x = fmaf(e, q.x, g.x);
-      g.y = fmaf(e, q.y, g.y);
-      g.z = fmaf(e, q.z, g.z);
-    }
+    if (FL != kValue) g = g + d3(e * q.x, e * q.y, e * q.z);
   }
   SdfOut out;
-  out.v = m + nd.tau * __logf(acc);
-  if (FL != kValue) {
-    const float inv = rcpf(acc);
-    out.g = f3(g.x * inv, g.y * inv, g.z * inv);
-  }
+  out.v = m + nd.tau_d * log(acc);
+  out.g = d3(0, 0, 0);
+  if (FL != kValue) out.g = dscale(g, rcp_d(acc));
   return out;
 }
 
-// Oriented pointcloud leaf: Gaussian-RBF weighted plane distances
-// (sdf.hpp:119-132). Pool per point: (p, -1/(2 th^2)), (n, 1/th^2).
+// Oriented pointcloud leaf (sdf.hpp:119-132). Pool per point: double4
+// (p, -1/(2 th^2)), double4 (n, 1/th^2). Sums in FP64.
 template <int FL>
-__device__ __forceinline__ SdfOut opc_leaf(const DevNode& nd, const float4* pool, float3 p) {
-  const float4* pt = pool + nd.offset;
-  float num = 0.0f, den = 1e-30f;
-  float3 dnum = f3(0.f, 0.f, 0.f), dden = f3(0.f, 0.f, 0.f);
+__device__ __forceinline__ SdfOut opc_leaf(const DevNode& nd, const double4* pool, double3 p) {
+  const double4* pt = pool + nd.offset;
+  double num = 0.0, den = 1e-30;
+  double3 dnum = d3(0, 0, 0), dden = d3(0, 0, 0);
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
-    const float4 a = pt[2 * i], b = pt[2 * i + 1];
-    const float rx = p.x - a.x, ry = p.y - a.y, rz = p.z - a.z;
-    const float w = __expf((rx * rx + ry * ry + rz * rz) * a.w);
-    const float nr = b.x * rx + b.y * ry + b.z * rz;
-    num = fmaf(w, nr, num);
+    const double4 a = pt[2 * i], b = pt[2 * i + 1];
+    const double rx = p.x - a.x, ry = p.y - a.y, rz = p.z - a.z;
+    const double arg = (rx * rx + ry * ry + rz * rz) * a.w;
+    const double w = exp(arg);
+    const double nr = b.x * rx + b.y * ry + b.z * rz;
+    num = fma(w, nr, num);
     den += w;
     if (FL != kValue) {
-      const float s = -w * b.w;  // dw = -w r / th^2
-      dnum.x += s * rx * nr + w * b.x;
-      dnum.y += s * ry * nr + w * b.y;
-      dnum.z += s * rz * nr + w * b.z;
-      dden.x += s * rx;
-      dden.y += s * ry;
-      dden.z += s * rz;
+      const double s = -w * b.w;  // dw = -w r / th^2
+      dnum = dnum + d3(s * rx * nr + w * b.x, s * ry * nr + w * b.y, s * rz * nr + w * b.z);
+      dden = dden + d3(s * rx, s * ry, s * rz);
     }
   }
   SdfOut out;
-  const float inv = __frcp_rn(den);
+  const double inv = 1.0 / den;
   out.v = num * inv;
+  out.g = d3(0, 0, 0);
   if (FL != kValue)
-    out.g = f3((dnum.x - out.v * dden.x) * inv, (dnum.y - out.v * dden.y) * inv,
+    out.g = d3((dnum.x - out.v * dden.x) * inv, (dnum.y - out.v * dden.y) * inv,
                (dnum.z - out.v * dden.z) * inv);
   return out;
 }
 
 template <int FL>
-__device__ __forceinline__ SdfOut leaf_eval(const DevNode& nd, const float4* pool, float3 p) {
+__device__ __forceinline__ SdfOut leaf_eval(const DevNode& nd, const double4* pool, double3 p) {
   if (nd.op == 0) return sq_leaf<FL>(nd.sq, p);
   if (nd.op == 1) return cp_leaf<FL>(nd, pool, p);
   return opc_leaf<FL>(nd, pool, p);
 }
 
-// Full program evaluation in the BODY frame.
-template <int FL_IN>
-__device__ SdfOut sdf_eval(const DevSdf& s, float3 p) {
-  if (s.kind == kSingleSq) return sq_leaf<FL_IN>(s.nodes[0].sq, p);
+// Full program evaluation in the BODY frame. KIND (SdfKind) is a compile-time
+// specialisation chosen on the host per surface: each kernel instantiation
+// carries only the field code it needs (I-cache footprint).
+template <int FL_IN, int KIND>
+__device__ SdfOut sdf_eval(const DevSdf& s, double3 p) {
+  if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN>(s.nodes[0].sq, p);
   // kNormalOnly skips phi only for a lone SQ leaf; compositions need the values.
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
-  if (s.kind == kSingleCp) return cp_leaf<FL>(s.nodes[0], s.pool, p);
+  constexpr bool kWantG = FL != kValue;
+  if constexpr (KIND == kSingleCp) return cp_leaf<FL>(s.nodes[0], s.pool, p);
   // Generic postfix interpreter (union: -LSE(-phi), subtraction: LSE(phi+, -phi-);
   // sdf.hpp:222-230, 260-287). Warp-uniform control flow.
-  float sv[kMaxStack], sx[kMaxStack], sy[kMaxStack], sz[kMaxStack];
+  double sv[kMaxStack];
+  double3 sg[kMaxStack];
   int sp = 0;
 #pragma unroll 1
   for (int i = 0; i < s.n_nodes; ++i) {
@@ -165,47 +200,44 @@ __device__ SdfOut sdf_eval(const DevSdf& s, float3 p) {
     if (nd.op <= 2) {
       const SdfOut r = leaf_eval<FL>(nd, s.pool, p);
       sv[sp] = r.v;
-      if (FL != kValue) { sx[sp] = r.g.x; sy[sp] = r.g.y; sz[sp] = r.g.z; }
+      sg[sp] = r.g;
       ++sp;
-    } else if (nd.op == 3) {  // union: weights softmin(phi_i / tau), first minimum
+    } else if (nd.op == 3) {  // union: softmin weights, first minimum
       const int n = nd.count, base = sp - n;
-      float m = sv[base];
+      double m = sv[base];
 #pragma unroll 1
-      for (int k = 1; k < n; ++k) m = fminf(m, sv[base + k]);
-      float acc = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+      for (int k = 1; k < n; ++k) m = fmin(m, sv[base + k]);
+      double acc = 0.0;
+      double3 g = d3(0, 0, 0);
 #pragma unroll 1
       for (int k = 0; k < n; ++k) {
-        const float e = __expf((m - sv[base + k]) * nd.inv_tau);
+        const double arg = (m - sv[base + k]) * nd.inv_tau_d;
+        const double e = exp(arg);
         acc += e;
-        if (FL != kValue) { gx = fmaf(e, sx[base + k], gx); gy = fmaf(e, sy[base + k], gy); gz = fmaf(e, sz[base + k], gz); }
+        if (kWantG) g = g + dscale(sg[base + k], e);
       }
       sp = base;
-      sv[sp] = m - nd.tau * __logf(acc);
-      if (FL != kValue) {
-        const float inv = rcpf(acc);
-        sx[sp] = gx * inv; sy[sp] = gy * inv; sz[sp] = gz * inv;
-      }
+      sv[sp] = m - nd.tau_d * log(acc);
+      sg[sp] = kWantG ? dscale(g, rcp_d(acc)) : d3(0, 0, 0);
       ++sp;
     } else {  // subtraction: args (phi+, -phi-), softmax weights
       const int a = sp - 2, b = sp - 1;
-      const float a0 = sv[a], a1 = -sv[b];
-      const float m = fmaxf(a0, a1);
-      const float e0 = __expf((a0 - m) * nd.inv_tau), e1 = __expf((a1 - m) * nd.inv_tau);
-      const float acc = e0 + e1;
-      sv[a] = m + nd.tau * __logf(acc);
-      if (FL != kValue) {
-        const float inv = rcpf(acc);
-        const float w0 = e0 * inv, w1 = e1 * inv;
-        sx[a] = w0 * sx[a] - w1 * sx[b];
-        sy[a] = w0 * sy[a] - w1 * sy[b];
-        sz[a] = w0 * sz[a] - w1 * sz[b];
+      const double a0 = sv[a], a1 = -sv[b];
+      const double m = fmax(a0, a1);
+      const double e0 = exp((a0 - m) * nd.inv_tau_d);
+      const double e1 = exp((a1 - m) * nd.inv_tau_d);
+      const double acc = e0 + e1;
+      sv[a] = m + nd.tau_d * log(acc);
+      if (kWantG) {
+        const double inv = rcp_d(acc);
+        sg[a] = dscale(sg[a], e0 * inv) - dscale(sg[b], e1 * inv);
       }
       sp = a + 1;
     }
   }
   SdfOut out;
   out.v = sv[0];
-  out.g = FL != kValue ? f3(sx[0], sy[0], sz[0]) : f3(0.f, 0.f, 0.f);
+  out.g = sg[0];
   return out;
 }
 

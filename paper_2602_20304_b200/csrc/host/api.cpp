@@ -75,21 +75,18 @@ void validate_config(const cmgb_config* c) {
 DevCfg device_config(const cmgb_config* c) {
   DevCfg d{};
   d.lambda = c->lambda;
-  d.tau_clip = (float)c->tau_clip;
-  d.inv_tau_clip = (float)(1.0 / c->tau_clip);
-  d.tau_min = (float)c->tau_min;
-  d.inv_tau_min = (float)(1.0 / c->tau_min);
-  d.tau_comp = (float)c->tau_comp;
-  d.inv_tau_comp = (float)(1.0 / c->tau_comp);
-  d.inv_tau_sign = (float)(1.0 / c->tau_sign);
-  d.inv_tau_pen = (float)(1.0 / c->tau_pen);
-  d.inv_tau_nn = (float)(1.0 / c->tau_nn);
-  d.inv_tau_clash = (float)(1.0 / c->tau_clash);
-  d.inv_tau_cont = (float)(1.0 / c->tau_cont);
-  d.tau_topk_v = (float)c->tau_topk_verts;
-  d.inv_tau_topk_v = (float)(1.0 / c->tau_topk_verts);
-  d.inv_tau_topk_e = (float)(1.0 / c->tau_topk_edges);
-  d.tau_normal = (float)c->tau_normal;
+  d.tau_clip = c->tau_clip;
+  d.inv_tau_clip = 1.0 / c->tau_clip;
+  d.inv_tau_min = 1.0 / c->tau_min;
+  d.inv_tau_comp = 1.0 / c->tau_comp;
+  d.inv_tau_sign = 1.0 / c->tau_sign;
+  d.inv_tau_pen = 1.0 / c->tau_pen;
+  d.inv_tau_nn = 1.0 / c->tau_nn;
+  d.inv_tau_clash = 1.0 / c->tau_clash;
+  d.inv_tau_cont = 1.0 / c->tau_cont;
+  d.inv_tau_topk_v = 1.0 / c->tau_topk_verts;
+  d.inv_tau_topk_e = 1.0 / c->tau_topk_edges;
+  d.tau_normal = c->tau_normal;
   d.hard_ops = c->hard_ops ? 1 : 0;
   d.trace_iters = (c->sphere_trace && c->sphere_trace_iters > 0) ? c->sphere_trace_iters : 0;
   d.containment = c->containment_safeguard ? 1 : 0;
@@ -119,7 +116,7 @@ DeviceSurface& device_image(cmgb_surface_s* s) {
   auto it = s->device.find(dev);
   if (it != s->device.end()) return it->second;
   DeviceSurface d;
-  std::vector<float4> pool;
+  std::vector<double4> pool;
   d.sdf = pack_program(s->program, &pool);
   cuda_check(cudaMalloc(&d.verts, sizeof(double) * s->mesh.vertices.size()), "cudaMalloc");
   cuda_check(cudaMemcpy(d.verts, s->mesh.vertices.data(), sizeof(double) * s->mesh.vertices.size(),
@@ -128,8 +125,8 @@ DeviceSurface& device_image(cmgb_surface_s* s) {
   cuda_check(cudaMemcpy(d.edges, s->mesh.edges.data(), sizeof(int32_t) * s->mesh.edges.size(),
                         cudaMemcpyHostToDevice), "cudaMemcpy");
   if (!pool.empty()) {
-    cuda_check(cudaMalloc(&d.pool, sizeof(float4) * pool.size()), "cudaMalloc");
-    cuda_check(cudaMemcpy(d.pool, pool.data(), sizeof(float4) * pool.size(), cudaMemcpyHostToDevice),
+    cuda_check(cudaMalloc(&d.pool, sizeof(double4) * pool.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(d.pool, pool.data(), sizeof(double4) * pool.size(), cudaMemcpyHostToDevice),
                "cudaMemcpy");
   }
   d.sdf.pool = d.pool;
@@ -200,11 +197,11 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   S.vslots = off; off = align16(off + nslot_v * 3 * 8);
   S.eslots = off; off = align16(off + nslot_e * 12 * 8);
   S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
-  S.scores = off; off = align16(off + nscore * 4);
-  S.sorted = off; off = align16(off + nscore * 4);
+  S.scores = off; off = align16(off + nscore * 8);
+  S.sorted = off; off = align16(off + nscore * 8);
   S.pairs = off; off = align16(off + P * kPairRec * 4);
   S.vsdist = off; off = align16(off + nslot_v * 4);
-  S.nnstat = off; off = align16(off + nslot_e * 2 * 4);
+  S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
   S.bytes = off;
 
   // Envs per block: ~288 threads of E-E work per CTA (2 box-box envs = 9 warps).

@@ -68,11 +68,11 @@ void se3_exp_host(const double xi[6], double R[9], double t[3]);
 struct DeviceSurface {
   double* verts = nullptr;
   int32_t* edges = nullptr;
-  float4* pool = nullptr;
+  double4* pool = nullptr;
   DevSdf sdf{};
 };
 
-DevSdf pack_program(const Program& prog, std::vector<float4>* pool);
+DevSdf pack_program(const Program& prog, std::vector<double4>* pool);
 
 }  // namespace cmgb
 

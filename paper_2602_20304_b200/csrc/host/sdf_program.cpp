@@ -193,7 +193,7 @@ int exact_int(double x) {
 
 }  // namespace
 
-DevSdf pack_program(const Program& prog, std::vector<float4>* pool) {
+DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
   DevSdf s{};
   const int n = static_cast<int>(prog.nodes.size());
   if (n > kMaxNodes)
@@ -212,40 +212,41 @@ DevSdf pack_program(const Program& prog, std::vector<float4>* pool) {
     DevNode& o = s.nodes[i];
     o.op = d.op;
     o.count = d.count;
-    o.tau = static_cast<float>(d.tau);
-    o.inv_tau = d.tau > 0.0 ? static_cast<float>(1.0 / d.tau) : 0.0f;
+    o.tau_d = d.tau;
+    o.inv_tau_d = d.tau > 0.0 ? 1.0 / d.tau : 0.0;
     o.offset = static_cast<int32_t>(pool->size());
     if (d.op == CMGB_SDF_SUPERQUADRIC) {
       DevSq& q = o.sq;
-      for (int k = 0; k < 3; ++k) q.inv_ax[k] = static_cast<float>(1.0 / d.axes[k]);
+      for (int k = 0; k < 3; ++k) q.inv_ax[k] = 1.0 / d.axes[k];
       const double p1 = 1.0 / d.eps2, p2 = d.eps2 / d.eps1, p3 = 1.0 / d.eps1, p4 = -d.eps1 / 2.0;
-      q.p1 = static_cast<float>(p1);
-      q.p2 = static_cast<float>(p2);
-      q.p3 = static_cast<float>(p3);
-      q.p4 = static_cast<float>(p4);
+      q.p1 = p1;
+      q.p2 = p2;
+      q.p3 = p3;
+      q.c_xy = 2.0 * p1 * p2;
+      q.c_z = 2.0 * p3;
+      q.p4 = p4;
       q.n1 = exact_int(p1);
       q.n2 = exact_int(p2);
       q.n3 = exact_int(p3);
-      q.p4kind = p4 == -0.5 ? kPowRsqrt : (p4 == -1.0 ? kPowRcp : kPowGeneral);
       bool ident = true;
       for (int k = 0; k < 6; ++k) ident = ident && d.pose[k] == 0.0;
       q.has_frame = ident ? 0 : 1;
-      for (int k = 0; k < 9; ++k) q.R[k] = static_cast<float>(d.R[k]);
-      for (int k = 0; k < 3; ++k) q.t[k] = static_cast<float>(d.t[k]);
+      for (int k = 0; k < 9; ++k) q.R[k] = d.R[k];
+      for (int k = 0; k < 3; ++k) q.t[k] = d.t[k];
     } else if (d.op == CMGB_SDF_CONVEX_POLYHEDRON) {
       for (int k = 0; k < d.count; ++k) {
         const double* nn = &d.normals[3 * k];
         const double* pp = &d.points[3 * k];
         const double off = nn[0] * pp[0] + nn[1] * pp[1] + nn[2] * pp[2];
-        pool->push_back(make_float4((float)nn[0], (float)nn[1], (float)nn[2], (float)off));
+        pool->push_back(make_double4(nn[0], nn[1], nn[2], off));
       }
     } else if (d.op == CMGB_SDF_ORIENTED_POINTCLOUD) {
       for (int k = 0; k < d.count; ++k) {
         const double th = d.lengthscales[k];
-        pool->push_back(make_float4((float)d.points[3 * k], (float)d.points[3 * k + 1],
-                                    (float)d.points[3 * k + 2], (float)(-1.0 / (2.0 * th * th))));
-        pool->push_back(make_float4((float)d.normals[3 * k], (float)d.normals[3 * k + 1],
-                                    (float)d.normals[3 * k + 2], (float)(1.0 / (th * th))));
+        pool->push_back(make_double4(d.points[3 * k], d.points[3 * k + 1], d.points[3 * k + 2],
+                                     -1.0 / (2.0 * th * th)));
+        pool->push_back(make_double4(d.normals[3 * k], d.normals[3 * k + 1], d.normals[3 * k + 2],
+                                     1.0 / (th * th)));
       }
     }
   }

@@ -3,8 +3,9 @@
 //   a batch, + mean_contact_distance (379-384), in ONE launch.
 //
 // Mapping: a CTA owns `envs_per_block` consecutive envs (all envs share the
-// same two surfaces, so every branch on geometry / config is warp-uniform).
-// Phases, separated by __syncthreads():
+// same two surfaces, so every branch on geometry / config is warp-uniform;
+// the SDF kind of each side is a template parameter). Phases, separated by
+// __syncthreads():
 //   A  pose -> (R, t)                         se3_exp            pose.hpp:78-91
 //   B  opposing-SDF vertex scores (top-K)     vertex/edge_penetrations 77-94
 //   C  rank sort of scores (top-K)            soft_topk sort     smooth_ops.hpp:180-185
@@ -29,6 +30,11 @@ namespace {
 
 constexpr int kMaxThreads = 512;
 
+// Pair record layout (floats; kPairRec = 24):
+//   0-2 p1 world, 3-5 p2 world, 6 dist1, 7 dist2, 8-10 normal1, 11-13 normal2,
+//   14 pen1, 15 pen2, 16 con, 17 clash, 18 cont, 20-21 dbar (FP64)
+constexpr int kRecDbar = 20;
+
 struct EnvView {
   unsigned char* base;
   const SmemLayout* L;
@@ -37,11 +43,12 @@ struct EnvView {
   __device__ double* vslot(int i) const { return reinterpret_cast<double*>(base + L->vslots) + 3 * i; }
   __device__ double* eslot(int i) const { return reinterpret_cast<double*>(base + L->eslots) + 12 * i; }
   __device__ int* prov() const { return reinterpret_cast<int*>(base + L->prov); }
-  __device__ float* scores() const { return reinterpret_cast<float*>(base + L->scores); }
-  __device__ float* sorted() const { return reinterpret_cast<float*>(base + L->sorted); }
+  __device__ double* scores() const { return reinterpret_cast<double*>(base + L->scores); }
+  __device__ double* sorted() const { return reinterpret_cast<double*>(base + L->sorted); }
   __device__ float* pair(int i) const { return reinterpret_cast<float*>(base + L->pairs) + kPairRec * i; }
   __device__ float* vsdist() const { return reinterpret_cast<float*>(base + L->vsdist); }
-  __device__ float* nnstat() const { return reinterpret_cast<float*>(base + L->nnstat); }
+  __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
+  __device__ double& dbar(int i) const { return *reinterpret_cast<double*>(pair(i) + kRecDbar); }
 };
 
 __device__ __forceinline__ double3 ld_vert(const double* v, int i) {
@@ -74,49 +81,53 @@ __device__ __forceinline__ void store_contact(float* dst, float px, float py, fl
   o[1] = make_float4(nx, ny, nz, a);
 }
 
+// normalize_smooth (vec3.hpp:56-62) in FP64.
+__device__ __forceinline__ double3 normalize_smooth(double3 v, double tau) {
+  return dscale(v, rsqrt_d(tau + ddot(v, v)));
+}
+
 // V-S contact for a selected vertex (world) against the opposing posed SDF
 // (vs_contacts, manifold.hpp:185-204).
+template <int KO>
 __device__ __forceinline__ void vs_contact(const DevSdf& opp, const double* Ro, const double* to,
                                            double3 pw, const DevCfg& c, float* out_dist,
                                            float* dst) {
-  const float3 pb = to_f3(to_body(Ro, to, pw));
-  const SdfOut s = sdf_eval<kNormalSource>(opp, pb);
-  const float inv = rsqf(c.tau_normal + fdot(s.g, s.g));  // normalize_smooth (vec3.hpp:56-62)
-  const float3 n = mul_R_f(Ro, f3(s.g.x * inv, s.g.y * inv, s.g.z * inv));
-  const float act = sigmoidf(-s.v * c.inv_tau_pen);  // sigma_greater(-phi, 0, tau_pen)
-  *out_dist = s.v;
-  store_contact(dst, (float)pw.x, (float)pw.y, (float)pw.z, s.v, n.x, n.y, n.z, act);
+  const SdfOut s = sdf_eval<kNormalSource, KO>(opp, to_body(Ro, to, pw));
+  const float3 n = to_f3v(mul_R(Ro, normalize_smooth(s.g, c.tau_normal)));
+  const double act = sigmoid_d(-s.v * c.inv_tau_pen);  // sigma_greater(-phi, 0, tau_pen)
+  *out_dist = (float)s.v;
+  store_contact(dst, (float)pw.x, (float)pw.y, (float)pw.z, (float)s.v, n.x, n.y, n.z, (float)act);
 }
 
-// sphere_trace_project (sdf.hpp:318-326) in the body frame, FP64 position.
+// sphere_trace_project (sdf.hpp:318-326) in the body frame, FP64.
+template <int K>
 __device__ __forceinline__ double3 trace(const DevSdf& sdf, double3 p, const DevCfg& c) {
 #pragma unroll 1
   for (int k = 0; k < c.trace_iters; ++k) {
-    const SdfOut s = sdf_eval<kGrad>(sdf, to_f3(p));
-    const float sc = s.v * rsqf(c.tau_normal + fdot(s.g, s.g));
-    p = p - d3((double)(s.g.x * sc), (double)(s.g.y * sc), (double)(s.g.z * sc));
+    const SdfOut s = sdf_eval<kGrad, K>(sdf, p);
+    p = p - dscale(normalize_smooth(s.g, c.tau_normal), s.v);
   }
   return p;
 }
 
 // E-E pair stage (ee_contacts loop body, manifold.hpp:237-287). Writes the
 // pair record consumed by the NN / activity phases.
+template <int K1, int K2>
 __device__ __forceinline__ void ee_pair(const ManifoldParams& p, const EnvView& ev, int k, int l,
                                         float* rec) {
   const DevCfg& c = p.cfg;
   const double* s1 = ev.eslot(k);
   const double* s2 = ev.eslot(p.m1 + l);
-  const double3 a1w = d3(s1[0], s1[1], s1[2]), b1w = d3(s1[3], s1[4], s1[5]);
-  const double3 a2w = d3(s2[0], s2[1], s2[2]), b2w = d3(s2[3], s2[4], s2[5]);
-  const QpSol w = ee_qp(a1w, b1w, a2w, b2w, c);
+  const QpSol w = ee_qp(d3(s1[0], s1[1], s1[2]), d3(s1[3], s1[4], s1[5]), d3(s2[0], s2[1], s2[2]),
+                        d3(s2[3], s2[4], s2[5]), c);
   // Witness points in their own body frames (edge_point, witness.hpp:130-133).
   const double3 a1b = d3(s1[6], s1[7], s1[8]), b1b = d3(s1[9], s1[10], s1[11]);
   const double3 a2b = d3(s2[6], s2[7], s2[8]), b2b = d3(s2[9], s2[10], s2[11]);
   double3 p1b = a1b + (b1b - a1b) * w.a1;
   double3 p2b = a2b + (b2b - a2b) * w.a2;
   if (c.trace_iters > 0) {
-    p1b = trace(p.side[0].sdf, p1b, c);
-    p2b = trace(p.side[1].sdf, p2b, c);
+    p1b = trace<K1>(p.side[0].sdf, p1b, c);
+    p2b = trace<K2>(p.side[1].sdf, p2b, c);
   }
   const double* R1 = ev.R(0);
   const double* t1 = ev.t(0);
@@ -126,46 +137,46 @@ __device__ __forceinline__ void ee_pair(const ManifoldParams& p, const EnvView& 
   const double3 p2w = to_world(R2, t2, p2b);
   const double3 de = p1w - p2w;
   const double dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
-  const double inv_dg = 1.0 / dg;
-  const float3 nb = f3((float)(de.x * inv_dg), (float)(de.y * inv_dg), (float)(de.z * inv_dg));
+  const double3 nb = d3(de.x / dg, de.y / dg, de.z / dg);
   SdfOut o1, o2;
   if (c.containment) {
-    o1 = sdf_eval<kNormalSource>(p.side[0].sdf, to_f3(p1b));
-    o2 = sdf_eval<kNormalSource>(p.side[1].sdf, to_f3(p2b));
+    o1 = sdf_eval<kNormalSource, K1>(p.side[0].sdf, p1b);
+    o2 = sdf_eval<kNormalSource, K2>(p.side[1].sdf, p2b);
   } else {
-    o1 = sdf_eval<kNormalOnly>(p.side[0].sdf, to_f3(p1b));
-    o2 = sdf_eval<kNormalOnly>(p.side[1].sdf, to_f3(p2b));
+    o1 = sdf_eval<kNormalOnly, K1>(p.side[0].sdf, p1b);
+    o2 = sdf_eval<kNormalOnly, K2>(p.side[1].sdf, p2b);
   }
-  const float i1 = rsqf(c.tau_normal + fdot(o1.g, o1.g));
-  const float i2 = rsqf(c.tau_normal + fdot(o2.g, o2.g));
-  const float3 n1 = mul_R_f(R1, f3(o1.g.x * i1, o1.g.y * i1, o1.g.z * i1));
-  const float3 n2 = mul_R_f(R2, f3(o2.g.x * i2, o2.g.y * i2, o2.g.z * i2));
-  float g1, g2;
-  const float d2 = fdot(n2, nb), d1 = fdot(n1, nb);
+  const double3 n1 = mul_R(R1, normalize_smooth(o1.g, c.tau_normal));
+  const double3 n2 = mul_R(R2, normalize_smooth(o2.g, c.tau_normal));
+  const double d2 = ddot(n2, nb), d1 = ddot(n1, nb);
+  double g1, g2;
   if (c.hard_ops) {  // sign_hard (smooth_ops.hpp:208)
-    g1 = d2 < 0.f ? -1.f : (d2 > 0.f ? 1.f : 0.f);
-    g2 = d1 < 0.f ? -1.f : (d1 > 0.f ? 1.f : 0.f);
-  } else {
-    g1 = tanh_acc(d2 * c.inv_tau_sign);
-    g2 = tanh_acc(d1 * c.inv_tau_sign);
+    g1 = d2 < 0.0 ? -1.0 : (d2 > 0.0 ? 1.0 : 0.0);
+    g2 = d1 < 0.0 ? -1.0 : (d1 > 0.0 ? 1.0 : 0.0);
+  } else {  // sign_s = tanh(x / tau_sign) (smooth_ops.hpp:57-62)
+    g1 = tanh(d2 * c.inv_tau_sign);
+    g2 = tanh(d1 * c.inv_tau_sign);
   }
   // Penetration of each witness point into the opposing surface.
-  const float v12 = sdf_eval<kValue>(p.side[1].sdf, to_f3(to_body(R2, t2, p1w))).v;
-  const float v21 = sdf_eval<kValue>(p.side[0].sdf, to_f3(to_body(R1, t1, p2w))).v;
+  const double v12 = sdf_eval<kValue, K2>(p.side[1].sdf, to_body(R2, t2, p1w)).v;
+  const double v21 = sdf_eval<kValue, K1>(p.side[0].sdf, to_body(R1, t1, p2w)).v;
   rec[0] = (float)p1w.x; rec[1] = (float)p1w.y; rec[2] = (float)p1w.z;
   rec[3] = (float)p2w.x; rec[4] = (float)p2w.y; rec[5] = (float)p2w.z;
-  rec[6] = nb.x; rec[7] = nb.y; rec[8] = nb.z;
-  rec[9] = g1;
-  rec[10] = g2;
-  rec[11] = (float)dg;
-  rec[12] = w.gamma;
-  rec[13] = sigmoidf(-v12 * c.inv_tau_pen);
-  rec[14] = sigmoidf(-v21 * c.inv_tau_pen);
-  rec[15] = sigmoidf(-fdot(n1, n2) * c.inv_tau_clash);
-  rec[16] = c.containment ? sigmoidf(-o1.v * c.inv_tau_cont) * sigmoidf(-o2.v * c.inv_tau_cont)
-                          : 1.0f;
+  // signed distances and normals (manifold.hpp:311-313, 321-323)
+  rec[6] = (float)(g1 * dg);
+  rec[7] = (float)(g2 * dg);
+  rec[8] = (float)(nb.x * g1); rec[9] = (float)(nb.y * g1); rec[10] = (float)(nb.z * g1);
+  rec[11] = (float)(nb.x * g2); rec[12] = (float)(nb.y * g2); rec[13] = (float)(nb.z * g2);
+  rec[14] = (float)sigmoid_d(-v12 * c.inv_tau_pen);              // pen1
+  rec[15] = (float)sigmoid_d(-v21 * c.inv_tau_pen);              // pen2
+  rec[16] = (float)w.gamma;                                      // con
+  rec[17] = (float)sigmoid_d(-ddot(n1, n2) * c.inv_tau_clash);   // clash
+  rec[18] = c.containment ? (float)(sigmoid_d(-o1.v * c.inv_tau_cont) * sigmoid_d(-o2.v * c.inv_tau_cont))
+                          : 1.0f;                                // containment safeguard
+  *reinterpret_cast<double*>(rec + kRecDbar) = dg;
 }
 
+template <int K1, int K2>
 __global__ void __launch_bounds__(kMaxThreads, 1)
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -205,8 +216,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const EnvView ev = env(e);
       const double3 pw = to_world(ev.R(s), ev.t(s), ld_vert(s == 0 ? S1.verts : S2.verts, vi));
       const double3 pb = to_body(ev.R(1 - s), ev.t(1 - s), pw);
-      const float pen = s == 0 ? sdf_eval<kValue>(S2.sdf, to_f3(pb)).v
-                               : sdf_eval<kValue>(S1.sdf, to_f3(pb)).v;
+      const double pen = s == 0 ? sdf_eval<kValue, K2>(S2.sdf, pb).v : sdf_eval<kValue, K1>(S1.sdf, pb).v;
       ev.scores()[i] = -pen;  // scores = negated penetrations (manifold.hpp:142-143)
     }
     __syncthreads();
@@ -218,10 +228,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const int ei = s == 0 ? i : i - S1.ne;
       const int32_t* E = s == 0 ? S1.edges : S2.edges;
       const int va = __ldg(E + 2 * ei), vb = __ldg(E + 2 * ei + 1);
-      float* sc = env(e).scores();
+      double* sc = env(e).scores();
       const int voff = s == 0 ? 0 : S1.nv;
-      const float pa = -sc[voff + va], pb = -sc[voff + vb];
-      sc[sets.off[2] + i] = -((pa + pb) * 0.5f);
+      const double pa = -sc[voff + va], pb = -sc[voff + vb];
+      sc[sets.off[2] + i] = -((pa + pb) * 0.5);
     }
     __syncthreads();
     // ---- C: descending rank sort (values only matter; smooth_ops.hpp:180-185)
@@ -231,11 +241,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
       const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
       if (!active) continue;
-      const float* sc = env(e).scores();
-      const float x = sc[i];
+      const double* sc = env(e).scores();
+      const double x = sc[i];
       int rank = 0;
       for (int j = sets.off[set]; j < sets.off[set + 1]; ++j) {
-        const float y = sc[j];
+        const double y = sc[j];
         rank += (y > x) || (y == x && j < i);
       }
       env(e).sorted()[sets.off[set] + rank] = x;
@@ -267,20 +277,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         }
       } else {  // soft top-K row r (smooth_ops.hpp:191-196, manifold.hpp:141-148, 168-180)
         const int set = (is_edge ? 2 : 0) + s;
-        const float* x = ev.scores() + sets.off[set];
+        const double* x = ev.scores() + sets.off[set];
         const int D = sets.off[set + 1] - sets.off[set];
-        const float sr = ev.sorted()[sets.off[set] + r];
-        const float inv_tau = is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
-        float tot = 0.f;
+        const double sr = ev.sorted()[sets.off[set] + r];
+        const double inv_tau = is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
+        double tot = 0.0;
         prov = -1;
         for (int i = 0; i < D; ++i) {
-          const float dist = fabsf(sr - x[i]);
-          tot += __expf(-dist * inv_tau);
-          if (prov < 0 && dist == 0.0f) prov = i;  // first argmax (hard_attribution, 110-121)
+          const double dist = fabs(sr - x[i]);
+          tot += exp(-dist * inv_tau);
+          if (prov < 0 && dist == 0.0) prov = i;  // first argmax (hard_attribution, 110-121)
         }
-        const float inv = rcpf(tot);
+        const double inv = 1.0 / tot;
         for (int i = 0; i < D; ++i) {
-          const double wi = (double)(__expf(-fabsf(sr - x[i]) * inv_tau) * inv);
+          const double wi = exp(-fabs(sr - x[i]) * inv_tau) * inv;
           if (is_edge) {
             a = a + ld_vert(S.verts, __ldg(S.edges + 2 * i)) * wi;
             b = b + ld_vert(S.verts, __ldg(S.edges + 2 * i + 1)) * wi;
@@ -315,8 +325,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const EnvView ev = env(e);
       const double* q = ev.vslot(r);
       float* dst = p.contacts + ((env0 + e) * C + r) * 8;
-      if (r < n1) vs_contact(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      else vs_contact(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
       if (p.src) {
         int* sp = p.src + ((env0 + e) * C + r) * 2;
         sp[0] = ev.prov()[r];
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     if (full) {
       for (int it = tid; it < n_here * P; it += nth) {
         const int e = it / P, i = it % P;
-        ee_pair(p, env(e), i / m2, i % m2, env(e).pair(i));
+        ee_pair<K1, K2>(p, env(e), i / m2, i % m2, env(e).pair(i));
       }
     }
   }
@@ -340,18 +350,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const EnvView ev = env(e);
       const bool row = r < m1;
       const int n = row ? m2 : m1;
-      float m = INFINITY;
-      for (int j = 0; j < n; ++j) {
+      double m = INFINITY;
+      for (int j = 0; j < n; ++j) {  // minimum shift (argmin_s, smooth_ops.hpp:130-136)
         const int i = row ? r * m2 + j : j * m2 + (r - m1);
-        m = fminf(m, ev.pair(i)[11]);
+        m = fmin(m, ev.dbar(i));
       }
-      float tot = 0.f;
+      double tot = 0.0;
       for (int j = 0; j < n; ++j) {
         const int i = row ? r * m2 + j : j * m2 + (r - m1);
-        tot += __expf((m - ev.pair(i)[11]) * c.inv_tau_nn);
+        tot += exp((m - ev.dbar(i)) * c.inv_tau_nn);
       }
       ev.nnstat()[2 * r] = m;
-      ev.nnstat()[2 * r + 1] = rcpf(tot);
+      ev.nnstat()[2 * r + 1] = 1.0 / tot;
     }
     __syncthreads();
     // ---- G: activity product + fixed-layout E-E output (303-330) -----------
@@ -360,41 +370,35 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const int k = i / m2, l = i % m2;
       const EnvView ev = env(e);
       const float* rec = ev.pair(i);
-      const float* ns = ev.nnstat();
-      const float dgf = rec[11];
-      const float nn1 = __expf((ns[2 * k] - dgf) * c.inv_tau_nn) * ns[2 * k + 1];
-      const float nn2 = __expf((ns[2 * (m1 + l)] - dgf) * c.inv_tau_nn) * ns[2 * (m1 + l) + 1];
-      const float con = rec[12], pen1 = rec[13], pen2 = rec[14], clash = rec[15], cont = rec[16];
-      const float act1 = con * pen1 * nn1 * clash * cont;
-      const float act2 = con * pen2 * nn2 * clash * cont;
-      const float g1 = rec[9], g2 = rec[10];
+      const double* ns = ev.nnstat();
+      const double dg = ev.dbar(i);
+      const double nn1 = exp((ns[2 * k] - dg) * c.inv_tau_nn) * ns[2 * k + 1];
+      const double nn2 = exp((ns[2 * (m1 + l)] - dg) * c.inv_tau_nn) * ns[2 * (m1 + l) + 1];
+      const double pen1 = rec[14], pen2 = rec[15], con = rec[16], clash = rec[17], cont = rec[18];
+      const float act1 = (float)(con * pen1 * nn1 * clash * cont);
+      const float act2 = (float)(con * pen2 * nn2 * clash * cont);
       const int64_t row = (env0 + e) * C + n1 + n2 + 2 * i;
       float* dst = p.contacts + row * 8;
-      store_contact(dst, rec[0], rec[1], rec[2], g1 * dgf, rec[6] * g1, rec[7] * g1, rec[8] * g1, act1);
-      store_contact(dst + 8, rec[3], rec[4], rec[5], g2 * dgf, rec[6] * g2, rec[7] * g2, rec[8] * g2, act2);
+      store_contact(dst, rec[0], rec[1], rec[2], rec[6], rec[8], rec[9], rec[10], act1);
+      store_contact(dst + 8, rec[3], rec[4], rec[5], rec[7], rec[11], rec[12], rec[13], act2);
       if (p.src) {
         int* sp = p.src + row * 2;
         const int sa = ev.prov()[n1 + n2 + k], sb = ev.prov()[n1 + n2 + m1 + l];
         sp[0] = sa; sp[1] = sb; sp[2] = sa; sp[3] = sb;
       }
-      if (p.ee) {
+      if (p.ee) {  // EeIndicatorMatrices (manifold.hpp:41-52)
         float* E = p.ee + (env0 + e) * 9 * P;
-        E[i] = dgf;
-        E[P + i] = con;
-        E[2 * P + i] = pen1;
-        E[3 * P + i] = pen2;
-        E[4 * P + i] = nn1;
-        E[5 * P + i] = nn2;
-        E[6 * P + i] = clash;
+        E[i] = (float)dg;
+        E[P + i] = (float)con;
+        E[2 * P + i] = (float)pen1;
+        E[3 * P + i] = (float)pen2;
+        E[4 * P + i] = (float)nn1;
+        E[5 * P + i] = (float)nn2;
+        E[6 * P + i] = (float)clash;
         E[7 * P + i] = act1;
         E[8 * P + i] = act2;
       }
-      // keep the signed distances for the mean reduction
-      float* w = const_cast<float*>(rec);
-      w[17] = g1 * dgf;
-      w[18] = g2 * dgf;
     }
-    __syncthreads();
   }
 
   // ---- H: mean contact distance, one warp per env, fixed reduction order --
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       double acc = 0.0;
       for (int r = lane; r < n1 + n2; r += 32) acc += (double)ev.vsdist()[r];
       if (full)
-        for (int i = lane; i < P; i += 32) acc += (double)ev.pair(i)[17] + (double)ev.pair(i)[18];
+        for (int i = lane; i < P; i += 32) acc += (double)ev.pair(i)[6] + (double)ev.pair(i)[7];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) p.mean_dist[env0 + e] = (float)(acc / (double)C);
@@ -413,17 +417,37 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
 }
 
+template <int K1, int K2>
+int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(manifold_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    configured = true;
+  }
+  manifold_kernel<K1, K2><<<grid, threads, smem, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+template <int K1>
+int launch_k2(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
+  switch (p.side[1].sdf.kind) {
+    case kSingleSq: return launch_kind<K1, kSingleSq>(p, threads, grid, smem, s);
+    case kSingleCp: return launch_kind<K1, kSingleCp>(p, threads, grid, smem, s);
+    default: return launch_kind<K1, kGeneric>(p, threads, grid, smem, s);
+  }
+}
+
 }  // namespace
 
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(manifold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (p.side[0].sdf.kind) {
+    case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);
+    case kSingleCp: return launch_k2<kSingleCp>(p, block_threads, grid, smem_bytes, s);
+    default: return launch_k2<kGeneric>(p, block_threads, grid, smem_bytes, s);
   }
-  manifold_kernel<<<grid, block_threads, smem_bytes, static_cast<cudaStream_t>(stream)>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int manifold_max_threads() { return kMaxThreads; }

@@ -48,8 +48,8 @@ def run_case(name, ws, cfg, n):
     if bad.any():
         idx = np.argwhere(bad)[:6]
         for i in idx:
-            e, c, f = (int(x) for x in i)
-            print(f"   bad env {e} contact {c} field {f}: got {got[e, c]} ref {ref['contacts'][e, c]}")
+            e, c = (int(x) for x in i)
+            print(f"   bad env {e} contact {c}: got {got[e, c]}\n                    ref {ref['contacts'][e, c]}")
 
 
 def main():

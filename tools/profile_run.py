@@ -1,0 +1,25 @@
+"""One warm launch of a kernel for ncu capture (python tools/profile_run.py manifold|ee|vf [n])."""
+import os, sys
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2602_20304_b200 import api
+from paper_2602_20304_b200.scene import SmoothingConfig
+from paper_2602_20304_b200 import workloads as W
+
+kind = sys.argv[1] if len(sys.argv) > 1 else "manifold"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
+if kind == "manifold":
+    ws = W.box_box(n)
+    s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
+    p1, p2 = ws.poses(n)
+    P1 = torch.as_tensor(p1, device="cuda"); P2 = torch.as_tensor(p2, device="cuda")
+    out = {}
+    for _ in range(3):
+        api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out)
+else:
+    pairs = torch.rand((n, 12), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        (api.run_ee_batch if kind == "ee" else api.run_vf_batch)(pairs, SmoothingConfig())
+torch.cuda.synchronize()
+print("ok")
