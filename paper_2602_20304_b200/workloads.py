@@ -197,6 +197,72 @@ def sq_obj_text(eps1: float, eps2: float, axes: Sequence[float], n_lat: int = 6,
     return "\n".join(lines) + "\n"
 
 
+def capsule_obj_text(radius: float, half_len: float, n_cap: int = 3, n_lon: int = 8) -> str:
+    """Tessellated capsule (two hemispherical caps joined by a cylinder band)."""
+    verts = [(0.0, 0.0, half_len + radius)]
+    rings = []
+    for cap_z, sgn in ((half_len, 1.0), (-half_len, -1.0)):
+        etas = [math.pi / 2 * (1 - i / n_cap) for i in range(1, n_cap + 1)]
+        if sgn < 0:
+            etas = [-e for e in reversed(etas)]
+        for eta in etas:
+            ring = []
+            for j in range(n_lon):
+                om = -math.pi + 2 * math.pi * j / n_lon
+                rho = radius * math.cos(eta)
+                verts.append((rho * math.cos(om), rho * math.sin(om), cap_z + radius * math.sin(eta)))
+                ring.append(len(verts))
+            rings.append(ring)
+    verts.append((0.0, 0.0, -half_len - radius))
+    south = len(verts)
+    lines = [f"v {x:.17g} {y:.17g} {z:.17g}" for x, y, z in verts]
+    for j in range(n_lon):
+        lines.append(f"f 1 {rings[0][j]} {rings[0][(j + 1) % n_lon]}")
+    for a, b in zip(rings[:-1], rings[1:]):
+        for j in range(n_lon):
+            lines.append(f"f {a[j]} {b[j]} {b[(j + 1) % n_lon]} {a[(j + 1) % n_lon]}")
+    for j in range(n_lon):
+        lines.append(f"f {south} {rings[-1][(j + 1) % n_lon]} {rings[-1][j]}")
+    return "\n".join(lines) + "\n"
+
+
+def _mixed_primitive(kind: str):
+    """(sdf, mesh spec, half height) of the config-C primitive families."""
+    from .scene import Union as _Union
+
+    if kind == "rounded_box":
+        ax = (0.3, 0.2, 0.15)
+        return Superquadric(0.2, 0.2, ax), MeshSpec(obj_text=sq_obj_text(0.2, 0.2, ax)), ax[2]
+    if kind == "cylinder":
+        ax = (0.15, 0.15, 0.25)
+        return Superquadric(0.1, 1.0, ax), MeshSpec(obj_text=sq_obj_text(0.1, 1.0, ax)), ax[2]
+    if kind == "ellipsoid":
+        ax = (0.3, 0.2, 0.15)
+        return Superquadric(1.0, 1.0, ax), MeshSpec(obj_text=sq_obj_text(1.0, 1.0, ax)), ax[2]
+    if kind == "capsule":
+        r, h = 0.1, 0.2
+        sdf = _Union([Superquadric(0.1, 1.0, (r, r, h)),
+                      Superquadric(1.0, 1.0, (r, r, r), (0, 0, h, 0, 0, 0)),
+                      Superquadric(1.0, 1.0, (r, r, r), (0, 0, -h, 0, 0, 0))], 0.01)
+        return sdf, MeshSpec(obj_text=capsule_obj_text(r, h)), h + r
+    raise ValueError(f"unknown mixed primitive {kind!r}")
+
+
+def mixed_bucket(kind: str, n_env: int = 65536) -> Workload:
+    """One bucket of config C: a primitive-family body (body 2, jittered) resting
+    on a convex mesh plate make_box_mesh({0.4,0.4,0.1}, 2) + box_planes
+    (body 1, fixed); budgets vertex_topk 16/16, edge_topk 8/8 -> 160 contacts
+    (builder-pinned parameters)."""
+    sdf, mesh, hz = _mixed_primitive(kind)
+    plate = BodySpec("plate", MeshSpec(box_half=(0.4, 0.4, 0.1), subdivisions=2),
+                     box_planes((0.4, 0.4, 0.1)), [0.0, 0.0, 0.0, 0.0, 0.0, 0.0], 16, 8, is_static=True)
+    prim = BodySpec(kind, mesh, sdf, [0.02, -0.03, 0.1 + hz - 0.01, 0.15, -0.1, 0.3], 16, 8)
+    return Workload(f"mixed-{kind}", [plate, prim], n_env,
+                    notes=f"{kind} vs convex mesh plate, soft top-K 16/16 vertices, 8/8 edges")
+
+
+MIXED_KINDS = ("rounded_box", "cylinder", "ellipsoid", "capsule")
+
 WORKLOADS = {
     "box-box": box_box,
     "box-on-plane": box_on_plane,

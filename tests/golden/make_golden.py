@@ -1,0 +1,125 @@
+"""Generate the committed golden fixtures from the COMPILED REFERENCE.
+
+Runs only where /root/reference exists (this container): builds
+oracle/_ref/libcmgref.so from the unmodified reference sources
+(oracle/Makefile) and records its outputs on the shared cases of
+tests/cases.py. The fixtures (*.npz next to this script) are what the CPU and
+GPU tests compare against; nothing at test time reads /root/reference.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import oracle  # noqa: E402
+from oracle import Ref  # noqa: E402
+from paper_2602_20304_b200.scene import SmoothingConfig  # noqa: E402
+from paper_2602_20304_b200 import workloads as W  # noqa: E402
+import cases  # noqa: E402
+
+
+def ref_mesh(b):
+    m = b.mesh
+    return Ref.Mesh.box(m.box_half, m.subdivisions, m.quad_edges) if m.box_half is not None \
+        else Ref.Mesh.parse_obj(m.obj_text)
+
+
+def cfg_vec(c: SmoothingConfig):
+    cc = c.to_c()
+    return np.array([getattr(cc, f) for f, _ in cc._fields_], dtype=np.float64)
+
+
+def main():
+    oracle.build(ref=True)
+    out = {}
+
+    # --- witness batches: make_random_ee_pairs(2000, seed 0) ---------------
+    pairs = Ref.random_pairs(2000, 0)
+    out["witness"] = dict(pairs=pairs)
+    for var in ("ours", "ours_ns"):
+        c = SmoothingConfig().for_variant(var)
+        out["witness"][f"ee_{var}"] = Ref.ee_witness_full(pairs, c)
+        out["witness"][f"vf_{var}"] = Ref.vf_batch(pairs, c)[0]
+        out["witness"][f"ee_checksum_{var}"] = np.array(Ref.ee_batch(pairs, c)[1])
+    # --- raw box QPs -----------------------------------------------------------
+    rng = np.random.default_rng(7)
+    A = rng.normal(size=(500, 2, 2))
+    Q = A @ np.transpose(A, (0, 2, 1)) + 1e-3 * np.eye(2)
+    cvec = rng.normal(size=(500, 2))
+    qp = np.stack([Q[:, 0, 0], Q[:, 0, 1], Q[:, 1, 1], cvec[:, 0], cvec[:, 1]], axis=1)
+    out["box_qp"] = dict(qp=qp, ours=Ref.box_qp(qp, SmoothingConfig()),
+                         ours_ns=Ref.box_qp(qp, SmoothingConfig().for_variant("ours_ns")))
+
+    # --- SDF field queries -----------------------------------------------------
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(-0.8, 0.8, size=(300, 3))
+    sdf = {"points": pts}
+    box = Ref.Mesh.box((0.5, 0.5, 0.5))
+    for name, prog in cases.SDF_PROGRAMS.items():
+        s = Ref.Surface(box, prog, 0, 0)
+        for fl in (0, 1, 2):
+            sdf[f"{name}_f{fl}"] = s.sdf_query(fl, pts)
+        sdf[f"{name}_trace5"] = s.sphere_trace([0.1, -0.2, 0.3, 0.2, 0.1, -0.3], pts[:50], 5)
+    out["sdf"] = sdf
+
+    # --- soft top-K ------------------------------------------------------------
+    xs = rng.normal(size=(20, 12))
+    xs[3, 5] = xs[3, 7]  # an exact tie
+    tk = {"xs": xs}
+    for i, x in enumerate(xs):
+        tk[f"w{i}"] = Ref.soft_topk(x, 4, 0.1)
+    out["soft_topk"] = tk
+
+    # --- meshes ------------------------------------------------------------------
+    me = {}
+    for i, (half, sub, quad) in enumerate(cases.BOX_MESHES):
+        m = Ref.Mesh.box(half, sub, quad)
+        me[f"box{i}_v"], me[f"box{i}_f"], me[f"box{i}_e"] = m.vertices, m.faces, m.edges
+    for name, txt in cases.OBJ_TEXTS.items():
+        m = Ref.Mesh.parse_obj(txt)
+        me[f"obj_{name}_v"], me[f"obj_{name}_f"], me[f"obj_{name}_e"] = m.vertices, m.faces, m.edges
+        me[f"obj_{name}_w"] = np.array(m.warnings, dtype=object).astype(str)
+    for name, txt in cases.OBJ_ERRORS.items():
+        try:
+            Ref.Mesh.parse_obj(txt)
+            me[f"err_{name}"] = np.array("no error")
+        except ValueError as e:
+            me[f"err_{name}"] = np.array(str(e))
+    out["meshes"] = me
+
+    # --- manifolds ----------------------------------------------------------------
+    for name, ws, c, n in cases.manifold_cases():
+        ms = [ref_mesh(b) for b in ws.bodies[:2]]
+        rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, ws.bodies[:2])]
+        p1, p2 = ws.poses(n)
+        r = Ref.manifold_batch(rs[0], rs[1], p1, p2, c, 1)
+        one = Ref.manifold(rs[0], rs[1], p1[0], p2[0], c)
+        out[f"manifold_{name}"] = dict(poses1=p1, poses2=p2, contacts=r["contacts"], meta=r["meta"],
+                                       mean_dist=r["mean_dist"], layout=r["layout"], ee0=one["ee"],
+                                       cfg=cfg_vec(c), warnings=np.array(rs[0].warnings + ["|"] + rs[1].warnings))
+
+    # --- forward-mode pose Jacobian (Dual12) on box-on-plane, one env ---------------
+    ws = W.box_on_plane()
+    ms = [ref_mesh(b) for b in ws.bodies]
+    rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, ws.bodies)]
+    j = Ref.manifold_jvp(rs[0], rs[1], ws.bodies[0].pose, ws.bodies[1].pose, SmoothingConfig())
+    out["jvp_box_on_plane"] = dict(contacts=j["contacts"], tangents=j["tangents"],
+                                   mean_dist=np.array(j["mean_dist"]), mean_dist_grad=j["mean_dist_grad"])
+
+    for name, d in out.items():
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **d)
+        print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+if __name__ == "__main__":
+    main()
