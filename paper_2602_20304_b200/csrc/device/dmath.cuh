@@ -6,7 +6,7 @@
 // the E-E separation vector) is FP64 on the B200's half-rate DFMA pipe; the
 // bounded transcendental corrections (sigmoid / softplus / softmin weights,
 // expm1 / log1p of small arguments) run in FP32 on the SFU (MUFU.EX2/LG2/RSQ/
-// RCP), and FP64 reciprocals are SFU seeds refined by one Newton step.
+// RCP).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -35,18 +35,11 @@ __device__ __forceinline__ float rsqf(float x) {
   return r;
 }
 
-// FP64 reciprocal square root / reciprocal: SFU seed + one Newton step
-// (relative error ~1e-14, a handful of DFMAs instead of the libdevice paths).
-__device__ __forceinline__ double rsqrt_d(double x) {
-  double y = (double)rsqf((float)x);
-  y = y * fma(-0.5 * x, y * y, 1.5);
-  return y;
-}
-__device__ __forceinline__ double rcp_d(double x) {
-  double y = (double)rcpf((float)x);
-  y = y * fma(-x, y, 2.0);
-  return y;
-}
+// FP64 reciprocal square root / reciprocal over the full double range
+// (MUFU.RSQ64H / RCP64H seeds + Newton in libdevice; an FP32 seed would
+// overflow for |grad f|^2 > 3.4e38, reached by sharp superquadrics far away).
+__device__ __forceinline__ double rsqrt_d(double x) { return rsqrt(x); }
+__device__ __forceinline__ double rcp_d(double x) { return __drcp_rn(x); }
 
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
 // function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each
