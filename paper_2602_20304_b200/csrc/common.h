@@ -15,7 +15,7 @@ namespace cmgb {
 
 constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param block
 constexpr int kMaxStack = 8;    // generic interpreter stack depth
-constexpr int kPairRec = 24;    // floats per E-E pair record in shared memory (96 B)
+constexpr int kPairRec = 36;    // floats per E-E pair record in shared memory (144 B)
 
 enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2 };
 enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
@@ -32,7 +32,7 @@ struct DevSq {
   double p4;             // -e1/2
   int32_t n1, n2, n3;    // integer exponents (1..64) or 0
   int32_t has_frame;     // primitive pose != identity
-  int32_t pad;
+  int32_t n4;            // -1/p4 = 2/e1 when an exact integer (1..64): f^p4 = 1 / f^(1/n4)
 };
 
 struct DevNode {
@@ -74,7 +74,10 @@ struct DevCfg {
   double inv_tau_sign, inv_tau_pen, inv_tau_nn, inv_tau_clash, inv_tau_cont;
   double inv_tau_topk_v, inv_tau_topk_e;
   double tau_normal;
+  double clip_C, comp_C;  // exp(-1/tau_clip), exp(-1/tau_comp): one exp per softplus / sigmoid pair
+  int32_t pair_exp;       // 1 when both C are normal doubles (1/tau < 700)
   int32_t hard_ops, trace_iters, containment, mode;
+  int32_t pad;
 };
 
 // Per-env shared-memory carve-up (bytes from the env's base), host-computed.

@@ -57,12 +57,39 @@ __device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp
   }
 }
 
-// 1 - f^p4 = -expm1(p4 ln f) for f > 0: cancellation-free near the surface
-// (f -> 1), with ln f = log1p(f - 1) there (f - 1 is exact in FP64).
-__device__ __forceinline__ double one_minus_pow(double f, double p4) {
+// 1 - f^p4 for f > 0, p4 < 0, cancellation-free near the surface (f -> 1).
+// When n = -1/p4 is an exact integer (eps1 = 0.1 -> 20, 0.2 -> 10, 1 -> 2),
+// f^p4 = 1/r with r = f^(1/n): an FP32 SFU seed refined by one FP64 Newton
+// step on r^n = f (relative error ~ (n-1)/2 * (3e-7)^2), then
+//   1 - f^p4 = (r - 1) / r        (r - 1 exact in FP64).
+// Otherwise -expm1(p4 ln f) with ln f = log1p(f - 1) near the surface.
+// Also returns 1/r (= f^p4) for the gradient.
+__device__ __forceinline__ double one_minus_pow(double f, double p4, int n, double* F) {
+  if (n > 0) {
+    // seed: r0 = 2^(log2(f) / n), log2 split into exponent + mantissa (any f > 0)
+    int e;
+    const double m = frexp(f, &e);
+    const float l = (float)e + lg2f((float)m);
+    const float q = floorf(l / (float)n);
+    const double r0 = ldexp((double)ex2f(l / (float)n - q), (int)q);
+    double rn = 1.0, b = r0;  // r0^n by binary powering (warp-uniform n)
+    int k = n;
+#pragma unroll 1
+    while (k) {
+      if (k & 1) rn *= b;
+      b *= b;
+      k >>= 1;
+    }
+    const double r = r0 * (1.0 - (rn - f) / (rn * (double)n));
+    const double inv_r = 1.0 / r;
+    *F = inv_r;
+    return (r - 1.0) * inv_r;
+  }
   const double d = f - 1.0;
   const double lnf = fabs(d) < 0.5 ? log1p(d) : log(f);
-  return -expm1(p4 * lnf);
+  const double em1 = expm1(p4 * lnf);
+  *F = 1.0 + em1;
+  return -em1;
 }
 
 // Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64).
@@ -83,7 +110,8 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   out.g = d3(0, 0, 0);
   if (FL == kValue) {
     const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
-    out.v = one_minus_pow(f, q.p4) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
+    double F;
+    out.v = one_minus_pow(f, q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
     return out;
   }
   // grad f through the normalisation: d(x2^p1)/dx = p1 x2^(p1-1) 2 xn / ax.
@@ -96,12 +124,13 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   }
   const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
   const double rinv = rsqrt_d(r2);
-  const double omF = one_minus_pow(f, q.p4);
+  double F;
+  const double omF = one_minus_pow(f, q.p4, q.n4, &F);
   const double phi = omF * rinv;
   out.v = phi;
   if (FL == kGrad) {
     // grad phi = (-p4 (F/f) grad f - phi (x~ / axes) / r) / r, F = 1 - omF
-    const double k = -q.p4 * (1.0 - omF) * rcp_d(f);
+    const double k = -q.p4 * F / f;
     const double h = phi * rinv;
     double3 gl = d3((k * df.x - h * xn * q.inv_ax[0]) * rinv, (k * df.y - h * yn * q.inv_ax[1]) * rinv,
                     (k * df.z - h * zn * q.inv_ax[2]) * rinv);

@@ -13,26 +13,40 @@
 
 namespace cmgb {
 
+// exp(-|x - 1| / tau) from a = exp(-|x| / tau) and C = exp(-1 / tau):
+// |x| and |x - 1| differ by exactly 1, so b = a C (x < 0), C / a (0 <= x <= 1),
+// a / C (x > 1) -- one SFU-free exponential per softplus / sigmoid pair.
+__device__ __forceinline__ double partner_exp(double x, double a, double C, double inv_tau, int pair) {
+  if (!pair) return exp(-fabs(x - 1.0) * inv_tau);
+  return x < 0.0 ? a * C : (x <= 1.0 ? C / a : a / C);
+}
+
 // clip01 (witness.hpp:45-52): clip_s(x, 0, 1, tau) = softplus(x) - softplus(x - 1)
-// (smooth_ops.hpp:85-89); hard: clamp.
+// (smooth_ops.hpp:66-89) = [max(x,0) - max(x-1,0)] + tau log1p((a - b) / (1 + b)),
+// a = exp(-|x|/tau), b = exp(-|x-1|/tau); hard: clamp.
 __device__ __forceinline__ double clip01(double x, const DevCfg& c) {
   if (c.hard_ops) return fmin(fmax(x, 0.0), 1.0);
-  return softplus_d(x, c.tau_clip, c.inv_tau_clip) - softplus_d(x - 1.0, c.tau_clip, c.inv_tau_clip);
+  const double a = exp(-fabs(x) * c.inv_tau_clip);
+  const double b = partner_exp(x, a, c.clip_C, c.inv_tau_clip, c.pair_exp);
+  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log1p((a - b) / (1.0 + b));
 }
 
 // within01 (witness.hpp:54-61): gamma = sigma(x/tau) sigma((1-x)/tau) and its
 // complement 1 - gamma = (1 - s1) + s1 (1 - s2), both relatively accurate;
 // hard mode: [0 <= x <= 1] exactly (within_hard, smooth_ops.hpp:204-206).
-__device__ __forceinline__ void within01(double x, double inv_tau, int hard, double* g, double* omg) {
+__device__ __forceinline__ void within01(double x, double inv_tau, double C, int pair, int hard,
+                                         double* g, double* omg) {
   if (hard) {
     const bool in = x >= 0.0 && x <= 1.0;
     *g = in ? 1.0 : 0.0;
     *omg = in ? 0.0 : 1.0;
     return;
   }
-  double s1, c1, s2, c2;
-  sigmoid_pair_d(x * inv_tau, &s1, &c1);
-  sigmoid_pair_d((1.0 - x) * inv_tau, &s2, &c2);
+  const double e1 = exp(-fabs(x) * inv_tau);              // sigma(x/tau) pair
+  const double e2 = partner_exp(x, e1, C, inv_tau, pair);  // sigma((1-x)/tau) pair
+  const double i1 = 1.0 / (1.0 + e1), i2 = 1.0 / (1.0 + e2);
+  const double s1 = x >= 0.0 ? i1 : e1 * i1, c1 = x >= 0.0 ? e1 * i1 : i1;
+  const double s2 = x <= 1.0 ? i2 : e2 * i2, c2 = x <= 1.0 ? e2 * i2 : i2;
   *g = s1 * s2;
   *omg = c1 + s1 * c2;
 }
@@ -65,7 +79,7 @@ __device__ __forceinline__ int pick_min(const double (&cost)[N], double (&w)[N],
   double total = 0.0;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    w[i] = exp((m - cost[i]) * inv_tau);
+    w[i] = i == best ? 1.0 : exp((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
     total += w[i];
   }
   const double inv = 1.0 / total;
@@ -103,8 +117,8 @@ __device__ __forceinline__ QpSol solve_box_qp_2(double q1, double q2, double q3,
   const double k0 = w[0] + w[2] * a2_1_a1 + w[3] * a2_0_a1;
   const double k1 = w[0] * a1_1_a2 + w[1] * a1_0_a2 + w[2];
   double g1, o1, g2, o2, in, out;
-  within01(a1u, c.inv_tau_comp, c.hard_ops, &g1, &o1);
-  within01(a2u, c.inv_tau_comp, c.hard_ops, &g2, &o2);
+  within01(a1u, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &g1, &o1);
+  within01(a2u, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &g2, &o2);
   within_and(g1, o1, g2, o2, &in, &out);
   QpSol s;
   s.a1 = a1u * in + k0 * out;
@@ -165,9 +179,9 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   const double bu = ddot(cross(dvp0, d20), n) / n_norm;
   const double bw = 1.0 - bu - bv;
   double gu, ou, gv, ov, gw, ow, guv, ouv, in, out;
-  within01(bu, c.inv_tau_comp, c.hard_ops, &gu, &ou);
-  within01(bv, c.inv_tau_comp, c.hard_ops, &gv, &ov);
-  within01(bw, c.inv_tau_comp, c.hard_ops, &gw, &ow);
+  within01(bu, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gu, &ou);
+  within01(bv, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gv, &ov);
+  within01(bw, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gw, &ow);
   within_and(gu, ou, gv, ov, &guv, &ouv);
   within_and(guv, ouv, gw, ow, &in, &out);
   if (label) *label = best | ((in >= 0.5) << 2);

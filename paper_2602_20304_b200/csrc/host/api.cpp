@@ -87,6 +87,9 @@ DevCfg device_config(const cmgb_config* c) {
   d.inv_tau_topk_v = 1.0 / c->tau_topk_verts;
   d.inv_tau_topk_e = 1.0 / c->tau_topk_edges;
   d.tau_normal = c->tau_normal;
+  d.clip_C = std::exp(-1.0 / c->tau_clip);
+  d.comp_C = std::exp(-1.0 / c->tau_comp);
+  d.pair_exp = (1.0 / c->tau_clip < 700.0 && 1.0 / c->tau_comp < 700.0) ? 1 : 0;
   d.hard_ops = c->hard_ops ? 1 : 0;
   d.trace_iters = (c->sphere_trace && c->sphere_trace_iters > 0) ? c->sphere_trace_iters : 0;
   d.containment = c->containment_safeguard ? 1 : 0;
@@ -204,16 +207,16 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
   S.bytes = off;
 
-  // Envs per block: ~288 threads of E-E work per CTA (2 box-box envs = 9 warps).
+  // Envs per block: ~288 items of E-E work per 288-thread CTA (2 box-box envs),
+  // shared memory capped so 3 CTAs fit per SM.
+  const int maxt = manifold_max_threads();
   const int per_env = std::max({P, nslot_v, 1});
-  int epb = std::max(1, 288 / per_env);
-  const size_t smem_cap = 96 * 1024;
+  int epb = std::max(1, maxt / per_env);
+  const size_t smem_cap = 72 * 1024;
   while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
   if ((size_t)S.bytes > 200 * 1024)
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
-  const int maxt = manifold_max_threads();
-  int threads = ((epb * per_env + 31) / 32) * 32;
-  threads = std::min(std::max(threads, 32), maxt);
+  const int threads = maxt;
   p.envs_per_block = epb;
   plan.threads = threads;
   plan.grid = static_cast<int>((n_env + epb - 1) / epb);

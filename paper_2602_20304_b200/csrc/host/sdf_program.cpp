@@ -228,6 +228,7 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       q.n1 = exact_int(p1);
       q.n2 = exact_int(p2);
       q.n3 = exact_int(p3);
+      q.n4 = exact_int(-1.0 / p4);
       bool ident = true;
       for (int k = 0; k < 6; ++k) ident = ident && d.pose[k] == 0.0;
       q.has_frame = ident ? 0 : 1;

@@ -28,13 +28,17 @@ namespace cmgb {
 
 namespace {
 
-constexpr int kMaxThreads = 512;
+// 9 warps per CTA (2 box-box envs x 144 E-E pairs); 3 CTAs per SM (<= 75 regs).
+constexpr int kMaxThreads = 288;
+constexpr int kMinBlocks = 3;
 
-// Pair record layout (floats; kPairRec = 24):
-//   0-2 p1 world, 3-5 p2 world, 6 dist1, 7 dist2, 8-10 normal1, 11-13 normal2,
-//   14 pen1, 15 pen2, 16 con, 17 clash, 18 cont, 20-21 dbar (FP64)
-constexpr int kRecDbar = 20;
-
+// Pair record (doubles; kPairRec = 36 floats = 18 doubles = 144 B), rewritten
+// in place by the E-E sub-phases:
+//   side s at 8 s: [0-2] witness point (body frame -> traced -> world),
+//                  [3-5] own normal (world), [6] phi_other(p), [7] phi_own(p)
+//   [16] con (gamma of the QP)
+// after E3: [3] dbar, [4] sign1, [5] sign2, [11-13] nbar, [6] pen1, [14] pen2,
+//           [7] cont, [15] clash, [0-2] / [8-10] world witness points
 struct EnvView {
   unsigned char* base;
   const SmemLayout* L;
@@ -45,10 +49,12 @@ struct EnvView {
   __device__ int* prov() const { return reinterpret_cast<int*>(base + L->prov); }
   __device__ double* scores() const { return reinterpret_cast<double*>(base + L->scores); }
   __device__ double* sorted() const { return reinterpret_cast<double*>(base + L->sorted); }
-  __device__ float* pair(int i) const { return reinterpret_cast<float*>(base + L->pairs) + kPairRec * i; }
+  __device__ double* pair(int i) const {
+    return reinterpret_cast<double*>(base + L->pairs) + (kPairRec / 2) * i;
+  }
   __device__ float* vsdist() const { return reinterpret_cast<float*>(base + L->vsdist); }
   __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
-  __device__ double& dbar(int i) const { return *reinterpret_cast<double*>(pair(i) + kRecDbar); }
+  __device__ double& dbar(int i) const { return pair(i)[3]; }
 };
 
 __device__ __forceinline__ double3 ld_vert(const double* v, int i) {
@@ -110,74 +116,90 @@ __device__ __forceinline__ double3 trace(const DevSdf& sdf, double3 p, const Dev
   return p;
 }
 
-// E-E pair stage (ee_contacts loop body, manifold.hpp:237-287). Writes the
-// pair record consumed by the NN / activity phases.
-template <int K1, int K2>
-__device__ __forceinline__ void ee_pair(const ManifoldParams& p, const EnvView& ev, int k, int l,
-                                        float* rec) {
-  const DevCfg& c = p.cfg;
+// E1: witness QP of pair (k, l) (ee_witness, witness.hpp:137-158; edges in the
+// world frame), witness points written in their own body frames.
+__device__ __forceinline__ void ee_stage_qp(const ManifoldParams& p, const EnvView& ev, int k, int l,
+                                            double* rec) {
   const double* s1 = ev.eslot(k);
   const double* s2 = ev.eslot(p.m1 + l);
   const QpSol w = ee_qp(d3(s1[0], s1[1], s1[2]), d3(s1[3], s1[4], s1[5]), d3(s2[0], s2[1], s2[2]),
-                        d3(s2[3], s2[4], s2[5]), c);
-  // Witness points in their own body frames (edge_point, witness.hpp:130-133).
-  const double3 a1b = d3(s1[6], s1[7], s1[8]), b1b = d3(s1[9], s1[10], s1[11]);
-  const double3 a2b = d3(s2[6], s2[7], s2[8]), b2b = d3(s2[9], s2[10], s2[11]);
-  double3 p1b = a1b + (b1b - a1b) * w.a1;
-  double3 p2b = a2b + (b2b - a2b) * w.a2;
-  if (c.trace_iters > 0) {
-    p1b = trace<K1>(p.side[0].sdf, p1b, c);
-    p2b = trace<K2>(p.side[1].sdf, p2b, c);
-  }
-  const double* R1 = ev.R(0);
-  const double* t1 = ev.t(0);
-  const double* R2 = ev.R(1);
-  const double* t2 = ev.t(1);
-  const double3 p1w = to_world(R1, t1, p1b);
-  const double3 p2w = to_world(R2, t2, p2b);
+                        d3(s2[3], s2[4], s2[5]), p.cfg);
+  // edge_point (witness.hpp:130-133) on the body-frame endpoints
+  rec[0] = s1[6] + (s1[9] - s1[6]) * w.a1;
+  rec[1] = s1[7] + (s1[10] - s1[7]) * w.a1;
+  rec[2] = s1[8] + (s1[11] - s1[8]) * w.a1;
+  rec[8] = s2[6] + (s2[9] - s2[6]) * w.a2;
+  rec[9] = s2[7] + (s2[10] - s2[7]) * w.a2;
+  rec[10] = s2[8] + (s2[11] - s2[8]) * w.a2;
+  rec[16] = w.gamma;
+}
+
+// E2: one side of a pair: sphere-trace the witness on its own surface
+// (manifold.hpp:245-247), own normal source (253-256), world point, and the
+// opposing surface's value for the penetration indicator (279-280).
+template <int KS, int KO>
+__device__ __forceinline__ void ee_stage_side(const ManifoldParams& p, const EnvView& ev, int s,
+                                              double* r) {
+  const DevCfg& c = p.cfg;
+  const DevSdf& own = p.side[s].sdf;
+  const DevSdf& oth = p.side[1 - s].sdf;
+  double3 pb = d3(r[0], r[1], r[2]);
+  if (c.trace_iters > 0) pb = trace<KS>(own, pb, c);
+  const SdfOut o = c.containment ? sdf_eval<kNormalSource, KS>(own, pb) : sdf_eval<kNormalOnly, KS>(own, pb);
+  const double* R = ev.R(s);
+  const double3 n = mul_R(R, normalize_smooth(o.g, c.tau_normal));
+  const double3 pw = to_world(R, ev.t(s), pb);
+  const double v_oth = sdf_eval<kValue, KO>(oth, to_body(ev.R(1 - s), ev.t(1 - s), pw)).v;
+  r[0] = pw.x; r[1] = pw.y; r[2] = pw.z;
+  r[3] = n.x; r[4] = n.y; r[5] = n.z;
+  r[6] = v_oth;
+  r[7] = o.v;
+}
+
+// sigma(x) in FP32 with the accurate expf (arguments are FP64-exact; the
+// indicators only scale the activity, tolerance 1e-5 relative).
+__device__ __forceinline__ float sigmoid_acc(double xd) {
+  const float x = (float)xd;
+  const float e = expf(-fabsf(x));
+  const float inv = 1.0f / (1.0f + e);
+  return x >= 0.0f ? inv : e * inv;
+}
+
+// E3: pair quantities (manifold.hpp:248-266, 279-285): separation, unsigned
+// normal, soft signs, penetration / clash / containment indicators.
+__device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
+  const double3 p1w = d3(r[0], r[1], r[2]), p2w = d3(r[8], r[9], r[10]);
+  const double3 n1 = d3(r[3], r[4], r[5]), n2 = d3(r[11], r[12], r[13]);
   const double3 de = p1w - p2w;
   const double dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
   const double3 nb = d3(de.x / dg, de.y / dg, de.z / dg);
-  SdfOut o1, o2;
-  if (c.containment) {
-    o1 = sdf_eval<kNormalSource, K1>(p.side[0].sdf, p1b);
-    o2 = sdf_eval<kNormalSource, K2>(p.side[1].sdf, p2b);
-  } else {
-    o1 = sdf_eval<kNormalOnly, K1>(p.side[0].sdf, p1b);
-    o2 = sdf_eval<kNormalOnly, K2>(p.side[1].sdf, p2b);
-  }
-  const double3 n1 = mul_R(R1, normalize_smooth(o1.g, c.tau_normal));
-  const double3 n2 = mul_R(R2, normalize_smooth(o2.g, c.tau_normal));
   const double d2 = ddot(n2, nb), d1 = ddot(n1, nb);
   double g1, g2;
   if (c.hard_ops) {  // sign_hard (smooth_ops.hpp:208)
     g1 = d2 < 0.0 ? -1.0 : (d2 > 0.0 ? 1.0 : 0.0);
     g2 = d1 < 0.0 ? -1.0 : (d1 > 0.0 ? 1.0 : 0.0);
-  } else {  // sign_s = tanh(x / tau_sign) (smooth_ops.hpp:57-62)
-    g1 = tanh(d2 * c.inv_tau_sign);
-    g2 = tanh(d1 * c.inv_tau_sign);
+  } else {  // sign_s = tanh(x / tau_sign) (smooth_ops.hpp:57-62), FP64-exact argument
+    g1 = (double)tanhf((float)(d2 * c.inv_tau_sign));
+    g2 = (double)tanhf((float)(d1 * c.inv_tau_sign));
   }
-  // Penetration of each witness point into the opposing surface.
-  const double v12 = sdf_eval<kValue, K2>(p.side[1].sdf, to_body(R2, t2, p1w)).v;
-  const double v21 = sdf_eval<kValue, K1>(p.side[0].sdf, to_body(R1, t1, p2w)).v;
-  rec[0] = (float)p1w.x; rec[1] = (float)p1w.y; rec[2] = (float)p1w.z;
-  rec[3] = (float)p2w.x; rec[4] = (float)p2w.y; rec[5] = (float)p2w.z;
-  // signed distances and normals (manifold.hpp:311-313, 321-323)
-  rec[6] = (float)(g1 * dg);
-  rec[7] = (float)(g2 * dg);
-  rec[8] = (float)(nb.x * g1); rec[9] = (float)(nb.y * g1); rec[10] = (float)(nb.z * g1);
-  rec[11] = (float)(nb.x * g2); rec[12] = (float)(nb.y * g2); rec[13] = (float)(nb.z * g2);
-  rec[14] = (float)sigmoid_d(-v12 * c.inv_tau_pen);              // pen1
-  rec[15] = (float)sigmoid_d(-v21 * c.inv_tau_pen);              // pen2
-  rec[16] = (float)w.gamma;                                      // con
-  rec[17] = (float)sigmoid_d(-ddot(n1, n2) * c.inv_tau_clash);   // clash
-  rec[18] = c.containment ? (float)(sigmoid_d(-o1.v * c.inv_tau_cont) * sigmoid_d(-o2.v * c.inv_tau_cont))
-                          : 1.0f;                                // containment safeguard
-  *reinterpret_cast<double*>(rec + kRecDbar) = dg;
+  const double pen1 = sigmoid_acc(-r[6] * c.inv_tau_pen);
+  const double pen2 = sigmoid_acc(-r[14] * c.inv_tau_pen);
+  const double clash = sigmoid_acc(-ddot(n1, n2) * c.inv_tau_clash);
+  const double cont = c.containment ? (double)sigmoid_acc(-r[7] * c.inv_tau_cont) *
+                                          (double)sigmoid_acc(-r[15] * c.inv_tau_cont)
+                                    : 1.0;
+  r[3] = dg;
+  r[4] = g1;
+  r[5] = g2;
+  r[11] = nb.x; r[12] = nb.y; r[13] = nb.z;
+  r[6] = pen1;
+  r[14] = pen2;
+  r[7] = cont;
+  r[15] = clash;
 }
 
 template <int K1, int K2>
-__global__ void __launch_bounds__(kMaxThreads, 1)
+__global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int epb = p.envs_per_block;
@@ -333,11 +355,33 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         sp[1] = -1;
       }
     }
-    if (full) {
-      for (int it = tid; it < n_here * P; it += nth) {
-        const int e = it / P, i = it % P;
-        ee_pair<K1, K2>(p, env(e), i / m2, i % m2, env(e).pair(i));
+  }
+  if (full) {
+    // E1: QP per pair
+    for (int it = tid; it < n_here * P; it += nth) {
+      const int e = it / P, i = it % P;
+      ee_stage_qp(p, env(e), i / m2, i % m2, env(e).pair(i));
+    }
+    __syncthreads();
+    // E2: per (pair, side): trace + own normal + opposing value. Items are
+    // side-major per env so warps stay on one surface.
+    const int n2p = 2 * P;
+    for (int it = tid; it < n_here * n2p; it += nth) {
+      const int e = it / n2p, j = it % n2p;
+      const int s = j >= P ? 1 : 0, i = j - s * P;
+      double* r = env(e).pair(i) + 8 * s;
+      if constexpr (K1 == K2) {
+        ee_stage_side<K1, K1>(p, env(e), s, r);
+      } else {
+        if (s == 0) ee_stage_side<K1, K2>(p, env(e), 0, r);
+        else ee_stage_side<K2, K1>(p, env(e), 1, r);
       }
+    }
+    __syncthreads();
+    // E3: pair quantities
+    for (int it = tid; it < n_here * P; it += nth) {
+      const int e = it / P, i = it % P;
+      ee_stage_pair(c, env(e).pair(i));
     }
   }
   __syncthreads();
@@ -358,7 +402,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       double tot = 0.0;
       for (int j = 0; j < n; ++j) {
         const int i = row ? r * m2 + j : j * m2 + (r - m1);
-        tot += exp((m - ev.dbar(i)) * c.inv_tau_nn);
+        tot += (double)expf((float)((m - ev.dbar(i)) * c.inv_tau_nn));
       }
       ev.nnstat()[2 * r] = m;
       ev.nnstat()[2 * r + 1] = 1.0 / tot;
@@ -369,18 +413,22 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const int e = it / P, i = it % P;
       const int k = i / m2, l = i % m2;
       const EnvView ev = env(e);
-      const float* rec = ev.pair(i);
+      const double* rec = ev.pair(i);
       const double* ns = ev.nnstat();
-      const double dg = ev.dbar(i);
-      const double nn1 = exp((ns[2 * k] - dg) * c.inv_tau_nn) * ns[2 * k + 1];
-      const double nn2 = exp((ns[2 * (m1 + l)] - dg) * c.inv_tau_nn) * ns[2 * (m1 + l) + 1];
-      const double pen1 = rec[14], pen2 = rec[15], con = rec[16], clash = rec[17], cont = rec[18];
+      const double dg = rec[3];
+      const double nn1 = (double)expf((float)((ns[2 * k] - dg) * c.inv_tau_nn)) * ns[2 * k + 1];
+      const double nn2 = (double)expf((float)((ns[2 * (m1 + l)] - dg) * c.inv_tau_nn)) * ns[2 * (m1 + l) + 1];
+      const double pen1 = rec[6], pen2 = rec[14], con = rec[16], clash = rec[15], cont = rec[7];
       const float act1 = (float)(con * pen1 * nn1 * clash * cont);
       const float act2 = (float)(con * pen2 * nn2 * clash * cont);
+      const double g1 = rec[4], g2 = rec[5];
       const int64_t row = (env0 + e) * C + n1 + n2 + 2 * i;
       float* dst = p.contacts + row * 8;
-      store_contact(dst, rec[0], rec[1], rec[2], rec[6], rec[8], rec[9], rec[10], act1);
-      store_contact(dst + 8, rec[3], rec[4], rec[5], rec[7], rec[11], rec[12], rec[13], act2);
+      // contacts (manifold.hpp:303-330): dist = sign * dbar, normal = sign * nbar
+      store_contact(dst, (float)rec[0], (float)rec[1], (float)rec[2], (float)(g1 * dg), (float)(rec[11] * g1),
+                    (float)(rec[12] * g1), (float)(rec[13] * g1), act1);
+      store_contact(dst + 8, (float)rec[8], (float)rec[9], (float)rec[10], (float)(g2 * dg),
+                    (float)(rec[11] * g2), (float)(rec[12] * g2), (float)(rec[13] * g2), act2);
       if (p.src) {
         int* sp = p.src + row * 2;
         const int sa = ev.prov()[n1 + n2 + k], sb = ev.prov()[n1 + n2 + m1 + l];
@@ -409,7 +457,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       double acc = 0.0;
       for (int r = lane; r < n1 + n2; r += 32) acc += (double)ev.vsdist()[r];
       if (full)
-        for (int i = lane; i < P; i += 32) acc += (double)ev.pair(i)[6] + (double)ev.pair(i)[7];
+        for (int i = lane; i < P; i += 32) {
+          const double* rec = ev.pair(i);
+          acc += (double)(float)(rec[4] * rec[3]) + (double)(float)(rec[5] * rec[3]);
+        }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) p.mean_dist[env0 + e] = (float)(acc / (double)C);
