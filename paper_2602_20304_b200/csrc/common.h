@@ -17,7 +17,9 @@ constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param bl
 constexpr int kMaxStack = 8;    // generic interpreter stack depth
 constexpr int kPairRec = 36;    // floats per E-E pair record in shared memory (144 B)
 
-enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2 };
+// kSqE01: a lone superquadric with eps1 = eps2 = 0.1 (the box-box benchmark
+// body), whose exponents (n1, n2, n3, n4) = (10, 1, 10, 20) are compiled in.
+enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2, kSqE01 = 3 };
 enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
 
 // Superquadric leaf, pre-digested on the host (sdf.hpp:85-108):
@@ -75,6 +77,7 @@ struct DevCfg {
   double inv_tau_topk_v, inv_tau_topk_e;
   double tau_normal;
   double clip_C, comp_C;  // exp(-1/tau_clip), exp(-1/tau_comp): one exp per softplus / sigmoid pair
+  double inv_clip_C, inv_comp_C;
   int32_t pair_exp;       // 1 when both C are normal doubles (1/tau < 700)
   int32_t hard_ops, trace_iters, containment, mode;
   int32_t pad;

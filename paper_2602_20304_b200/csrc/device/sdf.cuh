@@ -28,32 +28,62 @@ struct SdfOut {
   double3 g;
 };
 
+// x^n for a small positive integer n (warp-uniform), FP64 products.
+__device__ __forceinline__ double ipow_d(double x, int n) {
+  switch (n) {
+    case 1: return x;
+    case 2: return x * x;
+    case 4: { const double x2 = x * x; return x2 * x2; }
+    case 5: { const double x2 = x * x; return x2 * x2 * x; }
+    case 9: { const double x2 = x * x, x4 = x2 * x2; return x4 * x4 * x; }
+    case 10: { const double x2 = x * x, x4 = x2 * x2; return x4 * x4 * x2; }
+    case 19: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x2 * x; }
+    case 20: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x4; }
+    default: {
+      double r = 1.0, b = x;
+#pragma unroll 1
+      for (int e = n; e; e >>= 1) {
+        if (e & 1) r *= b;
+        b *= b;
+      }
+      return r;
+    }
+  }
+}
+
+// Compile-time integer power (N > 0) for specialised superquadric kinds.
+template <int N>
+__device__ __forceinline__ double cpow(double x) {
+  if constexpr (N == 1) return x;
+  else if constexpr (N % 2 == 0) { const double h = cpow<N / 2>(x); return h * h; }
+  else return cpow<N - 1>(x) * x;
+}
+
+// (x^p, x^(p-1)): compile-time exponent N > 0, or runtime (N == 0).
+template <int N>
+__device__ __forceinline__ void pow_pair_t(double x, int n, double p, double& xp, double& xpm1);
+
 // (x^p, x^(p-1)) in FP64: integer chains (no SFU) or libdevice pow.
 __device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp, double& xpm1) {
   if (n > 0) {
-    double r;
-    switch (n) {
-      case 1: r = 1.0; break;
-      case 2: r = x; break;
-      case 5: { const double x2 = x * x; r = x2 * x2; break; }
-      case 10: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4; r = x8 * x; break; }
-      default: {
-        double b = x;
-        r = 1.0;
-        int e = n - 1;
-#pragma unroll 1
-        while (e) {
-          if (e & 1) r *= b;
-          b *= b;
-          e >>= 1;
-        }
-      }
-    }
-    xpm1 = r;
-    xp = r * x;
+    xpm1 = n == 1 ? 1.0 : ipow_d(x, n - 1);
+    xp = xpm1 * x;
   } else {
     xp = pow(x, p);
-    xpm1 = xp / x;
+    xpm1 = div_d(xp, x);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void pow_pair_t(double x, int n, double p, double& xp, double& xpm1) {
+  if constexpr (N == 0) {
+    pow_pair_d(x, n, p, xp, xpm1);
+  } else if constexpr (N == 1) {
+    xpm1 = 1.0;
+    xp = x;
+  } else {
+    xpm1 = cpow<N - 1>(x);
+    xp = xpm1 * x;
   }
 }
 
@@ -64,24 +94,24 @@ __device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp
 //   1 - f^p4 = (r - 1) / r        (r - 1 exact in FP64).
 // Otherwise -expm1(p4 ln f) with ln f = log1p(f - 1) near the surface.
 // Also returns 1/r (= f^p4) for the gradient.
-__device__ __forceinline__ double one_minus_pow(double f, double p4, int n, double* F) {
+template <int N4 = 0>
+__device__ __forceinline__ double one_minus_pow(double f, double inv_f, double p4, int n_rt, double* F) {
+  const int n = N4 > 0 ? N4 : n_rt;
   if (n > 0) {
-    // seed: r0 = 2^(log2(f) / n), log2 split into exponent + mantissa (any f > 0)
-    int e;
-    const double m = frexp(f, &e);
-    const float l = (float)e + lg2f((float)m);
-    const float q = floorf(l / (float)n);
-    const double r0 = ldexp((double)ex2f(l / (float)n - q), (int)q);
-    double rn = 1.0, b = r0;  // r0^n by binary powering (warp-uniform n)
-    int k = n;
-#pragma unroll 1
-    while (k) {
-      if (k & 1) rn *= b;
-      b *= b;
-      k >>= 1;
-    }
-    const double r = r0 * (1.0 - (rn - f) / (rn * (double)n));
-    const double inv_r = 1.0 / r;
+    // seed r0 = 2^(log2(f) / n): log2 from the exponent bits + SFU lg2 of the
+    // mantissa in [1, 2); 2^q assembled from bits (normal f assumed)
+    const long long bits = __double_as_longlong(f);
+    const int ex = (int)((bits >> 52) & 0x7ff) - 1023;
+    const double mant = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+    const float l = ((float)ex + lg2f((float)mant)) / (float)n;
+    const float q = floorf(l);
+    const double r0 = (double)ex2f(l - q) * __longlong_as_double((long long)((int)q + 1023) << 52);
+    // one Newton step on r^n = f: r = r0 (1 - (r0^n - f) / (n r0^n)); the
+    // denominator r0^n -> f changes the step by O(n delta0) relative, i.e. the
+    // result by ~n delta0^2 ~ 1e-12 (same order as the quadratic term)
+    const double rn = N4 > 0 ? cpow<(N4 > 0 ? N4 : 1)>(r0) : ipow_d(r0, n);
+    const double r = r0 * (1.0 - (rn - f) * inv_f * (1.0 / (double)n));
+    const double inv_r = rcp_d(r);
     *F = inv_r;
     return (r - 1.0) * inv_r;
   }
@@ -92,18 +122,19 @@ __device__ __forceinline__ double one_minus_pow(double f, double p4, int n, doub
   return -em1;
 }
 
-// Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64).
-template <int FL>
+// Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64). N1..N4 > 0
+// compile in the exponents (kSqE01); 0 reads them from the descriptor.
+template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0>
 __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   if (q.has_frame) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));  // apply_inverse
   const double xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
   const double x2 = fma(xn, xn, 1e-30), y2 = fma(yn, yn, 1e-30), z2 = fma(zn, zn, 1e-30);
   double A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
-  pow_pair_d(x2, q.n1, q.p1, A, Am1);
-  pow_pair_d(y2, q.n1, q.p1, B, Bm1);
+  pow_pair_t<N1>(x2, q.n1, q.p1, A, Am1);
+  pow_pair_t<N1>(y2, q.n1, q.p1, B, Bm1);
   const double g = A + B;
-  pow_pair_d(g, q.n2, q.p2, G, Gm1);
-  pow_pair_d(z2, q.n3, q.p3, Cz, Czm1);
+  pow_pair_t<N2>(g, q.n2, q.p2, G, Gm1);
+  pow_pair_t<N3>(z2, q.n3, q.p3, Cz, Czm1);
   const double f = G + Cz;
   SdfOut out;
   out.v = 0.0;
@@ -111,7 +142,7 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   if (FL == kValue) {
     const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
     double F;
-    out.v = one_minus_pow(f, q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
+    out.v = one_minus_pow<N4>(f, rcp_d(f), q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
     return out;
   }
   // grad f through the normalisation: d(x2^p1)/dx = p1 x2^(p1-1) 2 xn / ax.
@@ -125,12 +156,13 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
   const double rinv = rsqrt_d(r2);
   double F;
-  const double omF = one_minus_pow(f, q.p4, q.n4, &F);
+  const double inv_f = rcp_d(f);
+  const double omF = one_minus_pow<N4>(f, inv_f, q.p4, q.n4, &F);
   const double phi = omF * rinv;
   out.v = phi;
   if (FL == kGrad) {
     // grad phi = (-p4 (F/f) grad f - phi (x~ / axes) / r) / r, F = 1 - omF
-    const double k = -q.p4 * F / f;
+    const double k = -q.p4 * F * inv_f;
     const double h = phi * rinv;
     double3 gl = d3((k * df.x - h * xn * q.inv_ax[0]) * rinv, (k * df.y - h * yn * q.inv_ax[1]) * rinv,
                     (k * df.z - h * zn * q.inv_ax[2]) * rinv);
@@ -192,7 +224,7 @@ __device__ __forceinline__ SdfOut opc_leaf(const DevNode& nd, const double4* poo
     }
   }
   SdfOut out;
-  const double inv = 1.0 / den;
+  const double inv = rcp_d(den);
   out.v = num * inv;
   out.g = d3(0, 0, 0);
   if (FL != kValue)
@@ -214,6 +246,7 @@ __device__ __forceinline__ SdfOut leaf_eval(const DevNode& nd, const double4* po
 template <int FL_IN, int KIND>
 __device__ SdfOut sdf_eval(const DevSdf& s, double3 p) {
   if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN>(s.nodes[0].sq, p);
+  if constexpr (KIND == kSqE01) return sq_leaf<FL_IN, 10, 1, 10, 20>(s.nodes[0].sq, p);
   // kNormalOnly skips phi only for a lone SQ leaf; compositions need the values.
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;

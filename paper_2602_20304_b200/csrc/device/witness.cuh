@@ -16,9 +16,10 @@ namespace cmgb {
 // exp(-|x - 1| / tau) from a = exp(-|x| / tau) and C = exp(-1 / tau):
 // |x| and |x - 1| differ by exactly 1, so b = a C (x < 0), C / a (0 <= x <= 1),
 // a / C (x > 1) -- one SFU-free exponential per softplus / sigmoid pair.
-__device__ __forceinline__ double partner_exp(double x, double a, double C, double inv_tau, int pair) {
+__device__ __forceinline__ double partner_exp(double x, double a, double C, double inv_C,
+                                              double inv_tau, int pair) {
   if (!pair) return exp(-fabs(x - 1.0) * inv_tau);
-  return x < 0.0 ? a * C : (x <= 1.0 ? C / a : a / C);
+  return x < 0.0 ? a * C : (x <= 1.0 ? C * rcp_d(a) : a * inv_C);
 }
 
 // clip01 (witness.hpp:45-52): clip_s(x, 0, 1, tau) = softplus(x) - softplus(x - 1)
@@ -27,15 +28,15 @@ __device__ __forceinline__ double partner_exp(double x, double a, double C, doub
 __device__ __forceinline__ double clip01(double x, const DevCfg& c) {
   if (c.hard_ops) return fmin(fmax(x, 0.0), 1.0);
   const double a = exp(-fabs(x) * c.inv_tau_clip);
-  const double b = partner_exp(x, a, c.clip_C, c.inv_tau_clip, c.pair_exp);
-  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log1p((a - b) / (1.0 + b));
+  const double b = partner_exp(x, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
+  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log1p((a - b) * rcp_d(1.0 + b));
 }
 
 // within01 (witness.hpp:54-61): gamma = sigma(x/tau) sigma((1-x)/tau) and its
 // complement 1 - gamma = (1 - s1) + s1 (1 - s2), both relatively accurate;
 // hard mode: [0 <= x <= 1] exactly (within_hard, smooth_ops.hpp:204-206).
-__device__ __forceinline__ void within01(double x, double inv_tau, double C, int pair, int hard,
-                                         double* g, double* omg) {
+__device__ __forceinline__ void within01(double x, double inv_tau, double C, double inv_C, int pair,
+                                         int hard, double* g, double* omg) {
   if (hard) {
     const bool in = x >= 0.0 && x <= 1.0;
     *g = in ? 1.0 : 0.0;
@@ -43,8 +44,8 @@ __device__ __forceinline__ void within01(double x, double inv_tau, double C, int
     return;
   }
   const double e1 = exp(-fabs(x) * inv_tau);              // sigma(x/tau) pair
-  const double e2 = partner_exp(x, e1, C, inv_tau, pair);  // sigma((1-x)/tau) pair
-  const double i1 = 1.0 / (1.0 + e1), i2 = 1.0 / (1.0 + e2);
+  const double e2 = partner_exp(x, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
+  const double i1 = rcp_d(1.0 + e1), i2 = rcp_d(1.0 + e2);
   const double s1 = x >= 0.0 ? i1 : e1 * i1, c1 = x >= 0.0 ? e1 * i1 : i1;
   const double s2 = x <= 1.0 ? i2 : e2 * i2, c2 = x <= 1.0 ? e2 * i2 : i2;
   *g = s1 * s2;
@@ -82,7 +83,7 @@ __device__ __forceinline__ int pick_min(const double (&cost)[N], double (&w)[N],
     w[i] = i == best ? 1.0 : exp((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
     total += w[i];
   }
-  const double inv = 1.0 / total;
+  const double inv = rcp_d(total);
 #pragma unroll
   for (int i = 0; i < N; ++i) w[i] *= inv;
   return best;
@@ -97,10 +98,11 @@ struct QpSol {
 // solve_box_qp_2 (witness.hpp:74-121), erratum-fixed cost 4 (witness.hpp:99).
 __device__ __forceinline__ QpSol solve_box_qp_2(double q1, double q2, double q3, double c1,
                                                 double c2, const DevCfg& c) {
-  const double q2_over_q1 = q2 / q1, q2_over_q3 = q2 / q3;
-  const double c1_over_q1 = c1 / q1, c2_over_q3 = c2 / q3;
-  const double a1u = (q2 * c2_over_q3 - c1) / (q1 - q2 * q2_over_q3);
-  const double a2u = (q2 * c1_over_q1 - c2) / (q3 - q2 * q2_over_q1);
+  const double i1 = rcp_d(q1), i3 = rcp_d(q3);
+  const double q2_over_q1 = q2 * i1, q2_over_q3 = q2 * i3;
+  const double c1_over_q1 = c1 * i1, c2_over_q3 = c2 * i3;
+  const double a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
+  const double a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
   const double a1_1_a2 = clip01(-(q2_over_q3 + c2_over_q3), c);
   const double a1_0_a2 = clip01(-c2_over_q3, c);
   const double a2_1_a1 = clip01(-(q2_over_q1 + c1_over_q1), c);
@@ -117,8 +119,8 @@ __device__ __forceinline__ QpSol solve_box_qp_2(double q1, double q2, double q3,
   const double k0 = w[0] + w[2] * a2_1_a1 + w[3] * a2_0_a1;
   const double k1 = w[0] * a1_1_a2 + w[1] * a1_0_a2 + w[2];
   double g1, o1, g2, o2, in, out;
-  within01(a1u, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &g1, &o1);
-  within01(a2u, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &g2, &o2);
+  within01(a1u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g1, &o1);
+  within01(a2u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g2, &o2);
   within_and(g1, o1, g2, o2, &in, &out);
   QpSol s;
   s.a1 = a1u * in + k0 * out;
@@ -179,9 +181,9 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   const double bu = ddot(cross(dvp0, d20), n) / n_norm;
   const double bw = 1.0 - bu - bv;
   double gu, ou, gv, ov, gw, ow, guv, ouv, in, out;
-  within01(bu, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gu, &ou);
-  within01(bv, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gv, &ov);
-  within01(bw, c.inv_tau_comp, c.comp_C, c.pair_exp, c.hard_ops, &gw, &ow);
+  within01(bu, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gu, &ou);
+  within01(bv, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gv, &ov);
+  within01(bw, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gw, &ow);
   within_and(gu, ou, gv, ov, &guv, &ouv);
   within_and(guv, ouv, gw, ow, &in, &out);
   if (label) *label = best | ((in >= 0.5) << 2);

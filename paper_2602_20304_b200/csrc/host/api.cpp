@@ -89,6 +89,8 @@ DevCfg device_config(const cmgb_config* c) {
   d.tau_normal = c->tau_normal;
   d.clip_C = std::exp(-1.0 / c->tau_clip);
   d.comp_C = std::exp(-1.0 / c->tau_comp);
+  d.inv_clip_C = 1.0 / d.clip_C;
+  d.inv_comp_C = 1.0 / d.comp_C;
   d.pair_exp = (1.0 / c->tau_clip < 700.0 && 1.0 / c->tau_comp < 700.0) ? 1 : 0;
   d.hard_ops = c->hard_ops ? 1 : 0;
   d.trace_iters = (c->sphere_trace && c->sphere_trace_iters > 0) ? c->sphere_trace_iters : 0;

