@@ -1,0 +1,138 @@
+// cmgb.hpp — header-only C++ wrapper over the C ABI (include/cmgb.h) that
+// mirrors the reference's C++ collision API (namespace cmg, /root/reference/
+// proj/include/cmg) so a C++ caller of the reference switches by changing
+// includes:
+//
+//   cmg::make_box_mesh / parse_obj        -> cmgb::Mesh::box / Mesh::parse_obj
+//   cmg::build_surface                     -> cmgb::Surface
+//   cmg::SmoothingConfig (+ variants)      -> cmgb::SmoothingConfig
+//   cmg::generate_manifold (per env loop)  -> cmgb::generate_manifold_batch
+//   cmg::run_ee_batch / run_vf_batch       -> cmgb::run_ee_batch / run_vf_batch
+//
+// Errors: the reference throws std::invalid_argument / MeshParseError; this
+// wrapper throws the same exception types with the library's message.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cmgb.h"
+
+namespace cmgb {
+
+struct MeshParseError : std::runtime_error {
+  MeshParseError(const std::string& what, int line) : std::runtime_error(what), line_number(line) {}
+  int line_number;
+};
+
+inline void check(int status) {
+  if (status == CMGB_OK) return;
+  const std::string msg = cmgb_last_error();
+  if (status == CMGB_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+struct SmoothingConfig : cmgb_config {
+  SmoothingConfig() { cmgb_config_default(this); }
+  static SmoothingConfig no_smoothing() {
+    SmoothingConfig c;
+    cmgb_config_no_smoothing(&c);
+    return c;
+  }
+  void validate() const { check(cmgb_config_validate(this)); }
+  SmoothingConfig for_variant(const std::string& v) const {
+    SmoothingConfig out;
+    check(cmgb_config_for_variant(v.c_str(), this, &out));
+    return out;
+  }
+};
+
+class Mesh {
+ public:
+  static Mesh box(const double half[3], int subdivisions = 1, bool quad_edges = true) {
+    cmgb_mesh m = nullptr;
+    check(cmgb_mesh_box(half, subdivisions, quad_edges ? 1 : 0, &m));
+    return Mesh(m);
+  }
+  static Mesh parse_obj(const std::string& text) {
+    cmgb_mesh m = nullptr;
+    int32_t line = 0;
+    const int st = cmgb_mesh_parse_obj(text.data(), text.size(), &m, &line);
+    if (st == CMGB_ERR_PARSE) throw MeshParseError(cmgb_last_error(), line);
+    check(st);
+    return Mesh(m);
+  }
+  Mesh(Mesh&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Mesh(const Mesh&) = delete;
+  ~Mesh() { cmgb_mesh_destroy(h_); }
+  cmgb_mesh handle() const { return h_; }
+
+ private:
+  explicit Mesh(cmgb_mesh h) : h_(h) {}
+  cmgb_mesh h_;
+};
+
+class Surface {
+ public:
+  // build_surface(mesh, sdf, vertex_topk, edge_topk, tolerance_fraction)
+  Surface(const Mesh& mesh, const std::vector<cmgb_sdf_node>& sdf_postfix, int vertex_topk = 0,
+          int edge_topk = 0, double tolerance_fraction = 1e-2) {
+    check(cmgb_surface_create(mesh.handle(), sdf_postfix.data(), (int32_t)sdf_postfix.size(),
+                              vertex_topk, edge_topk, tolerance_fraction, &h_));
+  }
+  Surface(Surface&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Surface(const Surface&) = delete;
+  ~Surface() { cmgb_surface_destroy(h_); }
+  cmgb_surface handle() const { return h_; }
+  cmgb_surface_info info() const {
+    cmgb_surface_info i{};
+    check(cmgb_surface_get_info(h_, &i));
+    return i;
+  }
+  std::vector<std::string> build_warnings() const {
+    std::vector<std::string> w;
+    for (int i = 0; i < info().n_warnings; ++i) w.emplace_back(cmgb_surface_warning(h_, i));
+    return w;
+  }
+
+ private:
+  cmgb_surface h_ = nullptr;
+};
+
+inline cmgb_layout layout(const Surface& a, const Surface& b, const SmoothingConfig& c) {
+  cmgb_layout L{};
+  check(cmgb_layout_query(a.handle(), b.handle(), &c, &L));
+  return L;
+}
+
+// Every env of a batch: device poses [n][6] (stride 0 = one pose for all),
+// device outputs (cmgb_manifold_out); stream-ordered on `stream`.
+inline void generate_manifold_batch(const Surface& a, const Surface& b, const double* poses1,
+                                    int pose1_stride, const double* poses2, int pose2_stride,
+                                    int64_t n_env, const SmoothingConfig& c,
+                                    const cmgb_manifold_out& out, void* stream = nullptr) {
+  check(cmgb_manifold_batch(a.handle(), b.handle(), poses1, pose1_stride, poses2, pose2_stride, n_env,
+                            &c, &out, stream));
+}
+
+// Host buffers in and out (copies inside the call).
+inline void generate_manifold_batch_host(const Surface& a, const Surface& b, const double* poses1,
+                                         int pose1_stride, const double* poses2, int pose2_stride,
+                                         int64_t n_env, const SmoothingConfig& c, float* mean_dist,
+                                         float* contacts = nullptr, void* stream = nullptr) {
+  check(cmgb_manifold_batch_host(a.handle(), b.handle(), poses1, pose1_stride, poses2, pose2_stride,
+                                 n_env, &c, mean_dist, contacts, stream));
+}
+
+inline void run_ee_batch(const double* pairs_device, int64_t n, const SmoothingConfig& c,
+                         float* out_device, void* stream = nullptr) {
+  check(cmgb_ee_witness_batch(pairs_device, 1, n, &c, out_device, nullptr, nullptr, stream));
+}
+
+inline void run_vf_batch(const double* pairs_device, int64_t n, const SmoothingConfig& c,
+                         float* out_device, void* stream = nullptr) {
+  check(cmgb_vf_witness_batch(pairs_device, 1, n, &c, out_device, nullptr, stream));
+}
+
+}  // namespace cmgb
