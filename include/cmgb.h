@@ -16,8 +16,9 @@
  *     include/cmg/surface.hpp:16-33; sdf.cpp:52-67 deep copy).
  *   - Batch entry points named *_batch take DEVICE pointers and a cudaStream_t
  *     passed as void*; they are stream-ordered and allocate nothing on the hot
- *     call. *_batch_host variants take HOST pointers and perform the H2D/D2H
- *     copies inside the call (the end-to-end path).
+ *     call when the caller supplies the workspace (cmgb_manifold_out). The
+ *     *_batch_host variants take HOST pointers and perform the H2D/D2H copies
+ *     inside the call (the end-to-end path).
  *   - Scalars follow the reference: poses and witness inputs are FP64 exactly
  *     as the reference receives them; contact outputs are FP32.
  */
@@ -180,7 +181,13 @@ typedef struct cmgb_manifold_out {
   float* ee;         /* optional: [n_env][9][m1*m2] dist,con,pen1,pen2,nn1,nn2,clash,act1,act2
                         (EeIndicatorMatrices, manifold.hpp:41-52); full mode only          */
   float* mean_dist;  /* optional: [n_env] mean_contact_distance (manifold.hpp:379-384)      */
+  void* workspace;   /* optional device scratch of cmgb_manifold_workspace_bytes(); when null
+                        the call takes it from the stream-ordered pool (cudaMallocAsync)     */
+  size_t workspace_bytes;
 } cmgb_manifold_out;
+
+/* Device scratch one cmgb_manifold_batch call needs (per-env pose frames). */
+size_t cmgb_manifold_workspace_bytes(int64_t n_env, int32_t pose1_stride, int32_t pose2_stride);
 
 /* poses*: DEVICE [n][6] FP64 (Pose6d = [t; axis-angle], pose.hpp:16-18).
  * pose1_stride / pose2_stride: 1 = one pose per env, 0 = the same pose for

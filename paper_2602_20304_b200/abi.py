@@ -90,6 +90,8 @@ class CmgbManifoldOut(C.Structure):
         ("src", C.c_void_p),
         ("ee", C.c_void_p),
         ("mean_dist", C.c_void_p),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
     ]
 
 
@@ -143,6 +145,7 @@ SIGNATURES = {
         [_P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P],
     ),
     "cmgb_device_count": (_I, [C.POINTER(C.c_int32)]),
+    "cmgb_manifold_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
 }
 
 _lib = None

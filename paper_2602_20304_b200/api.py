@@ -189,11 +189,16 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
         res["ee"] = torch.empty((n, 9, P), dtype=torch.float32, device=dev)
     if want_mean and "mean_dist" not in res:
         res["mean_dist"] = torch.empty((n,), dtype=torch.float32, device=dev)
+    ws = abi.load().cmgb_manifold_workspace_bytes(n, st1, st2)
+    if "workspace" not in res or res["workspace"].numel() < ws:
+        res["workspace"] = torch.empty((max(ws, 8),), dtype=torch.uint8, device=dev)
     o = abi.CmgbManifoldOut()
     o.contacts = res["contacts"].data_ptr()
     o.src = res["src"].data_ptr() if "src" in res else None
     o.ee = res["ee"].data_ptr() if "ee" in res else None
     o.mean_dist = res["mean_dist"].data_ptr() if "mean_dist" in res else None
+    o.workspace = res["workspace"].data_ptr()
+    o.workspace_bytes = res["workspace"].numel()
     with torch.cuda.device(dev):
         _ok(abi.load().cmgb_manifold_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
                                            C.byref(c), C.byref(o), _stream_ptr(stream)))

@@ -102,6 +102,8 @@ struct ManifoldParams {
   DevCfg cfg;
   const double* poses1;
   const double* poses2;
+  const double* frames1;  // [n1][12] R (row-major), t: device workspace filled by frames_kernel
+  const double* frames2;
   int32_t stride1, stride2;
   int64_t n_env;
   int32_t n1, n2, m1, m2, n_contacts;

@@ -186,6 +186,8 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   p.m1 = L.m1;
   p.m2 = L.m2;
   p.n_contacts = L.n_contacts;
+  p.frames1 = nullptr;  // bound by the caller (workspace)
+  p.frames2 = nullptr;
   p.contacts = out->contacts;
   p.src = out->src;
   p.ee = (L.m1 > 0 && L.m2 > 0) ? out->ee : nullptr;
@@ -232,8 +234,30 @@ struct HostScratch {
   double* poses2 = nullptr;
   float* contacts = nullptr;
   float* mean = nullptr;
-  size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0;
+  double* frames = nullptr;
+  size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0, cap_frames = 0;
 };
+
+size_t workspace_doubles(int64_t n_env, int st1, int st2) {
+  return 12 * (size_t)((st1 ? n_env : 1) + (st2 ? n_env : 1));
+}
+
+// Binds the frames workspace (caller's, or a stream-ordered pool block) and
+// launches frames_kernel + manifold_kernel on the stream.
+void launch_with_workspace(LaunchPlan& plan, int64_t n_env, int st1, int st2, void* ws, size_t ws_bytes,
+                           cudaStream_t stream) {
+  const size_t need = workspace_doubles(n_env, st1, st2) * sizeof(double);
+  void* buf = ws;
+  const bool pooled = ws == nullptr || ws_bytes < need;
+  if (pooled) cuda_check(cudaMallocAsync(&buf, need, stream), "cudaMallocAsync(workspace)");
+  double* f = static_cast<double*>(buf);
+  plan.p.frames1 = f;
+  plan.p.frames2 = f + 12 * (st1 ? n_env : 1);
+  const int rc = launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream);
+  if (pooled) cudaFreeAsync(buf, stream);
+  if (rc != 0)
+    throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
+}
 
 template <class T>
 void ensure(T** ptr, size_t* cap, size_t n) {
@@ -496,8 +520,8 @@ int cmgb_manifold_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1, 
   return guarded([&] {
     LaunchPlan plan = plan_manifold(s1, s2, poses1, st1, poses2, st2, n_env, cfg, out);
     if (n_env == 0 || plan.p.n_contacts == 0) return;
-    if (launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream) != 0)
-      throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
+    launch_with_workspace(plan, n_env, st1, st2, out->workspace, out->workspace_bytes,
+                          static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -525,10 +549,10 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
                "H2D poses1");
     cuda_check(cudaMemcpyAsync(sc.poses2, poses2_host, sizeof(double) * np2, cudaMemcpyHostToDevice, s),
                "H2D poses2");
-    cmgb_manifold_out out{sc.contacts, nullptr, nullptr, sc.mean};
+    ensure(&sc.frames, &sc.cap_frames, workspace_doubles(n_env, st1, st2));
+    cmgb_manifold_out out{sc.contacts, nullptr, nullptr, sc.mean, sc.frames, sc.cap_frames * sizeof(double)};
     LaunchPlan plan = plan_manifold(s1, s2, sc.poses1, st1, sc.poses2, st2, n_env, cfg, &out);
-    if (launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream) != 0)
-      throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
+    launch_with_workspace(plan, n_env, st1, st2, out.workspace, out.workspace_bytes, s);
     if (mean_dist_host)
       cuda_check(cudaMemcpyAsync(mean_dist_host, sc.mean, sizeof(float) * n_env, cudaMemcpyDeviceToHost, s),
                  "D2H mean");
@@ -565,6 +589,10 @@ int cmgb_vf_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     if (launch_vf_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
   });
+}
+
+size_t cmgb_manifold_workspace_bytes(int64_t n_env, int32_t st1, int32_t st2) {
+  return n_env > 0 ? workspace_doubles(n_env, st1, st2) * sizeof(double) : 0;
 }
 
 int cmgb_device_count(int32_t* count) {

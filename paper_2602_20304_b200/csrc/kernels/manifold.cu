@@ -198,6 +198,26 @@ __device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
   r[15] = clash;
 }
 
+// Pose -> frame (R, t) for every distinct pose (se3_exp, pose.hpp:78-91), one
+// thread each, ahead of the manifold kernel: keeps the FP64 sincos latency
+// chain off the manifold CTAs' critical path (they would otherwise idle at
+// the first barrier while 4 threads evaluate it).
+__global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ poses, int64_t n,
+                                                     double* __restrict__ frames) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xi[6], R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) xi[k] = __ldg(poses + 6 * i + k);
+  se3_exp_d(xi, R, t);
+  double* f = frames + 12 * i;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) f[k] = R[k];
+  f[9] = t[0];
+  f[10] = t[1];
+  f[11] = t[2];
+}
+
 template <int K1, int K2>
 __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
@@ -213,16 +233,12 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   const bool full = m1 > 0 && m2 > 0;
   auto env = [&](int e) { return EnvView{smem + (size_t)e * p.smem.bytes, &p.smem}; };
 
-  // ---- A: poses -> frames ------------------------------------------------
-  for (int i = tid; i < 2 * n_here; i += nth) {
-    const int e = i >> 1, s = i & 1;
-    const double* pose = s == 0 ? p.poses1 + 6 * (env0 + e) * p.stride1
-                                : p.poses2 + 6 * (env0 + e) * p.stride2;
-    double xi[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) xi[k] = __ldg(pose + k);
-    const EnvView ev = env(e);
-    se3_exp_d(xi, ev.R(s), ev.t(s));
+  // ---- A: frames (precomputed by frames_kernel) -> shared memory ----------
+  for (int i = tid; i < 24 * n_here; i += nth) {
+    const int e = i / 24, s = (i % 24) / 12, k = i % 12;
+    const double* f = s == 0 ? p.frames1 + 12 * (env0 + e) * p.stride1
+                             : p.frames2 + 12 * (env0 + e) * p.stride2;
+    env(e).R(s)[k] = __ldg(f + k);
   }
   __syncthreads();
 
@@ -341,8 +357,11 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   // ---- E: V-S contacts, then E-E pair stage ------------------------------
   const int C = p.n_contacts;
   {
+    // V-S items are dealt lane-major across warps (item j -> warp j % nwarps)
+    // so every warp carries the same small extra load before the pair stage.
     const int nvs = n1 + n2;
-    for (int it = tid; it < n_here * nvs; it += nth) {
+    const int nwarps = nth >> 5;
+    for (int it = (tid & 31) * nwarps + (tid >> 5); it < n_here * nvs; it += nth) {
       const int e = it / nvs, r = it % nvs;
       const EnvView ev = env(e);
       const double* q = ev.vslot(r);
@@ -366,8 +385,13 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
       const EnvView ev = env(e);
       double* r = ev.pair(i);
       ee_stage_qp(p, ev, i / m2, i % m2, r);
-      ee_stage_side<K1, K2>(p, ev, 0, r);
-      ee_stage_side<K2, K1>(p, ev, 1, r + 8);
+      if constexpr (K1 == K2) {  // one code copy for both sides (I-cache)
+#pragma unroll 1
+        for (int s = 0; s < 2; ++s) ee_stage_side<K1, K1>(p, ev, s, r + 8 * s);
+      } else {
+        ee_stage_side<K1, K2>(p, ev, 0, r);
+        ee_stage_side<K2, K1>(p, ev, 1, r + 8);
+      }
       ee_stage_pair(c, r);
     }
   }
@@ -455,6 +479,12 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   }
 }
 
+int launch_frames(const double* poses, int64_t n, double* frames, cudaStream_t s) {
+  if (n <= 0) return 0;
+  frames_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(poses, n, frames);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 template <int K1, int K2>
 int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   static bool configured = false;
@@ -486,6 +516,10 @@ int launch_k2(const ManifoldParams& p, int threads, int grid, size_t smem, cudaS
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n1 = p.stride1 ? p.n_env : 1, n2 = p.stride2 ? p.n_env : 1;
+  if (launch_frames(p.poses1, n1, const_cast<double*>(p.frames1), s) ||
+      launch_frames(p.poses2, n2, const_cast<double*>(p.frames2), s))
+    return 1;
   switch (p.side[0].sdf.kind) {
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
     case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);
