@@ -56,11 +56,68 @@ __device__ __forceinline__ double rsqrt_d(double x) {
 }
 __device__ __forceinline__ double div_d(double a, double b) { return a * rcp_d(b); }
 
+// exp(x) in FP64 for x <= ~709: x = k ln2 + r, |r| <= ln2/2 (Cody-Waite split
+// of ln2), e^r by its degree-12 Taylor polynomial (truncation < 1e-16
+// relative), 2^k spliced into the exponent field. exp(x < -708) returns 0
+// (the true value is < 2.3e-308). ~17 FP64 instructions, no branches beyond
+// the underflow select -- the libdevice version carries full special-case
+// handling the indicator arguments never need.
+__device__ __forceinline__ double exp_d(double x) {
+  const double k = rint(x * 1.4426950408889634);
+  double r = fma(-k, 6.93147180369123816490e-01, x);
+  r = fma(-k, 1.90821492927058770002e-10, r);
+  double p = 2.08767569878680989792e-09;           // 1/12!
+  p = fma(p, r, 2.50521083854417187751e-08);       // 1/11!
+  p = fma(p, r, 2.75573192239858906526e-07);       // 1/10!
+  p = fma(p, r, 2.75573192239858906526e-06);       // 1/9!
+  p = fma(p, r, 2.48015873015873015873e-05);       // 1/8!
+  p = fma(p, r, 1.98412698412698412698e-04);       // 1/7!
+  p = fma(p, r, 1.38888888888888888889e-03);       // 1/6!
+  p = fma(p, r, 8.33333333333333333333e-03);       // 1/5!
+  p = fma(p, r, 4.16666666666666666667e-02);       // 1/4!
+  p = fma(p, r, 1.66666666666666666667e-01);       // 1/3!
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int ki = (int)k;
+  const double s = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
+  return x < -708.0 ? 0.0 : s;
+}
+
+// log(v) in FP64 for finite v > 0: v = 2^e m, m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, odd series to s^23
+// (truncation < 1e-17).
+__device__ __forceinline__ double log_d(double v) {
+  int hi = __double2hiint(v);
+  int e = ((hi >> 20) & 0x7ff) - 1023;
+  hi = (hi & 0x000fffff) | 0x3ff00000;  // m in [1, 2)
+  double m = __hiloint2double(hi, __double2loint(v));
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const double s = (m - 1.0) * rcp_d(m + 1.0);
+  const double s2 = s * s;
+  double p = 1.0 / 23;
+  p = fma(p, s2, 1.0 / 21);
+  p = fma(p, s2, 1.0 / 19);
+  p = fma(p, s2, 1.0 / 17);
+  p = fma(p, s2, 1.0 / 15);
+  p = fma(p, s2, 1.0 / 13);
+  p = fma(p, s2, 1.0 / 11);
+  p = fma(p, s2, 1.0 / 9);
+  p = fma(p, s2, 1.0 / 7);
+  p = fma(p, s2, 1.0 / 5);
+  p = fma(p, s2, 1.0 / 3);
+  p = fma(p, s2, 1.0);
+  return fma((double)e, 6.93147180559945309417e-01, 2.0 * s * p);
+}
+
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
 // function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each
 // to full relative precision (the blends need the small one exactly).
 __device__ __forceinline__ void sigmoid_pair_d(double x, double* s, double* c) {
-  const double e = exp(-fabs(x));
+  const double e = exp_d(-fabs(x));
   const double inv = rcp_d(1.0 + e);
   const double small = e * inv;
   *s = x >= 0.0 ? inv : small;
@@ -75,7 +132,7 @@ __device__ __forceinline__ double sigmoid_d(double x) {
 // softplus_s (smooth_ops.hpp:66-81): max(x, 0) + tau log1p(exp(-|x|/tau)); both
 // reference arms are this function.
 __device__ __forceinline__ double softplus_d(double x, double tau, double inv_tau) {
-  return fmax(x, 0.0) + tau * log1p(exp(-fabs(x) * inv_tau));
+  return fmax(x, 0.0) + tau * log_d(1.0 + exp_d(-fabs(x) * inv_tau));
 }
 
 __device__ __forceinline__ double3 d3(double x, double y, double z) { return make_double3(x, y, z); }

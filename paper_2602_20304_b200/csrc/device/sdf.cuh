@@ -95,25 +95,23 @@ __device__ __forceinline__ void pow_pair_t(double x, int n, double p, double& xp
 // Otherwise -expm1(p4 ln f) with ln f = log1p(f - 1) near the surface.
 // Also returns 1/r (= f^p4) for the gradient.
 template <int N4 = 0>
-__device__ __forceinline__ double one_minus_pow(double f, double inv_f, double p4, int n_rt, double* F) {
+__device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, double* F) {
   const int n = N4 > 0 ? N4 : n_rt;
   if (n > 0) {
-    // seed r0 = 2^(log2(f) / n): log2 from the exponent bits + SFU lg2 of the
-    // mantissa in [1, 2); 2^q assembled from bits (normal f assumed)
-    const long long bits = __double_as_longlong(f);
-    const int ex = (int)((bits >> 52) & 0x7ff) - 1023;
-    const double mant = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-    const float l = ((float)ex + lg2f((float)mant)) / (float)n;
+    // F = f^(-1/n). Seed F0 = 2^(-log2(f)/n): log2 from the exponent bits +
+    // SFU lg2 of the mantissa, 2^q spliced from bits (any normal f). One
+    // Newton step on F^-n = f:  F = F0 (1 + (1 - f F0^n) / n), relative error
+    // ~ (n+1)/2 delta0^2 ~ 1e-12; then 1 - F is exact in FP64.
+    const int hi = __double2hiint(f);
+    const int ex = ((hi >> 20) & 0x7ff) - 1023;
+    const float mant = __int_as_float(((hi & 0x000fffff) << 3) | 0x3f800000);  // top mantissa bits
+    const float l = -((float)ex + lg2f(mant)) * (1.0f / (float)n);
     const float q = floorf(l);
-    const double r0 = (double)ex2f(l - q) * __longlong_as_double((long long)((int)q + 1023) << 52);
-    // one Newton step on r^n = f: r = r0 (1 - (r0^n - f) / (n r0^n)); the
-    // denominator r0^n -> f changes the step by O(n delta0) relative, i.e. the
-    // result by ~n delta0^2 ~ 1e-12 (same order as the quadratic term)
-    const double rn = N4 > 0 ? cpow<(N4 > 0 ? N4 : 1)>(r0) : ipow_d(r0, n);
-    const double r = r0 * (1.0 - (rn - f) * inv_f * (1.0 / (double)n));
-    const double inv_r = rcp_d(r);
-    *F = inv_r;
-    return (r - 1.0) * inv_r;
+    const double F0 = (double)ex2f(l - q) * __hiloint2double(((int)q + 1023) << 20, 0);
+    const double Fn = N4 > 0 ? cpow<(N4 > 0 ? N4 : 1)>(F0) : ipow_d(F0, n);
+    const double Fv = fma(F0 * fma(-f, Fn, 1.0), 1.0 / (double)n, F0);
+    *F = Fv;
+    return 1.0 - Fv;
   }
   const double d = f - 1.0;
   const double lnf = fabs(d) < 0.5 ? log1p(d) : log(f);
@@ -142,7 +140,7 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   if (FL == kValue) {
     const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
     double F;
-    out.v = one_minus_pow<N4>(f, rcp_d(f), q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
+    out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
     return out;
   }
   // grad f through the normalisation: d(x2^p1)/dx = p1 x2^(p1-1) 2 xn / ax.
@@ -157,7 +155,7 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   const double rinv = rsqrt_d(r2);
   double F;
   const double inv_f = rcp_d(f);
-  const double omF = one_minus_pow<N4>(f, inv_f, q.p4, q.n4, &F);
+  const double omF = one_minus_pow<N4>(f, q.p4, q.n4, &F);
   const double phi = omF * rinv;
   out.v = phi;
   if (FL == kGrad) {

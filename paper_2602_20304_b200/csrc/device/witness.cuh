@@ -18,7 +18,7 @@ namespace cmgb {
 // a / C (x > 1) -- one SFU-free exponential per softplus / sigmoid pair.
 __device__ __forceinline__ double partner_exp(double x, double a, double C, double inv_C,
                                               double inv_tau, int pair) {
-  if (!pair) return exp(-fabs(x - 1.0) * inv_tau);
+  if (!pair) return exp_d(-fabs(x - 1.0) * inv_tau);
   return x < 0.0 ? a * C : (x <= 1.0 ? C * rcp_d(a) : a * inv_C);
 }
 
@@ -27,9 +27,11 @@ __device__ __forceinline__ double partner_exp(double x, double a, double C, doub
 // a = exp(-|x|/tau), b = exp(-|x-1|/tau); hard: clamp.
 __device__ __forceinline__ double clip01(double x, const DevCfg& c) {
   if (c.hard_ops) return fmin(fmax(x, 0.0), 1.0);
-  const double a = exp(-fabs(x) * c.inv_tau_clip);
+  const double a = exp_d(-fabs(x) * c.inv_tau_clip);
   const double b = partner_exp(x, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
-  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log1p((a - b) * rcp_d(1.0 + b));
+  // tau (log1p(a) - log1p(b)) = tau log((1 + a) / (1 + b)); the quotient is
+  // formed in FP64 (absolute error ~1e-16, scaled by tau)
+  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log_d((1.0 + a) * rcp_d(1.0 + b));
 }
 
 // within01 (witness.hpp:54-61): gamma = sigma(x/tau) sigma((1-x)/tau) and its
@@ -43,7 +45,7 @@ __device__ __forceinline__ void within01(double x, double inv_tau, double C, dou
     *omg = in ? 0.0 : 1.0;
     return;
   }
-  const double e1 = exp(-fabs(x) * inv_tau);              // sigma(x/tau) pair
+  const double e1 = exp_d(-fabs(x) * inv_tau);            // sigma(x/tau) pair
   const double e2 = partner_exp(x, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
   const double i1 = rcp_d(1.0 + e1), i2 = rcp_d(1.0 + e2);
   const double s1 = x >= 0.0 ? i1 : e1 * i1, c1 = x >= 0.0 ? e1 * i1 : i1;
@@ -80,7 +82,7 @@ __device__ __forceinline__ int pick_min(const double (&cost)[N], double (&w)[N],
   double total = 0.0;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    w[i] = i == best ? 1.0 : exp((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
+    w[i] = i == best ? 1.0 : exp_d((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
     total += w[i];
   }
   const double inv = rcp_d(total);
