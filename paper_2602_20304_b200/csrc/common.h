@@ -15,7 +15,8 @@ namespace cmgb {
 
 constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param block
 constexpr int kMaxStack = 8;    // generic interpreter stack depth
-constexpr int kPairRec = 36;    // floats per E-E pair record in shared memory (144 B)
+constexpr int kPairRec = 38;    // floats per E-E pair record in shared memory (19 doubles:
+                                 // an odd stride keeps per-lane FP64 accesses bank-conflict free)
 
 // kSqE01: a lone superquadric with eps1 = eps2 = 0.1 (the box-box benchmark
 // body), whose exponents (n1, n2, n3, n4) = (10, 1, 10, 20) are compiled in.
@@ -97,6 +98,13 @@ struct SmemLayout {
   int32_t bytes;     // per env, 16-byte aligned
 };
 
+// n / d for 0 <= n < 2^32 / d: q = (n * mul) >> 32, mul = ceil(2^32 / d)
+// (64-bit: d = 1 needs mul = 2^32).
+struct FastDiv {
+  uint64_t mul;
+  uint32_t d, pad;
+};
+
 struct ManifoldParams {
   DevSide side[2];
   DevCfg cfg;
@@ -108,6 +116,7 @@ struct ManifoldParams {
   int64_t n_env;
   int32_t n1, n2, m1, m2, n_contacts;
   int32_t envs_per_block;
+  FastDiv div_pairs, div_m2, div_nvs, div_nslots, div_nrc, div_nv_all, div_ne_all, div_scores;
   SmemLayout smem;
   float* contacts;
   int32_t* src;

@@ -62,23 +62,30 @@ __device__ __forceinline__ double div_d(double a, double b) { return a * rcp_d(b
 // (the true value is < 2.3e-308). ~17 FP64 instructions, no branches beyond
 // the underflow select -- the libdevice version carries full special-case
 // handling the indicator arguments never need.
+// FP64 literals live in the constant bank so DFMA/DMUL read them as c[][]
+// operands (an immediate double costs two UMOVs + a uniform-pipe dependency).
+struct MathConsts {
+  double exp_c[13];  // 1/12! .. 1/0! (Horner order)
+  double log_c[12];  // 1/23, 1/21, ..., 1/3, 1
+  double log2e, ln2_hi, ln2_lo, ln2, sqrt2, floor30, floor20;
+};
+static __constant__ MathConsts kMC = {
+    {2.08767569878680989792e-09, 2.50521083854417187751e-08, 2.75573192239858906526e-07,
+     2.75573192239858906526e-06, 2.48015873015873015873e-05, 1.98412698412698412698e-04,
+     1.38888888888888888889e-03, 8.33333333333333333333e-03, 4.16666666666666666667e-02,
+     1.66666666666666666667e-01, 0.5, 1.0, 1.0},
+    {1.0 / 23, 1.0 / 21, 1.0 / 19, 1.0 / 17, 1.0 / 15, 1.0 / 13, 1.0 / 11, 1.0 / 9, 1.0 / 7, 1.0 / 5,
+     1.0 / 3, 1.0},
+    1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    6.93147180559945309417e-01, 1.4142135623730951, 1e-30, 1e-20};
+
 __device__ __forceinline__ double exp_d(double x) {
-  const double k = rint(x * 1.4426950408889634);
-  double r = fma(-k, 6.93147180369123816490e-01, x);
-  r = fma(-k, 1.90821492927058770002e-10, r);
-  double p = 2.08767569878680989792e-09;           // 1/12!
-  p = fma(p, r, 2.50521083854417187751e-08);       // 1/11!
-  p = fma(p, r, 2.75573192239858906526e-07);       // 1/10!
-  p = fma(p, r, 2.75573192239858906526e-06);       // 1/9!
-  p = fma(p, r, 2.48015873015873015873e-05);       // 1/8!
-  p = fma(p, r, 1.98412698412698412698e-04);       // 1/7!
-  p = fma(p, r, 1.38888888888888888889e-03);       // 1/6!
-  p = fma(p, r, 8.33333333333333333333e-03);       // 1/5!
-  p = fma(p, r, 4.16666666666666666667e-02);       // 1/4!
-  p = fma(p, r, 1.66666666666666666667e-01);       // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  const double k = rint(x * kMC.log2e);
+  double r = fma(-k, kMC.ln2_hi, x);
+  r = fma(-k, kMC.ln2_lo, r);
+  double p = kMC.exp_c[0];
+#pragma unroll
+  for (int i = 1; i < 13; ++i) p = fma(p, r, kMC.exp_c[i]);
   const int ki = (int)k;
   const double s = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   return x < -708.0 ? 0.0 : s;
@@ -92,25 +99,16 @@ __device__ __forceinline__ double log_d(double v) {
   int e = ((hi >> 20) & 0x7ff) - 1023;
   hi = (hi & 0x000fffff) | 0x3ff00000;  // m in [1, 2)
   double m = __hiloint2double(hi, __double2loint(v));
-  if (m > 1.4142135623730951) {
+  if (m > kMC.sqrt2) {
     m *= 0.5;
     e += 1;
   }
   const double s = (m - 1.0) * rcp_d(m + 1.0);
   const double s2 = s * s;
-  double p = 1.0 / 23;
-  p = fma(p, s2, 1.0 / 21);
-  p = fma(p, s2, 1.0 / 19);
-  p = fma(p, s2, 1.0 / 17);
-  p = fma(p, s2, 1.0 / 15);
-  p = fma(p, s2, 1.0 / 13);
-  p = fma(p, s2, 1.0 / 11);
-  p = fma(p, s2, 1.0 / 9);
-  p = fma(p, s2, 1.0 / 7);
-  p = fma(p, s2, 1.0 / 5);
-  p = fma(p, s2, 1.0 / 3);
-  p = fma(p, s2, 1.0);
-  return fma((double)e, 6.93147180559945309417e-01, 2.0 * s * p);
+  double p = kMC.log_c[0];
+#pragma unroll
+  for (int i = 1; i < 12; ++i) p = fma(p, s2, kMC.log_c[i]);
+  return fma((double)e, kMC.ln2, 2.0 * s * p);
 }
 
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same

@@ -126,7 +126,7 @@ template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0>
 __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   if (q.has_frame) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));  // apply_inverse
   const double xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
-  const double x2 = fma(xn, xn, 1e-30), y2 = fma(yn, yn, 1e-30), z2 = fma(zn, zn, 1e-30);
+  const double x2 = fma(xn, xn, kMC.floor30), y2 = fma(yn, yn, kMC.floor30), z2 = fma(zn, zn, kMC.floor30);
   double A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
   pow_pair_t<N1>(x2, q.n1, q.p1, A, Am1);
   pow_pair_t<N1>(y2, q.n1, q.p1, B, Bm1);
@@ -138,36 +138,37 @@ __device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
   out.v = 0.0;
   out.g = d3(0, 0, 0);
   if (FL == kValue) {
-    const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
+    const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
     double F;
     out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
     return out;
   }
-  // grad f through the normalisation: d(x2^p1)/dx = p1 x2^(p1-1) 2 xn / ax.
+  // grad f w.r.t. the normalised coordinates (d(x2^p1)/dxn = 2 p1 x2^(p1-1) xn);
+  // the body-frame gradient is diag(1/axes) times it.
   const double cxy = q.c_xy * Gm1;
-  const double3 df = d3(cxy * Am1 * xn * q.inv_ax[0], cxy * Bm1 * yn * q.inv_ax[1],
-                        q.c_z * Czm1 * zn * q.inv_ax[2]);
-  if (FL == kNormalOnly) {
+  const double3 dfn = d3(cxy * Am1 * xn, cxy * Bm1 * yn, q.c_z * Czm1 * zn);
+  if (FL == kNormalOnly || FL == kNormalSource) {
+    const double3 df = d3(dfn.x * q.inv_ax[0], dfn.y * q.inv_ax[1], dfn.z * q.inv_ax[2]);
+    if (FL == kNormalSource) {
+      const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
+      double F;
+      out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);
+    }
     out.g = q.has_frame ? mul_R(q.R, df) : df;
     return out;
   }
-  const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, 1e-20)));
+  // kGrad: grad phi = diag(1/axes) (-p4 (F/f) grad_n f - phi x~ / r) / r
+  const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
   const double rinv = rsqrt_d(r2);
   double F;
-  const double inv_f = rcp_d(f);
   const double omF = one_minus_pow<N4>(f, q.p4, q.n4, &F);
   const double phi = omF * rinv;
   out.v = phi;
-  if (FL == kGrad) {
-    // grad phi = (-p4 (F/f) grad f - phi (x~ / axes) / r) / r, F = 1 - omF
-    const double k = -q.p4 * F * inv_f;
-    const double h = phi * rinv;
-    double3 gl = d3((k * df.x - h * xn * q.inv_ax[0]) * rinv, (k * df.y - h * yn * q.inv_ax[1]) * rinv,
-                    (k * df.z - h * zn * q.inv_ax[2]) * rinv);
-    out.g = q.has_frame ? mul_R(q.R, gl) : gl;
-  } else {  // kNormalSource
-    out.g = q.has_frame ? mul_R(q.R, df) : df;
-  }
+  const double k = -q.p4 * F * rcp_d(f);
+  const double h = phi * rinv;
+  const double sx = q.inv_ax[0] * rinv, sy = q.inv_ax[1] * rinv, sz = q.inv_ax[2] * rinv;
+  const double3 gl = d3(sx * fma(k, dfn.x, -h * xn), sy * fma(k, dfn.y, -h * yn), sz * fma(k, dfn.z, -h * zn));
+  out.g = q.has_frame ? mul_R(q.R, gl) : gl;
   return out;
 }
 

@@ -222,6 +222,21 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
   const int threads = maxt;
   p.envs_per_block = epb;
+  auto fd = [](int d) {
+    FastDiv f;
+    f.d = (uint32_t)std::max(d, 1);
+    f.mul = ((1ULL << 32) + f.d - 1) / f.d;
+    f.pad = 0;
+    return f;
+  };
+  p.div_pairs = fd(P);
+  p.div_m2 = fd(L.m2);
+  p.div_nvs = fd(nslot_v);
+  p.div_nslots = fd(nslot_v + nslot_e);
+  p.div_nrc = fd(nslot_e);
+  p.div_nv_all = fd(p.side[0].nv + p.side[1].nv);
+  p.div_ne_all = fd(p.side[0].ne + p.side[1].ne);
+  p.div_scores = fd(p.side[0].nv + p.side[1].nv + p.side[0].ne + p.side[1].ne);
   plan.threads = threads;
   plan.grid = static_cast<int>((n_env + epb - 1) / epb);
   plan.smem = (size_t)epb * S.bytes;

@@ -32,7 +32,7 @@ namespace {
 constexpr int kMaxThreads = 288;
 constexpr int kMinBlocks = 3;
 
-// Pair record (doubles; kPairRec = 36 floats = 18 doubles = 144 B), rewritten
+// Pair record (doubles; kPairRec = 38 floats = 19 doubles = 152 B), rewritten
 // in place by the E-E sub-phases:
 //   side s at 8 s: [0-2] witness point (body frame -> traced -> world),
 //                  [3-5] own normal (world), [6] phi_other(p), [7] phi_own(p)
@@ -56,6 +56,15 @@ struct EnvView {
   __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
   __device__ double& dbar(int i) const { return pair(i)[3]; }
 };
+
+// q = n / d, r = n % d with the host-precomputed multiplier.
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return (int)(((uint64_t)(uint32_t)n * f.mul) >> 32);
+}
+__device__ __forceinline__ void fdivmod(int n, const FastDiv& f, int& q, int& r) {
+  q = fdiv(n, f);
+  r = n - q * (int)f.d;
+}
 
 __device__ __forceinline__ double3 ld_vert(const double* v, int i) {
   return d3(__ldg(v + 3 * i), __ldg(v + 3 * i + 1), __ldg(v + 3 * i + 2));
@@ -248,7 +257,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     // ---- B: vertex penetration scores (opposing posed SDF value) ----------
     const int nv_all = S1.nv + S2.nv;
     for (int it = tid; it < n_here * nv_all; it += nth) {
-      const int e = it / nv_all, i = it % nv_all;
+      int e, i;
+      fdivmod(it, p.div_nv_all, e, i);
       const int s = i < S1.nv ? 0 : 1;
       const int vi = s == 0 ? i : i - S1.nv;
       const EnvView ev = env(e);
@@ -261,7 +271,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     // edge scores: -(mean of endpoint penetrations) (edge_penetrations, 86-94)
     const int ne_all = S1.ne + S2.ne;
     for (int it = tid; it < n_here * ne_all; it += nth) {
-      const int e = it / ne_all, i = it % ne_all;
+      int e, i;
+      fdivmod(it, p.div_ne_all, e, i);
       const int s = i < S1.ne ? 0 : 1;
       const int ei = s == 0 ? i : i - S1.ne;
       const int32_t* E = s == 0 ? S1.edges : S2.edges;
@@ -275,7 +286,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     // ---- C: descending rank sort (values only matter; smooth_ops.hpp:180-185)
     const int total = sets.off[4];
     for (int it = tid; it < n_here * total; it += nth) {
-      const int e = it / total, i = it % total;
+      int e, i;
+      fdivmod(it, p.div_scores, e, i);
       const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
       const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
       if (!active) continue;
@@ -295,7 +307,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   {
     const int nsl = n1 + n2 + m1 + m2;
     for (int it = tid; it < n_here * nsl; it += nth) {
-      const int e = it / nsl, r0 = it % nsl;
+      int e, r0;
+      fdivmod(it, p.div_nslots, e, r0);
       const EnvView ev = env(e);
       const bool is_edge = r0 >= n1 + n2;
       const int s = is_edge ? (r0 - n1 - n2 < m1 ? 0 : 1) : (r0 < n1 ? 0 : 1);
@@ -362,7 +375,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     const int nvs = n1 + n2;
     const int nwarps = nth >> 5;
     for (int it = (tid & 31) * nwarps + (tid >> 5); it < n_here * nvs; it += nth) {
-      const int e = it / nvs, r = it % nvs;
+      int e, r;
+      fdivmod(it, p.div_nvs, e, r);
       const EnvView ev = env(e);
       const double* q = ev.vslot(r);
       float* dst = p.contacts + ((env0 + e) * C + r) * 8;
@@ -381,10 +395,12 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     // stage's registers are released): QP -> trace/normal/opposing value of
     // side 1 and side 2 -> pair quantities.
     for (int it = tid; it < n_here * P; it += nth) {
-      const int e = it / P, i = it % P;
+      int e, i, k, l;
+      fdivmod(it, p.div_pairs, e, i);
+      fdivmod(i, p.div_m2, k, l);
       const EnvView ev = env(e);
       double* r = ev.pair(i);
-      ee_stage_qp(p, ev, i / m2, i % m2, r);
+      ee_stage_qp(p, ev, k, l, r);
       if constexpr (K1 == K2) {  // one code copy for both sides (I-cache)
 #pragma unroll 1
         for (int s = 0; s < 2; ++s) ee_stage_side<K1, K1>(p, ev, s, r + 8 * s);
@@ -401,7 +417,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     // ---- F: NN softmin statistics: rows (side 1) and columns (side 2) -------
     const int nrc = m1 + m2;
     for (int it = tid; it < n_here * nrc; it += nth) {
-      const int e = it / nrc, r = it % nrc;
+      int e, r;
+      fdivmod(it, p.div_nrc, e, r);
       const EnvView ev = env(e);
       const bool row = r < m1;
       const int n = row ? m2 : m1;
@@ -421,8 +438,9 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     __syncthreads();
     // ---- G: activity product + fixed-layout E-E output (303-330) -----------
     for (int it = tid; it < n_here * P; it += nth) {
-      const int e = it / P, i = it % P;
-      const int k = i / m2, l = i % m2;
+      int e, i, k, l;
+      fdivmod(it, p.div_pairs, e, i);
+      fdivmod(i, p.div_m2, k, l);
       const EnvView ev = env(e);
       const double* rec = ev.pair(i);
       const double* ns = ev.nnstat();
