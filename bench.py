@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--n-env", type=int, default=65536, help="envs per GPU (weak scaling)")
     ap.add_argument("--cpu-sample", type=int, default=16384, help="envs in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop"],
+                    help="box-box = config B (headline); mixed = config C (4 x 65,536 envs of "
+                         "primitive families vs a convex mesh); drop = config D (all 10 body pairs "
+                         "of a 5-body scene, 32,768 envs)")
     return ap.parse_args()
 
 
@@ -155,6 +159,68 @@ def run_reference_arm(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_secondary(args, dev, rank, world):
+    """Configs C and D: device-resident throughput of the same path on the
+    mixed-primitive buckets / the all-pairs multi-body scene."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_20304_b200 import api
+    from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
+
+    cfg = SmoothingConfig()
+    if args.workload == "mixed":
+        n = 65536 if args.n_env == 65536 else args.n_env
+        calls = []
+        for kind in W.MIXED_KINDS:
+            ws = W.mixed_bucket(kind, n)
+            s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+            p1, p2 = ws.poses(n)
+            calls.append((s1, s2, torch.as_tensor(p1, device=dev), torch.as_tensor(p2, device=dev), {}))
+        units = n * len(calls)
+
+        def step():
+            for s1, s2, p1, p2, out in calls:
+                api.generate_manifold_batch(s1, s2, p1, p2, cfg, out=out)
+        metric, unit, cfgd = "contact manifolds/sec (mixed primitives vs convex mesh, 4 x %d envs)" % n, \
+            "manifolds/s", {"workload": "mixed (config C): rounded box / cylinder / ellipsoid / capsule vs "
+                            "convex mesh plate, soft top-K 16/16 vertices 8/8 edges, 160 contacts/env",
+                            "n_env_total": units}
+    else:
+        n = 32768 if args.n_env == 65536 else args.n_env
+        sc = W.drop_scene(n)
+        bodies = [api.surface_from_spec(b) for b in sc.bodies]
+        P = torch.as_tensor(sc.poses(n), device=dev)
+        outs = None
+        pairs = api.scene_pairs(len(bodies), sc.is_static())
+        units = n * len(pairs)
+
+        def step():
+            nonlocal outs
+            outs = api.generate_manifold_scene_batch(bodies, P, cfg, is_static=sc.is_static(), outs=outs)
+        metric, unit, cfgd = "pair manifolds/sec (5-body drop scene, all %d pairs, %d envs)" % (len(pairs), n), \
+            "manifolds/s", {"workload": "drop (config D): 4 stacked SQ boxes over a static box_planes "
+                            "ground, edge_topk 4, 48 contacts/pair", "n_env": n, "pairs_per_env": len(pairs)}
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    for _ in range(args.steps):
+        step()
+    t1.record(s)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    if rank == 0:
+        print(json.dumps({"metric": metric, "value": units / (ms * 1e-3), "unit": unit, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f64 (FP32 outputs)", "data": "synthetic", "config": cfgd}), flush=True)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -176,6 +242,9 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.workload != "box-box":
+        run_secondary(args, dev, rank, world)
+        return
 
     n_local = args.n_env
     n_total = n_local * world

@@ -206,6 +206,20 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
                              float* mean_dist_host, float* contacts_host, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * Multi-body scenes — the all-pairs loop of DemoSim::step (src/demosim.cpp:
+ * 88-104): every body pair (i < j) except static-static, for every env.
+ * ------------------------------------------------------------------------- */
+/* Enumerate the pairs in (i, j) lexicographic order; pairs may be null to
+ * query the count. is_static: [n_bodies] 0/1 (nullable = all dynamic). */
+int cmgb_scene_pairs(const int32_t* is_static, int32_t n_bodies, int32_t* pairs, int32_t* n_pairs);
+/* poses: DEVICE [n_env][n_bodies][6]; outs[q] receives pair q's manifolds
+ * (layout of cmgb_layout_query(bodies[i], bodies[j])). */
+int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                              int32_t n_pairs, const double* poses, int64_t n_env,
+                              const cmgb_config* cfg, const cmgb_manifold_out* outs,
+                              void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * Witness batches — run_ee_batch / run_vf_batch (src/batch.cpp:53-98) over
  * ee_witness / vf_witness (include/cmg/witness.hpp:137-158, 163-227).
  * pairs: DEVICE [n][12] (e1a,e1b,e2a,e2b | v,t0,t1,t2), FP64 if pairs_fp64

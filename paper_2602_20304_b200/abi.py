@@ -146,6 +146,12 @@ SIGNATURES = {
     ),
     "cmgb_device_count": (_I, [C.POINTER(C.c_int32)]),
     "cmgb_manifold_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
+    "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
+    "cmgb_manifold_scene_batch": (
+        _I,
+        [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig),
+         C.POINTER(CmgbManifoldOut), _P],
+    ),
 }
 
 _lib = None

@@ -205,6 +205,67 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
     return res
 
 
+def scene_pairs(n_bodies: int, is_static=None) -> np.ndarray:
+    """Body pairs (i < j, skipping static-static) in DemoSim::step's order
+    (src/demosim.cpp:88-104)."""
+    lib = abi.load()
+    st = None if is_static is None else np.ascontiguousarray(is_static, dtype=np.int32)
+    n = C.c_int32()
+    _ok(lib.cmgb_scene_pairs(st.ctypes.data if st is not None else None, n_bodies, None, C.byref(n)))
+    out = np.zeros((n.value, 2), np.int32)
+    _ok(lib.cmgb_scene_pairs(st.ctypes.data if st is not None else None, n_bodies, out.ctypes.data,
+                             C.byref(n)))
+    return out
+
+
+def generate_manifold_scene_batch(bodies, poses, cfg=None, *, is_static=None, pairs=None,
+                                  want_src: bool = False, want_ee: bool = False,
+                                  outs: Optional[list] = None, stream=None) -> list:
+    """All-pairs manifolds of a multi-body scene for every env: poses is a CUDA
+    float64 tensor [n_env, n_bodies, 6]; returns one result dict per pair (as
+    generate_manifold_batch) plus its (i, j)."""
+    import torch
+
+    c = _cfg(cfg)
+    P = poses.contiguous()
+    if P.dtype != torch.float64 or not P.is_cuda or P.dim() != 3 or P.shape[2] != 6:
+        raise ValueError("poses must be a CUDA float64 tensor [n_env, n_bodies, 6]")
+    n_env, nb = P.shape[0], P.shape[1]
+    if len(bodies) != nb:
+        raise ValueError("one surface per body")
+    pr = scene_pairs(nb, is_static) if pairs is None else np.ascontiguousarray(pairs, dtype=np.int32)
+    res = outs if outs is not None else [dict() for _ in range(len(pr))]
+    arr = (abi.CmgbManifoldOut * max(len(pr), 1))()
+    lib = abi.load()
+    for q, (i, j) in enumerate(pr):
+        L = layout(bodies[i], bodies[j], c)
+        r = res[q]
+        r["pair"] = (int(i), int(j))
+        if "contacts" not in r:
+            r["contacts"] = torch.empty((n_env, L["n_contacts"], 8), dtype=torch.float32, device=P.device)
+        if want_src and "src" not in r:
+            r["src"] = torch.empty((n_env, L["n_contacts"], 2), dtype=torch.int32, device=P.device)
+        if want_ee and L["m1"] * L["m2"] > 0 and "ee" not in r:
+            r["ee"] = torch.empty((n_env, 9, L["m1"] * L["m2"]), dtype=torch.float32, device=P.device)
+        if "mean_dist" not in r:
+            r["mean_dist"] = torch.empty((n_env,), dtype=torch.float32, device=P.device)
+        ws = lib.cmgb_manifold_workspace_bytes(n_env, 1, 1)
+        if "workspace" not in r or r["workspace"].numel() < ws:
+            r["workspace"] = torch.empty((max(ws, 8),), dtype=torch.uint8, device=P.device)
+        o = arr[q]
+        o.contacts = r["contacts"].data_ptr()
+        o.src = r["src"].data_ptr() if "src" in r else None
+        o.ee = r["ee"].data_ptr() if "ee" in r else None
+        o.mean_dist = r["mean_dist"].data_ptr()
+        o.workspace = r["workspace"].data_ptr()
+        o.workspace_bytes = r["workspace"].numel()
+    handles = (C.c_void_p * nb)(*[b._h.value if isinstance(b._h, C.c_void_p) else b._h for b in bodies])
+    with torch.cuda.device(P.device):
+        _ok(lib.cmgb_manifold_scene_batch(handles, nb, pr.ctypes.data, len(pr), P.data_ptr(), n_env,
+                                          C.byref(c), arr, _stream_ptr(stream)))
+    return res
+
+
 def generate_manifold_batch_host(s1: Surface, s2: Surface, poses1: np.ndarray, poses2: np.ndarray,
                                  cfg=None, mean_out: Optional[np.ndarray] = None,
                                  contacts_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:

@@ -112,7 +112,8 @@ struct ManifoldParams {
   const double* poses2;
   const double* frames1;  // [n1][12] R (row-major), t: device workspace filled by frames_kernel
   const double* frames2;
-  int32_t stride1, stride2;
+  int32_t stride1, stride2;            // frames: 1 = one per env, 0 = shared
+  int64_t pose_stride1, pose_stride2;  // poses: doubles between consecutive envs (0 = shared)
   int64_t n_env;
   int32_t n1, n2, m1, m2, n_contacts;
   int32_t envs_per_block;

@@ -180,6 +180,8 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   p.poses2 = poses2;
   p.stride1 = st1;
   p.stride2 = st2;
+  p.pose_stride1 = 6 * st1;
+  p.pose_stride2 = 6 * st2;
   p.n_env = n_env;
   p.n1 = L.n1;
   p.n2 = nsel[1];
@@ -603,6 +605,43 @@ int cmgb_vf_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, nullptr, labels};
     if (launch_vf_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_scene_pairs(const int32_t* is_static, int32_t n_bodies, int32_t* pairs, int32_t* n_pairs) {
+  return guarded([&] {
+    if (n_bodies < 0 || !n_pairs) invalid("scene_pairs: bad argument");
+    int32_t k = 0;
+    for (int i = 0; i < n_bodies; ++i)
+      for (int j = i + 1; j < n_bodies; ++j) {
+        if (is_static && is_static[i] && is_static[j]) continue;  // demosim.cpp:90
+        if (pairs) {
+          pairs[2 * k] = i;
+          pairs[2 * k + 1] = j;
+        }
+        ++k;
+      }
+    *n_pairs = k;
+  });
+}
+
+int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                              int32_t n_pairs, const double* poses, int64_t n_env,
+                              const cmgb_config* cfg, const cmgb_manifold_out* outs, void* stream) {
+  return guarded([&] {
+    if (!bodies || !pairs || !poses || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0)
+      invalid("manifold_scene_batch: bad argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int q = 0; q < n_pairs; ++q) {
+      const int i = pairs[2 * q], j = pairs[2 * q + 1];
+      if (i < 0 || j < 0 || i >= n_bodies || j >= n_bodies || i == j)
+        invalid("manifold_scene_batch: pair index out of range");
+      const cmgb_manifold_out& o = outs[q];
+      LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &o);
+      if (n_env == 0 || plan.p.n_contacts == 0) continue;
+      plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)n_bodies;
+      launch_with_workspace(plan, n_env, 1, 1, o.workspace, o.workspace_bytes, s);
+    }
   });
 }
 

@@ -211,13 +211,13 @@ __device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
 // thread each, ahead of the manifold kernel: keeps the FP64 sincos latency
 // chain off the manifold CTAs' critical path (they would otherwise idle at
 // the first barrier while 4 threads evaluate it).
-__global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ poses, int64_t n,
-                                                     double* __restrict__ frames) {
+__global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ poses, int64_t stride,
+                                                     int64_t n, double* __restrict__ frames) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double xi[6], R[9], t[3];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) xi[k] = __ldg(poses + 6 * i + k);
+  for (int k = 0; k < 6; ++k) xi[k] = __ldg(poses + stride * i + k);
   se3_exp_d(xi, R, t);
   double* f = frames + 12 * i;
 #pragma unroll
@@ -497,9 +497,9 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   }
 }
 
-int launch_frames(const double* poses, int64_t n, double* frames, cudaStream_t s) {
+int launch_frames(const double* poses, int64_t stride, int64_t n, double* frames, cudaStream_t s) {
   if (n <= 0) return 0;
-  frames_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(poses, n, frames);
+  frames_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(poses, stride, n, frames);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -535,8 +535,8 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n1 = p.stride1 ? p.n_env : 1, n2 = p.stride2 ? p.n_env : 1;
-  if (launch_frames(p.poses1, n1, const_cast<double*>(p.frames1), s) ||
-      launch_frames(p.poses2, n2, const_cast<double*>(p.frames2), s))
+  if (launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), s) ||
+      launch_frames(p.poses2, p.pose_stride2, n2, const_cast<double*>(p.frames2), s))
     return 1;
   switch (p.side[0].sdf.kind) {
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);

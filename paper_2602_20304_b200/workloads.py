@@ -263,6 +263,45 @@ def mixed_bucket(kind: str, n_env: int = 65536) -> Workload:
 
 MIXED_KINDS = ("rounded_box", "cylinder", "ellipsoid", "capsule")
 
+
+# ---------------------------------------------------------------------------
+# Config D: multi-body drop scene (all geom pairs), SURVEY §8(d) D
+# ---------------------------------------------------------------------------
+@dataclass
+class Scene:
+    name: str
+    bodies: List[BodySpec]
+    n_env: int
+    jitter: float = 0.05
+    seed: int = 0
+
+    def is_static(self) -> np.ndarray:
+        return np.array([b.is_static for b in self.bodies], dtype=np.int32)
+
+    def poses(self, n_env: Optional[int] = None) -> np.ndarray:
+        """[n_env, n_bodies, 6]: base poses; every dynamic body jittered by
+        U(-j, j)^6 from one std::mt19937_64(seed) stream in (env, body) order."""
+        n = self.n_env if n_env is None else n_env
+        base = np.array([b.pose for b in self.bodies], dtype=np.float64)
+        dyn = np.flatnonzero(~self.is_static().astype(bool))
+        j = mt19937_64_uniform(self.seed, 6 * n * len(dyn), -self.jitter, self.jitter).reshape(n, len(dyn), 6)
+        out = np.repeat(base[None], n, axis=0)
+        out[:, dyn] += j
+        return out
+
+
+def drop_scene(n_env: int = 32768, n_boxes: int = 4) -> Scene:
+    """4 dynamic boxes (quad cube half 0.5, SQ eps 0.1, vertex_topk 0, edge_topk
+    4) stacked with 1 cm overlaps and a yaw twist over a static ground
+    (box_planes 2x2x0.1, edge_topk 4): 6 box-box + 4 box-ground pairs, 48
+    contacts each (builder-pinned parameters of config D)."""
+    ground = BodySpec("ground", MeshSpec(box_half=(2.0, 2.0, 0.1)), box_planes((2.0, 2.0, 0.1)),
+                      [0.0, 0.0, -0.1, 0.0, 0.0, 0.0], 0, 4, is_static=True)
+    boxes = [BodySpec(f"box{k}", MeshSpec(box_half=(0.5, 0.5, 0.5)), BOX_SQ,
+                      [0.03 * k, -0.02 * k, 0.49 + 0.99 * k] + rz_axis_angle(0.2 * k + 0.05), 0, 4)
+             for k in range(n_boxes)]
+    return Scene("drop", [ground] + boxes, n_env)
+
 WORKLOADS = {
     "box-box": box_box,
     "box-on-plane": box_on_plane,

@@ -107,6 +107,21 @@ def main():
                                        mean_dist=r["mean_dist"], layout=r["layout"], ee0=one["ee"],
                                        cfg=cfg_vec(c), warnings=np.array(rs[0].warnings + ["|"] + rs[1].warnings))
 
+    # --- config D scene: all body pairs (DemoSim::step pair loop) ---------------------
+    sc = W.drop_scene(4)
+    P = sc.poses(4)
+    ms = [ref_mesh(b) for b in sc.bodies]
+    rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, sc.bodies)]
+    from paper_2602_20304_b200 import api
+    pairs = api.scene_pairs(len(sc.bodies), sc.is_static())
+    scene = {"poses": P, "pairs": pairs}
+    for q, (i, j) in enumerate(pairs):
+        r = Ref.manifold_batch(rs[i], rs[j], P[:, i], P[:, j], SmoothingConfig(), 1)
+        scene[f"contacts{q}"] = r["contacts"]
+        scene[f"meta{q}"] = r["meta"]
+        scene[f"mean{q}"] = r["mean_dist"]
+    out["scene_drop"] = scene
+
     # --- forward-mode pose Jacobian (Dual12) on box-on-plane, one env ---------------
     ws = W.box_on_plane()
     ms = [ref_mesh(b) for b in ws.bodies]

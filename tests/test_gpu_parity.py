@@ -222,3 +222,30 @@ def test_invalid_config_fails_loudly(cuda):
     p = torch.zeros((4, 6), dtype=torch.float64, device="cuda")
     with pytest.raises(ValueError, match="smoothing: tau_pen must be > 0"):
         api.generate_manifold_batch(s1, s2, p, p, SmoothingConfig(tau_pen=-1.0))
+
+
+def test_scene_batch_all_pairs(cuda):
+    """Config D shape: all body pairs of the drop scene in one scene call,
+    vs the reference (golden) and the oracle at a larger batch."""
+    g = gold("scene_drop")
+    sc = W.drop_scene(4)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    res = api.generate_manifold_scene_batch(bodies, torch.as_tensor(g["poses"], device="cuda"), SmoothingConfig(),
+                                            is_static=sc.is_static(), want_src=True)
+    torch.cuda.synchronize()
+    assert [r["pair"] for r in res] == [tuple(p) for p in g["pairs"]]
+    for q, r in enumerate(res):
+        assert_parity(r["contacts"].cpu().numpy(), g[f"contacts{q}"], what=f"scene pair {r['pair']}")
+        assert np.array_equal(r["src"].cpu().numpy(), g[f"meta{q}"][..., 2:])
+    n = 512
+    P = sc.poses(n)
+    res = api.generate_manifold_scene_batch(bodies, torch.as_tensor(P, device="cuda"), SmoothingConfig(),
+                                            is_static=sc.is_static(), want_src=True)
+    torch.cuda.synchronize()
+    meshes = [b.mesh for b in bodies]
+    o = [Oracle.Surface(m.vertices, m.edges, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(meshes, sc.bodies)]
+    for r in res:
+        i, j = r["pair"]
+        ref = Oracle.manifold_batch(o[i], o[j], P[:, i], P[:, j], SmoothingConfig())
+        assert_parity(r["contacts"].cpu().numpy(), ref["contacts"], what=f"scene pair {(i, j)} vs oracle")
+        assert np.array_equal(r["src"].cpu().numpy(), ref["meta"][..., 2:])

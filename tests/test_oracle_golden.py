@@ -157,3 +157,20 @@ def test_mt19937_matches_reference_generator():
     from paper_2602_20304_b200.workloads import mt19937_64_uniform
     assert np.array_equal(mt19937_64_uniform(0, 24000, 0.0, 1.0), g["pairs"].reshape(-1))
     assert np.array_equal(Oracle.uniform(0, 24000), g["pairs"].reshape(-1))
+
+
+def test_scene_pairs_match_reference():
+    """Config D: every body pair of the multi-body drop scene (DemoSim::step
+    pair loop, src/demosim.cpp:88-104)."""
+    from paper_2602_20304_b200 import workloads as W
+    g = gold("scene_drop")
+    sc = W.drop_scene(4)
+    assert np.array_equal(api.scene_pairs(len(sc.bodies), sc.is_static()), g["pairs"])
+    meshes = [api.surface_from_spec(b).mesh for b in sc.bodies]
+    s = [Oracle.Surface(m.vertices, m.edges, b.sdf, b.vertex_topk, b.edge_topk)
+         for m, b in zip(meshes, sc.bodies)]
+    P = g["poses"]
+    for q, (i, j) in enumerate(g["pairs"]):
+        r = Oracle.manifold_batch(s[i], s[j], P[:, i], P[:, j], SmoothingConfig(), threads=2)
+        assert np.array_equal(r["meta"], g[f"meta{q}"])
+        assert np.allclose(r["contacts"], g[f"contacts{q}"], rtol=1e-9, atol=1e-10)
