@@ -206,6 +206,28 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
                              float* mean_dist_host, float* contacts_host, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * Pose Jacobians — generate_manifold<Dual12> with seed_pose_tangents
+ * (include/cmg/dual.hpp:249-263; tests/test_dual.cpp gradchecks) for every
+ * env: each output scalar's derivative w.r.t. the 12 pose coordinates
+ * (pose1[0..5], pose2[0..5]). Smooth mode only: hard_ops != 0 returns
+ * CMGB_ERR_UNSUPPORTED (the reference's hard operators are double-only,
+ * smooth_ops.hpp:199).
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_manifold_jvp_out {
+  float* contacts;        /* required: [n_env][n_contacts][8] primal, as cmgb_manifold_out */
+  float* tangents;        /* required: [n_env][n_contacts][8][12] d(field)/d(pose coord)    */
+  int32_t* src;           /* optional: [n_env][n_contacts][2] provenance                     */
+  float* mean_dist;       /* optional: [n_env]                                               */
+  float* mean_dist_grad;  /* optional: [n_env][12] tangents of mean_contact_distance         */
+} cmgb_manifold_jvp_out;
+
+/* poses*: DEVICE [n][6] FP64, strides as cmgb_manifold_batch. */
+int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1,
+                            int32_t pose1_stride, const double* poses2, int32_t pose2_stride,
+                            int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_jvp_out* out,
+                            void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * Multi-body scenes — the all-pairs loop of DemoSim::step (src/demosim.cpp:
  * 88-104): every body pair (i < j) except static-static, for every env.
  * ------------------------------------------------------------------------- */

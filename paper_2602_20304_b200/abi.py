@@ -95,6 +95,16 @@ class CmgbManifoldOut(C.Structure):
     ]
 
 
+class CmgbManifoldJvpOut(C.Structure):
+    _fields_ = [
+        ("contacts", C.c_void_p),
+        ("tangents", C.c_void_p),
+        ("src", C.c_void_p),
+        ("mean_dist", C.c_void_p),
+        ("mean_dist_grad", C.c_void_p),
+    ]
+
+
 # Every exported symbol of include/cmgb.h with its ctypes signature.
 _P = C.c_void_p
 _I = C.c_int
@@ -146,6 +156,11 @@ SIGNATURES = {
     ),
     "cmgb_device_count": (_I, [C.POINTER(C.c_int32)]),
     "cmgb_manifold_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
+    "cmgb_manifold_jvp_batch": (
+        _I,
+        [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig),
+         C.POINTER(CmgbManifoldJvpOut), _P],
+    ),
     "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
     "cmgb_manifold_scene_batch": (
         _I,

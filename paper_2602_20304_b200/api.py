@@ -205,6 +205,49 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
     return res
 
 
+def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, *,
+                                want_src: bool = False, stream=None) -> dict:
+    """Pose Jacobians of the batched manifold: generate_manifold<Dual12> seeded
+    by seed_pose_tangents (dual.hpp:249-263) for every env. poses* as in
+    generate_manifold_batch. Returns CUDA tensors: contacts [n, C, 8] (primal),
+    tangents [n, C, 8, 12] (d field / d (pose1[0..5], pose2[0..5])), mean_dist [n],
+    mean_dist_grad [n, 12], optionally src [n, C, 2]. Smooth mode only."""
+    import torch
+
+    c = _cfg(cfg)
+    p1 = poses1.reshape(-1, 6)
+    p2 = poses2.reshape(-1, 6)
+    if p1.dtype != torch.float64 or p2.dtype != torch.float64 or not p1.is_cuda or not p2.is_cuda:
+        raise ValueError("poses must be CUDA float64 tensors")
+    p1 = p1.contiguous()
+    p2 = p2.contiguous()
+    n = max(p1.shape[0], p2.shape[0])
+    st1 = 1 if (p1.shape[0] == n and n > 1) else 0
+    st2 = 1 if (p2.shape[0] == n and n > 1) else 0
+    if n == 1:
+        st1 = st2 = 1
+    Cn = layout(s1, s2, c)["n_contacts"]
+    dev = p2.device
+    res = {
+        "contacts": torch.empty((n, Cn, 8), dtype=torch.float32, device=dev),
+        "tangents": torch.empty((n, Cn, 8, 12), dtype=torch.float32, device=dev),
+        "mean_dist": torch.empty((n,), dtype=torch.float32, device=dev),
+        "mean_dist_grad": torch.empty((n, 12), dtype=torch.float32, device=dev),
+    }
+    if want_src:
+        res["src"] = torch.empty((n, Cn, 2), dtype=torch.int32, device=dev)
+    o = abi.CmgbManifoldJvpOut()
+    o.contacts = res["contacts"].data_ptr()
+    o.tangents = res["tangents"].data_ptr()
+    o.src = res["src"].data_ptr() if want_src else None
+    o.mean_dist = res["mean_dist"].data_ptr()
+    o.mean_dist_grad = res["mean_dist_grad"].data_ptr()
+    with torch.cuda.device(dev):
+        _ok(abi.load().cmgb_manifold_jvp_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
+                                               C.byref(c), C.byref(o), _stream_ptr(stream)))
+    return res
+
+
 def scene_pairs(n_bodies: int, is_static=None) -> np.ndarray:
     """Body pairs (i < j, skipping static-static) in DemoSim::step's order
     (src/demosim.cpp:88-104)."""

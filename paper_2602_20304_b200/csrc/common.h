@@ -125,6 +125,20 @@ struct ManifoldParams {
   float* mean_dist;
 };
 
+// Pose-Jacobian (forward-mode, Dual12) batch: the geometry / config / slot
+// counts of a ManifoldParams plan, one CTA per (env, direction group), each
+// group carrying `nd` of the 12 pose tangent directions (dual.hpp:249-263).
+// Shared-memory offsets are in bytes from the CTA base (host-computed: the
+// scalar is nd + 1 doubles).
+struct JvpParams {
+  ManifoldParams m;
+  float* tangents;   // [n_env][C][8][12]
+  float* mean_grad;  // [n_env][12]
+  int32_t nd, groups;
+  int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
+  int32_t bytes;
+};
+
 struct WitnessParams {
   const void* pairs;
   int32_t fp64;
@@ -141,6 +155,8 @@ struct WitnessParams {
 namespace cmgb {
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream);
+int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
+int jvp_directions();  // tangent directions per thread of the compiled JVP kernel
 int launch_ee_witness(const WitnessParams& p, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);
 const char* last_cuda_error_string();

@@ -111,18 +111,24 @@ __device__ __forceinline__ double log_d(double v) {
   return fma((double)e, kMC.ln2, 2.0 * s * p);
 }
 
+// Primal of a scalar (the Dual<N> overload lives in dual.cuh): branches of the
+// templated routines read it, like the reference's HardBranchScope reads.
+__device__ __forceinline__ double pv(double x) { return x; }
+
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
 // function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each
 // to full relative precision (the blends need the small one exactly).
-__device__ __forceinline__ void sigmoid_pair_d(double x, double* s, double* c) {
-  const double e = exp_d(-fabs(x));
-  const double inv = rcp_d(1.0 + e);
-  const double small = e * inv;
-  *s = x >= 0.0 ? inv : small;
-  *c = x >= 0.0 ? small : inv;
+template <class T>
+__device__ __forceinline__ void sigmoid_pair_d(const T& x, T* s, T* c) {
+  const T e = exp_d(-fabs(x));
+  const T inv = rcp_d(1.0 + e);
+  const T small = e * inv;
+  *s = pv(x) >= 0.0 ? inv : small;
+  *c = pv(x) >= 0.0 ? small : inv;
 }
-__device__ __forceinline__ double sigmoid_d(double x) {
-  double s, c;
+template <class T>
+__device__ __forceinline__ T sigmoid_d(const T& x) {
+  T s, c;
   sigmoid_pair_d(x, &s, &c);
   return s;
 }
@@ -161,40 +167,40 @@ __device__ __forceinline__ float3 mul_R_f(const double* R, float3 v) {
 }
 
 // se3_exp (pose.hpp:37-91) in FP64; series branch below theta^2 = 1e-8.
-__device__ __forceinline__ void se3_exp_d(const double* xi, double* R, double* t) {
-  const double wx = xi[3], wy = xi[4], wz = xi[5];
-  const double th2 = wx * wx + wy * wy + wz * wz;
-  double a, b, c;
-  if (th2 < 1e-8) {
+// T = double (frames kernel) or Dual<N> (pose tangents, manifold_jvp.cu).
+template <class T>
+__device__ __forceinline__ void se3_exp_d(const T* xi, T* R, T* t) {
+  const T wx = xi[3], wy = xi[4], wz = xi[5];
+  const T th2 = wx * wx + wy * wy + wz * wz;
+  T a, b, c;
+  if (pv(th2) < 1e-8) {
     a = 1.0 - th2 / 6.0 + th2 * th2 / 120.0;
     b = 0.5 - th2 / 24.0 + th2 * th2 / 720.0;
     c = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
   } else {
-    const double th = sqrt(th2);
-    double s, co;
+    const T th = sqrt(th2);
+    T s, co;
     sincos(th, &s, &co);
     a = s / th;
     b = (1.0 - co) / th2;
     c = (1.0 - a) / th2;
   }
-  const double W[9] = {0.0, -wz, wy, wz, 0.0, -wx, -wy, wx, 0.0};
-  double W2[9];
+  const T W[9] = {0.0, -wz, wy, wz, 0.0, -wx, -wy, wx, 0.0};
+  T W2[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j)
       W2[3 * i + j] = W[3 * i] * W[j] + W[3 * i + 1] * W[3 + j] + W[3 * i + 2] * W[6 + j];
-  double V[9];
+  T V[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const double id = (i % 4 == 0) ? 1.0 : 0.0;
     R[i] = (id + W[i] * a) + W2[i] * b;
     V[i] = (id + W[i] * b) + W2[i] * c;
   }
-  const double3 r = mul_R(V, d3(xi[0], xi[1], xi[2]));
-  t[0] = r.x;
-  t[1] = r.y;
-  t[2] = r.z;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = V[3 * i] * xi[0] + V[3 * i + 1] * xi[1] + V[3 * i + 2] * xi[2];
 }
 
 }  // namespace cmgb

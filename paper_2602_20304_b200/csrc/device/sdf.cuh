@@ -20,27 +20,34 @@
 
 #include "../common.h"
 #include "dmath.cuh"
+#include "dual.cuh"
 
 namespace cmgb {
 
-struct SdfOut {
-  double v;
-  double3 g;
+// Every routine is templated on the scalar T: double for the value kernels,
+// Dual<N> for the pose-Jacobian kernel (dual.cuh). T = double compiles to the
+// same code as a plain double implementation.
+template <class T>
+struct SdfOutT {
+  T v;
+  vec3<T> g;
 };
+using SdfOut = SdfOutT<double>;
 
 // x^n for a small positive integer n (warp-uniform), FP64 products.
-__device__ __forceinline__ double ipow_d(double x, int n) {
+template <class T>
+__device__ __forceinline__ T ipow_d(const T& x, int n) {
   switch (n) {
     case 1: return x;
     case 2: return x * x;
-    case 4: { const double x2 = x * x; return x2 * x2; }
-    case 5: { const double x2 = x * x; return x2 * x2 * x; }
-    case 9: { const double x2 = x * x, x4 = x2 * x2; return x4 * x4 * x; }
-    case 10: { const double x2 = x * x, x4 = x2 * x2; return x4 * x4 * x2; }
-    case 19: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x2 * x; }
-    case 20: { const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x4; }
+    case 4: { const T x2 = x * x; return x2 * x2; }
+    case 5: { const T x2 = x * x; return x2 * x2 * x; }
+    case 9: { const T x2 = x * x, x4 = x2 * x2; return x4 * x4 * x; }
+    case 10: { const T x2 = x * x, x4 = x2 * x2; return x4 * x4 * x2; }
+    case 19: { const T x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x2 * x; }
+    case 20: { const T x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8; return x16 * x4; }
     default: {
-      double r = 1.0, b = x;
+      T r = 1.0, b = x;
 #pragma unroll 1
       for (int e = n; e; e >>= 1) {
         if (e & 1) r *= b;
@@ -52,21 +59,18 @@ __device__ __forceinline__ double ipow_d(double x, int n) {
 }
 
 // Compile-time integer power (N > 0) for specialised superquadric kinds.
-template <int N>
-__device__ __forceinline__ double cpow(double x) {
+template <int N, class T>
+__device__ __forceinline__ T cpow(const T& x) {
   if constexpr (N == 1) return x;
-  else if constexpr (N % 2 == 0) { const double h = cpow<N / 2>(x); return h * h; }
+  else if constexpr (N % 2 == 0) { const T h = cpow<N / 2>(x); return h * h; }
   else return cpow<N - 1>(x) * x;
 }
 
-// (x^p, x^(p-1)): compile-time exponent N > 0, or runtime (N == 0).
-template <int N>
-__device__ __forceinline__ void pow_pair_t(double x, int n, double p, double& xp, double& xpm1);
-
 // (x^p, x^(p-1)) in FP64: integer chains (no SFU) or libdevice pow.
-__device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp, double& xpm1) {
+template <class T>
+__device__ __forceinline__ void pow_pair_d(const T& x, int n, double p, T& xp, T& xpm1) {
   if (n > 0) {
-    xpm1 = n == 1 ? 1.0 : ipow_d(x, n - 1);
+    xpm1 = n == 1 ? T(1.0) : ipow_d(x, n - 1);
     xp = xpm1 * x;
   } else {
     xp = pow(x, p);
@@ -74,8 +78,9 @@ __device__ __forceinline__ void pow_pair_d(double x, int n, double p, double& xp
   }
 }
 
-template <int N>
-__device__ __forceinline__ void pow_pair_t(double x, int n, double p, double& xp, double& xpm1) {
+// (x^p, x^(p-1)): compile-time exponent N > 0, or runtime (N == 0).
+template <int N, class T>
+__device__ __forceinline__ void pow_pair_t(const T& x, int n, double p, T& xp, T& xpm1) {
   if constexpr (N == 0) {
     pow_pair_d(x, n, p, xp, xpm1);
   } else if constexpr (N == 1) {
@@ -120,183 +125,194 @@ __device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, d
   return -em1;
 }
 
+// Dual overload: primal by the routine above (bit-identical to the value
+// path), tangents by the chain rule d(f^p4) = p4 f^p4 / f df.
+template <int N4 = 0, int N>
+__device__ __forceinline__ Dual<N> one_minus_pow(const Dual<N>& f, double p4, int n_rt, Dual<N>* F) {
+  double Fv;
+  const double om = one_minus_pow<N4>(f.v, p4, n_rt, &Fv);
+  const double s = p4 * Fv * rcp_d(f.v);
+  *F = Dual<N>::chain(Fv, s, f);
+  return Dual<N>::chain(om, -s, f);
+}
+
 // Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64). N1..N4 > 0
 // compile in the exponents (kSqE01); 0 reads them from the descriptor.
-template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0>
-__device__ __forceinline__ SdfOut sq_leaf(const DevSq& q, double3 p) {
-  if (q.has_frame) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));  // apply_inverse
-  const double xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
-  const double x2 = fma(xn, xn, kMC.floor30), y2 = fma(yn, yn, kMC.floor30), z2 = fma(zn, zn, kMC.floor30);
-  double A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
+template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0, class T = double>
+__device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
+  if (q.has_frame) p = mul_Rt(q.R, p - mk3<T>(q.t[0], q.t[1], q.t[2]));  // apply_inverse
+  const T xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
+  const T x2 = fma(xn, xn, T(kMC.floor30)), y2 = fma(yn, yn, T(kMC.floor30)), z2 = fma(zn, zn, T(kMC.floor30));
+  T A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
   pow_pair_t<N1>(x2, q.n1, q.p1, A, Am1);
   pow_pair_t<N1>(y2, q.n1, q.p1, B, Bm1);
-  const double g = A + B;
+  const T g = A + B;
   pow_pair_t<N2>(g, q.n2, q.p2, G, Gm1);
   pow_pair_t<N3>(z2, q.n3, q.p3, Cz, Czm1);
-  const double f = G + Cz;
-  SdfOut out;
+  const T f = G + Cz;
+  SdfOutT<T> out;
   out.v = 0.0;
-  out.g = d3(0, 0, 0);
+  out.g = mk3<T>(0.0, 0.0, 0.0);
   if (FL == kValue) {
-    const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
-    double F;
+    const T r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, T(kMC.floor20))));
+    T F;
     out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);  // (1 - f^p4) / |x~|
     return out;
   }
   // grad f w.r.t. the normalised coordinates (d(x2^p1)/dxn = 2 p1 x2^(p1-1) xn);
   // the body-frame gradient is diag(1/axes) times it.
-  const double cxy = q.c_xy * Gm1;
-  const double3 dfn = d3(cxy * Am1 * xn, cxy * Bm1 * yn, q.c_z * Czm1 * zn);
+  const T cxy = q.c_xy * Gm1;
+  const vec3<T> dfn = mk3<T>(cxy * Am1 * xn, cxy * Bm1 * yn, q.c_z * Czm1 * zn);
   if (FL == kNormalOnly || FL == kNormalSource) {
-    const double3 df = d3(dfn.x * q.inv_ax[0], dfn.y * q.inv_ax[1], dfn.z * q.inv_ax[2]);
+    const vec3<T> df = mk3<T>(dfn.x * q.inv_ax[0], dfn.y * q.inv_ax[1], dfn.z * q.inv_ax[2]);
     if (FL == kNormalSource) {
-      const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
-      double F;
+      const T r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, T(kMC.floor20))));
+      T F;
       out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);
     }
     out.g = q.has_frame ? mul_R(q.R, df) : df;
     return out;
   }
   // kGrad: grad phi = diag(1/axes) (-p4 (F/f) grad_n f - phi x~ / r) / r
-  const double r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, kMC.floor20)));
-  const double rinv = rsqrt_d(r2);
-  double F;
-  const double omF = one_minus_pow<N4>(f, q.p4, q.n4, &F);
-  const double phi = omF * rinv;
+  const T r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, T(kMC.floor20))));
+  const T rinv = rsqrt_d(r2);
+  T F;
+  const T omF = one_minus_pow<N4>(f, q.p4, q.n4, &F);
+  const T phi = omF * rinv;
   out.v = phi;
-  const double k = -q.p4 * F * rcp_d(f);
-  const double h = phi * rinv;
-  const double sx = q.inv_ax[0] * rinv, sy = q.inv_ax[1] * rinv, sz = q.inv_ax[2] * rinv;
-  const double3 gl = d3(sx * fma(k, dfn.x, -h * xn), sy * fma(k, dfn.y, -h * yn), sz * fma(k, dfn.z, -h * zn));
+  const T k = -q.p4 * F * rcp_d(f);
+  const T h = phi * rinv;
+  const T sx = q.inv_ax[0] * rinv, sy = q.inv_ax[1] * rinv, sz = q.inv_ax[2] * rinv;
+  const vec3<T> gl = mk3<T>(sx * fma(k, dfn.x, -h * xn), sy * fma(k, dfn.y, -h * yn), sz * fma(k, dfn.z, -h * zn));
   out.g = q.has_frame ? mul_R(q.R, gl) : gl;
   return out;
 }
 
 // Convex polyhedron leaf: LSE over plane distances (sdf.hpp:110-117).
 // Pool per plane: double4 (n.x, n.y, n.z, n . point); distances in FP64.
-template <int FL>
-__device__ __forceinline__ SdfOut cp_leaf(const DevNode& nd, const double4* pool, double3 p) {
+template <int FL, class T = double>
+__device__ __forceinline__ SdfOutT<T> cp_leaf(const DevNode& nd, const double4* pool, vec3<T> p) {
   const double4* pl = pool + nd.offset;
-  double m = -INFINITY;
+  T m = -INFINITY;
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
     const double4 q = pl[i];
-    m = fmax(m, fma(q.x, p.x, fma(q.y, p.y, fma(q.z, p.z, -q.w))));
+    m = fmax(m, fma(T(q.x), p.x, fma(T(q.y), p.y, fma(T(q.z), p.z, T(-q.w)))));
   }
-  double acc = 0.0;
-  double3 g = d3(0, 0, 0);
+  T acc = 0.0;
+  vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
     const double4 q = pl[i];
-    const double d = fma(q.x, p.x, fma(q.y, p.y, fma(q.z, p.z, -q.w)));
-    const double e = exp((d - m) * nd.inv_tau_d);
+    const T d = fma(T(q.x), p.x, fma(T(q.y), p.y, fma(T(q.z), p.z, T(-q.w))));
+    const T e = exp((d - m) * nd.inv_tau_d);
     acc += e;
-    if (FL != kValue) g = g + d3(e * q.x, e * q.y, e * q.z);
+    if (FL != kValue) g = g + mk3<T>(e * q.x, e * q.y, e * q.z);
   }
-  SdfOut out;
+  SdfOutT<T> out;
   out.v = m + nd.tau_d * log(acc);
-  out.g = d3(0, 0, 0);
+  out.g = mk3<T>(0.0, 0.0, 0.0);
   if (FL != kValue) out.g = dscale(g, rcp_d(acc));
   return out;
 }
 
 // Oriented pointcloud leaf (sdf.hpp:119-132). Pool per point: double4
 // (p, -1/(2 th^2)), double4 (n, 1/th^2). Sums in FP64.
-template <int FL>
-__device__ __forceinline__ SdfOut opc_leaf(const DevNode& nd, const double4* pool, double3 p) {
+template <int FL, class T = double>
+__device__ __forceinline__ SdfOutT<T> opc_leaf(const DevNode& nd, const double4* pool, vec3<T> p) {
   const double4* pt = pool + nd.offset;
-  double num = 0.0, den = 1e-30;
-  double3 dnum = d3(0, 0, 0), dden = d3(0, 0, 0);
+  T num = 0.0, den = 1e-30;
+  vec3<T> dnum = mk3<T>(0.0, 0.0, 0.0), dden = mk3<T>(0.0, 0.0, 0.0);
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
     const double4 a = pt[2 * i], b = pt[2 * i + 1];
-    const double rx = p.x - a.x, ry = p.y - a.y, rz = p.z - a.z;
-    const double arg = (rx * rx + ry * ry + rz * rz) * a.w;
-    const double w = exp(arg);
-    const double nr = b.x * rx + b.y * ry + b.z * rz;
+    const T rx = p.x - a.x, ry = p.y - a.y, rz = p.z - a.z;
+    const T arg = (rx * rx + ry * ry + rz * rz) * a.w;
+    const T w = exp(arg);
+    const T nr = b.x * rx + b.y * ry + b.z * rz;
     num = fma(w, nr, num);
     den += w;
     if (FL != kValue) {
-      const double s = -w * b.w;  // dw = -w r / th^2
-      dnum = dnum + d3(s * rx * nr + w * b.x, s * ry * nr + w * b.y, s * rz * nr + w * b.z);
-      dden = dden + d3(s * rx, s * ry, s * rz);
+      const T s = -w * b.w;  // dw = -w r / th^2
+      dnum = dnum + mk3<T>(s * rx * nr + w * b.x, s * ry * nr + w * b.y, s * rz * nr + w * b.z);
+      dden = dden + mk3<T>(s * rx, s * ry, s * rz);
     }
   }
-  SdfOut out;
-  const double inv = rcp_d(den);
+  SdfOutT<T> out;
+  const T inv = rcp_d(den);
   out.v = num * inv;
-  out.g = d3(0, 0, 0);
+  out.g = mk3<T>(0.0, 0.0, 0.0);
   if (FL != kValue)
-    out.g = d3((dnum.x - out.v * dden.x) * inv, (dnum.y - out.v * dden.y) * inv,
+    out.g = mk3<T>((dnum.x - out.v * dden.x) * inv, (dnum.y - out.v * dden.y) * inv,
                (dnum.z - out.v * dden.z) * inv);
   return out;
 }
 
-template <int FL>
-__device__ __forceinline__ SdfOut leaf_eval(const DevNode& nd, const double4* pool, double3 p) {
-  if (nd.op == 0) return sq_leaf<FL>(nd.sq, p);
-  if (nd.op == 1) return cp_leaf<FL>(nd, pool, p);
-  return opc_leaf<FL>(nd, pool, p);
+template <int FL, class T = double>
+__device__ __forceinline__ SdfOutT<T> leaf_eval(const DevNode& nd, const double4* pool, vec3<T> p) {
+  if (nd.op == 0) return sq_leaf<FL, 0, 0, 0, 0, T>(nd.sq, p);
+  if (nd.op == 1) return cp_leaf<FL, T>(nd, pool, p);
+  return opc_leaf<FL, T>(nd, pool, p);
 }
 
 // Full program evaluation in the BODY frame. KIND (SdfKind) is a compile-time
 // specialisation chosen on the host per surface: each kernel instantiation
 // carries only the field code it needs (I-cache footprint).
-template <int FL_IN, int KIND>
-__device__ SdfOut sdf_eval(const DevSdf& s, double3 p) {
-  if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN>(s.nodes[0].sq, p);
-  if constexpr (KIND == kSqE01) return sq_leaf<FL_IN, 10, 1, 10, 20>(s.nodes[0].sq, p);
+template <int FL_IN, int KIND, class T = double>
+__device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
+  if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN, 0, 0, 0, 0, T>(s.nodes[0].sq, p);
+  if constexpr (KIND == kSqE01) return sq_leaf<FL_IN, 10, 1, 10, 20, T>(s.nodes[0].sq, p);
   // kNormalOnly skips phi only for a lone SQ leaf; compositions need the values.
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;
-  if constexpr (KIND == kSingleCp) return cp_leaf<FL>(s.nodes[0], s.pool, p);
+  if constexpr (KIND == kSingleCp) return cp_leaf<FL, T>(s.nodes[0], s.pool, p);
   // Generic postfix interpreter (union: -LSE(-phi), subtraction: LSE(phi+, -phi-);
   // sdf.hpp:222-230, 260-287). Warp-uniform control flow.
-  double sv[kMaxStack];
-  double3 sg[kMaxStack];
+  T sv[kMaxStack];
+  vec3<T> sg[kMaxStack];
   int sp = 0;
 #pragma unroll 1
   for (int i = 0; i < s.n_nodes; ++i) {
     const DevNode& nd = s.nodes[i];
     if (nd.op <= 2) {
-      const SdfOut r = leaf_eval<FL>(nd, s.pool, p);
+      const SdfOutT<T> r = leaf_eval<FL, T>(nd, s.pool, p);
       sv[sp] = r.v;
       sg[sp] = r.g;
       ++sp;
     } else if (nd.op == 3) {  // union: softmin weights, first minimum
       const int n = nd.count, base = sp - n;
-      double m = sv[base];
+      T m = sv[base];
 #pragma unroll 1
       for (int k = 1; k < n; ++k) m = fmin(m, sv[base + k]);
-      double acc = 0.0;
-      double3 g = d3(0, 0, 0);
+      T acc = 0.0;
+      vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
 #pragma unroll 1
       for (int k = 0; k < n; ++k) {
-        const double arg = (m - sv[base + k]) * nd.inv_tau_d;
-        const double e = exp(arg);
+        const T arg = (m - sv[base + k]) * nd.inv_tau_d;
+        const T e = exp(arg);
         acc += e;
         if (kWantG) g = g + dscale(sg[base + k], e);
       }
       sp = base;
       sv[sp] = m - nd.tau_d * log(acc);
-      sg[sp] = kWantG ? dscale(g, rcp_d(acc)) : d3(0, 0, 0);
+      sg[sp] = kWantG ? dscale(g, rcp_d(acc)) : mk3<T>(0.0, 0.0, 0.0);
       ++sp;
     } else {  // subtraction: args (phi+, -phi-), softmax weights
       const int a = sp - 2, b = sp - 1;
-      const double a0 = sv[a], a1 = -sv[b];
-      const double m = fmax(a0, a1);
-      const double e0 = exp((a0 - m) * nd.inv_tau_d);
-      const double e1 = exp((a1 - m) * nd.inv_tau_d);
-      const double acc = e0 + e1;
+      const T a0 = sv[a], a1 = -sv[b];
+      const T m = fmax(a0, a1);
+      const T e0 = exp((a0 - m) * nd.inv_tau_d);
+      const T e1 = exp((a1 - m) * nd.inv_tau_d);
+      const T acc = e0 + e1;
       sv[a] = m + nd.tau_d * log(acc);
       if (kWantG) {
-        const double inv = rcp_d(acc);
+        const T inv = rcp_d(acc);
         sg[a] = dscale(sg[a], e0 * inv) - dscale(sg[b], e1 * inv);
       }
       sp = a + 1;
     }
   }
-  SdfOut out;
+  SdfOutT<T> out;
   out.v = sv[0];
   out.g = sg[0];
   return out;

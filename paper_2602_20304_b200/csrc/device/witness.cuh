@@ -10,67 +10,74 @@
 
 #include "../common.h"
 #include "dmath.cuh"
+#include "dual.cuh"
 
 namespace cmgb {
 
 // exp(-|x - 1| / tau) from a = exp(-|x| / tau) and C = exp(-1 / tau):
 // |x| and |x - 1| differ by exactly 1, so b = a C (x < 0), C / a (0 <= x <= 1),
 // a / C (x > 1) -- one SFU-free exponential per softplus / sigmoid pair.
-__device__ __forceinline__ double partner_exp(double x, double a, double C, double inv_C,
-                                              double inv_tau, int pair) {
+// Templated on the scalar (double / Dual<N>, dual.cuh) like every routine here;
+// the partner identities hold as functions of x, so tangents are exact too.
+template <class T>
+__device__ __forceinline__ T partner_exp(const T& x, const T& a, double C, double inv_C,
+                                         double inv_tau, int pair) {
   if (!pair) return exp_d(-fabs(x - 1.0) * inv_tau);
-  return x < 0.0 ? a * C : (x <= 1.0 ? C * rcp_d(a) : a * inv_C);
+  return pv(x) < 0.0 ? a * C : (pv(x) <= 1.0 ? C * rcp_d(a) : a * inv_C);
 }
 
 // clip01 (witness.hpp:45-52): clip_s(x, 0, 1, tau) = softplus(x) - softplus(x - 1)
 // (smooth_ops.hpp:66-89) = [max(x,0) - max(x-1,0)] + tau log1p((a - b) / (1 + b)),
 // a = exp(-|x|/tau), b = exp(-|x-1|/tau); hard: clamp.
-__device__ __forceinline__ double clip01(double x, const DevCfg& c) {
-  if (c.hard_ops) return fmin(fmax(x, 0.0), 1.0);
-  const double a = exp_d(-fabs(x) * c.inv_tau_clip);
-  const double b = partner_exp(x, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
+template <class T>
+__device__ __forceinline__ T clip01(const T& x, const DevCfg& c) {
+  if (c.hard_ops) return fmin(fmax(x, T(0.0)), T(1.0));
+  const T a = exp_d(-fabs(x) * c.inv_tau_clip);
+  const T b = partner_exp(x, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
   // tau (log1p(a) - log1p(b)) = tau log((1 + a) / (1 + b)); the quotient is
   // formed in FP64 (absolute error ~1e-16, scaled by tau)
-  return (fmax(x, 0.0) - fmax(x - 1.0, 0.0)) + c.tau_clip * log_d((1.0 + a) * rcp_d(1.0 + b));
+  return (fmax(x, T(0.0)) - fmax(x - 1.0, T(0.0))) + c.tau_clip * log_d((1.0 + a) * rcp_d(1.0 + b));
 }
 
 // within01 (witness.hpp:54-61): gamma = sigma(x/tau) sigma((1-x)/tau) and its
 // complement 1 - gamma = (1 - s1) + s1 (1 - s2), both relatively accurate;
 // hard mode: [0 <= x <= 1] exactly (within_hard, smooth_ops.hpp:204-206).
-__device__ __forceinline__ void within01(double x, double inv_tau, double C, double inv_C, int pair,
-                                         int hard, double* g, double* omg) {
+template <class T>
+__device__ __forceinline__ void within01(const T& x, double inv_tau, double C, double inv_C, int pair,
+                                         int hard, T* g, T* omg) {
   if (hard) {
-    const bool in = x >= 0.0 && x <= 1.0;
+    const bool in = pv(x) >= 0.0 && pv(x) <= 1.0;
     *g = in ? 1.0 : 0.0;
     *omg = in ? 0.0 : 1.0;
     return;
   }
-  const double e1 = exp_d(-fabs(x) * inv_tau);            // sigma(x/tau) pair
-  const double e2 = partner_exp(x, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
-  const double i1 = rcp_d(1.0 + e1), i2 = rcp_d(1.0 + e2);
-  const double s1 = x >= 0.0 ? i1 : e1 * i1, c1 = x >= 0.0 ? e1 * i1 : i1;
-  const double s2 = x <= 1.0 ? i2 : e2 * i2, c2 = x <= 1.0 ? e2 * i2 : i2;
+  const T e1 = exp_d(-fabs(x) * inv_tau);            // sigma(x/tau) pair
+  const T e2 = partner_exp(x, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
+  const T i1 = rcp_d(1.0 + e1), i2 = rcp_d(1.0 + e2);
+  const bool ge0 = pv(x) >= 0.0, le1 = pv(x) <= 1.0;
+  const T s1 = ge0 ? i1 : e1 * i1, c1 = ge0 ? e1 * i1 : i1;
+  const T s2 = le1 ? i2 : e2 * i2, c2 = le1 ? e2 * i2 : i2;
   *g = s1 * s2;
   *omg = c1 + s1 * c2;
 }
 
 // Product of indicators and its complement: 1 - ab = (1 - a) + a (1 - b).
-__device__ __forceinline__ void within_and(double a, double oma, double b, double omb, double* g,
-                                           double* omg) {
+template <class T>
+__device__ __forceinline__ void within_and(const T& a, const T& oma, const T& b, const T& omb, T* g,
+                                           T* omg) {
   *g = a * b;
   *omg = oma + a * omb;
 }
 
 // argmin over n costs: soft (argmin_s, smooth_ops.hpp:126-144) or first-min
 // one-hot (argmin_hard, 210-218). Returns the winner = first argmax weight.
-template <int N>
-__device__ __forceinline__ int pick_min(const double (&cost)[N], double (&w)[N], double inv_tau,
-                                        int hard) {
+template <int N, class T>
+__device__ __forceinline__ int pick_min(const T (&cost)[N], T (&w)[N], double inv_tau, int hard) {
   int best = 0;
-  double m = cost[0];
+  T m = cost[0];
 #pragma unroll
   for (int i = 1; i < N; ++i)
-    if (cost[i] < m) {
+    if (pv(cost[i]) < pv(m)) {
       best = i;
       m = cost[i];
     }
@@ -79,68 +86,72 @@ __device__ __forceinline__ int pick_min(const double (&cost)[N], double (&w)[N],
     for (int i = 0; i < N; ++i) w[i] = i == best ? 1.0 : 0.0;
     return best;
   }
-  double total = 0.0;
+  T total = 0.0;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    w[i] = i == best ? 1.0 : exp_d((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
+    w[i] = i == best ? T(1.0) : exp_d((m - cost[i]) * inv_tau);  // exp(0) = 1 at the minimum
     total += w[i];
   }
-  const double inv = rcp_d(total);
+  const T inv = rcp_d(total);
 #pragma unroll
   for (int i = 0; i < N; ++i) w[i] *= inv;
   return best;
 }
 
-struct QpSol {
-  double a1, a2;
-  double gamma;
+template <class T>
+struct QpSolT {
+  T a1, a2;
+  T gamma;
   int label;
 };
+using QpSol = QpSolT<double>;
 
 // solve_box_qp_2 (witness.hpp:74-121), erratum-fixed cost 4 (witness.hpp:99).
-__device__ __forceinline__ QpSol solve_box_qp_2(double q1, double q2, double q3, double c1,
-                                                double c2, const DevCfg& c) {
-  const double i1 = rcp_d(q1), i3 = rcp_d(q3);
-  const double q2_over_q1 = q2 * i1, q2_over_q3 = q2 * i3;
-  const double c1_over_q1 = c1 * i1, c2_over_q3 = c2 * i3;
-  const double a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
-  const double a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
-  const double a1_1_a2 = clip01(-(q2_over_q3 + c2_over_q3), c);
-  const double a1_0_a2 = clip01(-c2_over_q3, c);
-  const double a2_1_a1 = clip01(-(q2_over_q1 + c1_over_q1), c);
-  const double a2_0_a1 = clip01(-c1_over_q1, c);
-  const double cost[4] = {
+template <class T>
+__device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, const T& q3, const T& c1,
+                                                    const T& c2, const DevCfg& c) {
+  const T i1 = rcp_d(q1), i3 = rcp_d(q3);
+  const T q2_over_q1 = q2 * i1, q2_over_q3 = q2 * i3;
+  const T c1_over_q1 = c1 * i1, c2_over_q3 = c2 * i3;
+  const T a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
+  const T a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
+  const T a1_1_a2 = clip01(-(q2_over_q3 + c2_over_q3), c);
+  const T a1_0_a2 = clip01(-c2_over_q3, c);
+  const T a2_1_a1 = clip01(-(q2_over_q1 + c1_over_q1), c);
+  const T a2_0_a1 = clip01(-c1_over_q1, c);
+  const T cost[4] = {
       0.5 * (q1 + 2.0 * q2 * a1_1_a2 + q3 * a1_1_a2 * a1_1_a2) + c1 + c2 * a1_1_a2,
       0.5 * q3 * a1_0_a2 * a1_0_a2 + c2 * a1_0_a2,
       0.5 * (q1 * a2_1_a1 * a2_1_a1 + 2.0 * q2 * a2_1_a1 + q3) + c1 * a2_1_a1 + c2,
       0.5 * q1 * a2_0_a1 * a2_0_a1 + c1 * a2_0_a1,
   };
-  double w[4];
+  T w[4];
   const int best = pick_min<4>(cost, w, c.inv_tau_min, c.hard_ops);
   // constrained = sum_i w_i cand_i (witness.hpp:101-113)
-  const double k0 = w[0] + w[2] * a2_1_a1 + w[3] * a2_0_a1;
-  const double k1 = w[0] * a1_1_a2 + w[1] * a1_0_a2 + w[2];
-  double g1, o1, g2, o2, in, out;
+  const T k0 = w[0] + w[2] * a2_1_a1 + w[3] * a2_0_a1;
+  const T k1 = w[0] * a1_1_a2 + w[1] * a1_0_a2 + w[2];
+  T g1, o1, g2, o2, in, out;
   within01(a1u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g1, &o1);
   within01(a2u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g2, &o2);
   within_and(g1, o1, g2, o2, &in, &out);
-  QpSol s;
+  QpSolT<T> s;
   s.a1 = a1u * in + k0 * out;
   s.a2 = a2u * in + k1 * out;
   s.gamma = in;
-  s.label = best | ((in >= 0.5) << 2);
+  s.label = best | ((pv(in) >= 0.5) << 2);
   return s;
 }
 
 // ee_witness Q/c construction (witness.hpp:137-158) for edges given in a
 // common frame: Q = A^T A + lambda I, c = b^T A - lambda/2, A = [t1, -t2].
-__device__ __forceinline__ QpSol ee_qp(double3 e1a, double3 e1b, double3 e2a, double3 e2b,
-                                       const DevCfg& c) {
-  const double3 t1 = e1b - e1a;
-  const double3 t2n = e2a - e2b;
-  const double3 b = e1a - e2a;
-  return solve_box_qp_2(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
-                        ddot(b, t1) - 0.5 * c.lambda, ddot(b, t2n) - 0.5 * c.lambda, c);
+template <class T = double>
+__device__ __forceinline__ QpSolT<T> ee_qp(vec3<T> e1a, vec3<T> e1b, vec3<T> e2a, vec3<T> e2b,
+                                           const DevCfg& c) {
+  const vec3<T> t1 = e1b - e1a;
+  const vec3<T> t2n = e2a - e2b;
+  const vec3<T> b = e1a - e2a;
+  return solve_box_qp_2<T>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
+                           ddot(b, t1) - 0.5 * c.lambda, ddot(b, t2n) - 0.5 * c.lambda, c);
 }
 
 // vf_witness (witness.hpp:163-227): clipped edge projections over the full

@@ -51,6 +51,9 @@ SDF_PROGRAMS = {
 }
 
 
+JVP_ENVS = 2  # envs per case with recorded reference pose Jacobians (Dual12)
+
+
 def manifold_cases():
     """(name, workload, cfg, n_env) for manifold golden fixtures / parity tests."""
     base = SmoothingConfig()

@@ -129,6 +129,20 @@ def main():
     j = Ref.manifold_jvp(rs[0], rs[1], ws.bodies[0].pose, ws.bodies[1].pose, SmoothingConfig())
     out["jvp_box_on_plane"] = dict(contacts=j["contacts"], tangents=j["tangents"],
                                    mean_dist=np.array(j["mean_dist"]), mean_dist_grad=j["mean_dist_grad"])
+    # every smooth manifold case, first JVP_ENVS envs of its jittered batch
+    jv = {}
+    for name, ws, c, n in cases.manifold_cases():
+        if c.hard_ops:
+            continue
+        ms = [ref_mesh(b) for b in ws.bodies[:2]]
+        rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, ws.bodies[:2])]
+        p1, p2 = ws.poses(n)
+        for e in range(cases.JVP_ENVS):
+            j = Ref.manifold_jvp(rs[0], rs[1], p1[min(e, len(p1) - 1)], p2[min(e, len(p2) - 1)], c)
+            jv[f"{name}_{e}_contacts"] = j["contacts"]
+            jv[f"{name}_{e}_tangents"] = j["tangents"].astype(np.float32)  # the ABI emits FP32
+            jv[f"{name}_{e}_mean"] = np.array([j["mean_dist"], *j["mean_dist_grad"]])
+    out["jvp_cases"] = jv
 
     for name, d in out.items():
         path = os.path.join(HERE, f"{name}.npz")

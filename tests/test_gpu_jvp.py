@@ -1,0 +1,99 @@
+"""GPU parity of the pose-Jacobian path: the sm_100a JVP
+kernel through cmgb_manifold_jvp_batch vs the compiled reference's
+generate_manifold<Dual12> (golden fixtures tests/golden/jvp_*.npz).
+
+Tolerance: primal contacts by the manifold parity rule (tests/helpers.py);
+tangents per contact and quantity block (point 3x12, dist 1x12, normal 3x12,
+activity 1x12) as matrices:
+    |J_gpu - J_ref|_F <= JAC_ATOL + JAC_RTOL |J_ref|_F
+(FP32 output of FP64-evaluated tangents; a block is compared as a whole for
+the same reason vectors are)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from cases import JVP_ENVS, manifold_cases
+from helpers import QUANTITIES, assert_parity
+from paper_2602_20304_b200 import api, abi
+from paper_2602_20304_b200 import workloads as W
+from paper_2602_20304_b200.scene import SmoothingConfig
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+JAC_RTOL = 1e-4
+JAC_ATOL = 1e-5
+SMOOTH = [c for c in manifold_cases() if not c[2].hard_ops]
+
+
+def jac_report(got, ref):
+    """Per-quantity worst ratio |dJ|_F / (atol + rtol |J|_F) over contacts [..., 8, 12]."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    out = {}
+    for name, sl in QUANTITIES.items():
+        d = np.sqrt(((got[..., sl, :] - ref[..., sl, :]) ** 2).sum(axis=(-2, -1)))
+        r = np.sqrt((ref[..., sl, :] ** 2).sum(axis=(-2, -1)))
+        out[name] = float((d / (JAC_ATOL + JAC_RTOL * r)).max()) if d.size else 0.0
+    return out
+
+
+def run_jvp(ws, cfg, p1, p2, **kw):
+    a1, a2 = (api.surface_from_spec(b) for b in ws.bodies[:2])
+    r = api.generate_manifold_jvp_batch(a1, a2, torch.as_tensor(p1, device="cuda"),
+                                        torch.as_tensor(p2, device="cuda"), cfg, **kw)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in r.items()}
+
+
+@pytest.mark.parametrize("case", [c[0] for c in SMOOTH])
+def test_jvp_matches_reference(case, cuda):
+    g = np.load(os.path.join(GOLD, "jvp_cases.npz"))
+    name, ws, cfg, n = [c for c in SMOOTH if c[0] == case][0]
+    p1, p2 = ws.poses(n)
+    r = run_jvp(ws, cfg, p1, p2, want_src=True)
+    for e in range(JVP_ENVS):
+        assert_parity(r["contacts"][e], g[f"{name}_{e}_contacts"], what=f"{name} env {e} primal")
+        rep = jac_report(r["tangents"][e], g[f"{name}_{e}_tangents"])
+        print(f"{name} env {e}: jacobian ratio {rep}")
+        assert max(rep.values()) <= 1.0, f"{name} env {e}: jacobian outside tolerance {rep}"
+        ref_mean = g[f"{name}_{e}_mean"]
+        assert abs(r["mean_dist"][e] - ref_mean[0]) <= 1e-6 + 1e-5 * abs(ref_mean[0])
+        dm = np.linalg.norm(r["mean_dist_grad"][e] - ref_mean[1:])
+        assert dm <= JAC_ATOL + JAC_RTOL * np.linalg.norm(ref_mean[1:]), (r["mean_dist_grad"][e], ref_mean[1:])
+
+
+def test_jvp_box_on_plane_single_env(cuda):
+    """The single-env fixture of test_dual-style use (manifold.hpp + dual.hpp)."""
+    g = np.load(os.path.join(GOLD, "jvp_box_on_plane.npz"))
+    ws = W.box_on_plane()
+    r = run_jvp(ws, SmoothingConfig(), np.array([ws.bodies[0].pose]), np.array([ws.bodies[1].pose]))
+    assert_parity(r["contacts"][0], g["contacts"], what="box_on_plane primal")
+    rep = jac_report(r["tangents"][0], g["tangents"])
+    assert max(rep.values()) <= 1.0, rep
+    assert np.linalg.norm(r["mean_dist_grad"][0] - g["mean_dist_grad"]) <= \
+        JAC_ATOL + JAC_RTOL * np.linalg.norm(g["mean_dist_grad"])
+
+
+def test_jvp_primal_matches_value_kernel(cuda):
+    """Size-independent property at a larger batch: the JVP's primal equals the
+    value kernel's contacts (both are the same pipeline) for every env."""
+    ws = W.box_box()
+    p1, p2 = ws.poses(2048)
+    a1, a2 = (api.surface_from_spec(b) for b in ws.bodies[:2])
+    t1, t2 = torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda")
+    j = api.generate_manifold_jvp_batch(a1, a2, t1, t2, SmoothingConfig(), want_src=True)
+    v = api.generate_manifold_batch(a1, a2, t1, t2, SmoothingConfig(), want_src=True)
+    torch.cuda.synchronize()
+    assert_parity(j["contacts"].cpu().numpy(), v["contacts"].cpu().numpy(), what="jvp primal vs value kernel")
+    assert torch.equal(j["src"], v["src"])
+    assert torch.isfinite(j["tangents"]).all()
+
+
+def test_jvp_rejects_hard_ops(cuda):
+    ws = W.box_box()
+    a1, a2 = (api.surface_from_spec(b) for b in ws.bodies[:2])
+    p = torch.zeros((2, 6), dtype=torch.float64, device="cuda")
+    with pytest.raises(abi.CmgbError, match="UNSUPPORTED"):
+        api.generate_manifold_jvp_batch(a1, a2, p, p, SmoothingConfig().for_variant("ours_ns"))
