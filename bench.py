@@ -41,10 +41,11 @@ def parse():
     ap.add_argument("--n-env", type=int, default=65536, help="envs per GPU (weak scaling)")
     ap.add_argument("--cpu-sample", type=int, default=16384, help="envs in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop"],
+    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop", "drop-fwd"],
                     help="box-box = config B (headline); mixed = config C (4 x 65,536 envs of "
                          "primitive families vs a convex mesh); drop = config D (all 10 body pairs "
-                         "of a 5-body scene, 32,768 envs)")
+                         "of a 5-body scene, 32,768 envs, forward + 12-tangent pose JVP); drop-fwd = "
+                         "config D forward only")
     return ap.parse_args()
 
 
@@ -196,12 +197,17 @@ def run_secondary(args, dev, rank, world):
         pairs = api.scene_pairs(len(bodies), sc.is_static())
         units = n * len(pairs)
 
+        jvp = args.workload == "drop"
+        fn = api.generate_manifold_scene_jvp_batch if jvp else api.generate_manifold_scene_batch
+
         def step():
             nonlocal outs
-            outs = api.generate_manifold_scene_batch(bodies, P, cfg, is_static=sc.is_static(), outs=outs)
-        metric, unit, cfgd = "pair manifolds/sec (5-body drop scene, all %d pairs, %d envs)" % (len(pairs), n), \
-            "manifolds/s", {"workload": "drop (config D): 4 stacked SQ boxes over a static box_planes "
-                            "ground, edge_topk 4, 48 contacts/pair", "n_env": n, "pairs_per_env": len(pairs)}
+            outs = fn(bodies, P, cfg, is_static=sc.is_static(), outs=outs)
+        what = "forward + 12-tangent pose JVP" if jvp else "forward only"
+        metric, unit, cfgd = "pair manifolds/sec, %s (5-body drop scene, all %d pairs, %d envs)" % (
+            what, len(pairs), n), "manifolds/s", {
+                "workload": "drop (config D): 4 stacked SQ boxes over a static box_planes ground, edge_topk 4, "
+                            "48 contacts/pair, %s" % what, "n_env": n, "pairs_per_env": len(pairs)}
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()

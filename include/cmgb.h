@@ -240,6 +240,13 @@ int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, cons
                               int32_t n_pairs, const double* poses, int64_t n_env,
                               const cmgb_config* cfg, const cmgb_manifold_out* outs,
                               void* cuda_stream);
+/* Config D's "forward + 12-tangent JVP per pair": pair q's primal contacts and
+ * pose Jacobians (w.r.t. the poses of bodies[pairs[2q]] and bodies[pairs[2q+1]])
+ * into outs[q], as cmgb_manifold_jvp_batch. */
+int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                                  int32_t n_pairs, const double* poses, int64_t n_env,
+                                  const cmgb_config* cfg, const cmgb_manifold_jvp_out* outs,
+                                  void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * Witness batches — run_ee_batch / run_vf_batch (src/batch.cpp:53-98) over

@@ -161,6 +161,11 @@ SIGNATURES = {
         [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig),
          C.POINTER(CmgbManifoldJvpOut), _P],
     ),
+    "cmgb_manifold_scene_jvp_batch": (
+        _I,
+        [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig),
+         C.POINTER(CmgbManifoldJvpOut), _P],
+    ),
     "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
     "cmgb_manifold_scene_batch": (
         _I,

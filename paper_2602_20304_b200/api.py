@@ -309,6 +309,50 @@ def generate_manifold_scene_batch(bodies, poses, cfg=None, *, is_static=None, pa
     return res
 
 
+def generate_manifold_scene_jvp_batch(bodies, poses, cfg=None, *, is_static=None, pairs=None,
+                                      want_src: bool = False, outs: Optional[list] = None,
+                                      stream=None) -> list:
+    """Config D's forward + 12-tangent JVP per pair: for every scene pair (i, j)
+    and env, the primal contacts and their Jacobian w.r.t. (pose_i, pose_j)
+    (as generate_manifold_jvp_batch). poses: CUDA float64 [n_env, n_bodies, 6]."""
+    import torch
+
+    c = _cfg(cfg)
+    P = poses.contiguous()
+    if P.dtype != torch.float64 or not P.is_cuda or P.dim() != 3 or P.shape[2] != 6:
+        raise ValueError("poses must be a CUDA float64 tensor [n_env, n_bodies, 6]")
+    n_env, nb = P.shape[0], P.shape[1]
+    if len(bodies) != nb:
+        raise ValueError("one surface per body")
+    pr = scene_pairs(nb, is_static) if pairs is None else np.ascontiguousarray(pairs, dtype=np.int32)
+    res = outs if outs is not None else [dict() for _ in range(len(pr))]
+    arr = (abi.CmgbManifoldJvpOut * max(len(pr), 1))()
+    dev = P.device
+    for q, (i, j) in enumerate(pr):
+        Cn = layout(bodies[i], bodies[j], c)["n_contacts"]
+        r = res[q]
+        r["pair"] = (int(i), int(j))
+        for k, shape, dt in (("contacts", (n_env, Cn, 8), torch.float32),
+                             ("tangents", (n_env, Cn, 8, 12), torch.float32),
+                             ("mean_dist", (n_env,), torch.float32),
+                             ("mean_dist_grad", (n_env, 12), torch.float32)):
+            if k not in r:
+                r[k] = torch.empty(shape, dtype=dt, device=dev)
+        if want_src and "src" not in r:
+            r["src"] = torch.empty((n_env, Cn, 2), dtype=torch.int32, device=dev)
+        o = arr[q]
+        o.contacts = r["contacts"].data_ptr()
+        o.tangents = r["tangents"].data_ptr()
+        o.src = r["src"].data_ptr() if "src" in r else None
+        o.mean_dist = r["mean_dist"].data_ptr()
+        o.mean_dist_grad = r["mean_dist_grad"].data_ptr()
+    handles = (C.c_void_p * nb)(*[b._h.value if isinstance(b._h, C.c_void_p) else b._h for b in bodies])
+    with torch.cuda.device(dev):
+        _ok(abi.load().cmgb_manifold_scene_jvp_batch(handles, nb, pr.ctypes.data, len(pr), P.data_ptr(), n_env,
+                                                     C.byref(c), arr, _stream_ptr(stream)))
+    return res
+
+
 def generate_manifold_batch_host(s1: Surface, s2: Surface, poses1: np.ndarray, poses2: np.ndarray,
                                  cfg=None, mean_out: Optional[np.ndarray] = None,
                                  contacts_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:

@@ -135,8 +135,9 @@ struct JvpParams {
   float* tangents;   // [n_env][C][8][12]
   float* mean_grad;  // [n_env][12]
   int32_t nd, groups;
+  int32_t units_per_block;
   int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
-  int32_t bytes;
+  int32_t bytes;  // per unit
 };
 
 struct WitnessParams {
@@ -156,7 +157,9 @@ namespace cmgb {
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream);
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
-int jvp_directions();  // tangent directions per thread of the compiled JVP kernel
+int jvp_directions();    // tangent directions per thread of the compiled JVP kernel
+int jvp_max_threads();   // CTA size of the JVP kernel
+int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan for
 int launch_ee_witness(const WitnessParams& p, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);
 const char* last_cuda_error_string();

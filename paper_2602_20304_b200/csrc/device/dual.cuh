@@ -103,12 +103,14 @@ struct Dual {
     const double e = exp_d(x.v);
     return chain(e, e, x);
   }
+  // exp / log of the LSE and top-K weights: the lean FP64 routines (<= 1 ulp
+  // from libdevice's; dmath.cuh)
   friend __device__ __forceinline__ Dual exp(const Dual& x) {
-    const double e = ::exp(x.v);
+    const double e = exp_d(x.v);
     return chain(e, e, x);
   }
   friend __device__ __forceinline__ Dual log_d(const Dual& x) { return chain(log_d(x.v), rcp_d(x.v), x); }
-  friend __device__ __forceinline__ Dual log(const Dual& x) { return chain(::log(x.v), rcp_d(x.v), x); }
+  friend __device__ __forceinline__ Dual log(const Dual& x) { return chain(log_d(x.v), rcp_d(x.v), x); }
   friend __device__ __forceinline__ Dual log1p(const Dual& x) {
     return chain(::log1p(x.v), rcp_d(1.0 + x.v), x);
   }

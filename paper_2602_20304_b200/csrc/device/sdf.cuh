@@ -100,7 +100,8 @@ __device__ __forceinline__ void pow_pair_t(const T& x, int n, double p, T& xp, T
 // Otherwise -expm1(p4 ln f) with ln f = log1p(f - 1) near the surface.
 // Also returns 1/r (= f^p4) for the gradient.
 template <int N4 = 0>
-__device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, double* F) {
+__device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, double* F,
+                                                double* inv_f = nullptr) {
   const int n = N4 > 0 ? N4 : n_rt;
   if (n > 0) {
     // F = f^(-1/n). Seed F0 = 2^(-log2(f)/n): log2 from the exponent bits +
@@ -114,25 +115,31 @@ __device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, d
     const float q = floorf(l);
     const double F0 = (double)ex2f(l - q) * __hiloint2double(((int)q + 1023) << 20, 0);
     const double Fn = N4 > 0 ? cpow<(N4 > 0 ? N4 : 1)>(F0) : ipow_d(F0, n);
-    const double Fv = fma(F0 * fma(-f, Fn, 1.0), 1.0 / (double)n, F0);
+    const double e = fma(-f, Fn, 1.0);  // f F0^n = 1 - e, |e| ~ n delta0
+    const double Fv = fma(F0 * e, 1.0 / (double)n, F0);
     *F = Fv;
+    // 1/f = F0^n / (1 - e) = F0^n (1 + e + e^2 + ...): two FMAs, error e^3
+    if (inv_f) *inv_f = fma(Fn, fma(e, e, e), Fn);
     return 1.0 - Fv;
   }
   const double d = f - 1.0;
   const double lnf = fabs(d) < 0.5 ? log1p(d) : log(f);
   const double em1 = expm1(p4 * lnf);
   *F = 1.0 + em1;
+  if (inv_f) *inv_f = rcp_d(f);
   return -em1;
 }
 
 // Dual overload: primal by the routine above (bit-identical to the value
 // path), tangents by the chain rule d(f^p4) = p4 f^p4 / f df.
 template <int N4 = 0, int N>
-__device__ __forceinline__ Dual<N> one_minus_pow(const Dual<N>& f, double p4, int n_rt, Dual<N>* F) {
-  double Fv;
-  const double om = one_minus_pow<N4>(f.v, p4, n_rt, &Fv);
-  const double s = p4 * Fv * rcp_d(f.v);
+__device__ __forceinline__ Dual<N> one_minus_pow(const Dual<N>& f, double p4, int n_rt, Dual<N>* F,
+                                                 Dual<N>* inv_f = nullptr) {
+  double Fv, rf;
+  const double om = one_minus_pow<N4>(f.v, p4, n_rt, &Fv, &rf);
+  const double s = p4 * Fv * rf;
   *F = Dual<N>::chain(Fv, s, f);
+  if (inv_f) *inv_f = Dual<N>::chain(rf, -rf * rf, f);
   return Dual<N>::chain(om, -s, f);
 }
 
@@ -176,11 +183,11 @@ __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
   // kGrad: grad phi = diag(1/axes) (-p4 (F/f) grad_n f - phi x~ / r) / r
   const T r2 = fma(xn, xn, fma(yn, yn, fma(zn, zn, T(kMC.floor20))));
   const T rinv = rsqrt_d(r2);
-  T F;
-  const T omF = one_minus_pow<N4>(f, q.p4, q.n4, &F);
+  T F, inv_f;
+  const T omF = one_minus_pow<N4>(f, q.p4, q.n4, &F, &inv_f);
   const T phi = omF * rinv;
   out.v = phi;
-  const T k = -q.p4 * F * rcp_d(f);
+  const T k = -q.p4 * F * inv_f;
   const T h = phi * rinv;
   const T sx = q.inv_ax[0] * rinv, sy = q.inv_ax[1] * rinv, sz = q.inv_ax[2] * rinv;
   const vec3<T> gl = mk3<T>(sx * fma(k, dfn.x, -h * xn), sy * fma(k, dfn.y, -h * yn), sz * fma(k, dfn.z, -h * zn));

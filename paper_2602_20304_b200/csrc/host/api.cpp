@@ -582,45 +582,89 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
 }
 
 // ---- pose Jacobians (Dual12 forward mode) -------------------------------------------
+namespace {
+
+void validate_jvp(const cmgb_config* cfg, const cmgb_manifold_jvp_out* out) {
+  if (!out || !out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
+  validate_config(cfg);
+  if (cfg->hard_ops)
+    throw Error(CMGB_ERR_UNSUPPORTED,
+                "manifold_jvp: hard_ops has no derivative path (the reference's hard operators are double-only)");
+}
+
+// JVP launch plan on top of a value plan: per-unit dual working set and units
+// per CTA (~one CTA's worth of E-E pairs, within the kernel's shared-memory
+// budget per CTA).
+JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
+  JvpParams j{};
+  j.m = plan.p;
+  j.tangents = out->tangents;
+  j.mean_grad = out->mean_dist_grad;
+  j.nd = jvp_directions();
+  j.groups = 12 / j.nd;
+  const ManifoldParams& m = j.m;
+  const int T = 8 * (j.nd + 1);  // bytes per dual scalar
+  const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2;
+  const bool topk = m.side[0].topk_v || m.side[1].topk_v || m.side[0].topk_e || m.side[1].topk_e;
+  const int nscore = topk ? (m.side[0].nv + m.side[1].nv + m.side[0].ne + m.side[1].ne) : 0;
+  int off = 0;
+  j.o_frames = off; off = align16(off + 24 * T);
+  j.o_scores = off; off = align16(off + nscore * T);
+  j.o_sorted = off; off = align16(off + nscore * T);
+  j.o_vslots = off; off = align16(off + nslot_v * 3 * T);
+  j.o_eslots = off; off = align16(off + nslot_e * 12 * T);
+  j.o_prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
+  j.o_pairs = off; off = align16(off + P * (kPairRec / 2) * T);
+  j.o_vsdist = off; off = align16(off + nslot_v * T);
+  j.o_nnstat = off; off = align16(off + nslot_e * 2 * T);
+  j.bytes = off;
+  if (j.bytes > 200 * 1024)
+    throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
+  const int per_unit = std::max({P, nslot_v, 1});
+  int upb = std::max(1, jvp_max_threads() / per_unit);
+  while (upb > 1 && (size_t)upb * j.bytes > (size_t)jvp_smem_cap()) --upb;
+  j.units_per_block = upb;
+  if ((m.n_env * j.groups + upb - 1) / upb > 0x7fffffffLL) invalid("manifold_jvp: n_env too large for one launch");
+  return j;
+}
+
+void launch_jvp(const JvpParams& j, cudaStream_t s) {
+  if (launch_manifold_jvp(j, 0, s) != 0)
+    throw Error(CMGB_ERR_CUDA, std::string("manifold_jvp launch: ") + cudaGetErrorString(cudaGetLastError()));
+}
+
+}  // namespace
+
 int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1, int32_t st1,
                             const double* poses2, int32_t st2, int64_t n_env, const cmgb_config* cfg,
                             const cmgb_manifold_jvp_out* out, void* stream) {
   return guarded([&] {
-    if (!out || !out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
-    validate_config(cfg);
-    if (cfg->hard_ops)
-      throw Error(CMGB_ERR_UNSUPPORTED,
-                  "manifold_jvp: hard_ops has no derivative path (the reference's hard operators are double-only)");
+    validate_jvp(cfg, out);
     cmgb_manifold_out mo{out->contacts, out->src, nullptr, out->mean_dist, nullptr, 0};
     LaunchPlan plan = plan_manifold(s1, s2, poses1, st1, poses2, st2, n_env, cfg, &mo);
     if (n_env == 0 || plan.p.n_contacts == 0) return;
-    JvpParams j{};
-    j.m = plan.p;
-    j.tangents = out->tangents;
-    j.mean_grad = out->mean_dist_grad;
-    j.nd = jvp_directions();
-    j.groups = 12 / j.nd;
-    const ManifoldParams& m = j.m;
-    const int T = 8 * (j.nd + 1);  // bytes per dual scalar
-    const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2;
-    const bool topk = m.side[0].topk_v || m.side[1].topk_v || m.side[0].topk_e || m.side[1].topk_e;
-    const int nscore = topk ? (m.side[0].nv + m.side[1].nv + m.side[0].ne + m.side[1].ne) : 0;
-    int off = 0;
-    j.o_frames = off; off = align16(off + 24 * T);
-    j.o_scores = off; off = align16(off + nscore * T);
-    j.o_sorted = off; off = align16(off + nscore * T);
-    j.o_vslots = off; off = align16(off + nslot_v * 3 * T);
-    j.o_eslots = off; off = align16(off + nslot_e * 12 * T);
-    j.o_prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
-    j.o_pairs = off; off = align16(off + P * (kPairRec / 2) * T);
-    j.o_vsdist = off; off = align16(off + nslot_v * T);
-    j.o_nnstat = off; off = align16(off + nslot_e * 2 * T);
-    j.bytes = off;
-    if (j.bytes > 200 * 1024)
-      throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
-    if (n_env * j.groups > 0x7fffffffLL) invalid("manifold_jvp: n_env too large for one launch");
-    if (launch_manifold_jvp(j, 0, stream) != 0)
-      throw Error(CMGB_ERR_CUDA, std::string("manifold_jvp launch: ") + cudaGetErrorString(cudaGetLastError()));
+    launch_jvp(plan_jvp(plan, out), static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                                  int32_t n_pairs, const double* poses, int64_t n_env,
+                                  const cmgb_config* cfg, const cmgb_manifold_jvp_out* outs, void* stream) {
+  return guarded([&] {
+    if (!bodies || !pairs || !poses || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0)
+      invalid("manifold_scene_jvp_batch: bad argument");
+    for (int q = 0; q < n_pairs; ++q) {
+      const int i = pairs[2 * q], j = pairs[2 * q + 1];
+      if (i < 0 || j < 0 || i >= n_bodies || j >= n_bodies || i == j)
+        invalid("manifold_scene_jvp_batch: pair index out of range");
+      const cmgb_manifold_jvp_out& o = outs[q];
+      validate_jvp(cfg, &o);
+      cmgb_manifold_out mo{o.contacts, o.src, nullptr, o.mean_dist, nullptr, 0};
+      LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &mo);
+      if (n_env == 0 || plan.p.n_contacts == 0) continue;
+      plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)n_bodies;
+      launch_jvp(plan_jvp(plan, &o), static_cast<cudaStream_t>(stream));
+    }
   });
 }
 

@@ -38,8 +38,24 @@ namespace cmgb {
 
 namespace {
 
-constexpr int kJvpND = 2;  // tangent directions per thread (6 groups)
-constexpr int kJvpThreads = 160;
+// Tangent directions per thread (12 / ND groups), CTA size and CTAs per SM;
+// overridable at build time for tuning (tools/jvp_variants.sh).
+#ifndef CMGB_JVP_ND
+#define CMGB_JVP_ND 2
+#endif
+#ifndef CMGB_JVP_THREADS
+#define CMGB_JVP_THREADS 128
+#endif
+#ifndef CMGB_JVP_MINB
+#define CMGB_JVP_MINB 4
+#endif
+#ifndef CMGB_JVP_SMEM_KB
+#define CMGB_JVP_SMEM_KB 56
+#endif
+constexpr int kJvpND = CMGB_JVP_ND;
+constexpr int kJvpThreads = CMGB_JVP_THREADS;
+constexpr int kJvpMinBlocks = CMGB_JVP_MINB;
+static_assert(12 % kJvpND == 0, "ND must divide the 12 pose directions");
 
 template <class T>
 struct Frame {
@@ -69,6 +85,8 @@ struct Unit {
   using T = Dual<ND>;
   unsigned char* base;
   const JvpParams* p;
+  int64_t env;
+  int group;
   __device__ Frame<T>& frame(int s) const { return reinterpret_cast<Frame<T>*>(base + p->o_frames)[s]; }
   __device__ T* scores() const { return reinterpret_cast<T*>(base + p->o_scores); }
   __device__ T* sorted() const { return reinterpret_cast<T*>(base + p->o_sorted); }
@@ -135,12 +153,17 @@ __device__ __forceinline__ void side_t(const JvpParams& p, const Unit<ND>& u, in
   r[7] = o.v;
 }
 
+// A CTA owns `units_per_block` consecutive units; unit U = (env U / groups,
+// direction group U % groups). Work items of all its units are spread over
+// the CTA's threads, phase by phase (as manifold.cu does with envs).
 template <int K1, int K2, int ND>
-__global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_constant__ JvpParams p) {
+__global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kernel(const __grid_constant__ JvpParams p) {
   using T = Dual<ND>;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t e = blockIdx.x / p.groups;
-  const int group = blockIdx.x % p.groups;
+  const int upb = p.units_per_block;
+  const int64_t u0 = (int64_t)blockIdx.x * upb;
+  const int64_t n_units = p.m.n_env * p.groups;
+  const int n_here = (int)(n_units - u0 < upb ? n_units - u0 : upb);
   const int tid = threadIdx.x, nth = blockDim.x;
   const ManifoldParams& m = p.m;
   const DevCfg& c = m.cfg;
@@ -149,19 +172,23 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
   const int n1 = m.n1, n2 = m.n2, m1 = m.m1, m2 = m.m2, P = m1 * m2;
   const bool full = m1 > 0 && m2 > 0;
   const int C = m.n_contacts;
-  const Unit<ND> u{smem, &p};
+  auto unit = [&](int k) {
+    const int64_t U = u0 + k;
+    return Unit<ND>{smem + (size_t)k * p.bytes, &p, U / p.groups, (int)(U % p.groups)};
+  };
 
-  // ---- A: poses seeded with this group's tangent directions, se3_exp -------
+  // ---- A: poses seeded with the unit's tangent directions, se3_exp ---------
   // Direction d = group * ND + j tracks pose1[d] (d < 6) or pose2[d - 6].
-  if (tid < 2) {
-    const int s = tid;
-    const double* pose = s == 0 ? m.poses1 + m.pose_stride1 * e : m.poses2 + m.pose_stride2 * e;
+  for (int it = tid; it < 2 * n_here; it += nth) {
+    const Unit<ND> u = unit(it >> 1);
+    const int s = it & 1;
+    const double* pose = s == 0 ? m.poses1 + m.pose_stride1 * u.env : m.poses2 + m.pose_stride2 * u.env;
     T xi[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
       xi[k] = T(__ldg(pose + k));
 #pragma unroll
-      for (int j = 0; j < ND; ++j) xi[k].d[j] = (group * ND + j == 6 * s + k) ? 1.0 : 0.0;
+      for (int j = 0; j < ND; ++j) xi[k].d[j] = (u.group * ND + j == 6 * s + k) ? 1.0 : 0.0;
     }
     Frame<T>& F = u.frame(s);
     se3_exp_d(xi, F.R, F.t);
@@ -172,7 +199,9 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
   const bool topk_any = S1.topk_v | S2.topk_v | S1.topk_e | S2.topk_e;
   if (topk_any) {
     // ---- B: scores (-penetration) of every vertex, then edges -------------
-    for (int i = tid; i < off2; i += nth) {
+    for (int it = tid; it < n_here * off2; it += nth) {
+      const int k = it / off2, i = it - k * off2;
+      const Unit<ND> u = unit(k);
       const int s = i < S1.nv ? 0 : 1;
       const int vi = s == 0 ? i : i - S1.nv;
       const vec3<T> pw = to_world_t(u.frame(s), dvert<T>(s == 0 ? S1.verts : S2.verts, vi));
@@ -181,7 +210,10 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
       u.scores()[i] = -pen;
     }
     __syncthreads();
-    for (int i = tid; i < S1.ne + S2.ne; i += nth) {
+    const int ne_all = S1.ne + S2.ne;
+    for (int it = tid; it < n_here * ne_all; it += nth) {
+      const int k = it / ne_all, i = it - k * ne_all;
+      const Unit<ND> u = unit(k);
       const int s = i < S1.ne ? 0 : 1;
       const int ei = s == 0 ? i : i - S1.ne;
       const int32_t* E = s == 0 ? S1.edges : S2.edges;
@@ -192,7 +224,9 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
     }
     __syncthreads();
     // ---- C: descending rank sort on primals, stable on ties -------------
-    for (int i = tid; i < off4; i += nth) {
+    for (int it = tid; it < n_here * off4; it += nth) {
+      const int k = it / off4, i = it - k * off4;
+      const Unit<ND> u = unit(k);
       const int set = i < off1 ? 0 : i < off2 ? 1 : i < off3 ? 2 : 3;
       const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
       if (!active) continue;
@@ -213,7 +247,9 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
   // ---- D: selected slots (pass-through or soft top-K rows) ---------------
   {
     const int nsl = n1 + n2 + m1 + m2;
-    for (int r0 = tid; r0 < nsl; r0 += nth) {
+    for (int it = tid; it < n_here * nsl; it += nth) {
+      const int k = it / nsl, r0 = it - k * nsl;
+      const Unit<ND> u = unit(k);
       const bool is_edge = r0 >= n1 + n2;
       const int s = is_edge ? (r0 - n1 - n2 < m1 ? 0 : 1) : (r0 < n1 ? 0 : 1);
       const int r = is_edge ? (s == 0 ? r0 - n1 - n2 : r0 - n1 - n2 - m1) : (s == 0 ? r0 : r0 - n1);
@@ -282,27 +318,34 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
   __syncthreads();
 
   // ---- E: V-S contacts (vs_contacts, manifold.hpp:185-204), E-E pairs -----
-  for (int r = tid; r < n1 + n2; r += nth) {
-    const bool first = r < n1;
-    const DevSdf& opp = first ? S2.sdf : S1.sdf;
-    const Frame<T>& Fo = u.frame(first ? 1 : 0);
-    const T* q = u.vslot(r);
-    const vec3<T> pw = mk3<T>(q[0], q[1], q[2]);
-    const SdfOutT<T> s = first ? sdf_eval<kNormalSource, K2, T>(opp, to_body_t(Fo, pw))
-                               : sdf_eval<kNormalSource, K1, T>(opp, to_body_t(Fo, pw));
-    const vec3<T> n = mul_R(Fo.R, normalize_smooth_t<T>(s.g, c.tau_normal));
-    const T act = sigmoid_d(-s.v * c.inv_tau_pen);
-    u.vsdist()[r] = s.v;
-    const int64_t row = e * C + r;
-    put_contact<ND>(p, group, row, pw, s.v, n, act);
-    if (group == 0 && m.src) {
-      m.src[row * 2] = u.prov()[r];
-      m.src[row * 2 + 1] = -1;
+  {
+    const int nvs = n1 + n2;
+    for (int it = tid; it < n_here * nvs; it += nth) {
+      const int k = it / nvs, r = it - k * nvs;
+      const Unit<ND> u = unit(k);
+      const bool first = r < n1;
+      const DevSdf& opp = first ? S2.sdf : S1.sdf;
+      const Frame<T>& Fo = u.frame(first ? 1 : 0);
+      const T* q = u.vslot(r);
+      const vec3<T> pw = mk3<T>(q[0], q[1], q[2]);
+      const SdfOutT<T> s = first ? sdf_eval<kNormalSource, K2, T>(opp, to_body_t(Fo, pw))
+                                 : sdf_eval<kNormalSource, K1, T>(opp, to_body_t(Fo, pw));
+      const vec3<T> n = mul_R(Fo.R, normalize_smooth_t<T>(s.g, c.tau_normal));
+      const T act = sigmoid_d(-s.v * c.inv_tau_pen);
+      u.vsdist()[r] = s.v;
+      const int64_t row = u.env * C + r;
+      put_contact<ND>(p, u.group, row, pw, s.v, n, act);
+      if (u.group == 0 && m.src) {
+        m.src[row * 2] = u.prov()[r];
+        m.src[row * 2 + 1] = -1;
+      }
     }
   }
   if (full) {
-    for (int i = tid; i < P; i += nth) {
-      const int k = i / m2, l = i % m2;
+    for (int it = tid; it < n_here * P; it += nth) {
+      const int ku = it / P, i = it - ku * P;
+      const Unit<ND> u = unit(ku);
+      const int k = i / m2, l = i - (i / m2) * m2;
       T* r = u.pair(i);
       // E1: witness QP (ee_witness, witness.hpp:137-158), body-frame points
       {
@@ -319,8 +362,13 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
         r[16] = w.gamma;
       }
       // E2: both sides
-      side_t<K1, K2, ND>(p, u, 0, r);
-      side_t<K2, K1, ND>(p, u, 1, r + 8);
+      if constexpr (K1 == K2) {  // one code copy for both sides (I-cache)
+#pragma unroll 1
+        for (int s = 0; s < 2; ++s) side_t<K1, K1, ND>(p, u, s, r + 8 * s);
+      } else {
+        side_t<K1, K2, ND>(p, u, 0, r);
+        side_t<K2, K1, ND>(p, u, 1, r + 8);
+      }
       // E3: pair quantities (manifold.hpp:248-266, 279-285)
       const vec3<T> de = mk3<T>(r[0] - r[8], r[1] - r[9], r[2] - r[10]);
       const T dg = sqrt(ddot(de, de) + 1e-12);
@@ -347,7 +395,10 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
 
   if (full) {
     // ---- F: NN softmin statistics, shift = first minimum (argmin_s) --------
-    for (int r = tid; r < m1 + m2; r += nth) {
+    const int nrc = m1 + m2;
+    for (int it = tid; it < n_here * nrc; it += nth) {
+      const int ku = it / nrc, r = it - ku * nrc;
+      const Unit<ND> u = unit(ku);
       const bool row = r < m1;
       const int n = row ? m2 : m1;
       auto idx = [&](int j) { return row ? r * m2 + j : j * m2 + (r - m1); };
@@ -362,8 +413,10 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
     }
     __syncthreads();
     // ---- G: activity product + fixed-layout E-E rows (303-330) ---------------
-    for (int i = tid; i < P; i += nth) {
-      const int k = i / m2, l = i % m2;
+    for (int it = tid; it < n_here * P; it += nth) {
+      const int ku = it / P, i = it - ku * P;
+      const Unit<ND> u = unit(ku);
+      const int k = i / m2, l = i - (i / m2) * m2;
       const T* rec = u.pair(i);
       const T* ns = u.nnstat();
       const T dg = rec[3];
@@ -373,10 +426,10 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
       const T act2 = rec[16] * rec[14] * nn2 * rec[15] * rec[7];
       const T g1 = rec[4], g2 = rec[5];
       const vec3<T> nb = mk3<T>(rec[11], rec[12], rec[13]);
-      const int64_t row = e * C + n1 + n2 + 2 * i;
-      put_contact<ND>(p, group, row, mk3<T>(rec[0], rec[1], rec[2]), g1 * dg, dscale(nb, g1), act1);
-      put_contact<ND>(p, group, row + 1, mk3<T>(rec[8], rec[9], rec[10]), g2 * dg, dscale(nb, g2), act2);
-      if (group == 0 && m.src) {
+      const int64_t row = u.env * C + n1 + n2 + 2 * i;
+      put_contact<ND>(p, u.group, row, mk3<T>(rec[0], rec[1], rec[2]), g1 * dg, dscale(nb, g1), act1);
+      put_contact<ND>(p, u.group, row + 1, mk3<T>(rec[8], rec[9], rec[10]), g2 * dg, dscale(nb, g2), act2);
+      if (u.group == 0 && m.src) {
         int* sp = m.src + row * 2;
         const int sa = u.prov()[n1 + n2 + k], sb = u.prov()[n1 + n2 + m1 + l];
         sp[0] = sa; sp[1] = sb; sp[2] = sa; sp[3] = sb;
@@ -386,19 +439,22 @@ __global__ void __launch_bounds__(kJvpThreads) manifold_jvp_kernel(const __grid_
   __syncthreads();
 
   // ---- H: mean contact distance (manifold.hpp:379-384), fixed order ---------
-  if (tid == 0 && (m.mean_dist || p.mean_grad)) {
-    T acc = 0.0;
-    for (int r = 0; r < n1 + n2; ++r) acc += u.vsdist()[r];
-    for (int i = 0; i < P && full; ++i) {
-      const T* rec = u.pair(i);
-      acc += rec[4] * rec[3];
-      acc += rec[5] * rec[3];
-    }
-    const T mean = acc * (1.0 / (double)C);
-    if (group == 0 && m.mean_dist) m.mean_dist[e] = (float)mean.v;
-    if (p.mean_grad)
+  if (m.mean_dist || p.mean_grad) {
+    for (int k = tid; k < n_here; k += nth) {
+      const Unit<ND> u = unit(k);
+      T acc = 0.0;
+      for (int r = 0; r < n1 + n2; ++r) acc += u.vsdist()[r];
+      for (int i = 0; i < P && full; ++i) {
+        const T* rec = u.pair(i);
+        acc += rec[4] * rec[3];
+        acc += rec[5] * rec[3];
+      }
+      const T mean = acc * (1.0 / (double)C);
+      if (u.group == 0 && m.mean_dist) m.mean_dist[u.env] = (float)mean.v;
+      if (p.mean_grad)
 #pragma unroll
-      for (int j = 0; j < ND; ++j) p.mean_grad[e * 12 + group * ND + j] = (float)mean.d[j];
+        for (int j = 0; j < ND; ++j) p.mean_grad[u.env * 12 + u.group * ND + j] = (float)mean.d[j];
+    }
   }
 }
 
@@ -410,8 +466,9 @@ int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
                          200 * 1024);
     configured = true;
   }
-  const int64_t grid = p.m.n_env * p.groups;
-  manifold_jvp_kernel<K1, K2, kJvpND><<<(unsigned)grid, threads, p.bytes, s>>>(p);
+  const int64_t units = p.m.n_env * p.groups;
+  const int64_t grid = (units + p.units_per_block - 1) / p.units_per_block;
+  manifold_jvp_kernel<K1, K2, kJvpND><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -432,6 +489,8 @@ int launch_jvp_k2(const JvpParams& p, int threads, cudaStream_t s) {
 }  // namespace
 
 int jvp_directions() { return kJvpND; }
+int jvp_max_threads() { return kJvpThreads; }
+int jvp_smem_cap() { return CMGB_JVP_SMEM_KB * 1024; }
 
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);

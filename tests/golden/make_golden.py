@@ -111,12 +111,12 @@ def main():
     sc = W.drop_scene(4)
     P = sc.poses(4)
     ms = [ref_mesh(b) for b in sc.bodies]
-    rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, sc.bodies)]
+    srs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(ms, sc.bodies)]
     from paper_2602_20304_b200 import api
     pairs = api.scene_pairs(len(sc.bodies), sc.is_static())
     scene = {"poses": P, "pairs": pairs}
     for q, (i, j) in enumerate(pairs):
-        r = Ref.manifold_batch(rs[i], rs[j], P[:, i], P[:, j], SmoothingConfig(), 1)
+        r = Ref.manifold_batch(srs[i], srs[j], P[:, i], P[:, j], SmoothingConfig(), 1)
         scene[f"contacts{q}"] = r["contacts"]
         scene[f"meta{q}"] = r["meta"]
         scene[f"mean{q}"] = r["mean_dist"]
@@ -142,6 +142,12 @@ def main():
             jv[f"{name}_{e}_contacts"] = j["contacts"]
             jv[f"{name}_{e}_tangents"] = j["tangents"].astype(np.float32)  # the ABI emits FP32
             jv[f"{name}_{e}_mean"] = np.array([j["mean_dist"], *j["mean_dist_grad"]])
+    # config D scene: pose Jacobians of every pair, env 0 (forward + 12-tangent JVP per pair)
+    for q, (i, j) in enumerate(pairs):
+        r = Ref.manifold_jvp(srs[i], srs[j], P[0, i], P[0, j], SmoothingConfig())
+        jv[f"drop_pair{q}_0_contacts"] = r["contacts"]
+        jv[f"drop_pair{q}_0_tangents"] = r["tangents"].astype(np.float32)
+        jv[f"drop_pair{q}_0_mean"] = np.array([r["mean_dist"], *r["mean_dist_grad"]])
     out["jvp_cases"] = jv
 
     for name, d in out.items():

@@ -97,3 +97,37 @@ def test_jvp_rejects_hard_ops(cuda):
     p = torch.zeros((2, 6), dtype=torch.float64, device="cuda")
     with pytest.raises(abi.CmgbError, match="UNSUPPORTED"):
         api.generate_manifold_jvp_batch(a1, a2, p, p, SmoothingConfig().for_variant("ours_ns"))
+
+
+def test_scene_jvp_matches_pair_jvp(cuda):
+    """Config D: the scene JVP call equals per-pair JVP calls on the same poses
+    (pose tangents of bodies i and j of each pair)."""
+    sc = W.drop_scene(64)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    P = torch.as_tensor(sc.poses(64), device="cuda")
+    res = api.generate_manifold_scene_jvp_batch(bodies, P, SmoothingConfig(), is_static=sc.is_static(),
+                                                want_src=True)
+    for r in res:
+        i, j = r["pair"]
+        one = api.generate_manifold_jvp_batch(bodies[i], bodies[j], P[:, i].contiguous(), P[:, j].contiguous(),
+                                              SmoothingConfig(), want_src=True)
+        torch.cuda.synchronize()
+        for k in ("contacts", "tangents", "src", "mean_dist", "mean_dist_grad"):
+            assert torch.equal(r[k], one[k]), (r["pair"], k)
+
+
+def test_scene_jvp_matches_reference(cuda):
+    """Config D vs the reference: every pair's Dual12 Jacobian, env 0."""
+    g = np.load(os.path.join(GOLD, "jvp_cases.npz"))
+    sc = W.drop_scene(4)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    P = torch.as_tensor(sc.poses(4), device="cuda")
+    res = api.generate_manifold_scene_jvp_batch(bodies, P, SmoothingConfig(), is_static=sc.is_static())
+    torch.cuda.synchronize()
+    for q, r in enumerate(res):
+        assert_parity(r["contacts"][0].cpu().numpy(), g[f"drop_pair{q}_0_contacts"], what=f"drop pair {q}")
+        rep = jac_report(r["tangents"][0].cpu().numpy(), g[f"drop_pair{q}_0_tangents"])
+        assert max(rep.values()) <= 1.0, (q, rep)
+        ref_mean = g[f"drop_pair{q}_0_mean"]
+        assert np.linalg.norm(r["mean_dist_grad"][0].cpu().numpy() - ref_mean[1:]) <= \
+            JAC_ATOL + JAC_RTOL * np.linalg.norm(ref_mean[1:])
