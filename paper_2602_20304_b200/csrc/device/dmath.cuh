@@ -57,25 +57,25 @@ __device__ __forceinline__ double rsqrt_d(double x) {
 __device__ __forceinline__ double div_d(double a, double b) { return a * rcp_d(b); }
 
 // exp(x) in FP64 for x <= ~709: x = k ln2 + r, |r| <= ln2/2 (Cody-Waite split
-// of ln2), e^r by its degree-12 Taylor polynomial (truncation < 1e-16
-// relative), 2^k spliced into the exponent field. exp(x < -708) returns 0
-// (the true value is < 2.3e-308). ~17 FP64 instructions, no branches beyond
-// the underflow select -- the libdevice version carries full special-case
-// handling the indicator arguments never need.
+// of ln2), e^r by a degree-10 near-minimax polynomial (Chebyshev
+// interpolation, tools/minimax_coeffs.py: max relative error 3.3e-16), 2^k
+// spliced into the exponent field. exp(x < -708) returns 0 (the true value is
+// < 2.3e-308). ~15 FP64 instructions, no branches beyond the underflow select --
+// the libdevice version carries full special-case handling the indicator
+// arguments never need.
 // FP64 literals live in the constant bank so DFMA/DMUL read them as c[][]
 // operands (an immediate double costs two UMOVs + a uniform-pipe dependency).
 struct MathConsts {
-  double exp_c[13];  // 1/12! .. 1/0! (Horner order)
-  double log_c[12];  // 1/23, 1/21, ..., 1/3, 1
+  double exp_c[11];  // degree 10 .. 0 (Horner order)
+  double log_c[8];   // atanh(s)/s = Q(s^2), degree 7 .. 0 in s^2
   double log2e, ln2_hi, ln2_lo, ln2, sqrt2, floor30, floor20;
 };
 static __constant__ MathConsts kMC = {
-    {2.08767569878680989792e-09, 2.50521083854417187751e-08, 2.75573192239858906526e-07,
-     2.75573192239858906526e-06, 2.48015873015873015873e-05, 1.98412698412698412698e-04,
-     1.38888888888888888889e-03, 8.33333333333333333333e-03, 4.16666666666666666667e-02,
-     1.66666666666666666667e-01, 0.5, 1.0, 1.0},
-    {1.0 / 23, 1.0 / 21, 1.0 / 19, 1.0 / 17, 1.0 / 15, 1.0 / 13, 1.0 / 11, 1.0 / 9, 1.0 / 7, 1.0 / 5,
-     1.0 / 3, 1.0},
+    {2.7626357241447223e-07, 2.764018079620985e-06, 2.4801504346997686e-05, 0.00019841170270440067,
+     0.0013888888932488599, 0.008333333385667782, 0.04166666666657314, 0.16666666666554406,
+     0.5000000000000006, 1.0000000000000067, 1.0},
+    {0.07404855180327638, 0.07656264074182095, 0.09091815840114664, 0.11111098528363024,
+     0.1428571438032084, 0.1999999999965117, 0.33333333333333826, 1.0},
     1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
     6.93147180559945309417e-01, 1.4142135623730951, 1e-30, 1e-20};
 
@@ -85,15 +85,15 @@ __device__ __forceinline__ double exp_d(double x) {
   r = fma(-k, kMC.ln2_lo, r);
   double p = kMC.exp_c[0];
 #pragma unroll
-  for (int i = 1; i < 13; ++i) p = fma(p, r, kMC.exp_c[i]);
+  for (int i = 1; i < 11; ++i) p = fma(p, r, kMC.exp_c[i]);
   const int ki = (int)k;
   const double s = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   return x < -708.0 ? 0.0 : s;
 }
 
 // log(v) in FP64 for finite v > 0: v = 2^e m, m in [sqrt(1/2), sqrt(2)),
-// log m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, odd series to s^23
-// (truncation < 1e-17).
+// log m = 2 atanh(s) = 2 s Q(s^2), s = (m - 1)/(m + 1), |s| <= 0.1716, Q a
+// degree-7 near-minimax polynomial (max relative error 3e-18).
 __device__ __forceinline__ double log_d(double v) {
   int hi = __double2hiint(v);
   int e = ((hi >> 20) & 0x7ff) - 1023;
@@ -107,7 +107,7 @@ __device__ __forceinline__ double log_d(double v) {
   const double s2 = s * s;
   double p = kMC.log_c[0];
 #pragma unroll
-  for (int i = 1; i < 12; ++i) p = fma(p, s2, kMC.log_c[i]);
+  for (int i = 1; i < 8; ++i) p = fma(p, s2, kMC.log_c[i]);
   return fma((double)e, kMC.ln2, 2.0 * s * p);
 }
 
