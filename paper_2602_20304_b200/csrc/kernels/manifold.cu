@@ -10,8 +10,9 @@
 //   B  opposing-SDF vertex scores (top-K)     vertex/edge_penetrations 77-94
 //   C  rank sort of scores (top-K)            soft_topk sort     smooth_ops.hpp:180-185
 //   D  selected vertex / edge slots           select_topk_*      manifold.hpp:128-181
-//   E  V-S contacts | E-E pair stage          vs_contacts 185-204, ee_contacts 237-287
+//   E  E-E pair stage                         ee_contacts 237-287
 //   F  row / column NN softmin statistics     ee_contacts 289-301
+//      + V-S contacts on the idle warps       vs_contacts 185-204
 //   G  activity product + fixed-layout store  ee_contacts 303-330
 //   H  per-env mean contact distance          mean_contact_distance 379-384
 // Per-env state lives in shared memory (SmemLayout); the only HBM traffic is
@@ -367,28 +368,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   }
   __syncthreads();
 
-  // ---- E: V-S contacts, then E-E pair stage ------------------------------
+  // ---- E: E-E pair stage --------------------------------------------------
   const int C = p.n_contacts;
-  {
-    // V-S items are dealt lane-major across warps (item j -> warp j % nwarps)
-    // so every warp carries the same small extra load before the pair stage.
-    const int nvs = n1 + n2;
-    const int nwarps = nth >> 5;
-    for (int it = (tid & 31) * nwarps + (tid >> 5); it < n_here * nvs; it += nth) {
-      int e, r;
-      fdivmod(it, p.div_nvs, e, r);
-      const EnvView ev = env(e);
-      const double* q = ev.vslot(r);
-      float* dst = p.contacts + ((env0 + e) * C + r) * 8;
-      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      if (p.src) {
-        int* sp = p.src + ((env0 + e) * C + r) * 2;
-        sp[0] = ev.prov()[r];
-        sp[1] = -1;
-      }
-    }
-  }
   if (full) {
     // E1-E3 per pair, one thread owning the pair end to end (no barriers in
     // between; state passes through the pair's shared-memory record so each
@@ -413,10 +394,15 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   }
   __syncthreads();
 
-  if (full) {
+  {
     // ---- F: NN softmin statistics: rows (side 1) and columns (side 2) -------
+    // and, on the warps the NN items leave idle, the V-S contacts (vs_contacts,
+    // manifold.hpp:185-204; they read only phase-D state). Dense warps: a V-S
+    // item is ~1/6 of a pair, and spreading a few over every warp of phase E
+    // cost each warp a pass at 3-4 active lanes.
     const int nrc = m1 + m2;
-    for (int it = tid; it < n_here * nrc; it += nth) {
+    const int nF = full ? n_here * nrc : 0;
+    for (int it = tid; it < nF; it += nth) {
       int e, r;
       fdivmod(it, p.div_nrc, e, r);
       const EnvView ev = env(e);
@@ -435,7 +421,26 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
       ev.nnstat()[2 * r] = m;
       ev.nnstat()[2 * r + 1] = 1.0 / tot;
     }
-    __syncthreads();
+    const int nvs = n1 + n2;
+    const int vs0 = ((nF + 31) & ~31) % nth;  // first thread of the first warp after the NN items
+    for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < n_here * nvs; it += nth) {
+      int e, r;
+      fdivmod(it, p.div_nvs, e, r);
+      const EnvView ev = env(e);
+      const double* q = ev.vslot(r);
+      float* dst = p.contacts + ((env0 + e) * C + r) * 8;
+      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      if (p.src) {
+        int* sp = p.src + ((env0 + e) * C + r) * 2;
+        sp[0] = ev.prov()[r];
+        sp[1] = -1;
+      }
+    }
+  }
+  __syncthreads();
+
+  if (full) {
     // ---- G: activity product + fixed-layout E-E output (303-330) -----------
     for (int it = tid; it < n_here * P; it += nth) {
       int e, i, k, l;
