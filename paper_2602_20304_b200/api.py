@@ -95,7 +95,7 @@ class Mesh:
         return Mesh(out)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and abi is not None and abi.load is not None:  # not at interpreter exit
             abi.load().cmgb_mesh_destroy(self._h)
             self._h = None
 
@@ -126,7 +126,7 @@ class Surface:
         return self.info["effective_edge_topk"]
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and abi is not None and abi.load is not None:  # not at interpreter exit
             abi.load().cmgb_surface_destroy(self._h)
             self._h = None
 
