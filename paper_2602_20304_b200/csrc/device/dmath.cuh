@@ -114,6 +114,13 @@ __device__ __forceinline__ double log_d(double v) {
 // Primal of a scalar (the Dual<N> overload lives in dual.cuh): branches of the
 // templated routines read it, like the reference's HardBranchScope reads.
 __device__ __forceinline__ double pv(double x) { return x; }
+__device__ __forceinline__ double pv(float x) { return x; }
+
+// FP32 members of the overload sets (the K6 witness batches' soft indicators,
+// witness.cuh): accurate libdevice expf / logf, IEEE reciprocal.
+__device__ __forceinline__ float exp_d(float x) { return expf(x); }
+__device__ __forceinline__ float log_d(float x) { return logf(x); }
+__device__ __forceinline__ float rcp_d(float x) { return __frcp_rn(x); }
 
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
 // function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each

@@ -28,7 +28,7 @@ struct EeSolve {
   template <typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
     const double3 e1a = load3(q), e1b = load3(q + 3), e2a = load3(q + 6), e2b = load3(q + 9);
-    const QpSol s = ee_qp(e1a, e1b, e2a, e2b, p.cfg);
+    const QpSol s = ee_qp<double, float>(e1a, e1b, e2a, e2b, p.cfg);  // FP32 indicators (witness.cuh)
     const double3 p1 = e1a + (e1b - e1a) * s.a1;  // edge_point (witness.hpp:130-133)
     const double3 p2 = e2a + (e2b - e2a) * s.a2;
     o[0] = (float)p1.x; o[1] = (float)p1.y; o[2] = (float)p1.z;
@@ -48,7 +48,7 @@ struct VfSolve {
   template <typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
     int label;
-    const double3 r = vf_witness(load3(q), load3(q + 3), load3(q + 6), load3(q + 9), p.cfg, &label);
+    const double3 r = vf_witness<float>(load3(q), load3(q + 3), load3(q + 6), load3(q + 9), p.cfg, &label);
     o[0] = (float)r.x; o[1] = (float)r.y; o[2] = (float)r.z;
     if (p.labels) p.labels[idx] = label;
   }
