@@ -253,7 +253,13 @@ struct HostScratch {
   float* mean = nullptr;
   double* frames = nullptr;
   size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0, cap_frames = 0;
+  cudaStream_t q[2] = {nullptr, nullptr};  // pipeline streams of the host-buffer API
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
 };
+
+// Smallest env chunk worth its own pipeline stage of the host-buffer API.
+constexpr int64_t kHostChunkMin = 8192;
 
 size_t workspace_doubles(int64_t n_env, int st1, int st2) {
   return 12 * (size_t)((st1 ? n_env : 1) + (st2 ? n_env : 1));
@@ -550,6 +556,7 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     if (!s1 || !s2) invalid("manifold_batch_host: null surface");
     validate_config(cfg);
     if (!poses1_host || !poses2_host) invalid("manifold_batch_host: null poses");
+    if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
     if (n_env == 0) return;
     const cmgb_layout L = layout_of(s1, s2, cfg);
     int dev = 0;
@@ -561,22 +568,64 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     ensure(&sc.poses2, &sc.cap_poses2, np2);
     ensure(&sc.contacts, &sc.cap_contacts, (size_t)n_env * L.n_contacts * 8);
     ensure(&sc.mean, &sc.cap_mean, (size_t)n_env);
+    // Pipelined over env chunks on two internal streams: chunk c+1's pose
+    // upload overlaps chunk c's kernels, and each chunk's results stream back
+    // as soon as it is done. Ordered after the caller's stream and joined back
+    // into it (then synchronised: the outputs are host memory).
+    if (!sc.q[0]) {
+      for (int k = 0; k < 2; ++k) {
+        cuda_check(cudaStreamCreateWithFlags(&sc.q[k], cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&sc.ev[k], cudaEventDisableTiming), "cudaEventCreate");
+      }
+      cuda_check(cudaEventCreateWithFlags(&sc.ev_start, cudaEventDisableTiming), "cudaEventCreate");
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cuda_check(cudaMemcpyAsync(sc.poses1, poses1_host, sizeof(double) * np1, cudaMemcpyHostToDevice, s),
-               "H2D poses1");
-    cuda_check(cudaMemcpyAsync(sc.poses2, poses2_host, sizeof(double) * np2, cudaMemcpyHostToDevice, s),
-               "H2D poses2");
-    ensure(&sc.frames, &sc.cap_frames, workspace_doubles(n_env, st1, st2));
-    cmgb_manifold_out out{sc.contacts, nullptr, nullptr, sc.mean, sc.frames, sc.cap_frames * sizeof(double)};
-    LaunchPlan plan = plan_manifold(s1, s2, sc.poses1, st1, sc.poses2, st2, n_env, cfg, &out);
-    launch_with_workspace(plan, n_env, st1, st2, out.workspace, out.workspace_bytes, s);
-    if (mean_dist_host)
-      cuda_check(cudaMemcpyAsync(mean_dist_host, sc.mean, sizeof(float) * n_env, cudaMemcpyDeviceToHost, s),
-                 "D2H mean");
-    if (contacts_host)
-      cuda_check(cudaMemcpyAsync(contacts_host, sc.contacts, sizeof(float) * n_env * L.n_contacts * 8,
-                                 cudaMemcpyDeviceToHost, s),
-                 "D2H contacts");
+    const int64_t nchunk = n_env >= 4 * kHostChunkMin ? 4 : (n_env >= 2 * kHostChunkMin ? 2 : 1);
+    const int64_t per = (n_env + nchunk - 1) / nchunk;
+    ensure(&sc.frames, &sc.cap_frames, 2 * workspace_doubles(per, st1, st2));
+    cuda_check(cudaEventRecord(sc.ev_start, s), "cudaEventRecord");
+    for (int k = 0; k < 2; ++k) cuda_check(cudaStreamWaitEvent(sc.q[k], sc.ev_start, 0), "cudaStreamWaitEvent");
+    // shared (stride-0) poses: uploaded once, before either stream uses them
+    for (int b = 0; b < 2; ++b) {
+      const bool shared = b == 0 ? !st1 : !st2;
+      if (!shared) continue;
+      cuda_check(cudaMemcpyAsync(b == 0 ? sc.poses1 : sc.poses2, b == 0 ? poses1_host : poses2_host,
+                                 sizeof(double) * 6, cudaMemcpyHostToDevice, sc.q[0]),
+                 "H2D shared pose");
+    }
+    cuda_check(cudaEventRecord(sc.ev[0], sc.q[0]), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(sc.q[1], sc.ev[0], 0), "cudaStreamWaitEvent");
+    const size_t C = (size_t)L.n_contacts;
+    for (int64_t c = 0; c < nchunk; ++c) {
+      const int64_t e0 = c * per, ne = std::min(per, n_env - e0);
+      if (ne <= 0) break;
+      cudaStream_t q = sc.q[c & 1];
+      double* p1 = sc.poses1 + (st1 ? 6 * e0 : 0);
+      double* p2 = sc.poses2 + (st2 ? 6 * e0 : 0);
+      if (st1)
+        cuda_check(cudaMemcpyAsync(p1, poses1_host + 6 * e0, sizeof(double) * 6 * ne, cudaMemcpyHostToDevice, q),
+                   "H2D poses1");
+      if (st2)
+        cuda_check(cudaMemcpyAsync(p2, poses2_host + 6 * e0, sizeof(double) * 6 * ne, cudaMemcpyHostToDevice, q),
+                   "H2D poses2");
+      // n == 1 chunks keep stride semantics: a single-env chunk with st = 1 is one pose
+      cmgb_manifold_out out{sc.contacts + e0 * C * 8, nullptr, nullptr, sc.mean + e0,
+                            sc.frames + (c & 1) * workspace_doubles(per, st1, st2),
+                            workspace_doubles(per, st1, st2) * sizeof(double)};
+      LaunchPlan plan = plan_manifold(s1, s2, p1, st1, p2, st2, ne, cfg, &out);
+      launch_with_workspace(plan, ne, st1, st2, out.workspace, out.workspace_bytes, q);
+      if (mean_dist_host)
+        cuda_check(cudaMemcpyAsync(mean_dist_host + e0, sc.mean + e0, sizeof(float) * ne, cudaMemcpyDeviceToHost, q),
+                   "D2H mean");
+      if (contacts_host)
+        cuda_check(cudaMemcpyAsync(contacts_host + e0 * C * 8, sc.contacts + e0 * C * 8, sizeof(float) * ne * C * 8,
+                                   cudaMemcpyDeviceToHost, q),
+                   "D2H contacts");
+    }
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaEventRecord(sc.ev[k], sc.q[k]), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(s, sc.ev[k], 0), "cudaStreamWaitEvent");
+    }
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   });
 }
