@@ -125,6 +125,33 @@ inline void generate_manifold_batch_host(const Surface& a, const Surface& b, con
                                  n_env, &c, mean_dist, contacts, stream));
 }
 
+// generate_manifold<Dual12> with seed_pose_tangents (dual.hpp:249-263) for every
+// env: primal contacts + their 12 pose tangents (smooth mode only).
+inline void generate_manifold_jvp_batch(const Surface& a, const Surface& b, const double* poses1,
+                                        int pose1_stride, const double* poses2, int pose2_stride,
+                                        int64_t n_env, const SmoothingConfig& c,
+                                        const cmgb_manifold_jvp_out& out, void* stream = nullptr) {
+  check(cmgb_manifold_jvp_batch(a.handle(), b.handle(), poses1, pose1_stride, poses2, pose2_stride, n_env,
+                                &c, &out, stream));
+}
+
+// DemoSim::step's pair loop (demosim.cpp:88-104): every non-static body pair.
+inline std::vector<int32_t> scene_pairs(const std::vector<int32_t>& is_static) {
+  int32_t n = 0;
+  check(cmgb_scene_pairs(is_static.data(), (int32_t)is_static.size(), nullptr, &n));
+  std::vector<int32_t> pairs(2 * (size_t)n);
+  check(cmgb_scene_pairs(is_static.data(), (int32_t)is_static.size(), pairs.data(), &n));
+  return pairs;
+}
+
+// poses: device [n_env][n_bodies][6]; outs[q] for pair q of `pairs`.
+inline void generate_scene_batch(const std::vector<cmgb_surface>& bodies, const std::vector<int32_t>& pairs,
+                                 const double* poses, int64_t n_env, const SmoothingConfig& c,
+                                 const std::vector<cmgb_manifold_out>& outs, void* stream = nullptr) {
+  check(cmgb_manifold_scene_batch(bodies.data(), (int32_t)bodies.size(), pairs.data(),
+                                  (int32_t)(pairs.size() / 2), poses, n_env, &c, outs.data(), stream));
+}
+
 inline void run_ee_batch(const double* pairs_device, int64_t n, const SmoothingConfig& c,
                          float* out_device, void* stream = nullptr) {
   check(cmgb_ee_witness_batch(pairs_device, 1, n, &c, out_device, nullptr, nullptr, stream));
