@@ -228,6 +228,45 @@ int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* pose
                             void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * Batched demo integrator — DemoSim::step (src/demosim.cpp:81-138) for every
+ * env of a batch: all-pairs manifolds -> penalty_forces (31-66) -> semi-
+ * implicit Euler on SE(3) with se3_log bookkeeping (108-133).
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_demo_params { /* PenaltyParams (include/cmg/demosim.hpp:24-31) */
+  double stiffness;         /* N/m */
+  double damping;           /* N s/m along the normal */
+  double friction;          /* Coulomb coefficient */
+  double friction_viscous;  /* N s/m tangential, capped by friction |Fn| */
+  double tau_force;         /* softplus temperature of max_s(-dist, 0) (m) */
+  double gravity[3];
+} cmgb_demo_params;
+
+typedef struct cmgb_demo_body { /* SceneBody's dynamics fields (include/cmg/scene.hpp:15-22) */
+  cmgb_surface surface;
+  double mass;
+  double inertia_diag[3]; /* all > 0, else derived from the mesh AABB (demosim.cpp:17-23) */
+  int32_t is_static;
+  int32_t reserved;
+} cmgb_demo_body;
+
+void cmgb_demo_params_default(cmgb_demo_params* p);
+
+/* Device scratch one cmgb_demo_step_batch call needs. */
+size_t cmgb_demo_workspace_bytes(const cmgb_demo_body* bodies, int32_t n_bodies, const cmgb_config* cfg,
+                                 int64_t n_env);
+
+/* One DemoSim::step(dt) for every env. poses / velocities: DEVICE
+ * [n_env][n_bodies][6] FP64, updated in place (velocity = world [linear;
+ * angular]). deepest: optional DEVICE [n_env] FP64 deepest_penetration();
+ * ok: optional DEVICE [n_env] int32, 0 where the state went non-finite (the
+ * reference's step() == false; that env's state is then undefined). workspace:
+ * optional (cmgb_demo_workspace_bytes), else taken from the stream-ordered pool. */
+int cmgb_demo_step_batch(const cmgb_demo_body* bodies, int32_t n_bodies, const cmgb_config* cfg,
+                         const cmgb_demo_params* params, double dt, int64_t n_env, double* poses,
+                         double* velocities, double* deepest, int32_t* ok, void* workspace,
+                         size_t workspace_bytes, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * Multi-body scenes — the all-pairs loop of DemoSim::step (src/demosim.cpp:
  * 88-104): every body pair (i < j) except static-static, for every env.
  * ------------------------------------------------------------------------- */

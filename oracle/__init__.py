@@ -250,6 +250,9 @@ class Ref:
                                                 C.POINTER(abi.CmgbConfig), C.c_int, _D, _I32, _D]
             L.cmgref_manifold_jvp.argtypes = [_P, _P, _D, _D, C.POINTER(abi.CmgbConfig), _D, _D, _D]
             L.cmgref_random_pairs.argtypes = [C.c_int64, C.c_uint64, _D]
+            L.cmgref_demo_run.restype = C.c_int
+            L.cmgref_demo_run.argtypes = [C.POINTER(_P), C.c_int, _I32, _D, _D, _D, _D, C.POINTER(abi.CmgbConfig),
+                                          C.POINTER(abi.CmgbDemoParams), C.c_double, C.c_int, _D, _D, _D, _D]
             L.cmgref_ee_batch.restype = C.c_double
             L.cmgref_ee_batch.argtypes = [_D, C.c_int64, C.POINTER(abi.CmgbConfig), C.c_int, _D]
             L.cmgref_vf_batch.restype = C.c_double
@@ -395,6 +398,32 @@ class Ref:
                                  _dp(tangents), _dp(md)):
             raise ValueError(Ref.err())
         return dict(contacts=contacts, tangents=tangents, mean_dist=md[0], mean_dist_grad=md[1:])
+
+    @staticmethod
+    def demo_run(surfaces, is_static, mass, inertia, poses, vels, cfg=None, params=None, dt=1e-3, steps=1):
+        """DemoSim (src/demosim.cpp) from a state: per-step poses / velocities
+        [steps, n, 6], deepest_penetration [steps], kinetic_energy [steps]."""
+        from paper_2602_20304_b200.scene import PenaltyParams
+
+        L = Ref.lib()
+        n = len(surfaces)
+        hs = (_P * n)(*[s.h for s in surfaces])
+        st = np.ascontiguousarray(is_static, dtype=np.int32)
+        m = np.ascontiguousarray(mass, dtype=np.float64)
+        I = np.ascontiguousarray(inertia, dtype=np.float64).reshape(n, 3)
+        P = np.ascontiguousarray(poses, dtype=np.float64).reshape(n, 6)
+        V = np.ascontiguousarray(vels, dtype=np.float64).reshape(n, 6)
+        po = np.zeros((steps, n, 6))
+        vo = np.zeros((steps, n, 6))
+        de = np.zeros(steps)
+        ke = np.zeros(steps)
+        c = _cfg(cfg)
+        pp = (params or PenaltyParams()).to_c()
+        done = L.cmgref_demo_run(hs, n, _ip(st), _dp(m), _dp(I), _dp(P), _dp(V), C.byref(c), C.byref(pp), dt, steps,
+                                 _dp(po), _dp(vo), _dp(de), _dp(ke))
+        if done < 0:
+            raise ValueError(Ref.err())
+        return dict(poses=po[:done], velocities=vo[:done], deepest=de[:done], kinetic_energy=ke[:done])
 
     @staticmethod
     def random_pairs(n, seed=0):

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "cmg/batch.hpp"
+#include "cmg/demosim.hpp"
 #include "cmg/manifold.hpp"
 #include "cmg/mesh.hpp"
 #include "cmg/pose.hpp"
@@ -539,6 +540,69 @@ int cmgref_config_validate(const cmgb_config* c) {
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// DemoSim (src/demosim.cpp:68-138) over a programmatic Scene (no JSON): runs
+// `steps` steps of dt from the given state, recording after every step the
+// poses / velocities [steps][n][6], deepest_penetration() and kinetic energy.
+// Returns the number of steps that succeeded (step() == true).
+int cmgref_demo_run(void* const* surfaces, int n, const int32_t* is_static, const double* mass,
+                    const double* inertia, const double* poses, const double* vels, const cmgb_config* c,
+                    const cmgb_demo_params* pp, double dt, int steps, double* poses_out, double* vels_out,
+                    double* deepest_out, double* ke_out) {
+  try {
+    Scene scene;
+    scene.smoothing = to_cfg(c);
+    for (int i = 0; i < n; ++i) {
+      SceneBody b;
+      b.name = "b" + std::to_string(i);
+      b.surface = *static_cast<SurfaceModel*>(surfaces[i]);
+      for (int k = 0; k < 6; ++k) b.pose[k] = poses[6 * i + k];
+      b.mass = mass[i];
+      b.inertia_diag = Vec3d{inertia[3 * i], inertia[3 * i + 1], inertia[3 * i + 2]};
+      b.is_static = is_static[i] != 0;
+      scene.bodies.push_back(std::move(b));
+    }
+    PenaltyParams params;
+    params.stiffness = pp->stiffness;
+    params.damping = pp->damping;
+    params.friction = pp->friction;
+    params.friction_viscous = pp->friction_viscous;
+    params.tau_force = pp->tau_force;
+    params.gravity = Vec3d{pp->gravity[0], pp->gravity[1], pp->gravity[2]};
+    DemoSim sim(scene, params);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < 6; ++k) sim.states()[i].velocity[k] = vels[6 * i + k];
+    int done = 0;
+    for (int s = 0; s < steps; ++s) {
+      if (!sim.step(dt)) break;
+      ++done;
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 6; ++k) {
+          poses_out[(s * n + i) * 6 + k] = sim.states()[i].pose[k];
+          vels_out[(s * n + i) * 6 + k] = sim.states()[i].velocity[k];
+        }
+      if (deepest_out) deepest_out[s] = sim.deepest_penetration();
+      if (ke_out) ke_out[s] = sim.kinetic_energy();
+    }
+    return done;
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+
+// PenaltyParams{} defaults (include/cmg/demosim.hpp:24-31).
+void cmgref_demo_params_default(cmgb_demo_params* p) {
+  const PenaltyParams d;
+  p->stiffness = d.stiffness;
+  p->damping = d.damping;
+  p->friction = d.friction;
+  p->friction_viscous = d.friction_viscous;
+  p->tau_force = d.tau_force;
+  p->gravity[0] = d.gravity.x;
+  p->gravity[1] = d.gravity.y;
+  p->gravity[2] = d.gravity.z;
 }
 
 }  // extern "C"

@@ -105,6 +105,29 @@ class CmgbManifoldJvpOut(C.Structure):
     ]
 
 
+class CmgbDemoParams(C.Structure):
+    """cmgb_demo_params == cmg::PenaltyParams (demosim.hpp:24-31)."""
+
+    _fields_ = [
+        ("stiffness", C.c_double),
+        ("damping", C.c_double),
+        ("friction", C.c_double),
+        ("friction_viscous", C.c_double),
+        ("tau_force", C.c_double),
+        ("gravity", C.c_double * 3),
+    ]
+
+
+class CmgbDemoBody(C.Structure):
+    _fields_ = [
+        ("surface", C.c_void_p),
+        ("mass", C.c_double),
+        ("inertia_diag", C.c_double * 3),
+        ("is_static", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
 # Every exported symbol of include/cmgb.h with its ctypes signature.
 _P = C.c_void_p
 _I = C.c_int
@@ -165,6 +188,14 @@ SIGNATURES = {
         _I,
         [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig),
          C.POINTER(CmgbManifoldJvpOut), _P],
+    ),
+    "cmgb_demo_params_default": (None, [C.POINTER(CmgbDemoParams)]),
+    "cmgb_demo_workspace_bytes": (C.c_size_t, [C.POINTER(CmgbDemoBody), C.c_int32, C.POINTER(CmgbConfig),
+                                               C.c_int64]),
+    "cmgb_demo_step_batch": (
+        _I,
+        [C.POINTER(CmgbDemoBody), C.c_int32, C.POINTER(CmgbConfig), C.POINTER(CmgbDemoParams), C.c_double,
+         C.c_int64, _P, _P, _P, _P, _P, C.c_size_t, _P],
     ),
     "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
     "cmgb_manifold_scene_batch": (

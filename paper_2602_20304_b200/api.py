@@ -431,3 +431,107 @@ def surface_from_spec(body) -> Surface:
     mesh = Mesh.box(m.box_half, m.subdivisions, m.quad_edges) if m.box_half is not None \
         else Mesh.parse_obj(m.obj_text)
     return Surface(mesh, body.sdf, body.vertex_topk, body.edge_topk)
+
+
+class DemoBatch:
+    """DemoSim (src/demosim.cpp:68-186) over a batch of n_env copies of a
+    scene, stepped on the GPU (cmgb_demo_step_batch): all-pairs manifolds ->
+    penalty_forces -> semi-implicit Euler on SE(3), every env in one call per
+    step. State lives in CUDA float64 tensors: poses / velocities
+    [n_env, n_bodies, 6] (velocity = world [linear; angular])."""
+
+    def __init__(self, bodies, masses=None, *, inertia=None, is_static=None, cfg=None, params=None,
+                 poses=None, velocities=None, n_env: int = 1, device="cuda"):
+        import torch
+
+        from .scene import PenaltyParams
+
+        nb = len(bodies)
+        self.bodies = list(bodies)
+        self.cfg = _cfg(cfg)
+        self.params = (params or PenaltyParams()).to_c()
+        masses = np.ones(nb) if masses is None else np.asarray(masses, dtype=np.float64)
+        inertia = np.zeros((nb, 3)) if inertia is None else np.asarray(inertia, dtype=np.float64).reshape(nb, 3)
+        is_static = np.zeros(nb, bool) if is_static is None else np.asarray(is_static, bool)
+        self.is_static = is_static
+        self.masses = masses
+        self._bodies = (abi.CmgbDemoBody * nb)()
+        for i, b in enumerate(bodies):
+            d = self._bodies[i]
+            d.surface = b._h.value if isinstance(b._h, C.c_void_p) else b._h
+            d.mass = float(masses[i])
+            for k in range(3):
+                d.inertia_diag[k] = float(inertia[i, k])
+            d.is_static = int(is_static[i])
+        P = np.zeros((n_env, nb, 6)) if poses is None else np.array(np.broadcast_to(
+            np.asarray(poses, dtype=np.float64), (n_env, nb, 6)))
+        V = np.zeros((n_env, nb, 6)) if velocities is None else np.array(np.broadcast_to(
+            np.asarray(velocities, dtype=np.float64), (n_env, nb, 6)))
+        self.poses = torch.as_tensor(np.ascontiguousarray(P), device=device)
+        self.velocities = torch.as_tensor(np.ascontiguousarray(V), device=device)
+        self.deepest = torch.zeros(n_env, dtype=torch.float64, device=device)
+        self.ok = torch.ones(n_env, dtype=torch.int32, device=device)
+        ws = abi.load().cmgb_demo_workspace_bytes(self._bodies, nb, C.byref(self.cfg), n_env)
+        self._ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=device)
+        self.n_env = n_env
+        self.time = 0.0
+
+    def step(self, dt: float, n: int = 1, stream=None) -> None:
+        """n DemoSim::step(dt) calls for every env (stream-ordered)."""
+        import torch
+
+        lib = abi.load()
+        with torch.cuda.device(self.poses.device):
+            for _ in range(n):
+                _ok(lib.cmgb_demo_step_batch(self._bodies, len(self.bodies), C.byref(self.cfg),
+                                             C.byref(self.params), float(dt), self.n_env,
+                                             self.poses.data_ptr(), self.velocities.data_ptr(),
+                                             self.deepest.data_ptr(), self.ok.data_ptr(), self._ws.data_ptr(),
+                                             self._ws.numel(), _stream_ptr(stream)))
+                self.time += dt
+
+    def inertia_diag(self) -> np.ndarray:
+        """Per-body inertia as DemoSim uses it: given, or the mesh-AABB box
+        inertia (demosim.cpp:17-23, 68-79)."""
+        out = np.zeros((len(self.bodies), 3))
+        for i, b in enumerate(self.bodies):
+            given = np.array([self._bodies[i].inertia_diag[k] for k in range(3)])
+            out[i] = given if (given > 0).all() else _box_inertia(self.masses[i], b.mesh.vertices)
+        return out
+
+    def kinetic_energy(self) -> np.ndarray:
+        """DemoSim::kinetic_energy (demosim.cpp:140-155) per env (host)."""
+        return kinetic_energy_np(self.poses.cpu().numpy(), self.velocities.cpu().numpy(), self.masses,
+                                 self.inertia_diag(), self.is_static)
+
+
+def kinetic_energy_np(poses, vels, masses, inertia, is_static) -> np.ndarray:
+    """DemoSim::kinetic_energy (demosim.cpp:140-155) for [n_env, n_bodies, 6] states."""
+    poses = np.asarray(poses, np.float64).reshape(-1, len(masses), 6)
+    vels = np.asarray(vels, np.float64).reshape(-1, len(masses), 6)
+    e = np.zeros(len(poses))
+    for i in range(len(masses)):
+        if is_static[i]:
+            continue
+        v = vels[:, i]
+        e += 0.5 * masses[i] * (v[:, :3] ** 2).sum(axis=1)
+        for n in range(len(poses)):
+            wb = _so3_exp_np(poses[n, i, 3:]).T @ v[n, 3:]
+            e[n] += 0.5 * float((inertia[i] * wb * wb).sum())
+    return e
+
+
+def _box_inertia(mass, vertices):
+    s = vertices.max(axis=0) - vertices.min(axis=0)
+    return mass / 12.0 * np.array([s[1] ** 2 + s[2] ** 2, s[0] ** 2 + s[2] ** 2, s[0] ** 2 + s[1] ** 2])
+
+
+def _so3_exp_np(w):
+    th2 = float(w @ w)
+    if th2 < 1e-8:
+        a, b = 1 - th2 / 6 + th2 * th2 / 120, 0.5 - th2 / 24 + th2 * th2 / 720
+    else:
+        th = np.sqrt(th2)
+        a, b = np.sin(th) / th, (1 - np.cos(th)) / th2
+    W = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
+    return np.eye(3) + W * a + (W @ W) * b

@@ -140,6 +140,45 @@ struct JvpParams {
   int32_t bytes;  // per unit
 };
 
+// Demo integrator (kernels/demo.cu). PenaltyParams (demosim.hpp:24-31).
+constexpr int kDemoMaxBodies = 16;
+constexpr int kDemoMaxPairs = kDemoMaxBodies * (kDemoMaxBodies - 1) / 2;
+
+struct DemoParamsDev {
+  double stiffness, damping, friction, friction_viscous, tau_force;
+  double gravity[3];
+};
+
+struct PenaltyArgs {
+  const float* contacts;  // [n_env][C][8] of pair (bi, bj)
+  const double* frames1;  // [n_env][12] R, t of body bi (the pair's frames workspace)
+  const double* frames2;
+  const double* vel;      // [n_env][nb][6]
+  int32_t nb, bi, bj;
+  int32_t C, n1, n2;      // layout: V-S rows of side 1 / side 2, then E-E rows alternating sides
+  int64_t n_env;
+  DemoParamsDev prm;
+  double* wrench;         // [n_env][12]: force1, torque1, force2, torque2
+  double* deepest;        // [n_env]
+};
+
+struct IntegrateArgs {
+  double* poses;                // [n_env][nb][6]
+  double* vel;                  // [n_env][nb][6]
+  const double* wrench;         // [n_pairs][n_env][12]
+  const double* pair_deepest;   // [n_pairs][n_env]
+  double* deepest;              // [n_env] or null
+  int32_t* ok;                  // [n_env] or null
+  int64_t n_env;
+  int32_t nb, n_pairs;
+  double dt;
+  double gravity[3];
+  double mass[kDemoMaxBodies];
+  double inertia[3 * kDemoMaxBodies];
+  int32_t is_static[kDemoMaxBodies];
+  int32_t pair_i[kDemoMaxPairs], pair_j[kDemoMaxPairs];
+};
+
 struct WitnessParams {
   const void* pairs;
   int32_t fp64;
@@ -161,6 +200,8 @@ int jvp_directions();    // tangent directions per thread of the compiled JVP ke
 int jvp_max_threads();   // CTA size of the JVP kernel
 int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan for
 int launch_ee_witness(const WitnessParams& p, void* stream);
+int launch_penalty(const PenaltyArgs& a, void* stream);
+int launch_integrate(const IntegrateArgs& a, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);
 const char* last_cuda_error_string();
 }  // namespace cmgb

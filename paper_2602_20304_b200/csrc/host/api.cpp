@@ -781,6 +781,167 @@ int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, cons
   });
 }
 
+// ---- batched demo integrator (DemoSim::step) -------------------------------------
+void cmgb_demo_params_default(cmgb_demo_params* p) {
+  if (!p) return;
+  // PenaltyParams{} (include/cmg/demosim.hpp:24-31)
+  p->stiffness = 1e4;
+  p->damping = 100.0;
+  p->friction = 0.5;
+  p->friction_viscous = 100.0;
+  p->tau_force = 1e-4;
+  p->gravity[0] = 0.0;
+  p->gravity[1] = 0.0;
+  p->gravity[2] = -9.81;
+}
+
+namespace {
+
+struct DemoPlan {
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<int> C;              // contacts per pair
+  std::vector<size_t> off_contacts, off_frames;
+  size_t off_wrench = 0, off_deep = 0, bytes = 0;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+DemoPlan plan_demo(const cmgb_demo_body* bodies, int32_t nb, const cmgb_config* cfg, int64_t n_env) {
+  if (!bodies || nb < 1) invalid("demo: bodies required");
+  if (nb > kDemoMaxBodies) invalid("demo: at most 16 bodies per scene");
+  validate_config(cfg);
+  if (n_env < 0) invalid("demo: n_env >= 0");
+  DemoPlan d;
+  for (int i = 0; i < nb; ++i) {
+    if (!bodies[i].surface) invalid("demo: null surface");
+    if (!(bodies[i].mass > 0.0)) invalid("demo: body mass must be > 0");
+  }
+  for (int i = 0; i < nb; ++i)
+    for (int j = i + 1; j < nb; ++j)
+      if (!(bodies[i].is_static && bodies[j].is_static)) d.pairs.emplace_back(i, j);
+  size_t off = 0;
+  for (const auto& [i, j] : d.pairs) {
+    const cmgb_layout L = layout_of(bodies[i].surface, bodies[j].surface, cfg);
+    d.C.push_back(L.n_contacts);
+    d.off_contacts.push_back(off);
+    off = align256(off + sizeof(float) * (size_t)n_env * L.n_contacts * 8);
+    d.off_frames.push_back(off);
+    off = align256(off + sizeof(double) * workspace_doubles(n_env, 1, 1));
+  }
+  d.off_wrench = off;
+  off = align256(off + sizeof(double) * d.pairs.size() * (size_t)n_env * 12);
+  d.off_deep = off;
+  off = align256(off + sizeof(double) * d.pairs.size() * (size_t)n_env);
+  d.bytes = std::max<size_t>(off, 256);
+  return d;
+}
+
+}  // namespace
+
+size_t cmgb_demo_workspace_bytes(const cmgb_demo_body* bodies, int32_t n_bodies, const cmgb_config* cfg,
+                                 int64_t n_env) {
+  try {
+    return plan_demo(bodies, n_bodies, cfg, n_env).bytes;
+  } catch (...) {
+    return 0;
+  }
+}
+
+int cmgb_demo_step_batch(const cmgb_demo_body* bodies, int32_t nb, const cmgb_config* cfg,
+                         const cmgb_demo_params* prm, double dt, int64_t n_env, double* poses,
+                         double* velocities, double* deepest, int32_t* ok, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!prm) invalid("demo: null params");
+    if (!poses || !velocities) invalid("demo: poses and velocities are required");
+    const DemoPlan d = plan_demo(bodies, nb, cfg, n_env);
+    if (n_env == 0) return;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* buf = workspace;
+    const bool pooled = workspace == nullptr || workspace_bytes < d.bytes;
+    if (pooled) cuda_check(cudaMallocAsync(&buf, d.bytes, s), "cudaMallocAsync(demo workspace)");
+    unsigned char* base = static_cast<unsigned char*>(buf);
+    DemoParamsDev P{prm->stiffness, prm->damping, prm->friction, prm->friction_viscous, prm->tau_force,
+                    {prm->gravity[0], prm->gravity[1], prm->gravity[2]}};
+    double* wrench = reinterpret_cast<double*>(base + d.off_wrench);
+    double* pdeep = reinterpret_cast<double*>(base + d.off_deep);
+    int rc = 0;
+    for (size_t q = 0; q < d.pairs.size() && rc == 0; ++q) {
+      const auto [i, j] = d.pairs[q];
+      float* contacts = reinterpret_cast<float*>(base + d.off_contacts[q]);
+      double* frames = reinterpret_cast<double*>(base + d.off_frames[q]);
+      cmgb_manifold_out out{contacts, nullptr, nullptr, nullptr, frames, sizeof(double) * workspace_doubles(n_env, 1, 1)};
+      LaunchPlan plan = plan_manifold(bodies[i].surface, bodies[j].surface, poses + 6 * i, 1, poses + 6 * j, 1,
+                                      n_env, cfg, &out);
+      if (plan.p.n_contacts == 0) {  // no contacts: zero wrench / deepest for this pair
+        cuda_check(cudaMemsetAsync(wrench + q * n_env * 12, 0, sizeof(double) * n_env * 12, s), "memset");
+        cuda_check(cudaMemsetAsync(pdeep + q * n_env, 0, sizeof(double) * n_env, s), "memset");
+        continue;
+      }
+      plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)nb;
+      launch_with_workspace(plan, n_env, 1, 1, frames, out.workspace_bytes, s);
+      PenaltyArgs a{};
+      a.contacts = contacts;
+      a.frames1 = frames;
+      a.frames2 = frames + 12 * n_env;
+      a.vel = velocities;
+      a.nb = nb;
+      a.bi = i;
+      a.bj = j;
+      a.C = plan.p.n_contacts;
+      a.n1 = plan.p.n1;
+      a.n2 = plan.p.n2;
+      a.n_env = n_env;
+      a.prm = P;
+      a.wrench = wrench + q * n_env * 12;
+      a.deepest = pdeep + q * n_env;
+      rc = launch_penalty(a, s);
+    }
+    if (rc == 0) {
+      IntegrateArgs g{};
+      g.poses = poses;
+      g.vel = velocities;
+      g.wrench = wrench;
+      g.pair_deepest = pdeep;
+      g.deepest = deepest;
+      g.ok = ok;
+      g.n_env = n_env;
+      g.nb = nb;
+      g.n_pairs = (int32_t)d.pairs.size();
+      g.dt = dt;
+      for (int k = 0; k < 3; ++k) g.gravity[k] = prm->gravity[k];
+      for (int b = 0; b < nb; ++b) {
+        g.mass[b] = bodies[b].mass;
+        g.is_static[b] = bodies[b].is_static ? 1 : 0;
+        const double* I = bodies[b].inertia_diag;
+        if (I[0] > 0.0 && I[1] > 0.0 && I[2] > 0.0) {
+          for (int k = 0; k < 3; ++k) g.inertia[3 * b + k] = I[k];
+        } else {  // box_inertia_diag over the mesh AABB (demosim.cpp:17-23)
+          const Mesh& M = bodies[b].surface->mesh;
+          double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+          for (int v = 0; v < M.nv(); ++v)
+            for (int k = 0; k < 3; ++k) {
+              lo[k] = std::min(lo[k], M.vertices[3 * v + k]);
+              hi[k] = std::max(hi[k], M.vertices[3 * v + k]);
+            }
+          const double sx = hi[0] - lo[0], sy = hi[1] - lo[1], sz = hi[2] - lo[2], m = bodies[b].mass;
+          g.inertia[3 * b] = m / 12.0 * (sy * sy + sz * sz);
+          g.inertia[3 * b + 1] = m / 12.0 * (sx * sx + sz * sz);
+          g.inertia[3 * b + 2] = m / 12.0 * (sx * sx + sy * sy);
+        }
+      }
+      for (size_t q = 0; q < d.pairs.size(); ++q) {
+        g.pair_i[q] = d.pairs[q].first;
+        g.pair_j[q] = d.pairs[q].second;
+      }
+      rc = launch_integrate(g, s);
+    }
+    if (pooled) cudaFreeAsync(buf, s);
+    if (rc != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("demo launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
 size_t cmgb_manifold_workspace_bytes(int64_t n_env, int32_t st1, int32_t st2) {
   return n_env > 0 ? workspace_doubles(n_env, st1, st2) * sizeof(double) : 0;
 }

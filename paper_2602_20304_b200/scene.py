@@ -82,6 +82,26 @@ _INT_FIELDS = {"hard_ops", "sphere_trace", "sphere_trace_iters", "containment_sa
 # ---------------------------------------------------------------------------
 # SDF program
 # ---------------------------------------------------------------------------
+@dataclass
+class PenaltyParams:
+    """cmg::PenaltyParams (include/cmg/demosim.hpp:24-31)."""
+
+    stiffness: float = 1e4
+    damping: float = 100.0
+    friction: float = 0.5
+    friction_viscous: float = 100.0
+    tau_force: float = 1e-4
+    gravity: tuple = (0.0, 0.0, -9.81)
+
+    def to_c(self) -> abi.CmgbDemoParams:
+        c = abi.CmgbDemoParams()
+        for f in ("stiffness", "damping", "friction", "friction_viscous", "tau_force"):
+            setattr(c, f, float(getattr(self, f)))
+        for k in range(3):
+            c.gravity[k] = float(self.gravity[k])
+        return c
+
+
 class SdfNode:
     """Base: ``postfix()`` returns this subtree's nodes in postfix order."""
 

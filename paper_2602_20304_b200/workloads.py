@@ -302,6 +302,18 @@ def drop_scene(n_env: int = 32768, n_boxes: int = 4) -> Scene:
              for k in range(n_boxes)]
     return Scene("drop", [ground] + boxes, n_env)
 
+def demo_scene(n_env: int = 4096, n_boxes: int = 3) -> Scene:
+    """Demo-integrator scene (DemoSim, src/demosim.cpp): n_boxes dynamic boxes
+    (as drop_scene) released with 5-7 cm gaps above a static box_planes
+    ground, pose jitter U(-0.02, 0.02): they fall, collide and settle."""
+    ground = BodySpec("ground", MeshSpec(box_half=(2.0, 2.0, 0.1)), box_planes((2.0, 2.0, 0.1)),
+                      [0.0, 0.0, -0.1, 0.0, 0.0, 0.0], 0, 4, is_static=True)
+    boxes = [BodySpec(f"box{k}", MeshSpec(box_half=(0.5, 0.5, 0.5)), BOX_SQ,
+                      [0.03 * k, -0.02 * k, 0.55 + 1.07 * k] + rz_axis_angle(0.2 * k + 0.05), 0, 4)
+             for k in range(n_boxes)]
+    return Scene("demo", [ground] + boxes, n_env, jitter=0.02)
+
+
 WORKLOADS = {
     "box-box": box_box,
     "box-on-plane": box_on_plane,

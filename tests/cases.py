@@ -52,6 +52,8 @@ SDF_PROGRAMS = {
 
 
 JVP_ENVS = 2  # envs per case with recorded reference pose Jacobians (Dual12)
+DEMO_DT = 1e-3  # DemoSim golden rollouts: step and length (demo scene, envs 0 and 1)
+DEMO_STEPS = 300
 
 
 def manifold_cases():

@@ -150,6 +150,29 @@ def main():
         jv[f"drop_pair{q}_0_mean"] = np.array([r["mean_dist"], *r["mean_dist_grad"]])
     out["jvp_cases"] = jv
 
+    # --- DemoSim rollouts (src/demosim.cpp) on the demo scene, envs 0 and 1 --------------
+    from paper_2602_20304_b200.scene import PenaltyParams
+    dsc = W.demo_scene(2)
+    DP = dsc.poses(2)
+    drs = [Ref.Surface(ref_mesh(b), b.sdf, b.vertex_topk, b.edge_topk) for b in dsc.bodies]
+    demo = {"init_poses": DP}
+    for e in range(2):
+        r = Ref.demo_run(drs, dsc.is_static(), np.ones(len(drs)), np.zeros((len(drs), 3)), DP[e],
+                         np.zeros((len(drs), 6)), SmoothingConfig(), PenaltyParams(), cases.DEMO_DT, cases.DEMO_STEPS)
+        for k, v in r.items():
+            demo[f"{k}{e}"] = v
+    # single box dropped on the ground, 16 jittered envs: poses after 100 / 200 steps
+    dsc1 = W.demo_scene(16, n_boxes=1)
+    DP1 = dsc1.poses(16)
+    drs1 = [Ref.Surface(ref_mesh(b), b.sdf, b.vertex_topk, b.edge_topk) for b in dsc1.bodies]
+    demo["box1_init_poses"] = DP1
+    for e in range(16):
+        r = Ref.demo_run(drs1, dsc1.is_static(), np.ones(2), np.zeros((2, 3)), DP1[e], np.zeros((2, 6)),
+                         SmoothingConfig(), PenaltyParams(), cases.DEMO_DT, 200)
+        demo[f"box1_{e}_s100"] = r["poses"][99]
+        demo[f"box1_{e}_s200"] = r["poses"][199]
+    out["demo"] = demo
+
     for name, d in out.items():
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **d)
