@@ -41,11 +41,11 @@ def parse():
     ap.add_argument("--n-env", type=int, default=65536, help="envs per GPU (weak scaling)")
     ap.add_argument("--cpu-sample", type=int, default=16384, help="envs in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop", "drop-fwd"],
+    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop", "drop-fwd", "demo"],
                     help="box-box = config B (headline); mixed = config C (4 x 65,536 envs of "
                          "primitive families vs a convex mesh); drop = config D (all 10 body pairs "
                          "of a 5-body scene, 32,768 envs, forward + 12-tangent pose JVP); drop-fwd = "
-                         "config D forward only")
+                         "config D forward only; demo = batched DemoSim steps of a 3-box scene")
     return ap.parse_args()
 
 
@@ -188,6 +188,20 @@ def run_secondary(args, dev, rank, world):
             "manifolds/s", {"workload": "mixed (config C): rounded box / cylinder / ellipsoid / capsule vs "
                             "convex mesh plate, soft top-K 16/16 vertices 8/8 edges, 160 contacts/env",
                             "n_env_total": units}
+    elif args.workload == "demo":
+        n = 32768 if args.n_env == 65536 else args.n_env
+        sc = W.demo_scene(n)
+        bodies = [api.surface_from_spec(b) for b in sc.bodies]
+        demo = api.DemoBatch(bodies, np.ones(len(bodies)), is_static=sc.is_static(), cfg=cfg, poses=sc.poses(n),
+                             n_env=n, device=dev)
+        units = n
+
+        def step():
+            demo.step(1e-3)
+        metric, unit, cfgd = "env steps/sec (DemoSim::step: all-pairs manifolds + penalty forces + SE(3) Euler, " \
+            "%d envs)" % n, "env-steps/s", {
+                "workload": "demo: 3 SQ boxes released over a static box_planes ground, 6 pairs x 48 contacts, "
+                            "dt 1 ms", "n_env": n, "pairs_per_env": 6}
     else:
         n = 32768 if args.n_env == 65536 else args.n_env
         sc = W.drop_scene(n)
