@@ -219,6 +219,8 @@ typedef struct cmgb_manifold_jvp_out {
   int32_t* src;           /* optional: [n_env][n_contacts][2] provenance                     */
   float* mean_dist;       /* optional: [n_env]                                               */
   float* mean_dist_grad;  /* optional: [n_env][12] tangents of mean_contact_distance         */
+  double* mean_dist_f64;       /* optional: [n_env] FP64 mean (as accumulated on the device)  */
+  double* mean_dist_grad_f64;  /* optional: [n_env][12] FP64 mean tangents (gradcheck)       */
 } cmgb_manifold_jvp_out;
 
 /* poses*: DEVICE [n][6] FP64, strides as cmgb_manifold_batch. */
@@ -299,6 +301,18 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
 int cmgb_ee_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
                           const cmgb_config* cfg, float* out, float* alpha_gamma,
                           int32_t* labels, void* cuda_stream);
+/* Reference-precision E-E witnesses: FP64 pairs in, FP64 soft indicators,
+ * FP64 outputs out [n][6] (alpha_gamma [n][3] FP64, labels optional): what
+ * ee_witness<double> returns (witness.hpp:137-158). */
+int cmgb_ee_witness_batch_f64(const double* pairs, int64_t n, const cmgb_config* cfg, double* out,
+                              double* alpha_gamma, int32_t* labels, void* cuda_stream);
+
+/* rotating_edge_sweep (src/sweep.cpp:17-56, Fig. 4): variant 0 = no smoothing,
+ * 1 = regularised only (hard, lambda 0.01), 2 = smooth (tau 0.1, lambda 0.01);
+ * out_host [n_samples][7] = theta, p1 (3), dp1/dtheta (3, central difference
+ * h = 1e-7), theta over [0, pi]. Synchronous (host buffers). */
+int cmgb_rotating_edge_sweep(int32_t variant, int32_t n_samples, double* out_host);
+
 int cmgb_vf_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
                           const cmgb_config* cfg, float* out, int32_t* labels,
                           void* cuda_stream);

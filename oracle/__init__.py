@@ -250,6 +250,17 @@ class Ref:
                                                 C.POINTER(abi.CmgbConfig), C.c_int, _D, _I32, _D]
             L.cmgref_manifold_jvp.argtypes = [_P, _P, _D, _D, C.POINTER(abi.CmgbConfig), _D, _D, _D]
             L.cmgref_random_pairs.argtypes = [C.c_int64, C.c_uint64, _D]
+            L.cmgref_sweep.argtypes = [C.c_int, C.c_int, _D]
+            L.cmgref_sweep_csv.argtypes = [C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+            L.cmgref_scene_parse.restype = _P
+            L.cmgref_scene_parse.argtypes = [C.c_char_p, C.c_char_p]
+            L.cmgref_scene_destroy.argtypes = [_P]
+            L.cmgref_scene_n_bodies.argtypes = [_P]
+            L.cmgref_scene_body.restype = _P
+            L.cmgref_scene_body.argtypes = [_P, C.c_int, _D, _D, _D, _I32, _I32, C.c_char_p, C.c_int]
+            L.cmgref_scene_smoothing.argtypes = [_P, C.POINTER(abi.CmgbConfig)]
+            L.cmgref_manifold_text.argtypes = [_P, _P, _D, _D, C.POINTER(abi.CmgbConfig), C.c_int, C.c_char_p,
+                                               C.c_int64, C.POINTER(C.c_int64)]
             L.cmgref_demo_run.restype = C.c_int
             L.cmgref_demo_run.argtypes = [C.POINTER(_P), C.c_int, _I32, _D, _D, _D, _D, C.POINTER(abi.CmgbConfig),
                                           C.POINTER(abi.CmgbDemoParams), C.c_double, C.c_int, _D, _D, _D, _D]
@@ -330,7 +341,7 @@ class Ref:
                              for i in range(int(info[5]))]
 
         def __del__(self):
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and getattr(self, "_owned", True):
                 Ref.lib().cmgref_surface_destroy(self.h)
                 self.h = None
 
@@ -424,6 +435,67 @@ class Ref:
         if done < 0:
             raise ValueError(Ref.err())
         return dict(poses=po[:done], velocities=vo[:done], deepest=de[:done], kinetic_energy=ke[:done])
+
+    @staticmethod
+    def sweep(variant, n):
+        """rotating_edge_sweep (src/sweep.cpp:44-56): [n, 7] theta, p1, dp1/dtheta."""
+        out = np.zeros((n, 7))
+        if Ref.lib().cmgref_sweep(variant, n, _dp(out)):
+            raise ValueError(Ref.err())
+        return out
+
+    @staticmethod
+    def _text(call):
+        n = C.c_int64()
+        call(None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        if call(buf, n.value + 1, C.byref(n)):
+            raise ValueError(Ref.err())
+        return buf.value.decode()
+
+    @staticmethod
+    def sweep_csv(n):
+        L = Ref.lib()
+        return Ref._text(lambda b, cap, ln: L.cmgref_sweep_csv(n, b, cap, ln))
+
+    @staticmethod
+    def manifold_text(s1, s2, pose1, pose2, cfg=None, as_json=False):
+        """write_manifold_csv / manifold_to_json (src/manifold_io.cpp) of one manifold."""
+        L = Ref.lib()
+        c = _cfg(cfg)
+        p1 = np.ascontiguousarray(pose1, dtype=np.float64)
+        p2 = np.ascontiguousarray(pose2, dtype=np.float64)
+        return Ref._text(lambda b, cap, ln: L.cmgref_manifold_text(s1.h, s2.h, _dp(p1), _dp(p2), C.byref(c),
+                                                                   int(as_json), b, cap, ln))
+
+    class SceneHandle:
+        """A parse_scene result (src/scene.cpp:130-172); body surfaces are owned
+        by the scene (SurfaceModel handles usable wherever Ref.Surface is)."""
+
+        def __init__(self, json_text, base_dir="."):
+            L = Ref.lib()
+            self.h = L.cmgref_scene_parse(json_text.encode(), base_dir.encode())
+            if not self.h:
+                raise ValueError(Ref.err())
+            self.bodies = []
+            for i in range(L.cmgref_scene_n_bodies(self.h)):
+                pose, mass, inertia = np.zeros(6), np.zeros(1), np.zeros(3)
+                st, topk = np.zeros(1, np.int32), np.zeros(2, np.int32)
+                name = C.create_string_buffer(256)
+                sh = L.cmgref_scene_body(self.h, i, _dp(pose), _dp(mass), _dp(inertia), _ip(st), _ip(topk), name, 256)
+                surf = Ref.Surface.__new__(Ref.Surface)
+                surf.h, surf._owned = sh, False
+                self.bodies.append(dict(name=name.value.decode(), pose=pose, mass=float(mass[0]), inertia=inertia,
+                                        is_static=bool(st[0]), vertex_topk=int(topk[0]), edge_topk=int(topk[1]),
+                                        surface=surf))
+            c = abi.CmgbConfig()
+            L.cmgref_scene_smoothing(self.h, C.byref(c))
+            self.smoothing = c
+
+        def __del__(self):
+            if getattr(self, "h", None):
+                Ref.lib().cmgref_scene_destroy(self.h)
+                self.h = None
 
     @staticmethod
     def random_pairs(n, seed=0):

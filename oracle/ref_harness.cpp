@@ -16,6 +16,7 @@
 //   ee_witness / vf_witness  proj/include/cmg/witness.hpp:137-227
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -26,6 +27,8 @@
 
 #include "cmg/batch.hpp"
 #include "cmg/demosim.hpp"
+#include "cmg/manifold_io.hpp"
+#include "cmg/sweep.hpp"
 #include "cmg/manifold.hpp"
 #include "cmg/mesh.hpp"
 #include "cmg/pose.hpp"
@@ -603,6 +606,111 @@ void cmgref_demo_params_default(cmgb_demo_params* p) {
   p->gravity[0] = d.gravity.x;
   p->gravity[1] = d.gravity.y;
   p->gravity[2] = d.gravity.z;
+}
+
+// ---- sweep / scene / writers (src/sweep.cpp, src/scene.cpp, src/manifold_io.cpp) ----
+// rotating_edge_sweep: out [n][7] = theta, p1, dp1/dtheta.
+int cmgref_sweep(int variant, int n, double* out) {
+  try {
+    const auto v = variant == 0 ? SweepVariant::kNoSmoothing
+                                : (variant == 1 ? SweepVariant::kRegularizedOnly : SweepVariant::kSmooth);
+    const auto s = rotating_edge_sweep(v, n);
+    for (int i = 0; i < n; ++i) {
+      const double row[7] = {s[i].theta, s[i].p1.x, s[i].p1.y, s[i].p1.z,
+                             s[i].dp1_dtheta.x, s[i].dp1_dtheta.y, s[i].dp1_dtheta.z};
+      std::memcpy(out + 7 * i, row, sizeof(row));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// write_sweep_csv of the three variants (the CLI's sweep-edges output).
+int cmgref_sweep_csv(int n, char* buf, int64_t cap, int64_t* len) {
+  try {
+    std::ostringstream os;
+    write_sweep_csv(os, rotating_edge_sweep(SweepVariant::kNoSmoothing, n),
+                    rotating_edge_sweep(SweepVariant::kRegularizedOnly, n),
+                    rotating_edge_sweep(SweepVariant::kSmooth, n));
+    const std::string t = os.str();
+    *len = (int64_t)t.size();
+    if (buf && cap > (int64_t)t.size()) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// parse_scene: a heap Scene, queried below.
+void* cmgref_scene_parse(const char* json_text, const char* base_dir) {
+  try {
+    return new Scene(parse_scene(json_text, base_dir));
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+void cmgref_scene_destroy(void* s) { delete static_cast<Scene*>(s); }
+int cmgref_scene_n_bodies(void* s) { return (int)static_cast<Scene*>(s)->bodies.size(); }
+// body i: pose[6], mass, inertia[3], static, vertex/edge topk; surface handle (owned by the scene)
+void* cmgref_scene_body(void* s, int i, double* pose, double* mass, double* inertia, int32_t* is_static,
+                        int32_t* topk, char* name, int cap) {
+  auto& b = static_cast<Scene*>(s)->bodies[i];
+  for (int k = 0; k < 6; ++k) pose[k] = b.pose[k];
+  *mass = b.mass;
+  inertia[0] = b.inertia_diag.x;
+  inertia[1] = b.inertia_diag.y;
+  inertia[2] = b.inertia_diag.z;
+  *is_static = b.is_static ? 1 : 0;
+  topk[0] = b.surface.vertex_topk;
+  topk[1] = b.surface.edge_topk;
+  std::snprintf(name, cap, "%s", b.name.c_str());
+  return &b.surface;
+}
+void cmgref_scene_smoothing(void* s, cmgb_config* out) {
+  const SmoothingConfig& c = static_cast<Scene*>(s)->smoothing;
+  out->lambda = c.lambda;
+  out->tau_clip = c.tau_clip;
+  out->tau_min = c.tau_min;
+  out->tau_comp = c.tau_comp;
+  out->tau_sign = c.tau_sign;
+  out->tau_pen = c.tau_pen;
+  out->tau_nn = c.tau_nn;
+  out->tau_clash = c.tau_clash;
+  out->tau_cont = c.tau_cont;
+  out->tau_topk_verts = c.tau_topk_verts;
+  out->tau_topk_edges = c.tau_topk_edges;
+  out->tau_normal = c.tau_normal;
+  out->tau_union = c.tau_union;
+  out->hard_ops = c.hard_ops;
+  out->sphere_trace = c.sphere_trace;
+  out->sphere_trace_iters = c.sphere_trace_iters;
+  out->containment_safeguard = c.containment_safeguard;
+  out->mode = (int32_t)c.mode;
+  out->reserved = 0;
+}
+
+// write_manifold_csv / manifold_to_json of one generate_manifold<double>.
+int cmgref_manifold_text(void* h1, void* h2, const double* pose1, const double* pose2, const cmgb_config* c,
+                         int as_json, char* buf, int64_t cap, int64_t* len) {
+  try {
+    const auto m = generate_manifold(*static_cast<SurfaceModel*>(h1), *static_cast<SurfaceModel*>(h2),
+                                     pose6(pose1), pose6(pose2), to_cfg(c));
+    std::string t;
+    if (as_json) {
+      t = manifold_to_json(m) + "\n";
+    } else {
+      std::ostringstream os;
+      write_manifold_csv(os, m);
+      t = os.str();
+    }
+    *len = (int64_t)t.size();
+    if (buf && cap > (int64_t)t.size()) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 }  // extern "C"

@@ -131,6 +131,14 @@ class Surface:
             self._h = None
 
 
+def validate_config(cfg) -> None:
+    """SmoothingConfig::validate (config.hpp:57-73): raises ValueError with the
+    reference's message."""
+    c = _cfg(cfg)
+    if abi.load().cmgb_config_validate(C.byref(c)) != abi.CMGB_OK:
+        raise ValueError(abi.load().cmgb_last_error().decode())
+
+
 def layout(s1: Surface, s2: Surface, cfg=None) -> dict:
     """ContactManifold sizes (manifold.hpp:62-72)."""
     L = abi.CmgbLayout()
@@ -206,7 +214,7 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
 
 
 def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, *,
-                                want_src: bool = False, stream=None) -> dict:
+                                want_src: bool = False, want_f64_mean: bool = False, stream=None) -> dict:
     """Pose Jacobians of the batched manifold: generate_manifold<Dual12> seeded
     by seed_pose_tangents (dual.hpp:249-263) for every env. poses* as in
     generate_manifold_batch. Returns CUDA tensors: contacts [n, C, 8] (primal),
@@ -236,12 +244,17 @@ def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=No
     }
     if want_src:
         res["src"] = torch.empty((n, Cn, 2), dtype=torch.int32, device=dev)
+    if want_f64_mean:  # FP64 mean + tangents (as accumulated on the device; for gradchecks)
+        res["mean_dist_f64"] = torch.empty((n,), dtype=torch.float64, device=dev)
+        res["mean_dist_grad_f64"] = torch.empty((n, 12), dtype=torch.float64, device=dev)
     o = abi.CmgbManifoldJvpOut()
     o.contacts = res["contacts"].data_ptr()
     o.tangents = res["tangents"].data_ptr()
     o.src = res["src"].data_ptr() if want_src else None
     o.mean_dist = res["mean_dist"].data_ptr()
     o.mean_dist_grad = res["mean_dist_grad"].data_ptr()
+    o.mean_dist_f64 = res["mean_dist_f64"].data_ptr() if want_f64_mean else None
+    o.mean_dist_grad_f64 = res["mean_dist_grad_f64"].data_ptr() if want_f64_mean else None
     with torch.cuda.device(dev):
         _ok(abi.load().cmgb_manifold_jvp_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
                                                C.byref(c), C.byref(o), _stream_ptr(stream)))
@@ -406,6 +419,43 @@ def run_ee_batch(pairs, cfg=None, *, want_alpha: bool = False, want_labels: bool
             res["alpha_gamma"].data_ptr() if want_alpha else None,
             res["labels"].data_ptr() if want_labels else None, _stream_ptr(stream)))
     return res
+
+
+def run_ee_batch_f64(pairs, cfg=None, *, want_alpha: bool = False, want_labels: bool = False,
+                     stream=None) -> dict:
+    """Reference-precision E-E witnesses (FP64 indicators, FP64 outputs) on a
+    CUDA [n, 12] float64 tensor: what ee_witness<double> returns."""
+    import torch
+
+    c = _cfg(cfg)
+    pr = pairs.reshape(-1, 12).contiguous()
+    if pr.dtype != torch.float64:
+        raise ValueError("pairs must be float64")
+    n = pr.shape[0]
+    res = {"out": torch.empty((n, 6), dtype=torch.float64, device=pr.device)}
+    if want_alpha:
+        res["alpha_gamma"] = torch.empty((n, 3), dtype=torch.float64, device=pr.device)
+    if want_labels:
+        res["labels"] = torch.empty((n,), dtype=torch.int32, device=pr.device)
+    with torch.cuda.device(pr.device):
+        _ok(abi.load().cmgb_ee_witness_batch_f64(
+            pr.data_ptr(), n, C.byref(c), res["out"].data_ptr(),
+            res["alpha_gamma"].data_ptr() if want_alpha else None,
+            res["labels"].data_ptr() if want_labels else None, _stream_ptr(stream)))
+    return res
+
+
+SWEEP_VARIANTS = {"no_smoothing": 0, "l2": 1, "smooth": 2}
+
+
+def rotating_edge_sweep(variant, n_samples: int = 10000) -> np.ndarray:
+    """rotating_edge_sweep (src/sweep.cpp:44-56, the paper's Fig. 4) on the GPU:
+    [n, 7] = theta, p1 (3), dp1/dtheta (3). variant: 0 / "no_smoothing", 1 /
+    "l2", 2 / "smooth"."""
+    v = SWEEP_VARIANTS.get(variant, variant)
+    out = np.zeros((n_samples, 7))
+    _ok(abi.load().cmgb_rotating_edge_sweep(int(v), int(n_samples), out.ctypes.data))
+    return out
 
 
 def run_vf_batch(pairs, cfg=None, *, want_labels: bool = False, stream=None) -> dict:

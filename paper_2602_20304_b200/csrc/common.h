@@ -134,6 +134,8 @@ struct JvpParams {
   ManifoldParams m;
   float* tangents;   // [n_env][C][8][12]
   float* mean_grad;  // [n_env][12]
+  double* mean_f64;       // [n_env] or null
+  double* mean_grad_f64;  // [n_env][12] or null
   int32_t nd, groups;
   int32_t units_per_block;
   int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
@@ -184,9 +186,10 @@ struct WitnessParams {
   int32_t fp64;
   int64_t n;
   DevCfg cfg;
-  float* out;
+  void* out_any;          // float [n][W], or double for the FP64-output solver
   float* alpha_gamma;
   int32_t* labels;
+  void* alpha_gamma_f64;  // double [n][3] (FP64-output solver)
 };
 
 }  // namespace cmgb
@@ -200,6 +203,7 @@ int jvp_directions();    // tangent directions per thread of the compiled JVP ke
 int jvp_max_threads();   // CTA size of the JVP kernel
 int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan for
 int launch_ee_witness(const WitnessParams& p, void* stream);
+int launch_ee_witness_f64(const WitnessParams& p, void* stream);
 int launch_penalty(const PenaltyArgs& a, void* stream);
 int launch_integrate(const IntegrateArgs& a, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);

@@ -125,14 +125,29 @@ struct QpSolT {
 using QpSol = QpSolT<double>;
 
 // solve_box_qp_2 (witness.hpp:74-121), erratum-fixed cost 4 (witness.hpp:99).
-template <class T, class I = T>
+// kIeee: IEEE quotients instead of the one-Newton reciprocals (the unconstrained
+// solve of a near-parallel pair at lambda = 1e-6 amplifies a 1e-12 quotient
+// error ~1e4-fold; the reference-precision K6 solver opts in).
+template <class T, class I = T, bool kIeee = false>
 __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, const T& q3, const T& c1,
                                                     const T& c2, const DevCfg& c) {
-  const T i1 = rcp_d(q1), i3 = rcp_d(q3);
-  const T q2_over_q1 = q2 * i1, q2_over_q3 = q2 * i3;
-  const T c1_over_q1 = c1 * i1, c2_over_q3 = c2 * i3;
-  const T a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
-  const T a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
+  T q2_over_q1, q2_over_q3, c1_over_q1, c2_over_q3, a1u, a2u;
+  if constexpr (kIeee) {
+    q2_over_q1 = q2 / q1;
+    q2_over_q3 = q2 / q3;
+    c1_over_q1 = c1 / q1;
+    c2_over_q3 = c2 / q3;
+    a1u = (q2 * c2_over_q3 - c1) / (q1 - q2 * q2_over_q3);
+    a2u = (q2 * c1_over_q1 - c2) / (q3 - q2 * q2_over_q1);
+  } else {
+    const T i1 = rcp_d(q1), i3 = rcp_d(q3);
+    q2_over_q1 = q2 * i1;
+    q2_over_q3 = q2 * i3;
+    c1_over_q1 = c1 * i1;
+    c2_over_q3 = c2 * i3;
+    a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
+    a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
+  }
   const T a1_1_a2 = clip01<T, I>(-(q2_over_q3 + c2_over_q3), c);
   const T a1_0_a2 = clip01<T, I>(-c2_over_q3, c);
   const T a2_1_a1 = clip01<T, I>(-(q2_over_q1 + c1_over_q1), c);
@@ -163,13 +178,13 @@ __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, co
 
 // ee_witness Q/c construction (witness.hpp:137-158) for edges given in a
 // common frame: Q = A^T A + lambda I, c = b^T A - lambda/2, A = [t1, -t2].
-template <class T = double, class I = T>
+template <class T = double, class I = T, bool kIeee = false>
 __device__ __forceinline__ QpSolT<T> ee_qp(vec3<T> e1a, vec3<T> e1b, vec3<T> e2a, vec3<T> e2b,
                                            const DevCfg& c) {
   const vec3<T> t1 = e1b - e1a;
   const vec3<T> t2n = e2a - e2b;
   const vec3<T> b = e1a - e2a;
-  return solve_box_qp_2<T, I>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
+  return solve_box_qp_2<T, I, kIeee>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
                               ddot(b, t1) - 0.5 * c.lambda, ddot(b, t2n) - 0.5 * c.lambda, c);
 }
 

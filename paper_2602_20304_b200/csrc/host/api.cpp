@@ -649,6 +649,8 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   j.m = plan.p;
   j.tangents = out->tangents;
   j.mean_grad = out->mean_dist_grad;
+  j.mean_f64 = out->mean_dist_f64;
+  j.mean_grad_f64 = out->mean_dist_grad_f64;
   j.nd = jvp_directions();
   j.groups = 12 / j.nd;
   const ManifoldParams& m = j.m;
@@ -725,9 +727,80 @@ int cmgb_ee_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     if (n < 0) invalid("ee_witness_batch: n >= 0");
     if (n == 0) return;
     if (!pairs || !out) invalid("ee_witness_batch: null buffer");
-    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, alpha_gamma, labels};
+    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, alpha_gamma, labels, nullptr};
     if (launch_ee_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("ee_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_ee_witness_batch_f64(const double* pairs, int64_t n, const cmgb_config* cfg, double* out,
+                              double* alpha_gamma, int32_t* labels, void* stream) {
+  return guarded([&] {
+    validate_config(cfg);
+    if (n < 0) invalid("ee_witness_batch_f64: n >= 0");
+    if (n == 0) return;
+    if (!pairs || !out) invalid("ee_witness_batch_f64: null buffer");
+    WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, alpha_gamma};
+    if (launch_ee_witness_f64(p, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("ee_witness_f64 launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+// Rotating-edge sweep (src/sweep.cpp:17-56): edge 1 = +/-(sin t, cos t, 0), edge 2
+// = x in [-2, 2] at y = -1.2; witness p1 and its central difference (h = 1e-7)
+// for n_samples angles over [0, pi], all 3 n_samples QPs in one FP64 launch.
+int cmgb_rotating_edge_sweep(int32_t variant, int32_t n_samples, double* out_host) {
+  return guarded([&] {
+    if (variant < 0 || variant > 2) invalid("rotating_edge_sweep: variant must be 0 (no smoothing), 1 (l2), 2 (smooth)");
+    if (n_samples < 2 || !out_host) invalid("rotating_edge_sweep: n_samples >= 2 and an output buffer");
+    cmgb_config cfg;
+    cmgb_config_default(&cfg);
+    if (variant == 0) {
+      cmgb_config_no_smoothing(&cfg);
+    } else if (variant == 1) {
+      cmgb_config_no_smoothing(&cfg);
+      cfg.lambda = 0.01;
+    } else {
+      cfg.lambda = 0.01;
+      cfg.tau_clip = cfg.tau_min = cfg.tau_comp = 0.1;
+    }
+    const double h = 1e-7;
+    const double pi = 3.14159265358979323846;
+    std::vector<double> pairs((size_t)n_samples * 3 * 12);
+    std::vector<double> theta(n_samples);
+    for (int i = 0; i < n_samples; ++i) {
+      theta[i] = pi * i / (n_samples - 1);
+      const double th3[3] = {theta[i], theta[i] + h, theta[i] - h};
+      for (int k = 0; k < 3; ++k) {
+        double* q = pairs.data() + ((size_t)i * 3 + k) * 12;
+        const double sx = std::sin(th3[k]), cy = std::cos(th3[k]);
+        q[0] = -sx; q[1] = -cy; q[2] = -0.0;
+        q[3] = sx; q[4] = cy; q[5] = 0.0;
+        q[6] = -2.0; q[7] = -1.2; q[8] = 0.0;
+        q[9] = 2.0; q[10] = -1.2; q[11] = 0.0;
+      }
+    }
+    const size_t np = pairs.size() / 12;
+    double *d_pairs = nullptr, *d_out = nullptr;
+    cuda_check(cudaMalloc(&d_pairs, sizeof(double) * pairs.size()), "cudaMalloc");
+    cuda_check(cudaMalloc(&d_out, sizeof(double) * np * 6), "cudaMalloc");
+    std::vector<double> res(np * 6);
+    int rc = cudaMemcpy(d_pairs, pairs.data(), sizeof(double) * pairs.size(), cudaMemcpyHostToDevice);
+    WitnessParams p{d_pairs, 1, (int64_t)np, device_config(&cfg), d_out, nullptr, nullptr, nullptr};
+    if (rc == cudaSuccess) rc = launch_ee_witness_f64(p, nullptr) == 0 ? cudaSuccess : cudaErrorLaunchFailure;
+    if (rc == cudaSuccess) rc = cudaMemcpy(res.data(), d_out, sizeof(double) * np * 6, cudaMemcpyDeviceToHost);
+    cudaFree(d_pairs);
+    cudaFree(d_out);
+    if (rc != cudaSuccess) throw Error(CMGB_ERR_CUDA, "rotating_edge_sweep: CUDA failure");
+    for (int i = 0; i < n_samples; ++i) {
+      const double* c = res.data() + (size_t)i * 18;
+      double* o = out_host + (size_t)i * 7;
+      o[0] = theta[i];
+      for (int k = 0; k < 3; ++k) {
+        o[1 + k] = c[k];                                  // p1(theta)
+        o[4 + k] = (c[6 + k] - c[12 + k]) / (2.0 * h);    // (p1(t+h) - p1(t-h)) / 2h
+      }
+    }
   });
 }
 
@@ -738,7 +811,7 @@ int cmgb_vf_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     if (n < 0) invalid("vf_witness_batch: n >= 0");
     if (n == 0) return;
     if (!pairs || !out) invalid("vf_witness_batch: null buffer");
-    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, nullptr, labels};
+    WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, nullptr, labels, nullptr};
     if (launch_vf_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
   });

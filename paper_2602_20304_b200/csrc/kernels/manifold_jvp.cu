@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
   __syncthreads();
 
   // ---- H: mean contact distance (manifold.hpp:379-384), fixed order ---------
-  if (m.mean_dist || p.mean_grad) {
+  if (m.mean_dist || p.mean_grad || p.mean_f64 || p.mean_grad_f64) {
     for (int k = tid; k < n_here; k += nth) {
       const Unit<ND> u = unit(k);
       T acc = 0.0;
@@ -454,6 +454,10 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       if (p.mean_grad)
 #pragma unroll
         for (int j = 0; j < ND; ++j) p.mean_grad[u.env * 12 + u.group * ND + j] = (float)mean.d[j];
+      if (u.group == 0 && p.mean_f64) p.mean_f64[u.env] = mean.v;
+      if (p.mean_grad_f64)
+#pragma unroll
+        for (int j = 0; j < ND; ++j) p.mean_grad_f64[u.env * 12 + u.group * ND + j] = mean.d[j];
     }
   }
 }

@@ -24,6 +24,7 @@ __device__ __forceinline__ double3 load3(const T* p) {
 }
 
 struct EeSolve {
+  using Out = float;
   static constexpr int kOut = 6;
   template <typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
@@ -43,7 +44,32 @@ struct EeSolve {
   }
 };
 
+// Reference-precision E-E witness (FP64 indicators and outputs): what
+// ee_witness<double> returns, for callers that difference the witness points
+// (the rotating-edge sweep's theta-derivative, sweep.cpp:44-56).
+struct EeSolve64 {
+  using Out = double;
+  static constexpr int kOut = 6;
+  template <typename T>
+  __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, double* o) {
+    const double3 e1a = load3(q), e1b = load3(q + 3), e2a = load3(q + 6), e2b = load3(q + 9);
+    const QpSol s = ee_qp<double, double, true>(e1a, e1b, e2a, e2b, p.cfg);
+    const double3 p1 = e1a + (e1b - e1a) * s.a1;
+    const double3 p2 = e2a + (e2b - e2a) * s.a2;
+    o[0] = p1.x; o[1] = p1.y; o[2] = p1.z;
+    o[3] = p2.x; o[4] = p2.y; o[5] = p2.z;
+    if (p.alpha_gamma_f64) {
+      double* ag = static_cast<double*>(p.alpha_gamma_f64) + 3 * idx;
+      ag[0] = s.a1;
+      ag[1] = s.a2;
+      ag[2] = s.gamma;
+    }
+    if (p.labels) p.labels[idx] = s.label;
+  }
+};
+
 struct VfSolve {
+  using Out = float;
   static constexpr int kOut = 3;
   template <typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
@@ -61,8 +87,9 @@ struct VfSolve {
 template <typename T, class Solve>
 __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_constant__ WitnessParams p) {
   constexpr int W = Solve::kOut;
+  using Out = typename Solve::Out;
   __shared__ __align__(128) T tile[2][kWitnessThreads * 12];
-  __shared__ __align__(16) float otile[kWitnessThreads * W];
+  __shared__ __align__(16) Out otile[kWitnessThreads * W];
   __shared__ __align__(8) uint64_t bar[2];
   const T* __restrict__ in = static_cast<const T*>(p.pairs);
   const int tid = threadIdx.x;
@@ -93,7 +120,7 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
     mbar_wait(&bar[b], (it >> 1) & 1);
     if (tid < count) Solve::run(p, tile[b] + 12 * tid, first + tid, otile + W * tid);
     __syncthreads();
-    float* __restrict__ out = p.out + first * W;
+    Out* __restrict__ out = static_cast<Out*>(p.out_any) + first * W;
     for (int k = tid; k < count * W; k += kWitnessThreads) out[k] = otile[k];
     __syncthreads();
   }
@@ -120,6 +147,10 @@ int launch_witness(const WitnessParams& p, cudaStream_t s) {
 int launch_ee_witness(const WitnessParams& p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return p.fp64 ? launch_witness<double, EeSolve>(p, s) : launch_witness<float, EeSolve>(p, s);
+}
+
+int launch_ee_witness_f64(const WitnessParams& p, void* stream) {
+  return launch_witness<double, EeSolve64>(p, static_cast<cudaStream_t>(stream));
 }
 
 int launch_vf_witness(const WitnessParams& p, void* stream) {

@@ -173,6 +173,17 @@ def main():
         demo[f"box1_{e}_s200"] = r["poses"][199]
     out["demo"] = demo
 
+    # --- Fig. 4 rotating-edge sweep + the reference tool's text outputs on the scene files ----
+    tools = {f"sweep{v}": Ref.sweep(v, 1001) for v in range(3)}
+    scenes_dir = os.path.join(os.path.dirname(HERE), "scenes")
+    for name in ("box_on_plane", "capsule_vs_hollow"):
+        sh = Ref.SceneHandle(open(os.path.join(scenes_dir, f"{name}.json")).read(), scenes_dir)
+        b0, b1 = sh.bodies[0], sh.bodies[1]
+        m = Ref.manifold(b0["surface"], b1["surface"], b0["pose"], b1["pose"], sh.smoothing)
+        tools[f"{name}_contacts"] = m["contacts"]
+        tools[f"{name}_meta"] = m["meta"]
+    out["tools"] = tools
+
     for name, d in out.items():
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **d)
