@@ -116,13 +116,19 @@ __device__ __forceinline__ void vs_contact(const DevSdf& opp, const double* Ro, 
 }
 
 // sphere_trace_project (sdf.hpp:318-326) in the body frame, FP64.
+// One step p -= normalize_smooth(grad phi) phi, as p - g (phi / sqrt(tau + |g|^2)):
+// one product for the scale, three FMAs for the update.
+template <int K>
+__device__ __forceinline__ double3 trace_step(const DevSdf& sdf, double3 p, double tau_normal) {
+  const SdfOut s = sdf_eval<kGrad, K>(sdf, p);
+  const double sc = rsqrt_d(tau_normal + ddot(s.g, s.g)) * s.v;
+  return d3(fma(-s.g.x, sc, p.x), fma(-s.g.y, sc, p.y), fma(-s.g.z, sc, p.z));
+}
+
 template <int K>
 __device__ __forceinline__ double3 trace(const DevSdf& sdf, double3 p, const DevCfg& c) {
 #pragma unroll 1
-  for (int k = 0; k < c.trace_iters; ++k) {
-    const SdfOut s = sdf_eval<kGrad, K>(sdf, p);
-    p = p - dscale(normalize_smooth(s.g, c.tau_normal), s.v);
-  }
+  for (int k = 0; k < c.trace_iters; ++k) p = trace_step<K>(sdf, p, c.tau_normal);
   return p;
 }
 
@@ -306,10 +312,16 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
 
   // ---- D: selected slots (pass-through or soft top-K rows) --------------
   {
+    // With soft top-K active, each slot is a group of 4 adjacent lanes that
+    // splits the row's candidates (shuffle-reduced): the rows are long serial
+    // loops (D up to ~100) that otherwise keep the whole CTA at the barrier.
+    const int lshift = topk_any ? 2 : 0;
+    const int lanes = 1 << lshift;
     const int nsl = n1 + n2 + m1 + m2;
-    for (int it = tid; it < n_here * nsl; it += nth) {
+    for (int it = tid; it < (n_here * nsl) << lshift; it += nth) {
+      const int ql = it & (lanes - 1);
       int e, r0;
-      fdivmod(it, p.div_nslots, e, r0);
+      fdivmod(it >> lshift, p.div_nslots, e, r0);
       const EnvView ev = env(e);
       const bool is_edge = r0 >= n1 + n2;
       const int s = is_edge ? (r0 - n1 - n2 < m1 ? 0 : 1) : (r0 < n1 ? 0 : 1);
@@ -333,24 +345,46 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
         const int D = sets.off[set + 1] - sets.off[set];
         const double sr = ev.sorted()[sets.off[set] + r];
         const double inv_tau = is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
+        // One pass: unnormalised weights e_i = exp(-|sr - x_i| / tau) accumulate
+        // the total and the payload, normalised once at the end. The row's own
+        // element has e = 1, so the total is >= 1 and a term below e^-50 moves
+        // neither it nor the payload at FP64 resolution: those are skipped.
         double tot = 0.0;
-        prov = -1;
-        for (int i = 0; i < D; ++i) {
+        int first = 0x7fffffff;
+        for (int i = ql; i < D; i += lanes) {
           const double dist = fabs(sr - x[i]);
-          tot += exp(-dist * inv_tau);
-          if (prov < 0 && dist == 0.0) prov = i;  // first argmax (hard_attribution, 110-121)
-        }
-        const double inv = 1.0 / tot;
-        for (int i = 0; i < D; ++i) {
-          const double wi = exp(-fabs(sr - x[i]) * inv_tau) * inv;
+          if (first == 0x7fffffff && dist == 0.0) first = i;  // first argmax (hard_attribution, 110-121)
+          const double arg = -dist * inv_tau;
+          if (arg < -50.0) continue;
+          const double e = exp_d(arg);
+          tot += e;
           if (is_edge) {
-            a = a + ld_vert(S.verts, __ldg(S.edges + 2 * i)) * wi;
-            b = b + ld_vert(S.verts, __ldg(S.edges + 2 * i + 1)) * wi;
+            a = a + ld_vert(S.verts, __ldg(S.edges + 2 * i)) * e;
+            b = b + ld_vert(S.verts, __ldg(S.edges + 2 * i + 1)) * e;
           } else {
-            a = a + ld_vert(S.verts, i) * wi;
+            a = a + ld_vert(S.verts, i) * e;
           }
         }
+        if (lanes > 1) {  // reduce over the slot's lane group (fixed order)
+          const unsigned gm = 0xFu << ((tid & 31) & ~3);
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            tot += __shfl_xor_sync(gm, tot, o);
+            a.x += __shfl_xor_sync(gm, a.x, o);
+            a.y += __shfl_xor_sync(gm, a.y, o);
+            a.z += __shfl_xor_sync(gm, a.z, o);
+            b.x += __shfl_xor_sync(gm, b.x, o);
+            b.y += __shfl_xor_sync(gm, b.y, o);
+            b.z += __shfl_xor_sync(gm, b.z, o);
+            first = min(first, __shfl_xor_sync(gm, first, o));
+          }
+        }
+        prov = first == 0x7fffffff ? -1 : first;
+        const double inv = 1.0 / tot;
+        a = a * inv;
+        b = b * inv;
       }
+      if (ql != 0) continue;  // lane 0 of the group stores the slot
       ev.prov()[r0] = prov;
       if (is_edge) {
         double* q = ev.eslot(r0 - n1 - n2);

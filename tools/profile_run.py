@@ -9,7 +9,15 @@ from paper_2602_20304_b200 import workloads as W
 
 kind = sys.argv[1] if len(sys.argv) > 1 else "manifold"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
-if kind == "manifold":
+if kind.startswith("mixed:"):
+    ws = W.mixed_bucket(kind.split(":", 1)[1], n)
+    s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
+    p1, p2 = ws.poses(n)
+    P1 = torch.as_tensor(p1, device="cuda"); P2 = torch.as_tensor(p2, device="cuda")
+    out = {}
+    for _ in range(3):
+        api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out)
+elif kind == "manifold":
     ws = W.box_box(n)
     s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
     p1, p2 = ws.poses(n)
