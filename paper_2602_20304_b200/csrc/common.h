@@ -20,7 +20,10 @@ constexpr int kPairRec = 38;    // floats per E-E pair record in shared memory (
 
 // kSqE01: a lone superquadric with eps1 = eps2 = 0.1 (the box-box benchmark
 // body), whose exponents (n1, n2, n3, n4) = (10, 1, 10, 20) are compiled in.
-enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2, kSqE01 = 3 };
+// kBoxCp: a lone convex polyhedron whose 6 planes are the axis-aligned box
+// pattern of box_planes (scene.cpp:49-62: +x, -x, +y, -y, +z, -z unit
+// normals): plane distances are +-p_i - w_i (bit-identical to the FMA dot).
+enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2, kSqE01 = 3, kBoxCp = 4 };
 enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
 
 // Superquadric leaf, pre-digested on the host (sdf.hpp:85-108):
@@ -46,6 +49,7 @@ struct DevNode {
   double tau_d;
   double inv_tau_d;
   DevSq sq;
+  double box_w[6];  // kBoxCp: plane offsets n . point in the +x, -x, +y, -y, +z, -z order
 };
 
 struct DevSdf {

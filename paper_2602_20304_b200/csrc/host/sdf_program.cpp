@@ -255,6 +255,20 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
     const DevSq& q = s.nodes[0].sq;
     if (q.n1 == 10 && q.n2 == 1 && q.n3 == 10 && q.n4 == 20) s.kind = kSqE01;
   }
+  if (s.kind == kSingleCp && prog.nodes[0].count == 6) {
+    // the box_planes pattern: unit normals +x, -x, +y, -y, +z, -z in this order
+    const ProgramNode& d = prog.nodes[0];
+    bool box = true;
+    for (int k = 0; k < 6 && box; ++k)
+      for (int a = 0; a < 3; ++a) {
+        const double want = a == k / 2 ? (k % 2 == 0 ? 1.0 : -1.0) : 0.0;
+        box = box && d.normals[3 * k + a] == want;
+      }
+    if (box) {
+      s.kind = kBoxCp;
+      for (int k = 0; k < 6; ++k) s.nodes[0].box_w[k] = (*pool)[s.nodes[0].offset + k].w;
+    }
+  }
   return s;
 }
 

@@ -291,21 +291,26 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     }
     __syncthreads();
     // ---- C: descending rank sort (values only matter; smooth_ops.hpp:180-185)
+    // 4 adjacent lanes per score split the comparisons (shuffle-summed rank)
     const int total = sets.off[4];
-    for (int it = tid; it < n_here * total; it += nth) {
+    for (int it = tid; it < (n_here * total) << 2; it += nth) {
+      const int ql = it & 3;
       int e, i;
-      fdivmod(it, p.div_scores, e, i);
+      fdivmod(it >> 2, p.div_scores, e, i);
       const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
       const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
       if (!active) continue;
       const double* sc = env(e).scores();
       const double x = sc[i];
       int rank = 0;
-      for (int j = sets.off[set]; j < sets.off[set + 1]; ++j) {
+      for (int j = sets.off[set] + ql; j < sets.off[set + 1]; j += 4) {
         const double y = sc[j];
         rank += (y > x) || (y == x && j < i);
       }
-      env(e).sorted()[sets.off[set] + rank] = x;
+      const unsigned gm = 0xFu << ((tid & 31) & ~3);
+      rank += __shfl_xor_sync(gm, rank, 1);
+      rank += __shfl_xor_sync(gm, rank, 2);
+      if (ql == 0) env(e).sorted()[sets.off[set] + rank] = x;
     }
     __syncthreads();
   }
@@ -558,12 +563,13 @@ template <int K1>
 int launch_k2(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   switch (p.side[1].sdf.kind) {
     case kSqE01:
-      if constexpr (K1 == kSqE01 || K1 == kSingleSq || K1 == kSingleCp)
+      if constexpr (K1 == kSqE01 || K1 == kSingleSq || K1 == kSingleCp || K1 == kBoxCp)
         return launch_kind<K1, kSqE01>(p, threads, grid, smem, s);
       else
         return launch_kind<K1, kSingleSq>(p, threads, grid, smem, s);
     case kSingleSq: return launch_kind<K1, kSingleSq>(p, threads, grid, smem, s);
     case kSingleCp: return launch_kind<K1, kSingleCp>(p, threads, grid, smem, s);
+    case kBoxCp: return launch_kind<K1, kBoxCp>(p, threads, grid, smem, s);
     default: return launch_kind<K1, kGeneric>(p, threads, grid, smem, s);
   }
 }
@@ -581,6 +587,7 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
     case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);
     case kSingleCp: return launch_k2<kSingleCp>(p, block_threads, grid, smem_bytes, s);
+    case kBoxCp: return launch_k2<kBoxCp>(p, block_threads, grid, smem_bytes, s);
     default: return launch_k2<kGeneric>(p, block_threads, grid, smem_bytes, s);
   }
 }

@@ -479,7 +479,7 @@ int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
 // SQ kinds share the runtime-exponent path (kSqE01 -> kSingleSq): the JVP is
 // not the throughput path, one instantiation per shape class keeps the
 // library small.
-constexpr int jvp_kind(int k) { return k == kSqE01 ? kSingleSq : k; }
+constexpr int jvp_kind(int k) { return k == kSqE01 ? kSingleSq : (k == kBoxCp ? kSingleCp : k); }
 
 template <int K1>
 int launch_jvp_k2(const JvpParams& p, int threads, cudaStream_t s) {
