@@ -1,0 +1,44 @@
+// Host-side launch helpers shared by the kernel files.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace cmgb {
+
+// Runs f() once per CUDA device (function attributes such as the dynamic
+// shared-memory limit are per device); idempotent f, so a racing second call is
+// harmless.
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class F>
+  void operator()(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
+
+// Per-device cached integer (e.g. a persistent-grid size), computed on first use.
+struct PerDeviceInt {
+  std::atomic<int> v[64] = {};
+  template <class F>
+  int get(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>& slot = v[dev & 63];
+    int x = slot.load(std::memory_order_acquire);
+    if (x == 0) {
+      x = f();
+      slot.store(x, std::memory_order_release);
+    }
+    return x;
+  }
+};
+
+}  // namespace cmgb

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "../common.h"
+#include "launch_util.cuh"
 #include "../device/dmath.cuh"
 #include "../device/sdf.cuh"
 #include "../device/witness.cuh"
@@ -549,12 +550,10 @@ int launch_frames(const double* poses, int64_t stride, int64_t n, double* frames
 
 template <int K1, int K2>
 int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(manifold_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  configured([] {  // per device: the attribute does not carry across devices
+    cudaFuncSetAttribute(manifold_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
   manifold_kernel<K1, K2><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include "../common.h"
+#include "launch_util.cuh"
 #include "../device/dmath.cuh"
 #include "../device/dual.cuh"
 #include "../device/sdf.cuh"
@@ -464,12 +465,11 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
 
 template <int K1, int K2>
 int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  configured([] {  // per device: the attribute does not carry across devices
     cudaFuncSetAttribute(manifold_jvp_kernel<K1, K2, kJvpND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    configured = true;
-  }
+  });
   const int64_t units = p.m.n_env * p.groups;
   const int64_t grid = (units + p.units_per_block - 1) / p.units_per_block;
   manifold_jvp_kernel<K1, K2, kJvpND><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block, s>>>(p);

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "../common.h"
+#include "launch_util.cuh"
 #include "../device/bulk.cuh"
 #include "../device/witness.cuh"
 
@@ -128,14 +129,14 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
 
 template <typename T, class Solve>
 int launch_witness(const WitnessParams& p, cudaStream_t s) {
-  static int cap = 0;  // persistent grid: SMs x resident CTAs (cached per kernel)
-  if (cap == 0) {
+  static PerDeviceInt cap_cache;  // persistent grid: SMs x resident CTAs, per device
+  const int cap = cap_cache.get([] {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, witness_kernel<T, Solve>, kWitnessThreads, 0);
-    cap = sms * (per_sm > 0 ? per_sm : 1);
-  }
+    return sms * (per_sm > 0 ? per_sm : 1);
+  });
   const int64_t need = (p.n + kWitnessThreads - 1) / kWitnessThreads;
   const int grid = (int)(need < cap ? (need > 0 ? need : 1) : cap);
   witness_kernel<T, Solve><<<grid, kWitnessThreads, 0, s>>>(p);
