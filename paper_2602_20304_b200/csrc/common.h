@@ -127,6 +127,8 @@ struct ManifoldParams {
   int32_t* src;
   float* ee;
   float* mean_dist;
+  double* pairs_gmem;   // pair records in global memory ([n_env][pair_stride] doubles), or null = shared
+  int64_t pair_stride;  // doubles per env in pairs_gmem
 };
 
 // Pose-Jacobian (forward-mode, Dual12) batch: the geometry / config / slot

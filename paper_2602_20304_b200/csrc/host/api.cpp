@@ -144,6 +144,7 @@ struct LaunchPlan {
   ManifoldParams p{};
   int threads = 0, grid = 0;
   size_t smem = 0;
+  bool pairs_global = false;  // pair records in a global workspace (large pass-through pair sets)
 };
 
 LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* poses1, int st1,
@@ -152,8 +153,9 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   validate_config(cfg);
   if (!s1 || !s2) invalid("manifold: null surface");
   if (n_env < 0) invalid("manifold: n_env >= 0");
-  if (!out || !out->contacts) invalid("manifold: contacts output is required");
-  if (!poses1 || !poses2) invalid("manifold: null poses");
+  if (!out) invalid("manifold: null output descriptor");
+  if (n_env > 0 && !out->contacts) invalid("manifold: contacts output is required");
+  if (n_env > 0 && (!poses1 || !poses2)) invalid("manifold: null poses");
   if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
   const cmgb_layout L = layout_of(s1, s2, cfg);
   LaunchPlan plan;
@@ -201,17 +203,33 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   const bool topk = p.side[0].topk_v || p.side[1].topk_v || p.side[0].topk_e || p.side[1].topk_e;
   const int nscore = topk ? (p.side[0].nv + p.side[1].nv + p.side[0].ne + p.side[1].ne) : 0;
   SmemLayout& S = p.smem;
-  int off = 0;
-  S.frames = off; off = align16(off + 24 * 8);
-  S.vslots = off; off = align16(off + nslot_v * 3 * 8);
-  S.eslots = off; off = align16(off + nslot_e * 12 * 8);
-  S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
-  S.scores = off; off = align16(off + nscore * 8);
-  S.sorted = off; off = align16(off + nscore * 8);
-  S.pairs = off; off = align16(off + P * kPairRec * 4);
-  S.vsdist = off; off = align16(off + nslot_v * 4);
-  S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
-  S.bytes = off;
+  // pairs_in_smem: the per-pair records live in shared memory unless the env's
+  // working set would exceed the per-CTA budget; then they move to a global
+  // workspace (L2-resident per chunk of envs, launch_with_workspace).
+  auto carve = [&](bool pairs_in_smem) {
+    int off = 0;
+    S.frames = off; off = align16(off + 24 * 8);
+    S.vslots = off; off = align16(off + nslot_v * 3 * 8);
+    S.eslots = off; off = align16(off + nslot_e * 12 * 8);
+    S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
+    S.scores = off; off = align16(off + nscore * 8);
+    S.sorted = off; off = align16(off + nscore * 8);
+    S.pairs = off; off = align16(off + (pairs_in_smem ? P * kPairRec * 4 : 0));
+    S.vsdist = off; off = align16(off + nslot_v * 4);
+    S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
+    S.bytes = off;
+  };
+  const size_t kSmemMax = 200 * 1024;
+  carve(true);
+  p.pairs_gmem = nullptr;
+  p.pair_stride = 0;
+  plan.pairs_global = (size_t)S.bytes > kSmemMax;
+  if (plan.pairs_global) {
+    carve(false);
+    p.pair_stride = (int64_t)P * (kPairRec / 2);
+    if ((size_t)S.bytes > kSmemMax)
+      throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
+  }
 
   // Envs per block: ~288 items of E-E work per 288-thread CTA (2 box-box envs),
   // shared memory capped so 3 CTAs fit per SM.
@@ -220,8 +238,6 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   int epb = std::max(1, maxt / per_env);
   const size_t smem_cap = 72 * 1024;
   while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
-  if ((size_t)S.bytes > 200 * 1024)
-    throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
   const int threads = maxt;
   p.envs_per_block = epb;
   auto fd = [](int d) {
@@ -276,7 +292,36 @@ void launch_with_workspace(LaunchPlan& plan, int64_t n_env, int st1, int st2, vo
   double* f = static_cast<double*>(buf);
   plan.p.frames1 = f;
   plan.p.frames2 = f + 12 * (st1 ? n_env : 1);
-  const int rc = launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream);
+  int rc = 0;
+  if (!plan.pairs_global) {
+    rc = launch_manifold(plan.p, plan.threads, plan.grid, plan.smem, stream);
+  } else {
+    // Pair records in global memory: env chunks whose records fit a 512 MB
+    // stream-ordered block, one launch each (frames land in the caller's slots).
+    const size_t rec_bytes = sizeof(double) * (size_t)plan.p.pair_stride;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_env, (512ll << 20) / (int64_t)rec_bytes));
+    double* rec = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&rec), rec_bytes * chunk, stream),
+               "cudaMallocAsync(pair records)");
+    const int C = plan.p.n_contacts, P = plan.p.m1 * plan.p.m2;
+    for (int64_t c0 = 0; c0 < n_env && rc == 0; c0 += chunk) {
+      const int64_t cn = std::min(chunk, n_env - c0);
+      ManifoldParams q = plan.p;
+      q.n_env = cn;
+      q.poses1 += q.pose_stride1 * c0;
+      q.poses2 += q.pose_stride2 * c0;
+      q.frames1 += 12 * c0 * q.stride1;
+      q.frames2 += 12 * c0 * q.stride2;
+      q.contacts += c0 * C * 8;
+      if (q.src) q.src += c0 * C * 2;
+      if (q.ee) q.ee += c0 * 9 * P;
+      if (q.mean_dist) q.mean_dist += c0;
+      q.pairs_gmem = rec;
+      const int grid = (int)((cn + q.envs_per_block - 1) / q.envs_per_block);
+      rc = launch_manifold(q, plan.threads, grid, plan.smem, stream);
+    }
+    cudaFreeAsync(rec, stream);
+  }
   if (pooled) cudaFreeAsync(buf, stream);
   if (rc != 0)
     throw Error(CMGB_ERR_CUDA, std::string("manifold launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -555,9 +600,9 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
   return guarded([&] {
     if (!s1 || !s2) invalid("manifold_batch_host: null surface");
     validate_config(cfg);
-    if (!poses1_host || !poses2_host) invalid("manifold_batch_host: null poses");
     if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
     if (n_env == 0) return;
+    if (!poses1_host || !poses2_host) invalid("manifold_batch_host: null poses");
     const cmgb_layout L = layout_of(s1, s2, cfg);
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
@@ -634,7 +679,7 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
 namespace {
 
 void validate_jvp(const cmgb_config* cfg, const cmgb_manifold_jvp_out* out) {
-  if (!out || !out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
+  if (!out) invalid("manifold_jvp: null output descriptor");
   validate_config(cfg);
   if (cfg->hard_ops)
     throw Error(CMGB_ERR_UNSUPPORTED,
@@ -694,6 +739,7 @@ int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* pose
     cmgb_manifold_out mo{out->contacts, out->src, nullptr, out->mean_dist, nullptr, 0};
     LaunchPlan plan = plan_manifold(s1, s2, poses1, st1, poses2, st2, n_env, cfg, &mo);
     if (n_env == 0 || plan.p.n_contacts == 0) return;
+    if (!out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
     launch_jvp(plan_jvp(plan, out), static_cast<cudaStream_t>(stream));
   });
 }
@@ -702,7 +748,8 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
                                   int32_t n_pairs, const double* poses, int64_t n_env,
                                   const cmgb_config* cfg, const cmgb_manifold_jvp_out* outs, void* stream) {
   return guarded([&] {
-    if (!bodies || !pairs || !poses || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0)
+    if (!bodies || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0 || (n_pairs > 0 && !pairs) ||
+        (n_env > 0 && !poses))
       invalid("manifold_scene_jvp_batch: bad argument");
     for (int q = 0; q < n_pairs; ++q) {
       const int i = pairs[2 * q], j = pairs[2 * q + 1];
@@ -713,6 +760,7 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
       cmgb_manifold_out mo{o.contacts, o.src, nullptr, o.mean_dist, nullptr, 0};
       LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &mo);
       if (n_env == 0 || plan.p.n_contacts == 0) continue;
+      if (!o.contacts || !o.tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
       plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)n_bodies;
       launch_jvp(plan_jvp(plan, &o), static_cast<cudaStream_t>(stream));
     }
@@ -838,7 +886,8 @@ int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, cons
                               int32_t n_pairs, const double* poses, int64_t n_env,
                               const cmgb_config* cfg, const cmgb_manifold_out* outs, void* stream) {
   return guarded([&] {
-    if (!bodies || !pairs || !poses || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0)
+    if (!bodies || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0 || (n_pairs > 0 && !pairs) ||
+        (n_env > 0 && !poses))
       invalid("manifold_scene_batch: bad argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     for (int q = 0; q < n_pairs; ++q) {
@@ -926,9 +975,9 @@ int cmgb_demo_step_batch(const cmgb_demo_body* bodies, int32_t nb, const cmgb_co
                          size_t workspace_bytes, void* stream) {
   return guarded([&] {
     if (!prm) invalid("demo: null params");
-    if (!poses || !velocities) invalid("demo: poses and velocities are required");
     const DemoPlan d = plan_demo(bodies, nb, cfg, n_env);
     if (n_env == 0) return;
+    if (!poses || !velocities) invalid("demo: poses and velocities are required");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     void* buf = workspace;
     const bool pooled = workspace == nullptr || workspace_bytes < d.bytes;

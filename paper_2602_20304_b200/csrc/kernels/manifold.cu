@@ -44,6 +44,7 @@ constexpr int kMinBlocks = 3;
 struct EnvView {
   unsigned char* base;
   const SmemLayout* L;
+  double* prec;  // this env's pair records: shared memory, or the global workspace
   __device__ double* R(int s) const { return reinterpret_cast<double*>(base + L->frames) + 12 * s; }
   __device__ double* t(int s) const { return R(s) + 9; }
   __device__ double* vslot(int i) const { return reinterpret_cast<double*>(base + L->vslots) + 3 * i; }
@@ -51,9 +52,7 @@ struct EnvView {
   __device__ int* prov() const { return reinterpret_cast<int*>(base + L->prov); }
   __device__ double* scores() const { return reinterpret_cast<double*>(base + L->scores); }
   __device__ double* sorted() const { return reinterpret_cast<double*>(base + L->sorted); }
-  __device__ double* pair(int i) const {
-    return reinterpret_cast<double*>(base + L->pairs) + (kPairRec / 2) * i;
-  }
+  __device__ double* pair(int i) const { return prec + (kPairRec / 2) * i; }
   __device__ float* vsdist() const { return reinterpret_cast<float*>(base + L->vsdist); }
   __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
   __device__ double& dbar(int i) const { return pair(i)[3]; }
@@ -235,7 +234,9 @@ __global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ 
   f[11] = t[2];
 }
 
-template <int K1, int K2>
+// kGP: pair records in the global workspace (p.pairs_gmem; large pass-through
+// pair sets, one generic instantiation) instead of shared memory.
+template <int K1, int K2, bool kGP = false>
 __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -248,7 +249,11 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
   const DevSide& S2 = p.side[1];
   const int n1 = p.n1, n2 = p.n2, m1 = p.m1, m2 = p.m2, P = m1 * m2;
   const bool full = m1 > 0 && m2 > 0;
-  auto env = [&](int e) { return EnvView{smem + (size_t)e * p.smem.bytes, &p.smem}; };
+  auto env = [&](int e) {
+    unsigned char* b = smem + (size_t)e * p.smem.bytes;
+    if constexpr (kGP) return EnvView{b, &p.smem, p.pairs_gmem + (env0 + e) * p.pair_stride};
+    else return EnvView{b, &p.smem, reinterpret_cast<double*>(b + p.smem.pairs)};
+  };
 
   // ---- A: frames (precomputed by frames_kernel) -> shared memory ----------
   for (int i = tid; i < 24 * n_here; i += nth) {
@@ -548,13 +553,13 @@ int launch_frames(const double* poses, int64_t stride, int64_t n, double* frames
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-template <int K1, int K2>
+template <int K1, int K2, bool kGP = false>
 int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   static PerDeviceOnce configured;
   configured([] {  // per device: the attribute does not carry across devices
-    cudaFuncSetAttribute(manifold_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(manifold_kernel<K1, K2, kGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
-  manifold_kernel<K1, K2><<<grid, threads, smem, s>>>(p);
+  manifold_kernel<K1, K2, kGP><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -582,6 +587,8 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
   if (launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), s) ||
       launch_frames(p.poses2, p.pose_stride2, n2, const_cast<double*>(p.frames2), s))
     return 1;
+  if (p.pairs_gmem)  // the generic interpreter evaluates every SDF kind
+    return launch_kind<kGeneric, kGeneric, true>(p, block_threads, grid, smem_bytes, s);
   switch (p.side[0].sdf.kind) {
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
     case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);

@@ -1,0 +1,97 @@
+"""Edge cases of the batched path (GPU): empty batches on every entry point,
+ragged batch sizes around the CTA packing, pass-through budgets (K = D) at the
+largest shared-memory working set, and the documented limit failing loudly."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import assert_parity, surfaces
+from oracle import Oracle
+from paper_2602_20304_b200 import abi, api
+from paper_2602_20304_b200 import workloads as W
+from paper_2602_20304_b200.scene import PenaltyParams, Superquadric, SmoothingConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def test_empty_batches_everywhere(cuda):
+    ws = W.box_box()
+    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+    z = torch.zeros((0, 6), dtype=torch.float64, device="cuda")
+    r = api.generate_manifold_batch(s1, s2, z, z, SmoothingConfig(), want_src=True, want_ee=True)
+    assert r["contacts"].shape == (0, 304, 8)
+    j = api.generate_manifold_jvp_batch(s1, s2, z, z, SmoothingConfig())
+    assert j["tangents"].shape == (0, 304, 8, 12)
+    assert api.generate_manifold_batch_host(s1, s2, np.zeros((0, 6)), np.zeros((0, 6))).shape == (0,)
+    e = api.run_ee_batch(torch.zeros((0, 12), dtype=torch.float64, device="cuda"))
+    assert e["out"].shape == (0, 6)
+    v = api.run_vf_batch(torch.zeros((0, 12), dtype=torch.float64, device="cuda"))
+    assert v["out"].shape == (0, 3)
+    sc = W.drop_scene(0)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    P = torch.zeros((0, len(bodies), 6), dtype=torch.float64, device="cuda")
+    assert all(x["contacts"].shape[0] == 0 for x in
+               api.generate_manifold_scene_batch(bodies, P, SmoothingConfig(), is_static=sc.is_static()))
+    d = api.DemoBatch(bodies, np.ones(len(bodies)), is_static=sc.is_static(), n_env=0)
+    d.step(1e-3)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 145, 1001])
+def test_ragged_batch_sizes(cuda, n):
+    """Batch sizes that leave the last CTA partly empty (2 box-box envs per CTA)
+    and a mixed-family case (top-K, 4 envs per CTA)."""
+    for ws in (W.box_box(n), W.mixed_bucket("capsule", n)):
+        (a1, a2), (o1, o2) = surfaces(ws)
+        p1, p2 = ws.poses(n)
+        ref = Oracle.manifold_batch(o1, o2, p1, p2, SmoothingConfig())
+        r = api.generate_manifold_batch(a1, a2, torch.as_tensor(p1, device="cuda"),
+                                        torch.as_tensor(p2, device="cuda"), SmoothingConfig(), want_src=True)
+        torch.cuda.synchronize()
+        assert_parity(r["contacts"].cpu().numpy(), ref["contacts"], what=f"{ws.name} n={n}")
+        assert np.array_equal(r["src"].cpu().numpy(), ref["meta"][..., 2:])
+
+
+def big_boxes(m):
+    """Two subdivided boxes with pass-through edge budgets (K = D): m edges each."""
+    ws = W.box_box(64)
+    for b in ws.bodies:
+        b.mesh.subdivisions = 2
+        b.edge_topk = m
+    return ws
+
+
+def test_pass_through_large_pair_sets(cuda):
+    """All 48 edges of two subdivided boxes (pass-through K = D, P = 2,304 pairs:
+    the pair records exceed shared memory and live in the global workspace,
+    processed in env chunks) vs the oracle."""
+    ws = big_boxes(0)
+    a1 = api.surface_from_spec(ws.bodies[0])
+    m = a1.mesh.edges.shape[0]
+    for b in ws.bodies:
+        b.edge_topk = m
+    (a1, a2), (o1, o2) = surfaces(ws)
+    L = api.layout(a1, a2, SmoothingConfig())
+    assert L["m1"] == m and L["m1"] * L["m2"] > 2000
+    p1, p2 = ws.poses(16)
+    ref = Oracle.manifold_batch(o1, o2, p1, p2, SmoothingConfig())
+    r = api.generate_manifold_batch(a1, a2, torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda"),
+                                    SmoothingConfig())
+    torch.cuda.synchronize()
+    assert_parity(r["contacts"].cpu().numpy(), ref["contacts"], what=f"pass-through P={L['m1'] * L['m2']}")
+
+
+def test_working_set_limit_fails_loudly(cuda):
+    """A per-env working set whose slots alone exceed the shared-memory budget
+    (2 x 2,352 pass-through edges) is refused with CMGB_ERR_UNSUPPORTED
+    (DESIGN.md §3), never silently truncated."""
+    ws = W.box_box(4)
+    for b in ws.bodies:
+        b.mesh.subdivisions = 14
+    e = api.surface_from_spec(ws.bodies[0]).mesh.edges.shape[0]
+    for b in ws.bodies:
+        b.edge_topk = e  # pass-through: all edges (budgets are validated to lie in [1, E])
+    a1, a2 = (api.surface_from_spec(b) for b in ws.bodies)
+    p = torch.zeros((4, 6), dtype=torch.float64, device="cuda")
+    with pytest.raises(abi.CmgbError, match="UNSUPPORTED"):
+        api.generate_manifold_batch(a1, a2, p, p, SmoothingConfig())
