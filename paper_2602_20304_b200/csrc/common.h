@@ -204,6 +204,7 @@ struct WitnessParams {
 namespace cmgb {
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream);
+int manifold_min_blocks(int k1, int k2);  // resident CTAs / SM the kernel for this kind pair is built for
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
 int jvp_directions();    // tangent directions per thread of the compiled JVP kernel
 int jvp_max_threads();   // CTA size of the JVP kernel

@@ -236,7 +236,9 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   const int maxt = manifold_max_threads();
   const int per_env = std::max({P, nslot_v, 1});
   int epb = std::max(1, maxt / per_env);
-  const size_t smem_cap = 72 * 1024;
+  // shared memory per CTA such that the kernel's resident-CTA target fits the SM
+  const size_t smem_cap =
+      (size_t)(216 * 1024) / manifold_min_blocks(p.side[0].sdf.kind, p.side[1].sdf.kind);
   while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
   const int threads = maxt;
   p.envs_per_block = epb;
