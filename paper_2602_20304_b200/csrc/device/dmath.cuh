@@ -117,10 +117,12 @@ __device__ __forceinline__ double pv(double x) { return x; }
 __device__ __forceinline__ double pv(float x) { return x; }
 
 // FP32 members of the overload sets (the K6 witness batches' soft indicators,
-// witness.cuh): accurate libdevice expf / logf, IEEE reciprocal.
-__device__ __forceinline__ float exp_d(float x) { return expf(x); }
-__device__ __forceinline__ float log_d(float x) { return logf(x); }
-__device__ __forceinline__ float rcp_d(float x) { return __frcp_rn(x); }
+// witness.cuh): SFU forms. Their arguments are FP64 values rounded to FP32,
+// which already costs |x| 6e-8 relative in exp; ex2/lg2/rcp.approx stay within
+// that budget (alpha error <= tau_clip * 1e-6 on the witness points).
+__device__ __forceinline__ float exp_d(float x) { return __expf(x); }
+__device__ __forceinline__ float log_d(float x) { return __logf(x); }
+__device__ __forceinline__ float rcp_d(float x) { return rcpf(x); }
 
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same
 // function; returns sigma(x) and its complement 1 - sigma(x) = sigma(-x), each
