@@ -395,7 +395,7 @@ def main():
                 "frac": hbm_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None},
         "kernel_ms": kernel_ms,
     }
-    cb = None if args.no_cpu_baseline else cpu_reference_run(args.cpu_sample)
+    cb = None if args.no_cpu_baseline else cpu_reference_run(args.cpu_sample, reps=3)
     line = {
         "metric": "contact manifolds/sec (box-box, 65,536 envs)",
         "value": value, "unit": "manifolds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
