@@ -1,7 +1,7 @@
 // Batched demo integrator: DemoSim::step (src/demosim.cpp:81-138) for every env
 // of a batch, on the manifolds the scene batch leaves in device memory.
 //
-//   penalty_kernel   one warp per (env, pair): penalty_forces (demosim.cpp:31-66)
+//   penalty_kernel   16 lanes per (env, pair): penalty_forces (demosim.cpp:31-66)
 //                    over the pair's fixed-layout contacts, fixed-order warp
 //                    reduction -> the pair's two wrenches + deepest penetration
 //   integrate_kernel one thread per env: per body, wrench sum in pair order, then
@@ -24,17 +24,23 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
   c[2] = a[0] * b[1] - a[1] * b[0];
 }
 
-// softplus_s (smooth_ops.hpp:66-81), both arms as in the reference
+// softplus_s (smooth_ops.hpp:66-81), both arms as in the reference; the
+// exponential is exp_d and below e^-40 log1p(e) = e to double precision.
 __device__ __forceinline__ double softplus_ref(double x, double tau) {
   const double scaled = x / tau;
-  if (scaled > 0.0) return x + tau * log1p(exp(-scaled));
-  return tau * log1p(exp(scaled));
+  const double e = exp_d(-fabs(scaled));
+  const double l = e < 4e-18 ? e : log1p(e);
+  return scaled > 0.0 ? x + tau * l : tau * l;
 }
 
+// A 16-lane group per env (two envs per warp): 48-contact pair manifolds are
+// 3 contacts per lane with no idle second pass.
+constexpr int kPenaltyLanes = 16;
+
 __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ PenaltyArgs a) {
-  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (e >= a.n_env) return;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPenaltyLanes;
+  const int lane = threadIdx.x & (kPenaltyLanes - 1);
+  if (e >= a.n_env) return;  // a whole 16-lane group exits; the shuffles below use the group's mask
   const DemoParamsDev& P = a.prm;
   // transforms[i].t is the COM (demosim.cpp:84, 96-97)
   const double* f1 = a.frames1 + 12 * e;
@@ -47,7 +53,7 @@ __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ Pe
 #pragma unroll
   for (int k = 0; k < 12; ++k) acc[k] = 0.0;
   double deep = 0.0;
-  for (int r = lane; r < a.C; r += 32) {
+  for (int r = lane; r < a.C; r += kPenaltyLanes) {
     const float4* cp = reinterpret_cast<const float4*>(a.contacts + (e * a.C + r) * 8);
     const float4 c0 = cp[0], c1 = cp[1];
     const double act = c1.w, dist = c0.w;
@@ -56,7 +62,7 @@ __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ Pe
     const double pt[3] = {c0.x, c0.y, c0.z};
     const double pressure = P.stiffness * softplus_ref(-dist, P.tau_force);
     const double nraw[3] = {c1.x, c1.y, c1.z};
-    const double sc = 1.0 / sqrt(1e-12 + (nraw[0] * nraw[0] + nraw[1] * nraw[1] + nraw[2] * nraw[2]));
+    const double sc = rsqrt_d(1e-12 + (nraw[0] * nraw[0] + nraw[1] * nraw[1] + nraw[2] * nraw[2]));
     const double nh[3] = {nraw[0] * sc, nraw[1] * sc, nraw[2] * sc};
     // side of contact r in the fixed layout (manifold.hpp:14-17)
     const bool side1 = r < a.n1 ? true : (r < a.n1 + a.n2 ? false : (((r - a.n1 - a.n2) & 1) == 0));
@@ -93,12 +99,13 @@ __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ Pe
       oth[3 + k] -= tt[k];
     }
   }
-  // fixed-order butterfly reduction (deterministic)
+  // fixed-order butterfly reduction within the env's 16 lanes (deterministic)
+  const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = kPenaltyLanes / 2; o > 0; o >>= 1) {
 #pragma unroll
-    for (int k = 0; k < 12; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-    deep = fmin(deep, __shfl_xor_sync(0xffffffffu, deep, o));
+    for (int k = 0; k < 12; ++k) acc[k] += __shfl_xor_sync(gm, acc[k], o);
+    deep = fmin(deep, __shfl_xor_sync(gm, deep, o));
   }
   if (lane == 0) {
     double* w = a.wrench + e * 12;
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(128) integrate_kernel(const __grid_constant__ 
 
 int launch_penalty(const PenaltyArgs& a, void* stream) {
   if (a.n_env <= 0) return 0;
-  const int64_t threads = a.n_env * 32;
+  const int64_t threads = a.n_env * kPenaltyLanes;
   penalty_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
