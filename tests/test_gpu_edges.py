@@ -95,3 +95,24 @@ def test_working_set_limit_fails_loudly(cuda):
     p = torch.zeros((4, 6), dtype=torch.float64, device="cuda")
     with pytest.raises(abi.CmgbError, match="UNSUPPORTED"):
         api.generate_manifold_batch(a1, a2, p, p, SmoothingConfig())
+
+
+def test_config_e_size_batch(cuda):
+    """1,048,576 envs in one call (config E's size on one GPU, ~10 GB of
+    contacts): 64-bit indexing end to end -- the first 4,096 envs and the last
+    env equal separate smaller batches bit for bit, everything finite."""
+    n = 1 << 20
+    ws = W.box_box(n)
+    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+    p1, p2 = ws.poses(n)
+    t1, t2 = torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda")
+    big = api.generate_manifold_batch(s1, s2, t1, t2, SmoothingConfig())
+    head = api.generate_manifold_batch(s1, s2, t1, t2[:4096].contiguous(), SmoothingConfig())
+    last = api.generate_manifold_batch(s1, s2, t1, t2[n - 1:].contiguous(), SmoothingConfig())
+    torch.cuda.synchronize()
+    assert torch.equal(big["contacts"][:4096], head["contacts"])
+    assert torch.equal(big["contacts"][n - 1:], last["contacts"])
+    assert torch.equal(big["mean_dist"][:4096], head["mean_dist"])
+    assert bool(torch.isfinite(big["mean_dist"]).all())
+    del big
+    torch.cuda.empty_cache()
