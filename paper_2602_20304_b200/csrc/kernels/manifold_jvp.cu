@@ -319,9 +319,12 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
   __syncthreads();
 
   // ---- E: V-S contacts (vs_contacts, manifold.hpp:185-204), E-E pairs -----
+  // V-S items start on the thread after the last pair item, so the two kinds
+  // run side by side instead of V-S then pairs on the same threads.
   {
     const int nvs = n1 + n2;
-    for (int it = tid; it < n_here * nvs; it += nth) {
+    const int vs0 = full ? (n_here * P) % nth : 0;
+    for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < n_here * nvs; it += nth) {
       const int k = it / nvs, r = it - k * nvs;
       const Unit<ND> u = unit(k);
       const bool first = r < n1;
