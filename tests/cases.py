@@ -78,6 +78,7 @@ def manifold_cases():
         out.append((name, W.mixed_bucket(name.split("_", 1)[1]), base, 8))
     out.append(("opc_vs_box", opc_vs_box(), base, 8))
     out.append(("subtraction_vs_box", subtraction_vs_box(), base, 8))
+    out.append(("octahedron_vs_box", octahedron_vs_box(), base, 8))
     return out
 
 
@@ -98,6 +99,23 @@ def subtraction_vs_box():
     b2 = W.BodySpec("box", W.MeshSpec(box_half=(0.2, 0.2, 0.2)), Superquadric(0.1, 0.1, (0.2, 0.2, 0.2)),
                     [0.05, 0.0, 1.1, 0.0, 0.0, math.pi / 5], 6, 8)
     return W.Workload("subtraction-vs-box", [b1, b2], 8)
+
+
+def octahedron_vs_box():
+    """A general convex polyhedron (8 oblique planes: the kSingleCp path) with
+    its own OBJ mesh against an SQ box."""
+    r = 0.45
+    verts = [(r, 0, 0), (-r, 0, 0), (0, r, 0), (0, -r, 0), (0, 0, r), (0, 0, -r)]
+    faces = [(1, 3, 5), (3, 2, 5), (2, 4, 5), (4, 1, 5), (3, 1, 6), (2, 3, 6), (4, 2, 6), (1, 4, 6)]
+    obj = "\n".join([f"v {x} {y} {z}" for x, y, z in verts] + [f"f {a} {b} {c}" for a, b, c in faces]) + "\n"
+    s3 = 1.0 / math.sqrt(3.0)
+    normals = [(sx * s3, sy * s3, sz * s3) for sx in (1, -1) for sy in (1, -1) for sz in (1, -1)]
+    points = [(sx * r, 0.0, 0.0) for sx in (1, -1) for _ in (1, -1) for _ in (1, -1)]
+    octa = W.BodySpec("octa", W.MeshSpec(obj_text=obj), ConvexPolyhedron(np.array(normals), np.array(points), 1e-3),
+                      [0.02, -0.01, 0.0, 0.1, 0.05, 0.2], 0, 6)
+    box = W.BodySpec("box", W.MeshSpec(box_half=(0.3, 0.3, 0.3)), Superquadric(0.1, 0.1, (0.3, 0.3, 0.3)),
+                     [0.05, 0.02, 0.72, 0.0, 0.1, 0.3], 0, 6)
+    return W.Workload("octahedron-vs-box", [octa, box], 8)
 
 
 OBJ_TEXTS = {
