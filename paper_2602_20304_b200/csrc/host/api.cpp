@@ -627,7 +627,7 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
       cuda_check(cudaEventCreateWithFlags(&sc.ev_start, cudaEventDisableTiming), "cudaEventCreate");
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t nchunk = n_env >= 4 * kHostChunkMin ? 4 : (n_env >= 2 * kHostChunkMin ? 2 : 1);
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, n_env / kHostChunkMin));
     const int64_t per = (n_env + nchunk - 1) / nchunk;
     ensure(&sc.frames, &sc.cap_frames, 2 * workspace_doubles(per, st1, st2));
     cuda_check(cudaEventRecord(sc.ev_start, s), "cudaEventRecord");
