@@ -261,6 +261,30 @@ def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=No
     return res
 
 
+def mean_contact_distance(contacts, tangents=None):
+    """mean_contact_distance (manifold.hpp:379-384) over contacts [..., C, 8]
+    (torch or numpy); with tangents [..., C, 8, 12] also its 12 pose tangents.
+    (The batch calls return it per env directly; this is the reduction for
+    caller-side use.)"""
+    d = contacts[..., 3]
+    m = d.mean(-1)
+    if tangents is None:
+        return m
+    return m, tangents[..., 3, :].mean(-2)
+
+
+def activity_weighted_distance(contacts, tangents=None):
+    """activity_weighted_distance (manifold.hpp:386-391): sum of activity x
+    dist over contacts [..., C, 8]; with tangents [..., C, 8, 12] also its pose
+    tangents (product rule: act' dist + act dist')."""
+    d, a = contacts[..., 3], contacts[..., 7]
+    v = (a * d).sum(-1)
+    if tangents is None:
+        return v
+    g = (tangents[..., 7, :] * d[..., None] + a[..., None] * tangents[..., 3, :]).sum(-2)
+    return v, g
+
+
 def scene_pairs(n_bodies: int, is_static=None) -> np.ndarray:
     """Body pairs (i < j, skipping static-static) in DemoSim::step's order
     (src/demosim.cpp:88-104)."""

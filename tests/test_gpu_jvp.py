@@ -131,3 +131,22 @@ def test_scene_jvp_matches_reference(cuda):
         ref_mean = g[f"drop_pair{q}_0_mean"]
         assert np.linalg.norm(r["mean_dist_grad"][0].cpu().numpy() - ref_mean[1:]) <= \
             JAC_ATOL + JAC_RTOL * np.linalg.norm(ref_mean[1:])
+
+
+def test_manifold_reductions_and_their_tangents(cuda):
+    """mean_contact_distance / activity_weighted_distance (manifold.hpp:379-391)
+    on the JVP outputs: the mean equals the kernel's own, and the reductions'
+    tangents equal those the reference's Dual12 gives (fixtures: contacts and
+    tangents of the reference run)."""
+    g = np.load(os.path.join(GOLD, "jvp_cases.npz"))
+    name, ws, cfg, n = [c for c in SMOOTH if c[0] == "box_box_topk"][0]
+    p1, p2 = ws.poses(n)
+    r = run_jvp(ws, cfg, p1, p2)
+    m, mg = api.mean_contact_distance(r["contacts"][0].astype(np.float64), r["tangents"][0].astype(np.float64))
+    assert abs(m - r["mean_dist"][0]) <= 1e-6 + 1e-5 * abs(m)
+    assert np.allclose(mg, r["mean_dist_grad"][0], rtol=1e-4, atol=1e-6)
+    rc, rt = g[f"{name}_0_contacts"], g[f"{name}_0_tangents"].astype(np.float64)
+    v, vg = api.activity_weighted_distance(r["contacts"][0].astype(np.float64), r["tangents"][0].astype(np.float64))
+    v_ref, vg_ref = api.activity_weighted_distance(rc, rt)
+    assert abs(v - v_ref) <= 1e-6 + 1e-5 * abs(v_ref)
+    assert np.linalg.norm(vg - vg_ref) <= 1e-5 + 1e-4 * np.linalg.norm(vg_ref)
