@@ -301,6 +301,19 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
 int cmgb_ee_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
                           const cmgb_config* cfg, float* out, float* alpha_gamma,
                           int32_t* labels, void* cuda_stream);
+/* SDF queries on one surface (SmoothSdf::value / value_and_gradient /
+ * value_and_normal_source, include/cmg/sdf.hpp:177-195): points DEVICE [n][3]
+ * in the body frame; out DEVICE [n][4] = value, gradient (flavor 1) or normal
+ * source (flavor 2; zeros for flavor 0). */
+int cmgb_sdf_query(cmgb_surface s, int32_t flavor, const double* points, int64_t n, double* out,
+                   void* cuda_stream);
+
+/* sphere_trace_project against the posed SDF (sdf.hpp:318-326): world points
+ * DEVICE [n][3], pose HOST [6], iters steps with normalisation tau; out DEVICE
+ * [n][3] world points. */
+int cmgb_sphere_trace(cmgb_surface s, const double* pose, const double* points, int64_t n, int32_t iters,
+                      double tau, double* out, void* cuda_stream);
+
 /* Reference-precision E-E witnesses: FP64 pairs in, FP64 soft indicators,
  * FP64 outputs out [n][6] (alpha_gamma [n][3] FP64, labels optional): what
  * ee_witness<double> returns (witness.hpp:137-158). */

@@ -180,6 +180,8 @@ SIGNATURES = {
         [_P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P],
     ),
     "cmgb_device_count": (_I, [C.POINTER(C.c_int32)]),
+    "cmgb_sdf_query": (_I, [_P, C.c_int32, _P, C.c_int64, _P, _P]),
+    "cmgb_sphere_trace": (_I, [_P, _P, _P, C.c_int64, C.c_int32, C.c_double, _P, _P]),
     "cmgb_ee_witness_batch_f64": (_I, [_P, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P, _P]),
     "cmgb_rotating_edge_sweep": (_I, [C.c_int32, C.c_int32, _P]),
     "cmgb_manifold_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),

@@ -261,6 +261,34 @@ def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=No
     return res
 
 
+def sdf_query(surface: Surface, points, flavor: int = 1, stream=None):
+    """SmoothSdf queries (sdf.hpp:177-195) on the GPU: points CUDA float64
+    [n, 3] in the body frame -> [n, 4] value + gradient (flavor 1), normal
+    source (2) or value only (0)."""
+    import torch
+
+    pts = points.reshape(-1, 3).contiguous()
+    out = torch.empty((pts.shape[0], 4), dtype=torch.float64, device=pts.device)
+    with torch.cuda.device(pts.device):
+        _ok(abi.load().cmgb_sdf_query(surface._h, int(flavor), pts.data_ptr(), pts.shape[0], out.data_ptr(),
+                                      _stream_ptr(stream)))
+    return out
+
+
+def sphere_trace(surface: Surface, pose, points, iters: int = 5, tau: float = 1e-9, stream=None):
+    """sphere_trace_project (sdf.hpp:318-326) of world points [n, 3] (CUDA
+    float64) against the surface posed by pose [6]."""
+    import torch
+
+    pts = points.reshape(-1, 3).contiguous()
+    pose = np.ascontiguousarray(pose, dtype=np.float64)
+    out = torch.empty_like(pts)
+    with torch.cuda.device(pts.device):
+        _ok(abi.load().cmgb_sphere_trace(surface._h, pose.ctypes.data, pts.data_ptr(), pts.shape[0], int(iters),
+                                         float(tau), out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
 def mean_contact_distance(contacts, tangents=None):
     """mean_contact_distance (manifold.hpp:379-384) over contacts [..., C, 8]
     (torch or numpy); with tangents [..., C, 8, 12] also its 12 pose tangents.

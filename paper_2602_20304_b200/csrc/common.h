@@ -187,6 +187,17 @@ struct IntegrateArgs {
   int32_t pair_i[kDemoMaxPairs], pair_j[kDemoMaxPairs];
 };
 
+// Batched SDF queries / sphere traces on one surface (kernels/sdf_query.cu).
+struct SdfQueryParams {
+  DevSdf sdf;
+  const double* points;  // [n][3]
+  int64_t n;
+  double* out;           // [n][4] value, gradient | [n][3] traced points
+  double R[9], t[3];     // trace: posed surface
+  int32_t iters;
+  double tau;
+};
+
 struct WitnessParams {
   const void* pairs;
   int32_t fp64;
@@ -212,6 +223,7 @@ int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan fo
 int launch_ee_witness(const WitnessParams& p, void* stream);
 int launch_ee_witness_f64(const WitnessParams& p, void* stream);
 int launch_penalty(const PenaltyArgs& a, void* stream);
+int launch_sdf_query(const SdfQueryParams& q, int mode, void* stream);
 int launch_integrate(const IntegrateArgs& a, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);
 const char* last_cuda_error_string();

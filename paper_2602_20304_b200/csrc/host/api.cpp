@@ -769,6 +769,44 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
   });
 }
 
+// ---- SDF queries / sphere tracing ---------------------------------------------------
+int cmgb_sdf_query(cmgb_surface s, int32_t flavor, const double* points, int64_t n, double* out, void* stream) {
+  return guarded([&] {
+    if (!s) invalid("sdf_query: null surface");
+    if (flavor < 0 || flavor > 2) invalid("sdf_query: flavor must be 0 (value), 1 (gradient) or 2 (normal source)");
+    if (n < 0) invalid("sdf_query: n >= 0");
+    if (n == 0) return;
+    if (!points || !out) invalid("sdf_query: null buffer");
+    SdfQueryParams q{};
+    q.sdf = device_image(s).sdf;
+    q.points = points;
+    q.n = n;
+    q.out = out;
+    if (launch_sdf_query(q, flavor, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("sdf_query launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+int cmgb_sphere_trace(cmgb_surface s, const double* pose_host, const double* points, int64_t n, int32_t iters,
+                      double tau, double* out, void* stream) {
+  return guarded([&] {
+    if (!s || !pose_host) invalid("sphere_trace: null surface or pose");
+    if (n < 0 || iters < 0) invalid("sphere_trace: n >= 0 and iters >= 0");
+    if (n == 0) return;
+    if (!points || !out) invalid("sphere_trace: null buffer");
+    SdfQueryParams q{};
+    q.sdf = device_image(s).sdf;
+    q.points = points;
+    q.n = n;
+    q.out = out;
+    q.iters = iters;
+    q.tau = tau;
+    se3_exp_host(pose_host, q.R, q.t);
+    if (launch_sdf_query(q, 3, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("sphere_trace launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
 // ---- witness batches --------------------------------------------------------------
 int cmgb_ee_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb_config* cfg,
                           float* out, float* alpha_gamma, int32_t* labels, void* stream) {

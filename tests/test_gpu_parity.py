@@ -264,3 +264,21 @@ def test_scene_batch_all_pairs(cuda):
         ref = Oracle.manifold_batch(o[i], o[j], P[:, i], P[:, j], SmoothingConfig())
         assert_parity(r["contacts"].cpu().numpy(), ref["contacts"], what=f"scene pair {(i, j)} vs oracle")
         assert np.array_equal(r["src"].cpu().numpy(), ref["meta"][..., 2:])
+
+
+@pytest.mark.parametrize("name", list(__import__("cases").SDF_PROGRAMS))
+def test_sdf_queries_vs_reference_golden(cuda, name):
+    """The device field code directly: values, true
+    gradients and normal sources of every SDF program, and 5-step sphere traces
+    of a posed surface, vs the reference's (tests/golden/sdf.npz)."""
+    from cases import SDF_PROGRAMS
+    g = gold("sdf")
+    s = api.Surface(api.Mesh.box((0.5, 0.5, 0.5)), SDF_PROGRAMS[name])
+    pts = torch.as_tensor(g["points"], device="cuda")
+    for fl in (0, 1, 2):
+        got = api.sdf_query(s, pts, fl).cpu().numpy()
+        ref = g[f"{name}_f{fl}"]
+        err = np.abs(got - ref) / (1e-11 + 1e-9 * np.abs(ref))
+        assert err.max() <= 1.0, (name, fl, float(err.max()))
+    tr = api.sphere_trace(s, [0.1, -0.2, 0.3, 0.2, 0.1, -0.3], pts[:50], 5).cpu().numpy()
+    assert np.allclose(tr, g[f"{name}_trace5"], rtol=1e-8, atol=1e-10), np.abs(tr - g[f"{name}_trace5"]).max()
