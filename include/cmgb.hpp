@@ -152,6 +152,42 @@ inline void generate_scene_batch(const std::vector<cmgb_surface>& bodies, const 
                                   (int32_t)(pairs.size() / 2), poses, n_env, &c, outs.data(), stream));
 }
 
+// SmoothSdf queries / sphere_trace_project on one surface (device buffers).
+inline void sdf_query(const Surface& s, int flavor, const double* points, int64_t n, double* out,
+                      void* stream = nullptr) {
+  check(cmgb_sdf_query(s.handle(), flavor, points, n, out, stream));
+}
+inline void sphere_trace(const Surface& s, const double pose[6], const double* points, int64_t n, int iters,
+                         double tau, double* out, void* stream = nullptr) {
+  check(cmgb_sphere_trace(s.handle(), pose, points, n, iters, tau, out, stream));
+}
+
+// rotating_edge_sweep (src/sweep.cpp): rows of theta, p1 (3), dp1/dtheta (3).
+inline std::vector<double> rotating_edge_sweep(int variant, int n_samples) {
+  std::vector<double> out(7 * (size_t)n_samples);
+  check(cmgb_rotating_edge_sweep(variant, n_samples, out.data()));
+  return out;
+}
+
+// PenaltyParams{} and one DemoSim::step for a batch of scenes (device state,
+// [n_env][n_bodies][6] poses / velocities updated in place).
+inline cmgb_demo_params default_penalty_params() {
+  cmgb_demo_params p;
+  cmgb_demo_params_default(&p);
+  return p;
+}
+inline void demo_step(const std::vector<cmgb_demo_body>& bodies, const SmoothingConfig& c,
+                      const cmgb_demo_params& params, double dt, int64_t n_env, double* poses, double* velocities,
+                      double* deepest = nullptr, int32_t* ok = nullptr, void* stream = nullptr) {
+  check(cmgb_demo_step_batch(bodies.data(), (int32_t)bodies.size(), &c, &params, dt, n_env, poses, velocities,
+                             deepest, ok, nullptr, 0, stream));
+}
+
+inline void run_ee_batch_f64(const double* pairs_device, int64_t n, const SmoothingConfig& c, double* out_device,
+                             void* stream = nullptr) {
+  check(cmgb_ee_witness_batch_f64(pairs_device, n, &c, out_device, nullptr, nullptr, stream));
+}
+
 inline void run_ee_batch(const double* pairs_device, int64_t n, const SmoothingConfig& c,
                          float* out_device, void* stream = nullptr) {
   check(cmgb_ee_witness_batch(pairs_device, 1, n, &c, out_device, nullptr, nullptr, stream));

@@ -11,7 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = r"""
 #include <cstdio>
 #include "cmgb.hpp"
-int main() {
+int main(int argc, char** argv) {
+  (void)argv;
   const double half[3] = {0.5, 0.5, 0.5};
   cmgb::Mesh box = cmgb::Mesh::box(half);
   cmgb_sdf_node sq{};
@@ -27,6 +28,21 @@ int main() {
   try { bad.validate(); } catch (const std::invalid_argument& e) { std::printf("err %s\n", e.what()); }
   try { cmgb::Mesh::parse_obj("v 0 0 0\nf 1 2 3\n"); }
   catch (const cmgb::MeshParseError& e) { std::printf("parse %d %s\n", e.line_number, e.what()); }
+  const cmgb_demo_params pp = cmgb::default_penalty_params();
+  std::printf("penalty %g %g %g\n", pp.stiffness, pp.tau_force, pp.gravity[2]);
+  std::printf("pairs %zu\n", cmgb::scene_pairs({1, 0, 0, 0, 0}).size() / 2);
+  if (argc > 99) {  // device entry points: compiled and linked here, exercised by the GPU suites
+    double* d = nullptr;
+    cmgb::sdf_query(s, 1, d, 0, d);
+    const double pose[6] = {0, 0, 0, 0, 0, 0};
+    cmgb::sphere_trace(s, pose, d, 0, 5, 1e-9, d);
+    cmgb::rotating_edge_sweep(2, 16);
+    cmgb_demo_body b{s.handle(), 1.0, {0, 0, 0}, 0, 0};
+    cmgb::demo_step({b, b}, cfg, pp, 1e-3, 0, d, d);
+    cmgb::run_ee_batch_f64(d, 0, cfg, d);
+    cmgb_manifold_jvp_out jo{};
+    cmgb::generate_manifold_jvp_batch(s, s, d, 1, d, 1, 0, cfg, jo);
+  }
   return 0;
 }
 """
@@ -46,3 +62,5 @@ def test_cpp_header_host_api(tmp_path):
     assert lines[0] == "contacts 304 warnings 1"
     assert lines[1] == "err smoothing: tau_pen must be > 0"
     assert lines[2] == "parse 2 face index out of range (line 2)"
+    assert lines[3] == "penalty 10000 0.0001 -9.81"  # PenaltyParams{} (demosim.hpp:24-31)
+    assert lines[4] == "pairs 10"  # DemoSim::step's pairs of a 5-body scene with one static body
