@@ -601,6 +601,23 @@ class DemoBatch:
             out[i] = given if (given > 0).all() else _box_inertia(self.masses[i], b.mesh.vertices)
         return out
 
+    def linear_momentum(self):
+        """DemoSim::linear_momentum (demosim.cpp:157-166) per env: [n_env, 3]
+        (CUDA tensor; static bodies excluded)."""
+        import torch
+
+        m = torch.as_tensor(np.where(self.is_static, 0.0, self.masses), device=self.velocities.device)
+        return (self.velocities[:, :, :3] * m[None, :, None]).sum(dim=1)
+
+    def states(self):
+        """DemoSim::states (demosim.hpp:57-58): (poses, velocities), each
+        [n_env, n_bodies, 6] on the device (velocity = world [linear; angular])."""
+        return self.poses, self.velocities
+
+    def deepest_penetration(self):
+        """DemoSim::deepest_penetration (demosim.hpp:63-64) of the last step, per env."""
+        return self.deepest
+
     def kinetic_energy(self) -> np.ndarray:
         """DemoSim::kinetic_energy (demosim.cpp:140-155) per env (host)."""
         return kinetic_energy_np(self.poses.cpu().numpy(), self.velocities.cpu().numpy(), self.masses,
