@@ -11,6 +11,7 @@ Exit codes and stdout lines follow main.cpp:124-254."""
 from __future__ import annotations
 
 import argparse
+import math
 import sys
 
 import numpy as np
@@ -225,7 +226,7 @@ def cmd_sim(a) -> int:
     sim = api.DemoBatch([b.surface for b in sc.bodies], [b.mass for b in sc.bodies],
                         inertia=[b.inertia_diag for b in sc.bodies], is_static=[b.is_static for b in sc.bodies],
                         cfg=cfg, params=PenaltyParams(), poses=np.array([b.pose for b in sc.bodies]), n_env=1)
-    steps = int(round(a.duration / a.dt))
+    steps = int(math.floor(a.duration / a.dt + 0.5))  # std::llround (half away from zero)
     with open(a.out, "w") as f:
         f.write("time")
         for b in sc.bodies:
