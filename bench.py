@@ -35,7 +35,7 @@ BYTES_PER_ENV = 48.0 + 304 * 32.0  # FP32 poses-equivalent in + fixed-layout con
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-env", type=int, default=65536, help="envs per GPU (weak scaling)")
@@ -71,6 +71,20 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
+    def wait_first(self, busy, timeout=3.0):
+        """Keep the GPU loaded (busy()) until nvidia-smi has produced its first
+        sample, so the samples that follow fall inside the timed region."""
+        import torch
+
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            busy()
+            torch.cuda.synchronize()
+
+    def mark(self):
+        """Samples before this point are dropped when later ones exist."""
+        self.n_pre = len(self.lines)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -84,9 +98,10 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        lines = self.lines[getattr(self, "n_pre", 0):] or self.lines
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -303,6 +318,8 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
+    clocks.wait_first(step)
+    clocks.mark()
     barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

@@ -132,10 +132,10 @@ struct ManifoldParams {
 };
 
 // Pose-Jacobian (forward-mode, Dual12) batch: the geometry / config / slot
-// counts of a ManifoldParams plan, one CTA per (env, direction group), each
-// group carrying `nd` of the 12 pose tangent directions (dual.hpp:249-263).
-// Shared-memory offsets are in bytes from the CTA base (host-computed: the
-// scalar is nd + 1 doubles).
+// counts of a ManifoldParams plan; one unit = one env with all 12 pose tangent
+// directions (dual.hpp:249-263), `units_per_block` envs per CTA. Shared-memory
+// offsets are in bytes from the env's base (host-computed; tangent records
+// are an FP64 primal + 12 FP32 tangents, 56 bytes).
 struct JvpParams {
   ManifoldParams m;
   float* tangents;   // [n_env][C][8][12]
@@ -145,6 +145,7 @@ struct JvpParams {
   int32_t nd, groups;
   int32_t units_per_block;
   int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
+  int32_t o_sj, o_qp;  // per-pair side Jacobian / witness QP records (E1 -> E2)
   int32_t bytes;  // per unit
 };
 
