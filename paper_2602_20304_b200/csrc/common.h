@@ -146,6 +146,8 @@ struct JvpParams {
   int32_t units_per_block;
   int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
   int32_t o_sj, o_qp;  // per-pair side Jacobian / witness QP records (E1 -> E2)
+  int32_t o_ebuf, o_aux, ebuf_stride;
+  int32_t o_vsrec, o_prec;  // V-S / E-E pair primal records (E1 -> E2)  // soft top-K row weights (FP32, stride per slot) / row totals
   int32_t bytes;  // per unit
 };
 
@@ -221,6 +223,7 @@ int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
 int jvp_directions();    // tangent directions per thread of the compiled JVP kernel
 int jvp_max_threads();   // CTA size of the JVP kernel
 int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan for
+int jvp_lane_width();    // tangent columns per E1 lane of the JVP kernel (Dual<W>)
 int launch_ee_witness(const WitnessParams& p, void* stream);
 int launch_ee_witness_f64(const WitnessParams& p, void* stream);
 int launch_penalty(const PenaltyArgs& a, void* stream);

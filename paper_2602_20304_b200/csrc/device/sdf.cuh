@@ -230,23 +230,23 @@ __device__ __forceinline__ SdfOutT<T> cp_leaf(const DevNode& nd, const double4* 
 // FMA dot of cp_leaf is exactly +-p_i - w_k (the zero products add exact
 // zeros) and the gradient sum is (e0 - e1, e2 - e3, e4 - e5): bit-identical to
 // cp_leaf without the plane loads and 18 of its 24 FMAs per pass.
-template <int FL>
-__device__ __forceinline__ SdfOut box_cp_leaf(const DevNode& nd, double3 p) {
-  const double d[6] = {p.x - nd.box_w[0], -p.x - nd.box_w[1], p.y - nd.box_w[2],
-                       -p.y - nd.box_w[3], p.z - nd.box_w[4], -p.z - nd.box_w[5]};
-  double m = -INFINITY;
+template <int FL, class T = double>
+__device__ __forceinline__ SdfOutT<T> box_cp_leaf(const DevNode& nd, vec3<T> p) {
+  const T d[6] = {p.x - nd.box_w[0], -p.x - nd.box_w[1], p.y - nd.box_w[2],
+                  -p.y - nd.box_w[3], p.z - nd.box_w[4], -p.z - nd.box_w[5]};
+  T m = -INFINITY;
 #pragma unroll
   for (int i = 0; i < 6; ++i) m = fmax(m, d[i]);
-  double e[6], acc = 0.0;
+  T e[6], acc = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     e[i] = exp_d((d[i] - m) * nd.inv_tau_d);
     acc += e[i];
   }
-  SdfOut out;
+  SdfOutT<T> out;
   out.v = m + nd.tau_d * log_d(acc);
-  out.g = d3(0, 0, 0);
-  if (FL != kValue) out.g = dscale(d3(e[0] - e[1], e[2] - e[3], e[4] - e[5]), rcp_d(acc));
+  out.g = mk3<T>(0.0, 0.0, 0.0);
+  if (FL != kValue) out.g = dscale(mk3<T>(e[0] - e[1], e[2] - e[3], e[4] - e[5]), rcp_d(acc));
   return out;
 }
 
@@ -300,7 +300,7 @@ __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;
   if constexpr (KIND == kSingleCp) return cp_leaf<FL, T>(s.nodes[0], s.pool, p);
-  if constexpr (KIND == kBoxCp) return box_cp_leaf<FL>(s.nodes[0], p);
+  if constexpr (KIND == kBoxCp) return box_cp_leaf<FL, T>(s.nodes[0], p);
   // Generic postfix interpreter (union: -LSE(-phi), subtraction: LSE(phi+, -phi-);
   // sdf.hpp:222-230, 260-287). Warp-uniform control flow.
   T sv[kMaxStack];

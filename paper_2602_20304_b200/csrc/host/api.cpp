@@ -700,36 +700,50 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   j.mean_grad_f64 = out->mean_dist_grad_f64;
   // One unit = one env carrying all 12 pose directions (manifold_jvp.cu).
   // Tangent records: FP64 primal + 12 FP32 tangents (56 B). The top-K scores /
-  // order are dead after the slot phase and share their bytes with the pair
-  // side-Jacobian / QP records (E1 -> E2).
+  // order / row weights are dead after the slot phase and share their bytes
+  // with the pair side-Jacobian / QP records (E1 -> E2).
   j.nd = jvp_directions();
   j.groups = 1;
   const ManifoldParams& m = j.m;
-  const int T = 8 + 12 * 4;          // bytes per tangent record
-  const int SJ = 38 * 8, QP = 18 * 8;  // SideJac, QpRec (manifold_jvp.cu)
-  const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2;
+  const int T = 8 + 12 * 4;                  // bytes per tangent record
+  const int SJ = 32 * 8, QP = 18 * 8, AUX = 16, VS = 21 * 8, PR = 17 * 8;  // manifold_jvp.cu records
+  const int FRAMES = 2 * 12 * 8 + 12 * 6 * 8;  // 2 x Frame + 12 x Vel
+  const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2, nsl = nslot_v + nslot_e;
   const bool topk = m.side[0].topk_v || m.side[1].topk_v || m.side[0].topk_e || m.side[1].topk_e;
   const int nscore = topk ? (m.side[0].nv + m.side[1].nv + m.side[0].ne + m.side[1].ne) : 0;
+  int dmax = 0;
+  for (int k = 0; k < 2; ++k) {
+    if (m.side[k].topk_v) dmax = std::max(dmax, m.side[k].nv);
+    if (m.side[k].topk_e) dmax = std::max(dmax, m.side[k].ne);
+  }
+  j.ebuf_stride = dmax;
   int off = 0;
-  j.o_frames = off; off = align16(off + 24 * T);
+  j.o_frames = off; off = align16(off + FRAMES);
   j.o_vslots = off; off = align16(off + nslot_v * 3 * T);
   j.o_eslots = off; off = align16(off + nslot_e * 12 * T);
-  j.o_prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
+  j.o_prov = off; off = align16(off + nsl * 4);
   j.o_pairs = off; off = align16(off + P * 4 * T);
   j.o_vsdist = off; off = align16(off + nslot_v * T);
   j.o_nnstat = off; off = align16(off + nslot_e * 2 * T);
   const int u0 = off;
   j.o_scores = off; off = align16(off + nscore * T);
   j.o_sorted = off; off = align16(off + nscore * 4);
+  j.o_aux = off; off = align16(off + (topk ? nsl * AUX : 0));
+  j.o_ebuf = off; off = align16(off + nsl * dmax * 4);
   const int end_topk = off;
   off = u0;
   j.o_sj = off; off = align16(off + 2 * P * SJ);
   j.o_qp = off; off = align16(off + P * QP);
+  j.o_vsrec = off; off = align16(off + nslot_v * VS);
+  j.o_prec = off; off = align16(off + P * PR);
   j.bytes = std::max(off, end_topk);
   if (j.bytes > 200 * 1024)
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
-  const int per_unit = std::max({2 * P, nslot_v, 1});  // E1 items: one per pair side
-  int upb = std::max(1, jvp_max_threads() / per_unit);
+  // E0 / E1 lanes: 5 per pair QP; 3 / W per pair side and per V-S contact; as
+  // many envs per CTA as its shared-memory budget holds (about 2 passes of lanes)
+  const int lw = 3 / jvp_lane_width();
+  const int per_unit = std::max(2 * lw * P + lw * nslot_v, 1);
+  int upb = std::max(1, (2 * jvp_max_threads() + per_unit - 1) / per_unit);
   while (upb > 1 && (size_t)upb * j.bytes > (size_t)jvp_smem_cap()) --upb;
   j.units_per_block = upb;
   if ((m.n_env + upb - 1) / upb > 0x7fffffffLL) invalid("manifold_jvp: n_env too large for one launch");

@@ -1,0 +1,897 @@
+// Forward-mode pose Jacobian of the batched contact manifold:
+// kernel template (instantiated per side-1 SDF kind in manifold_jvp_{sq,cp,gen}.cu,
+// which compile in parallel; dispatch in manifold_jvp.cu).
+//   generate_manifold<Dual12> seeded by seed_pose_tangents (dual.hpp:249-263)
+//   and mean_contact_distance (manifold.hpp:379-384), for every env.
+//
+// The reference carries 12 tangents through every scalar of the pipeline. Most
+// of its arithmetic (the sphere trace, ~73%, plus the normal sources and the
+// opposing-field values) is a function of a single 3-D body-frame point, so
+// its 12-direction tangent factors through a 3x3 Jacobian: here those stages
+// run ONCE per item in Dual<3> arithmetic seeded at the point (dual.cuh), and
+// the 12 pose directions are then pushed through the small Jacobians by
+// explicit chain-rule loops. The same holds for the witness QP, a function of
+// the 5 numbers (Q, c) (witness.hpp:74-121): Dual<5>. Everything outside those
+// bottlenecks (frames, slot payloads, pair quantities, NN softmins, activity)
+// carries the 12 tangents directly (Dual<12> records in shared memory,
+// per-direction loops in registers).
+//
+// Work mapping (one CTA owns `units_per_block` consecutive envs; items of all
+// its envs spread over the CTA's threads phase by phase, as manifold.cu):
+//   A  frames: se3_exp in Dual<6> per pose (pose.hpp:78-91)
+//   B  top-K scores: opposing field value + gradient (double), 12-direction chain
+//   C  rank sort on primals, stable on ties (smooth_ops.hpp:180-185)
+//   D  slots: soft top-K rows / pass-through, one item per (slot, direction)
+//   E  E-E pairs (QP Dual<5>, two sides' trace + normal Dual<3>, opposing
+//      value gradient) and V-S items (normal source Dual<3>); then the 12
+//      directions through the Jacobians; point / dist / normal rows out
+//   F  NN softmin statistics (argmin_s shift carries its tangent)
+//   G  activity product + its tangents
+//   H  mean contact distance + gradient (fixed order)
+// Semantics that touch tangents are the reference's: branches on primals,
+// fabs subgradient 0 at the kink (dual.hpp:236-246), soft top-K sort stable on
+// ties (libstdc++ insertion sort for D <= 16), argmin / LSE shifts carry their
+// tangents. hard_ops is rejected by the host (smooth_ops.hpp:199).
+//
+// Outputs: contacts (primal, FP32), tangents [n_env][C][8][12] FP32, mean_dist
+// and its 12 tangents.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../common.h"
+#include "launch_util.cuh"
+#include "../device/dmath.cuh"
+#include "../device/dual.cuh"
+#include "../device/sdf.cuh"
+#include "../device/witness.cuh"
+
+namespace cmgb {
+
+namespace {
+
+#ifndef CMGB_JVP_THREADS
+#define CMGB_JVP_THREADS 128
+#endif
+#ifndef CMGB_JVP_MINB
+#define CMGB_JVP_MINB 3
+#endif
+#ifndef CMGB_JVP_SMEM_KB
+#define CMGB_JVP_SMEM_KB 74
+#endif
+#ifndef CMGB_JVP_W
+#define CMGB_JVP_W 3
+#endif
+constexpr int kJvpThreads = CMGB_JVP_THREADS;
+// Tangent columns per E1 lane (Dual<W>): 3 = one lane per Jacobian, 1 = three.
+constexpr int kJvpW = CMGB_JVP_W;
+static_assert(kJvpW == 1 || kJvpW == 3, "W divides the 3 columns");
+constexpr int kJvpMinBlocks = CMGB_JVP_MINB;
+
+using D3 = Dual<3>;
+
+// Shared-memory tangent record: FP64 primal, 12 FP32 pose tangents (the
+// tangent outputs are FP32; every combination of tangents, differences
+// included, is formed in FP64 registers).
+struct T12 {
+  double v;
+  float d[12];
+};
+
+// Pose frames: primal R (row-major), t. The 12 pose directions enter as rigid
+// velocities: direction j moves body s_j = j / 6 only, with world angular
+// velocity w_j = vee(dR/dj R^T) and linear velocity v_j = dt/dj, so a point x
+// attached to that body moves by u_j(x) = w_j x (x - t_{s_j}) + v_j.
+struct Frame {
+  double R[9];
+  double t[3];
+};
+struct Vel {
+  double w[3];
+  double v[3];
+};
+
+// ---- primal / tangent views ------------------------------------------------------
+__device__ __forceinline__ double3 val3(const T12* q) { return d3(q[0].v, q[1].v, q[2].v); }
+__device__ __forceinline__ double3 tan3(const T12* q, int j) { return d3(q[0].d[j], q[1].d[j], q[2].d[j]); }
+__device__ __forceinline__ double3 fR(const Frame& F, double3 v) { return mul_R(F.R, v); }
+__device__ __forceinline__ double3 fRt(const Frame& F, double3 v) { return mul_Rt(F.R, v); }
+__device__ __forceinline__ double3 ft(const Frame& F) { return d3(F.t[0], F.t[1], F.t[2]); }
+__device__ __forceinline__ double3 cross3(double3 a, double3 b) {
+  return d3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+// M v for a row-major 3x3 held in registers / shared memory
+__device__ __forceinline__ double3 mv3(const double* M, double3 v) { return mul_R(M, v); }
+// C = A B (row-major 3x3)
+__device__ __forceinline__ void mm3(const double* A, const double* B, double* Cm) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Cm[3 * r + c] = A[3 * r] * B[c] + A[3 * r + 1] * B[3 + c] + A[3 * r + 2] * B[6 + c];
+}
+__device__ __forceinline__ void put3(T12* q, double3 v) {
+  q[0].v = v.x;
+  q[1].v = v.y;
+  q[2].v = v.z;
+}
+__device__ __forceinline__ void put3d(T12* q, double3 v, int j) {
+  q[0].d[j] = v.x;
+  q[1].d[j] = v.y;
+  q[2].d[j] = v.z;
+}
+__device__ __forceinline__ double3 dvert(const double* v, int i) {
+  return d3(__ldg(v + 3 * i), __ldg(v + 3 * i + 1), __ldg(v + 3 * i + 2));
+}
+
+// A 3-vector of Dual<3> seeded with the identity at p (d p_r / d p_c = delta).
+__device__ __forceinline__ V3<D3> seed3(double3 p) {
+  V3<D3> q;
+  q.x = D3(p.x);
+  q.y = D3(p.y);
+  q.z = D3(p.z);
+  q.x.d[0] = 1.0;
+  q.y.d[1] = 1.0;
+  q.z.d[2] = 1.0;
+  return q;
+}
+__device__ __forceinline__ double3 prim3(const V3<D3>& q) { return d3(q.x.v, q.y.v, q.z.v); }
+__device__ __forceinline__ void jac3(const V3<D3>& q, double* J) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    J[c] = q.x.d[c];
+    J[3 + c] = q.y.d[c];
+    J[6 + c] = q.z.d[c];
+  }
+}
+
+template <class T>
+__device__ __forceinline__ V3<T> normalize_smooth_t(const V3<T>& v, double tau) {
+  return dscale(v, rsqrt_d(tau + ddot(v, v)));
+}
+
+// Tangent output of one contact field: t[(row * 8 + k) * 12 + j].
+__device__ __forceinline__ void put_t(const JvpParams& p, int64_t row, int k, int j, double x) {
+  p.tangents[(row * 8 + k) * 12 + j] = (float)x;
+}
+
+// One side of an E-E pair, direction-independent part (manifold.hpp:245-256,
+// 279-280), in WORLD form: M = R_s d pb5 / d pb0 (trace), N = R_s d n_body /
+// d pb0 (own normal), the world point / normal, the opposing field's value and
+// world gradient at the point, and the own value with its body gradient
+// (containment).
+struct SideJac {
+  double M[9], N[9];
+  double3 pw, nw, gvw, gown;
+  double vo, phi_own;
+};
+
+// Witness QP of a pair as a function of (Q11, Q12, Q22, c1, c2): primal
+// alpha / gamma and their 3x5 Jacobian (witness.hpp:74-121).
+struct QpRec {
+  double a1, a2, gam;
+  double J[15];
+};
+
+// V-S contact (vs_contacts, manifold.hpp:185-204), direction-independent part:
+// world point / normal, the opposing field's value gradient and normal Jacobian
+// in its body frame (one column per lane), value and activity (+ complement).
+struct VsRec {
+  double3 pw, n, gb;  // gb: gradient of the opposing value in its body frame
+  double Jb[9];       // d n_body / d x_body
+  double v, act, cact;
+};
+
+// E-E pair quantities (manifold.hpp:248-266, 279-285), primal, FP64.
+struct PairRec {
+  double3 nbar;
+  double dg, idg, g1, g2;
+  double pen1, cpen1, pen2, cpen2, cl, ccl, ct1, cct1, ct2, cct2;
+};
+
+// Soft top-K row of a slot: the row total and first-minimum shift index; the
+// unnormalised weights e_i live in the env's FP32 weight buffer.
+struct SlotAux {
+  double tot;
+  int imin, pad;
+};
+
+static_assert(sizeof(T12) == 56 && sizeof(SideJac) == 32 * 8 && sizeof(QpRec) == 18 * 8 && sizeof(SlotAux) == 16 &&
+                  sizeof(VsRec) == 21 * 8 && sizeof(PairRec) == 17 * 8 &&
+                  sizeof(Frame) == 12 * 8 && sizeof(Vel) == 6 * 8,
+              "record sizes are mirrored by plan_jvp (host/api.cpp)");
+
+struct EnvUnit {
+  unsigned char* base;
+  const JvpParams* p;
+  int64_t env;
+  __device__ Frame& frame(int s) const { return reinterpret_cast<Frame*>(base + p->o_frames)[s]; }
+  __device__ Vel& vel(int j) const { return reinterpret_cast<Vel*>(base + p->o_frames + 2 * sizeof(Frame))[j]; }
+  // rigid velocity of direction j's body at the world point x
+  __device__ double3 uvel(int j, double3 x) const {
+    const Vel& V = vel(j);
+    return cross3(d3(V.w[0], V.w[1], V.w[2]), x - ft(frame(j / 6))) + d3(V.v[0], V.v[1], V.v[2]);
+  }
+  __device__ double3 omega(int j) const { return d3(vel(j).w[0], vel(j).w[1], vel(j).w[2]); }
+  __device__ T12* scores() const { return reinterpret_cast<T12*>(base + p->o_scores); }
+  __device__ int* order() const { return reinterpret_cast<int*>(base + p->o_sorted); }
+  __device__ float* ebuf(int slot) const { return reinterpret_cast<float*>(base + p->o_ebuf) + slot * p->ebuf_stride; }
+  __device__ SlotAux& aux(int slot) const { return reinterpret_cast<SlotAux*>(base + p->o_aux)[slot]; }
+  __device__ T12* vslot(int i) const { return reinterpret_cast<T12*>(base + p->o_vslots) + 3 * i; }
+  __device__ T12* eslot(int i) const { return reinterpret_cast<T12*>(base + p->o_eslots) + 12 * i; }
+  __device__ int* prov() const { return reinterpret_cast<int*>(base + p->o_prov); }
+  // per pair: dg, A1 = con pen1 clash cont, A2, dist1 + dist2
+  __device__ T12* pair(int i) const { return reinterpret_cast<T12*>(base + p->o_pairs) + 4 * i; }
+  __device__ SideJac& sj(int i, int s) const { return reinterpret_cast<SideJac*>(base + p->o_sj)[2 * i + s]; }
+  __device__ QpRec& qrec(int i) const { return reinterpret_cast<QpRec*>(base + p->o_qp)[i]; }
+  __device__ VsRec& vsrec(int r) const { return reinterpret_cast<VsRec*>(base + p->o_vsrec)[r]; }
+  __device__ PairRec& prec(int i) const { return reinterpret_cast<PairRec*>(base + p->o_prec)[i]; }
+  __device__ T12* vsdist() const { return reinterpret_cast<T12*>(base + p->o_vsdist); }
+  __device__ T12* nnstat() const { return reinterpret_cast<T12*>(base + p->o_nnstat); }
+};
+
+// Columns [W lane, W lane + W) of the side's Jacobians (one of the side's 3 / W
+// lanes): the trace and own normal in Dual<W> seeded at pb0 + e_c. Lane 0 also
+// writes the primal world point / normal and the opposing value and gradient.
+template <int W>
+__device__ __forceinline__ V3<Dual<W>> seed_cols(double3 x, int lane) {
+  using DW = Dual<W>;
+  V3<DW> q{DW(x.x), DW(x.y), DW(x.z)};
+#pragma unroll
+  for (int t = 0; t < W; ++t) {
+    const int col = lane * W + t;
+    (col == 0 ? q.x : col == 1 ? q.y : q.z).d[t] = 1.0;
+  }
+  return q;
+}
+
+template <int KS, int KO, int W>
+__device__ __forceinline__ void side_jac_lane(const DevSdf& own, const DevSdf& oth, const Frame& Fs, const Frame& Fo,
+                                              double3 pb0, const DevCfg& c, int lane, SideJac& r) {
+  using DW = Dual<W>;
+  V3<DW> p = seed_cols<W>(pb0, lane);
+#pragma unroll 1
+  for (int k = 0; k < c.trace_iters; ++k) {
+    const SdfOutT<DW> s = sdf_eval<kGrad, KS, DW>(own, p);
+    p = p - dscale(normalize_smooth_t<DW>(s.g, c.tau_normal), s.v);
+  }
+  const SdfOutT<DW> o = c.containment ? sdf_eval<kNormalSource, KS, DW>(own, p)
+                                      : sdf_eval<kNormalOnly, KS, DW>(own, p);
+  const V3<DW> nb = normalize_smooth_t<DW>(o.g, c.tau_normal);
+#pragma unroll
+  for (int t = 0; t < W; ++t) {
+    const int col = lane * W + t;
+    const double3 mc = fR(Fs, d3(p.x.d[t], p.y.d[t], p.z.d[t]));
+    const double3 nc = fR(Fs, d3(nb.x.d[t], nb.y.d[t], nb.z.d[t]));
+    r.M[col] = mc.x;
+    r.M[3 + col] = mc.y;
+    r.M[6 + col] = mc.z;
+    r.N[col] = nc.x;
+    r.N[3 + col] = nc.y;
+    r.N[6 + col] = nc.z;
+    (col == 0 ? r.gown.x : col == 1 ? r.gown.y : r.gown.z) = o.v.d[t];
+  }
+  if (lane == 0) {
+    r.phi_own = o.v.v;
+    r.pw = fR(Fs, d3(p.x.v, p.y.v, p.z.v)) + ft(Fs);
+    r.nw = fR(Fs, d3(nb.x.v, nb.y.v, nb.z.v));
+    const SdfOut v = sdf_eval<kGrad, KO>(oth, fRt(Fo, r.pw - ft(Fo)));
+    r.vo = v.v;
+    r.gvw = fR(Fo, v.g);
+  }
+}
+
+// Direction j of side s: world point / normal / opposing value / own value
+// tangents from the body-frame witness tangent dpb0.
+__device__ __forceinline__ void side_tan(const EnvUnit& u, const SideJac& r, int s, double3 dpb0, int j,
+                                         double3& dpw, double3& dn, double& dvo, double& dphi) {
+  dpw = mv3(r.M, dpb0);
+  dn = mv3(r.N, dpb0);
+  const double3 uj = u.uvel(j, r.pw);
+  double3 dxo;  // world displacement of the point relative to the opposing body
+  if (j / 6 == s) {
+    dpw = dpw + uj;
+    dn = dn + cross3(u.omega(j), r.nw);
+    dxo = dpw;
+  } else {
+    dxo = dpw - uj;
+  }
+  dvo = ddot(r.gvw, dxo);
+  dphi = ddot(r.gown, dpb0);
+}
+
+template <int K1, int K2>
+__global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kernel(const __grid_constant__ JvpParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int upb = p.units_per_block;
+  const int64_t u0 = (int64_t)blockIdx.x * upb;
+  const ManifoldParams& m = p.m;
+  const int n_here = (int)(m.n_env - u0 < upb ? m.n_env - u0 : upb);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const DevCfg& c = m.cfg;
+  const DevSide& S1 = m.side[0];
+  const DevSide& S2 = m.side[1];
+  const int n1 = m.n1, n2 = m.n2, m1 = m.m1, m2 = m.m2, P = m1 * m2;
+  const bool full = m1 > 0 && m2 > 0;
+  const int C = m.n_contacts;
+  auto unit = [&](int k) { return EnvUnit{smem + (size_t)k * p.bytes, &p, u0 + k}; };
+
+  // ---- A: frames, se3_exp (pose.hpp:78-91), one Dual<1> lane per pose
+  // coordinate k (seed_pose_tangents, dual.hpp:252-262); lane 0 writes R, t ----
+  for (int it = tid; it < 12 * n_here; it += nth) {
+    const EnvUnit u = unit(it / 12);
+    const int jj = it - (it / 12) * 12, s = jj / 6, k = jj - s * 6;
+    const double* pose = s == 0 ? m.poses1 + m.pose_stride1 * u.env : m.poses2 + m.pose_stride2 * u.env;
+    Dual<1> xi[6], R[9], t[3];
+#pragma unroll
+    for (int z = 0; z < 6; ++z) {
+      xi[z] = Dual<1>(__ldg(pose + z));
+      xi[z].d[0] = z == k ? 1.0 : 0.0;
+    }
+    se3_exp_d(xi, R, t);
+    if (k == 0) {
+      Frame& F = u.frame(s);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) F.R[i] = R[i].v;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) F.t[i] = t[i].v;
+    }
+    // W = dR/dk R^T is skew: w = vee(W) (antisymmetric part)
+    double dR[9], W[9], Rt[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      dR[i] = R[i].d[0];
+      Rt[i] = R[3 * (i % 3) + i / 3].v;
+    }
+    mm3(dR, Rt, W);
+    Vel& V = u.vel(jj);
+    V.w[0] = 0.5 * (W[7] - W[5]);
+    V.w[1] = 0.5 * (W[2] - W[6]);
+    V.w[2] = 0.5 * (W[3] - W[1]);
+    V.v[0] = t[0].d[0];
+    V.v[1] = t[1].d[0];
+    V.v[2] = t[2].d[0];
+  }
+  __syncthreads();
+
+  const int off1 = S1.nv, off2 = S1.nv + S2.nv, off3 = off2 + S1.ne, off4 = off3 + S2.ne;
+  const bool topk_any = S1.topk_v | S2.topk_v | S1.topk_e | S2.topk_e;
+  if (topk_any) {
+    // ---- B: vertex scores -phi_opp(vertex) (vertex_penetrations, 77-84) ----------
+    for (int it = tid; it < n_here * off2; it += nth) {
+      const int k = it / off2, i = it - k * off2;
+      const EnvUnit u = unit(k);
+      const int s = i < S1.nv ? 0 : 1;
+      const int vi = s == 0 ? i : i - S1.nv;
+      const Frame& Fs = u.frame(s);
+      const Frame& Fo = u.frame(1 - s);
+      const double3 pw = fR(Fs, dvert(s == 0 ? S1.verts : S2.verts, vi)) + ft(Fs);
+      const double3 q = fRt(Fo, pw - ft(Fo));
+      const SdfOut o = s == 0 ? sdf_eval<kGrad, K2>(S2.sdf, q) : sdf_eval<kGrad, K1>(S1.sdf, q);
+      const double3 gw = fR(Fo, o.g);
+      T12& sc = u.scores()[i];
+      sc.v = -o.v;
+      // the vertex moves with its body (j / 6 == s) or the field moves under it
+#pragma unroll 1
+      for (int j = 0; j < 12; ++j) {
+        const double d = ddot(gw, u.uvel(j, pw));
+        sc.d[j] = j / 6 == s ? -d : d;
+      }
+    }
+    __syncthreads();
+    // edge scores: -(mean of endpoint penetrations) (edge_penetrations, 86-94)
+    const int ne_all = S1.ne + S2.ne;
+    for (int it = tid; it < n_here * ne_all * 13; it += nth) {
+      const int k = it / (ne_all * 13), r = it - k * ne_all * 13;
+      const int i = r / 13, j = r - (r / 13) * 13;  // j = 12: primal
+      const EnvUnit u = unit(k);
+      const int s = i < S1.ne ? 0 : 1;
+      const int ei = s == 0 ? i : i - S1.ne;
+      const int32_t* E = s == 0 ? S1.edges : S2.edges;
+      const int voff = s == 0 ? 0 : S1.nv;
+      T12* sc = u.scores();
+      const T12& A = sc[voff + __ldg(E + 2 * ei)];
+      const T12& B = sc[voff + __ldg(E + 2 * ei + 1)];
+      if (j == 12) sc[off2 + i].v = -((-A.v + -B.v) * 0.5);
+      else sc[off2 + i].d[j] = -((-A.d[j] + -B.d[j]) * 0.5);
+    }
+    __syncthreads();
+    // ---- C: descending rank sort on primals, stable on ties -------------------
+    for (int it = tid; it < n_here * off4; it += nth) {
+      const int k = it / off4, i = it - k * off4;
+      const EnvUnit u = unit(k);
+      const int set = i < off1 ? 0 : i < off2 ? 1 : i < off3 ? 2 : 3;
+      const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
+      if (!active) continue;
+      const int lo = set == 0 ? 0 : set == 1 ? off1 : set == 2 ? off2 : off3;
+      const int hi = set == 0 ? off1 : set == 1 ? off2 : set == 2 ? off3 : off4;
+      const T12* sc = u.scores();
+      const double x = sc[i].v;
+      int rank = 0;
+      for (int j = lo; j < hi; ++j) {
+        const double y = sc[j].v;
+        rank += (y > x) || (y == x && j < i);
+      }
+      u.order()[lo + rank] = i;
+    }
+    __syncthreads();
+  }
+
+  // ---- D: selected slots (pass-through or soft top-K rows) -------------------
+  // D1 primal per slot (row weights cached), D2 one item per (slot, direction).
+  const int nsl = n1 + n2 + m1 + m2;
+  struct SlotId {
+    bool is_edge;
+    int s, r, set;
+  };
+  auto slot_id = [&](int r0) {
+    SlotId q;
+    q.is_edge = r0 >= n1 + n2;
+    q.s = q.is_edge ? (r0 - n1 - n2 < m1 ? 0 : 1) : (r0 < n1 ? 0 : 1);
+    q.r = q.is_edge ? (q.s == 0 ? r0 - n1 - n2 : r0 - n1 - n2 - m1) : (q.s == 0 ? r0 : r0 - n1);
+    q.set = (q.is_edge ? 2 : 0) + q.s;
+    return q;
+  };
+  auto set_lo = [&](int set) { return set == 0 ? 0 : set == 1 ? off1 : set == 2 ? off2 : off3; };
+  auto set_hi = [&](int set) { return set == 0 ? off1 : set == 1 ? off2 : set == 2 ? off3 : off4; };
+  auto sgn = [](double z) { return z < 0.0 ? -1.0 : (z > 0.0 ? 1.0 : 0.0); };
+  for (int it = tid; it < n_here * nsl; it += nth) {
+    const int k = it / nsl, r0 = it - k * nsl;
+    const EnvUnit u = unit(k);
+    const SlotId q = slot_id(r0);
+    const DevSide& S = q.s == 0 ? S1 : S2;
+    const bool sel = q.is_edge ? S.topk_e : S.topk_v;
+    double3 a, b = d3(0, 0, 0);
+    int prov = q.r;
+    if (!sel) {  // K == D pass-through (manifold.hpp:135-140, 158-167): constant body points
+      if (q.is_edge) {
+        a = dvert(S.verts, __ldg(S.edges + 2 * q.r));
+        b = dvert(S.verts, __ldg(S.edges + 2 * q.r + 1));
+      } else {
+        a = dvert(S.verts, q.r);
+      }
+    } else {  // soft top-K row r (smooth_ops.hpp:186-196; manifold.hpp:141-148, 168-180)
+      const int lo = set_lo(q.set), D = set_hi(q.set) - lo;
+      const T12* x = u.scores() + lo;
+      const double sr = u.scores()[u.order()[lo + q.r]].v;
+      const double inv_tau = q.is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
+      // argmin_s shift: the first minimal distance (smooth_ops.hpp:130-136)
+      int imin = 0;
+      double dmin = fabs(sr - x[0].v);
+      for (int i = 1; i < D; ++i) {
+        const double di = fabs(sr - x[i].v);
+        if (di < dmin) { dmin = di; imin = i; }
+      }
+      float* eb = u.ebuf(r0);
+      double tot = 0.0;
+      double3 Sa = d3(0, 0, 0), Sb = Sa;
+      prov = -1;
+      for (int i = 0; i < D; ++i) {
+        const double dist = fabs(sr - x[i].v);
+        if (prov < 0 && dist == 0.0) prov = i;  // first argmax (hard_attribution, 110-121)
+        const double e = exp_d((dmin - dist) * inv_tau);
+        eb[i] = (float)e;
+        tot += e;
+        if (q.is_edge) {
+          Sa = Sa + dvert(S.verts, __ldg(S.edges + 2 * i)) * e;
+          Sb = Sb + dvert(S.verts, __ldg(S.edges + 2 * i + 1)) * e;
+        } else {
+          Sa = Sa + dvert(S.verts, i) * e;
+        }
+      }
+      const double inv = rcp_d(tot);
+      a = Sa * inv;
+      b = Sb * inv;
+      u.aux(r0).tot = tot;
+      u.aux(r0).imin = imin;
+    }
+    const Frame& F = u.frame(q.s);
+    u.prov()[r0] = prov;
+    if (q.is_edge) {
+      T12* e = u.eslot(r0 - n1 - n2);
+      put3(e, fR(F, a) + ft(F));
+      put3(e + 3, fR(F, b) + ft(F));
+      put3(e + 6, a);
+      put3(e + 9, b);
+    } else {
+      put3(u.vslot(r0), fR(F, a) + ft(F));
+    }
+  }
+  __syncthreads();
+  for (int it = tid; it < n_here * nsl * 12; it += nth) {
+    const int k = it / (nsl * 12), rr = it - k * nsl * 12;
+    const int r0 = rr / 12, j = rr - (rr / 12) * 12;
+    const EnvUnit u = unit(k);
+    const SlotId q = slot_id(r0);
+    const DevSide& S = q.s == 0 ? S1 : S2;
+    const bool sel = q.is_edge ? S.topk_e : S.topk_v;
+    T12* dst = q.is_edge ? u.eslot(r0 - n1 - n2) : u.vslot(r0);
+    double3 da = d3(0, 0, 0), db = d3(0, 0, 0);
+    if (sel) {
+      // w_i = e_i / tot, d e_i = e_i u_i, u_i = (d m - d|s_r - x_i|) / tau:
+      //   d a = (sum e_i u_i v_i - (sum e_i u_i) a) / tot
+      const int lo = set_lo(q.set), D = set_hi(q.set) - lo;
+      const T12* x = u.scores() + lo;
+      const T12& sr = u.scores()[u.order()[lo + q.r]];
+      const double inv_tau = q.is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
+      const SlotAux ax = u.aux(r0);
+      const double srd = sr.d[j];
+      const double dm = sgn(sr.v - x[ax.imin].v) * (srd - x[ax.imin].d[j]);
+      const float* eb = u.ebuf(r0);
+      double T = 0.0;
+      double3 Sua = d3(0, 0, 0), Sub = Sua;
+      for (int i = 0; i < D; ++i) {
+        const double eu = (double)eb[i] * (dm - sgn(sr.v - x[i].v) * (srd - x[i].d[j])) * inv_tau;
+        T += eu;
+        if (q.is_edge) {
+          Sua = Sua + dvert(S.verts, __ldg(S.edges + 2 * i)) * eu;
+          Sub = Sub + dvert(S.verts, __ldg(S.edges + 2 * i + 1)) * eu;
+        } else {
+          Sua = Sua + dvert(S.verts, i) * eu;
+        }
+      }
+      const double inv = rcp_d(ax.tot);
+      const double3 a = q.is_edge ? val3(dst + 6) : fRt(u.frame(q.s), val3(dst) - ft(u.frame(q.s)));
+      da = (Sua - a * T) * inv;
+      if (q.is_edge) db = (Sub - val3(dst + 9) * T) * inv;
+    }
+    const Frame& F = u.frame(q.s);
+    const bool moves = j / 6 == q.s;
+    const double3 aw = val3(dst);
+    put3d(dst, fR(F, da) + (moves ? u.uvel(j, aw) : d3(0, 0, 0)), j);
+    if (q.is_edge) {
+      const double3 bw = val3(dst + 3);
+      put3d(dst + 3, fR(F, db) + (moves ? u.uvel(j, bw) : d3(0, 0, 0)), j);
+      put3d(dst + 6, da, j);
+      put3d(dst + 9, db, j);
+    }
+  }
+  __syncthreads();
+
+  // ---- E0: witness QP Jacobian in (Q11, Q12, Q22, c1, c2) (witness.hpp:74-158),
+  // one Dual<1> lane per input; lane 0 writes the primal alpha / gamma ---------
+  const int NP = full ? n_here * P : 0;
+  const int nvs = n1 + n2, NV = n_here * nvs;
+  constexpr int LW = 3 / kJvpW;  // lanes per 3-column Jacobian
+  for (int it = tid; it < 5 * NP; it += nth) {
+    const int pi = it / 5, lane = it - pi * 5;
+    const int ku = pi / P, i = pi - ku * P;
+    const EnvUnit u = unit(ku);
+    const int k = i / m2, l = i - (i / m2) * m2;
+    const T12* s1 = u.eslot(k);
+    const T12* s2 = u.eslot(m1 + l);
+    const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+    Dual<1> in[5] = {Dual<1>(ddot(t1, t1) + c.lambda), Dual<1>(ddot(t1, t2n)), Dual<1>(ddot(t2n, t2n) + c.lambda),
+                     Dual<1>(ddot(bv, t1) - 0.5 * c.lambda), Dual<1>(ddot(bv, t2n) - 0.5 * c.lambda)};
+#pragma unroll
+    for (int z = 0; z < 5; ++z) in[z].d[0] = z == lane ? 1.0 : 0.0;
+    const QpSolT<Dual<1>> w = solve_box_qp_2<Dual<1>>(in[0], in[1], in[2], in[3], in[4], c);
+    QpRec& qr = u.qrec(i);
+    qr.J[lane] = w.a1.d[0];
+    qr.J[5 + lane] = w.a2.d[0];
+    qr.J[10 + lane] = w.gamma.d[0];
+    if (lane == 0) {
+      qr.a1 = w.a1.v;
+      qr.a2 = w.a2.v;
+      qr.gam = w.gamma.v;
+    }
+  }
+  __syncthreads();
+
+  // ---- E1: trace / own-normal Jacobians per pair side and opposing normal-source
+  // Jacobians per V-S contact, Dual<W> lanes (3 / W per 3-column Jacobian).
+  // Side-major order keeps warps on one SDF kind; every lane recomputes its
+  // primal (bit-identical) and lane 0 writes it.
+  for (int it = tid; it < 2 * LW * NP + LW * NV; it += nth) {
+    if (it < 2 * LW * NP) {
+      const int s = it >= LW * NP ? 1 : 0;
+      const int q = it - s * LW * NP;
+      const int pi = q / LW, lane = q - pi * LW;
+      const int ku = pi / P, i = pi - ku * P;
+      const EnvUnit u = unit(ku);
+      const int k = i / m2, l = i - (i / m2) * m2;
+      const QpRec& qr = u.qrec(i);
+      // edge_point (witness.hpp:130-133) on the body-frame endpoints of this side
+      const T12* se = s == 0 ? u.eslot(k) : u.eslot(m1 + l);
+      const double3 pb0 = val3(se + 6) + (val3(se + 9) - val3(se + 6)) * (s == 0 ? qr.a1 : qr.a2);
+      if constexpr (K1 == K2) {
+        side_jac_lane<K1, K1, kJvpW>(m.side[s].sdf, m.side[1 - s].sdf, u.frame(s), u.frame(1 - s), pb0, c, lane,
+                                     u.sj(i, s));
+      } else {
+        if (s == 0) side_jac_lane<K1, K2, kJvpW>(S1.sdf, S2.sdf, u.frame(0), u.frame(1), pb0, c, lane, u.sj(i, 0));
+        else side_jac_lane<K2, K1, kJvpW>(S2.sdf, S1.sdf, u.frame(1), u.frame(0), pb0, c, lane, u.sj(i, 1));
+      }
+    } else {
+      const int q = it - 2 * LW * NP;
+      const int vi = q / LW, lane = q - vi * LW;
+      const int k = vi / nvs, r = vi - k * nvs;
+      const EnvUnit u = unit(k);
+      const int o = r < n1 ? 1 : 0;  // the opposing body
+      const Frame& Fo = u.frame(o);
+      const double3 pw = val3(u.vslot(r));
+      // vs_contacts (manifold.hpp:185-204): normal source of the opposing field
+      // in its body point
+      using DW = Dual<kJvpW>;
+      const V3<DW> xd = seed_cols<kJvpW>(fRt(Fo, pw - ft(Fo)), lane);
+      const SdfOutT<DW> sv = o == 1 ? sdf_eval<kNormalSource, K2, DW>(S2.sdf, xd)
+                                    : sdf_eval<kNormalSource, K1, DW>(S1.sdf, xd);
+      const V3<DW> nbd = normalize_smooth_t<DW>(sv.g, c.tau_normal);
+      VsRec& vr = u.vsrec(r);
+#pragma unroll
+      for (int t = 0; t < kJvpW; ++t) {
+        const int col = lane * kJvpW + t;
+        vr.Jb[col] = nbd.x.d[t];
+        vr.Jb[3 + col] = nbd.y.d[t];
+        vr.Jb[6 + col] = nbd.z.d[t];
+        (col == 0 ? vr.gb.x : col == 1 ? vr.gb.y : vr.gb.z) = sv.v.d[t];
+      }
+      if (lane == 0) {
+        vr.pw = pw;
+        vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
+        vr.v = sv.v.v;
+        sigmoid_pair_d(-sv.v.v * c.inv_tau_pen, &vr.act, &vr.cact);
+        const int64_t row = u.env * C + r;
+        float* dst = m.contacts + row * 8;
+        dst[0] = (float)pw.x; dst[1] = (float)pw.y; dst[2] = (float)pw.z; dst[3] = (float)sv.v.v;
+        dst[4] = (float)vr.n.x; dst[5] = (float)vr.n.y; dst[6] = (float)vr.n.z; dst[7] = (float)vr.act;
+        if (m.src) {
+          m.src[row * 2] = u.prov()[r];
+          m.src[row * 2 + 1] = -1;
+        }
+        u.vsdist()[r].v = sv.v.v;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- E1b: E-E pair quantities, primal (manifold.hpp:248-266, 279-285) ----------
+  for (int it = tid; it < NP; it += nth) {
+    const int ku = it / P, i = it - ku * P;
+    const EnvUnit u = unit(ku);
+    const int k = i / m2, l = i - (i / m2) * m2;
+    const SideJac& r1 = u.sj(i, 0);
+    const SideJac& r2 = u.sj(i, 1);
+    PairRec& pr = u.prec(i);
+    const double3 de = r1.pw - r2.pw;
+    pr.dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
+    pr.idg = rcp_d(pr.dg);
+    pr.nbar = de * pr.idg;
+    pr.g1 = tanh(ddot(r2.nw, pr.nbar) * c.inv_tau_sign);
+    pr.g2 = tanh(ddot(r1.nw, pr.nbar) * c.inv_tau_sign);
+    sigmoid_pair_d(-r1.vo * c.inv_tau_pen, &pr.pen1, &pr.cpen1);
+    sigmoid_pair_d(-r2.vo * c.inv_tau_pen, &pr.pen2, &pr.cpen2);
+    sigmoid_pair_d(-ddot(r1.nw, r2.nw) * c.inv_tau_clash, &pr.cl, &pr.ccl);
+    pr.ct1 = pr.ct2 = 1.0;
+    pr.cct1 = pr.cct2 = 0.0;
+    if (c.containment) {
+      sigmoid_pair_d(-r1.phi_own * c.inv_tau_cont, &pr.ct1, &pr.cct1);
+      sigmoid_pair_d(-r2.phi_own * c.inv_tau_cont, &pr.ct2, &pr.cct2);
+    }
+    const double base = u.qrec(i).gam * pr.cl * (pr.ct1 * pr.ct2);
+    const int64_t row = u.env * C + n1 + n2 + 2 * i;
+    float* dst = m.contacts + row * 8;
+    const double3 o1 = pr.nbar * pr.g1, o2 = pr.nbar * pr.g2;
+    dst[0] = (float)r1.pw.x; dst[1] = (float)r1.pw.y; dst[2] = (float)r1.pw.z; dst[3] = (float)(pr.g1 * pr.dg);
+    dst[4] = (float)o1.x; dst[5] = (float)o1.y; dst[6] = (float)o1.z;
+    dst[8] = (float)r2.pw.x; dst[9] = (float)r2.pw.y; dst[10] = (float)r2.pw.z; dst[11] = (float)(pr.g2 * pr.dg);
+    dst[12] = (float)o2.x; dst[13] = (float)o2.y; dst[14] = (float)o2.z;
+    if (m.src) {
+      int* sp = m.src + row * 2;
+      const int sa = u.prov()[n1 + n2 + k], sb = u.prov()[n1 + n2 + m1 + l];
+      sp[0] = sa; sp[1] = sb; sp[2] = sa; sp[3] = sb;
+    }
+    T12* rec = u.pair(i);
+    rec[0].v = pr.dg;
+    rec[1].v = base * pr.pen1;
+    rec[2].v = base * pr.pen2;
+    rec[3].v = pr.g1 * pr.dg + pr.g2 * pr.dg;
+  }
+  __syncthreads();
+
+  // ---- E2: tangents, one item per (V-S contact | pair, direction); the
+  // direction is the fastest index so a warp's tangent stores are contiguous ----
+  for (int it = tid; it < 12 * (NV + NP); it += nth) {
+    const int item = it / 12, j = it - item * 12;
+    if (item < NV) {
+      const int k = item / nvs, r = item - k * nvs;
+      const EnvUnit u = unit(k);
+      const int o = r < n1 ? 1 : 0;
+      const VsRec& vr = u.vsrec(r);
+      const Frame& Fo = u.frame(o);
+      const double3 dpw = tan3(u.vslot(r), j);
+      const bool om = j / 6 == o;  // the field moves under the point
+      const double3 dxb = fRt(Fo, om ? dpw - u.uvel(j, vr.pw) : dpw);  // body-frame displacement
+      const double dv = ddot(vr.gb, dxb);
+      double3 dn = fR(Fo, mv3(vr.Jb, dxb));
+      if (om) dn = dn + cross3(u.omega(j), vr.n);
+      u.vsdist()[r].d[j] = dv;
+      const int64_t row = u.env * C + r;
+      put_t(p, row, 0, j, dpw.x);
+      put_t(p, row, 1, j, dpw.y);
+      put_t(p, row, 2, j, dpw.z);
+      put_t(p, row, 3, j, dv);
+      put_t(p, row, 4, j, dn.x);
+      put_t(p, row, 5, j, dn.y);
+      put_t(p, row, 6, j, dn.z);
+      put_t(p, row, 7, j, -vr.act * vr.cact * c.inv_tau_pen * dv);
+      continue;
+    }
+    const int pi = item - NV;
+    const int ku = pi / P, i = pi - ku * P;
+    const EnvUnit u = unit(ku);
+    const int k = i / m2, l = i - (i / m2) * m2;
+    const T12* s1 = u.eslot(k);
+    const T12* s2 = u.eslot(m1 + l);
+    const QpRec& qr = u.qrec(i);
+    const PairRec& pr = u.prec(i);
+    const SideJac& r1 = u.sj(i, 0);
+    const SideJac& r2 = u.sj(i, 1);
+    // QP inputs -> alpha, gamma tangents
+    const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+    const double3 dt1 = tan3(s1 + 3, j) - tan3(s1, j), dt2n = tan3(s2, j) - tan3(s2 + 3, j);
+    const double3 dbv = tan3(s1, j) - tan3(s2, j);
+    const double dq[5] = {2.0 * ddot(t1, dt1), ddot(dt1, t2n) + ddot(t1, dt2n), 2.0 * ddot(t2n, dt2n),
+                          ddot(dbv, t1) + ddot(bv, dt1), ddot(dbv, t2n) + ddot(bv, dt2n)};
+    double da1 = 0.0, da2 = 0.0, dgam = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      da1 = fma(qr.J[q], dq[q], da1);
+      da2 = fma(qr.J[5 + q], dq[q], da2);
+      dgam = fma(qr.J[10 + q], dq[q], dgam);
+    }
+    const double3 e1 = val3(s1 + 9) - val3(s1 + 6), e2 = val3(s2 + 9) - val3(s2 + 6);
+    const double3 dpb1 = tan3(s1 + 6, j) + (tan3(s1 + 9, j) - tan3(s1 + 6, j)) * qr.a1 + e1 * da1;
+    const double3 dpb2 = tan3(s2 + 6, j) + (tan3(s2 + 9, j) - tan3(s2 + 6, j)) * qr.a2 + e2 * da2;
+    double3 dp1, dn1, dp2, dn2;
+    double dvo1, dph1, dvo2, dph2;
+    side_tan(u, r1, 0, dpb1, j, dp1, dn1, dvo1, dph1);
+    side_tan(u, r2, 1, dpb2, j, dp2, dn2, dvo2, dph2);
+    const double3 nbar = pr.nbar;
+    const double dg = pr.dg, g1 = pr.g1, g2 = pr.g2, gam = qr.gam;
+    const double3 dde = dp1 - dp2;
+    const double ddg = ddot(nbar, dde);
+    const double3 dnbar = (dde - nbar * ddg) * pr.idg;
+    const double dg1 = (1.0 - g1 * g1) * c.inv_tau_sign * (ddot(dn2, nbar) + ddot(r2.nw, dnbar));
+    const double dg2 = (1.0 - g2 * g2) * c.inv_tau_sign * (ddot(dn1, nbar) + ddot(r1.nw, dnbar));
+    const double dpen1 = -pr.pen1 * pr.cpen1 * c.inv_tau_pen * dvo1;
+    const double dpen2 = -pr.pen2 * pr.cpen2 * c.inv_tau_pen * dvo2;
+    const double dcl = -pr.cl * pr.ccl * c.inv_tau_clash * (ddot(dn1, r2.nw) + ddot(r1.nw, dn2));
+    const double cont = pr.ct1 * pr.ct2;
+    const double dcont =
+        c.containment ? -c.inv_tau_cont * (pr.ct1 * pr.cct1 * dph1 * pr.ct2 + pr.ct1 * pr.ct2 * pr.cct2 * dph2) : 0.0;
+    const double base = gam * pr.cl * cont;
+    const double dbase = (dgam * pr.cl + gam * dcl) * cont + gam * pr.cl * dcont;
+    const double dd1 = dg1 * dg + g1 * ddg, dd2 = dg2 * dg + g2 * ddg;
+    T12* rec = u.pair(i);
+    rec[0].d[j] = ddg;
+    rec[1].d[j] = dbase * pr.pen1 + base * dpen1;
+    rec[2].d[j] = dbase * pr.pen2 + base * dpen2;
+    rec[3].d[j] = dd1 + dd2;
+    const double3 dm1 = nbar * dg1 + dnbar * g1, dm2 = nbar * dg2 + dnbar * g2;
+    const int64_t row = u.env * C + n1 + n2 + 2 * i;
+    put_t(p, row, 0, j, dp1.x);
+    put_t(p, row, 1, j, dp1.y);
+    put_t(p, row, 2, j, dp1.z);
+    put_t(p, row, 3, j, dd1);
+    put_t(p, row, 4, j, dm1.x);
+    put_t(p, row, 5, j, dm1.y);
+    put_t(p, row, 6, j, dm1.z);
+    put_t(p, row + 1, 0, j, dp2.x);
+    put_t(p, row + 1, 1, j, dp2.y);
+    put_t(p, row + 1, 2, j, dp2.z);
+    put_t(p, row + 1, 3, j, dd2);
+    put_t(p, row + 1, 4, j, dm2.x);
+    put_t(p, row + 1, 5, j, dm2.y);
+    put_t(p, row + 1, 6, j, dm2.z);
+  }
+  __syncthreads();
+
+  if (full) {
+    // ---- F: NN softmin statistics, shift = first minimum (argmin_s 126-144) ----
+    const int nrc = m1 + m2;
+    for (int it = tid; it < n_here * nrc * 13; it += nth) {
+      const int ku = it / (nrc * 13), rr = it - ku * nrc * 13;
+      const int r = rr / 13, j = rr - (rr / 13) * 13;  // j = 12: primal
+      const EnvUnit u = unit(ku);
+      const bool row = r < m1;
+      const int n = row ? m2 : m1;
+      auto dgv = [&](int q) -> const T12& { return u.pair(row ? r * m2 + q : q * m2 + (r - m1))[0]; };
+      int jm = 0;
+      for (int q = 1; q < n; ++q)
+        if (dgv(q).v < dgv(jm).v) jm = q;
+      const double mn = dgv(jm).v;
+      const double dmn = j < 12 ? dgv(jm).d[j] : 0.0;
+      double tot = 0.0, dtot = 0.0;
+      for (int q = 0; q < n; ++q) {
+        const T12& x = dgv(q);
+        const double e = exp_d((mn - x.v) * c.inv_tau_nn);
+        tot += e;
+        if (j < 12) dtot = fma(e, (dmn - x.d[j]) * c.inv_tau_nn, dtot);
+      }
+      const double inv = rcp_d(tot);
+      T12* ns = u.nnstat() + 2 * r;
+      if (j == 12) {
+        ns[0].v = mn;
+        ns[1].v = inv;
+      } else {
+        ns[0].d[j] = dmn;
+        ns[1].d[j] = -inv * inv * dtot;
+      }
+    }
+    __syncthreads();
+    // ---- G: activity = con pen_b nn_b clash cont (manifold.hpp:303-330) -------
+    for (int it = tid; it < 12 * NP; it += nth) {
+      const int pi = it / 12, j = it - pi * 12;
+      const int ku = pi / P, i = pi - ku * P;
+      const EnvUnit u = unit(ku);
+      const int k = i / m2, l = i - (i / m2) * m2;
+      const T12* rec = u.pair(i);
+      const T12* na = u.nnstat() + 2 * k;
+      const T12* nb = u.nnstat() + 2 * (m1 + l);
+      const double dg = rec[0].v;
+      const double e1 = exp_d((na[0].v - dg) * c.inv_tau_nn), e2 = exp_d((nb[0].v - dg) * c.inv_tau_nn);
+      const double nn1 = e1 * na[1].v, nn2 = e2 * nb[1].v;
+      const int64_t row = u.env * C + n1 + n2 + 2 * i;
+      if (j == 0) {
+        m.contacts[row * 8 + 7] = (float)(rec[1].v * nn1);
+        m.contacts[row * 8 + 15] = (float)(rec[2].v * nn2);
+      }
+      const double dnn1 = fma(e1 * (na[0].d[j] - rec[0].d[j]) * c.inv_tau_nn, na[1].v, e1 * na[1].d[j]);
+      const double dnn2 = fma(e2 * (nb[0].d[j] - rec[0].d[j]) * c.inv_tau_nn, nb[1].v, e2 * nb[1].d[j]);
+      put_t(p, row, 7, j, rec[1].d[j] * nn1 + rec[1].v * dnn1);
+      put_t(p, row + 1, 7, j, rec[2].d[j] * nn2 + rec[2].v * dnn2);
+    }
+  }
+  __syncthreads();
+
+  // ---- H: mean contact distance (manifold.hpp:379-384), fixed order ---------
+  if (m.mean_dist || p.mean_grad || p.mean_f64 || p.mean_grad_f64) {
+    for (int it = tid; it < n_here * 13; it += nth) {
+      const int k = it / 13, j = it - k * 13;  // j = 12: primal
+      const EnvUnit u = unit(k);
+      double acc = 0.0;
+      for (int r = 0; r < n1 + n2; ++r) acc += j < 12 ? u.vsdist()[r].d[j] : u.vsdist()[r].v;
+      for (int i = 0; i < P && full; ++i) acc += j < 12 ? u.pair(i)[3].d[j] : u.pair(i)[3].v;
+      const double mean = acc * (1.0 / (double)C);
+      if (j == 12) {
+        if (m.mean_dist) m.mean_dist[u.env] = (float)mean;
+        if (p.mean_f64) p.mean_f64[u.env] = mean;
+      } else {
+        if (p.mean_grad) p.mean_grad[u.env * 12 + j] = (float)mean;
+        if (p.mean_grad_f64) p.mean_grad_f64[u.env * 12 + j] = mean;
+      }
+    }
+  }
+}
+
+template <int K1, int K2>
+int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
+  static PerDeviceOnce configured;
+  configured([] {  // per device: the attribute does not carry across devices
+    cudaFuncSetAttribute(manifold_jvp_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  const int64_t grid = (p.m.n_env + p.units_per_block - 1) / p.units_per_block;
+  manifold_jvp_kernel<K1, K2><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// Specialised kinds for the benchmark bodies (eps = 0.1 superquadric, box_planes
+// leaf); every other program runs through the generic interpreter (same leaf
+// code): three kinds per side keep the library small.
+constexpr int jvp_kind(int k) { return k == kSqE01 || k == kBoxCp ? k : kGeneric; }
+
+template <int K1>
+int launch_jvp_k2(const JvpParams& p, int threads, cudaStream_t s) {
+  switch (jvp_kind(p.m.side[1].sdf.kind)) {
+    case kSqE01: return launch_jvp_kind<K1, kSqE01>(p, threads, s);
+    case kBoxCp: return launch_jvp_kind<K1, kBoxCp>(p, threads, s);
+    default: return launch_jvp_kind<K1, kGeneric>(p, threads, s);
+  }
+}
+
+}  // namespace
+
+int launch_jvp_k1_sq(const JvpParams& p, int threads, cudaStream_t s);
+int launch_jvp_k1_cp(const JvpParams& p, int threads, cudaStream_t s);
+int launch_jvp_k1_gen(const JvpParams& p, int threads, cudaStream_t s);
+
+}  // namespace cmgb

@@ -1,0 +1,6 @@
+// manifold_jvp_kernel instantiations with side 1 = kSqE01 (manifold_jvp.cuh).
+#include "manifold_jvp.cuh"
+
+namespace cmgb {
+int launch_jvp_k1_sq(const JvpParams& p, int threads, cudaStream_t s) { return launch_jvp_k2<kSqE01>(p, threads, s); }
+}  // namespace cmgb

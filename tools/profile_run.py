@@ -1,4 +1,4 @@
-"""One warm launch of a kernel for ncu capture (python tools/profile_run.py manifold|ee|vf [n])."""
+"""One warm launch of a kernel for ncu capture (python tools/profile_run.py manifold|mixed:<bucket>|drop|drop-fwd|ee|vf [n])."""
 import os, sys
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -17,6 +17,14 @@ if kind.startswith("mixed:"):
     out = {}
     for _ in range(3):
         api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out)
+elif kind in ("drop", "drop-fwd"):
+    sc = W.drop_scene(n)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    P = torch.as_tensor(sc.poses(n), device="cuda")
+    fn = api.generate_manifold_scene_jvp_batch if kind == "drop" else api.generate_manifold_scene_batch
+    outs = None
+    for _ in range(2):
+        outs = fn(bodies, P, SmoothingConfig(), is_static=sc.is_static(), outs=outs)
 elif kind == "manifold":
     ws = W.box_box(n)
     s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
