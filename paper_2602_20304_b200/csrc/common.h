@@ -223,7 +223,6 @@ int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
 int jvp_directions();    // tangent directions per thread of the compiled JVP kernel
 int jvp_max_threads();   // CTA size of the JVP kernel
 int jvp_smem_cap();      // shared-memory bytes per JVP CTA the host may plan for
-int jvp_lane_width();    // tangent columns per E1 lane of the JVP kernel (Dual<W>)
 int launch_ee_witness(const WitnessParams& p, void* stream);
 int launch_ee_witness_f64(const WitnessParams& p, void* stream);
 int launch_penalty(const PenaltyArgs& a, void* stream);

@@ -739,10 +739,9 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   j.bytes = std::max(off, end_topk);
   if (j.bytes > 200 * 1024)
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
-  // E0 / E1 lanes: 5 per pair QP; 3 / W per pair side and per V-S contact; as
-  // many envs per CTA as its shared-memory budget holds (about 2 passes of lanes)
-  const int lw = 3 / jvp_lane_width();
-  const int per_unit = std::max(2 * lw * P + lw * nslot_v, 1);
+  // E1 items: 2 sides + 1 QP per pair, 1 per V-S contact; as many envs per CTA
+  // as its shared-memory budget holds (about 2 passes of items)
+  const int per_unit = std::max(3 * P + nslot_v, 1);
   int upb = std::max(1, (2 * jvp_max_threads() + per_unit - 1) / per_unit);
   while (upb > 1 && (size_t)upb * j.bytes > (size_t)jvp_smem_cap()) --upb;
   j.units_per_block = upb;

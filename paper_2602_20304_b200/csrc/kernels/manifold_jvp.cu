@@ -7,7 +7,6 @@ namespace cmgb {
 int jvp_directions() { return 12; }
 int jvp_max_threads() { return kJvpThreads; }
 int jvp_smem_cap() { return CMGB_JVP_SMEM_KB * 1024; }
-int jvp_lane_width() { return kJvpW; }
 
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);

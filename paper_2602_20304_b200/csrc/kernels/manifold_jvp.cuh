@@ -59,13 +59,8 @@ namespace {
 #ifndef CMGB_JVP_SMEM_KB
 #define CMGB_JVP_SMEM_KB 74
 #endif
-#ifndef CMGB_JVP_W
-#define CMGB_JVP_W 3
-#endif
 constexpr int kJvpThreads = CMGB_JVP_THREADS;
-// Tangent columns per E1 lane (Dual<W>): 3 = one lane per Jacobian, 1 = three.
-constexpr int kJvpW = CMGB_JVP_W;
-static_assert(kJvpW == 1 || kJvpW == 3, "W divides the 3 columns");
+constexpr int kJvpW = 3;  // tangent columns per E1 Jacobian item (Dual<3>)
 constexpr int kJvpMinBlocks = CMGB_JVP_MINB;
 
 using D3 = Dual<3>;
@@ -547,62 +542,61 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
   }
   __syncthreads();
 
-  // ---- E0: witness QP Jacobian in (Q11, Q12, Q22, c1, c2) (witness.hpp:74-158),
-  // one Dual<1> lane per input; lane 0 writes the primal alpha / gamma ---------
+  // ---- E1: direction-independent Jacobians, one item per
+  //   pair side: trace + own normal in Dual<3> (its primal alpha from the
+  //     double QP, bit-identical to the QP item's primal),
+  //   pair: witness QP in Dual<5> over (Q11, Q12, Q22, c1, c2) (witness.hpp:74-158),
+  //   V-S contact: opposing normal source in Dual<3>.
+  // Kind-major order keeps every warp on one code path and SDF kind.
   const int NP = full ? n_here * P : 0;
   const int nvs = n1 + n2, NV = n_here * nvs;
-  constexpr int LW = 3 / kJvpW;  // lanes per 3-column Jacobian
-  for (int it = tid; it < 5 * NP; it += nth) {
-    const int pi = it / 5, lane = it - pi * 5;
-    const int ku = pi / P, i = pi - ku * P;
-    const EnvUnit u = unit(ku);
-    const int k = i / m2, l = i - (i / m2) * m2;
-    const T12* s1 = u.eslot(k);
-    const T12* s2 = u.eslot(m1 + l);
-    const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
-    Dual<1> in[5] = {Dual<1>(ddot(t1, t1) + c.lambda), Dual<1>(ddot(t1, t2n)), Dual<1>(ddot(t2n, t2n) + c.lambda),
-                     Dual<1>(ddot(bv, t1) - 0.5 * c.lambda), Dual<1>(ddot(bv, t2n) - 0.5 * c.lambda)};
-#pragma unroll
-    for (int z = 0; z < 5; ++z) in[z].d[0] = z == lane ? 1.0 : 0.0;
-    const QpSolT<Dual<1>> w = solve_box_qp_2<Dual<1>>(in[0], in[1], in[2], in[3], in[4], c);
-    QpRec& qr = u.qrec(i);
-    qr.J[lane] = w.a1.d[0];
-    qr.J[5 + lane] = w.a2.d[0];
-    qr.J[10 + lane] = w.gamma.d[0];
-    if (lane == 0) {
-      qr.a1 = w.a1.v;
-      qr.a2 = w.a2.v;
-      qr.gam = w.gamma.v;
-    }
-  }
-  __syncthreads();
-
-  // ---- E1: trace / own-normal Jacobians per pair side and opposing normal-source
-  // Jacobians per V-S contact, Dual<W> lanes (3 / W per 3-column Jacobian).
-  // Side-major order keeps warps on one SDF kind; every lane recomputes its
-  // primal (bit-identical) and lane 0 writes it.
-  for (int it = tid; it < 2 * LW * NP + LW * NV; it += nth) {
-    if (it < 2 * LW * NP) {
-      const int s = it >= LW * NP ? 1 : 0;
-      const int q = it - s * LW * NP;
-      const int pi = q / LW, lane = q - pi * LW;
+  for (int it = tid; it < 3 * NP + NV; it += nth) {
+    if (it < 2 * NP) {
+      const int s = it >= NP ? 1 : 0;
+      const int pi = it - s * NP;
       const int ku = pi / P, i = pi - ku * P;
       const EnvUnit u = unit(ku);
       const int k = i / m2, l = i - (i / m2) * m2;
-      const QpRec& qr = u.qrec(i);
+      const T12* s1 = u.eslot(k);
+      const T12* s2 = u.eslot(m1 + l);
+      // ee_witness (witness.hpp:137-158) on the world edges: primal alpha
+      const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+      const QpSol w = solve_box_qp_2<double>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
+                                             ddot(bv, t1) - 0.5 * c.lambda, ddot(bv, t2n) - 0.5 * c.lambda, c);
       // edge_point (witness.hpp:130-133) on the body-frame endpoints of this side
-      const T12* se = s == 0 ? u.eslot(k) : u.eslot(m1 + l);
-      const double3 pb0 = val3(se + 6) + (val3(se + 9) - val3(se + 6)) * (s == 0 ? qr.a1 : qr.a2);
+      const T12* se = s == 0 ? s1 : s2;
+      const double3 pb0 = val3(se + 6) + (val3(se + 9) - val3(se + 6)) * (s == 0 ? w.a1 : w.a2);
       if constexpr (K1 == K2) {
-        side_jac_lane<K1, K1, kJvpW>(m.side[s].sdf, m.side[1 - s].sdf, u.frame(s), u.frame(1 - s), pb0, c, lane,
-                                     u.sj(i, s));
+        side_jac_lane<K1, K1, 3>(m.side[s].sdf, m.side[1 - s].sdf, u.frame(s), u.frame(1 - s), pb0, c, 0, u.sj(i, s));
       } else {
-        if (s == 0) side_jac_lane<K1, K2, kJvpW>(S1.sdf, S2.sdf, u.frame(0), u.frame(1), pb0, c, lane, u.sj(i, 0));
-        else side_jac_lane<K2, K1, kJvpW>(S2.sdf, S1.sdf, u.frame(1), u.frame(0), pb0, c, lane, u.sj(i, 1));
+        if (s == 0) side_jac_lane<K1, K2, 3>(S1.sdf, S2.sdf, u.frame(0), u.frame(1), pb0, c, 0, u.sj(i, 0));
+        else side_jac_lane<K2, K1, 3>(S2.sdf, S1.sdf, u.frame(1), u.frame(0), pb0, c, 0, u.sj(i, 1));
+      }
+    } else if (it < 3 * NP) {
+      const int pi = it - 2 * NP;
+      const int ku = pi / P, i = pi - ku * P;
+      const EnvUnit u = unit(ku);
+      const int k = i / m2, l = i - (i / m2) * m2;
+      const T12* s1 = u.eslot(k);
+      const T12* s2 = u.eslot(m1 + l);
+      const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+      Dual<5> in[5] = {Dual<5>(ddot(t1, t1) + c.lambda), Dual<5>(ddot(t1, t2n)), Dual<5>(ddot(t2n, t2n) + c.lambda),
+                       Dual<5>(ddot(bv, t1) - 0.5 * c.lambda), Dual<5>(ddot(bv, t2n) - 0.5 * c.lambda)};
+#pragma unroll
+      for (int z = 0; z < 5; ++z) in[z].d[z] = 1.0;
+      const QpSolT<Dual<5>> w = solve_box_qp_2<Dual<5>>(in[0], in[1], in[2], in[3], in[4], c);
+      QpRec& qr = u.qrec(i);
+      qr.a1 = w.a1.v;
+      qr.a2 = w.a2.v;
+      qr.gam = w.gamma.v;
+#pragma unroll
+      for (int z = 0; z < 5; ++z) {
+        qr.J[z] = w.a1.d[z];
+        qr.J[5 + z] = w.a2.d[z];
+        qr.J[10 + z] = w.gamma.d[z];
       }
     } else {
-      const int q = it - 2 * LW * NP;
-      const int vi = q / LW, lane = q - vi * LW;
+      const int vi = it - 3 * NP;
       const int k = vi / nvs, r = vi - k * nvs;
       const EnvUnit u = unit(k);
       const int o = r < n1 ? 1 : 0;  // the opposing body
@@ -610,35 +604,32 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       const double3 pw = val3(u.vslot(r));
       // vs_contacts (manifold.hpp:185-204): normal source of the opposing field
       // in its body point
-      using DW = Dual<kJvpW>;
-      const V3<DW> xd = seed_cols<kJvpW>(fRt(Fo, pw - ft(Fo)), lane);
+      using DW = Dual<3>;
+      const V3<DW> xd = seed_cols<3>(fRt(Fo, pw - ft(Fo)), 0);
       const SdfOutT<DW> sv = o == 1 ? sdf_eval<kNormalSource, K2, DW>(S2.sdf, xd)
                                     : sdf_eval<kNormalSource, K1, DW>(S1.sdf, xd);
       const V3<DW> nbd = normalize_smooth_t<DW>(sv.g, c.tau_normal);
       VsRec& vr = u.vsrec(r);
 #pragma unroll
-      for (int t = 0; t < kJvpW; ++t) {
-        const int col = lane * kJvpW + t;
-        vr.Jb[col] = nbd.x.d[t];
-        vr.Jb[3 + col] = nbd.y.d[t];
-        vr.Jb[6 + col] = nbd.z.d[t];
-        (col == 0 ? vr.gb.x : col == 1 ? vr.gb.y : vr.gb.z) = sv.v.d[t];
+      for (int t = 0; t < 3; ++t) {
+        vr.Jb[t] = nbd.x.d[t];
+        vr.Jb[3 + t] = nbd.y.d[t];
+        vr.Jb[6 + t] = nbd.z.d[t];
       }
-      if (lane == 0) {
-        vr.pw = pw;
-        vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
-        vr.v = sv.v.v;
-        sigmoid_pair_d(-sv.v.v * c.inv_tau_pen, &vr.act, &vr.cact);
-        const int64_t row = u.env * C + r;
-        float* dst = m.contacts + row * 8;
-        dst[0] = (float)pw.x; dst[1] = (float)pw.y; dst[2] = (float)pw.z; dst[3] = (float)sv.v.v;
-        dst[4] = (float)vr.n.x; dst[5] = (float)vr.n.y; dst[6] = (float)vr.n.z; dst[7] = (float)vr.act;
-        if (m.src) {
-          m.src[row * 2] = u.prov()[r];
-          m.src[row * 2 + 1] = -1;
-        }
-        u.vsdist()[r].v = sv.v.v;
+      vr.gb = d3(sv.v.d[0], sv.v.d[1], sv.v.d[2]);
+      vr.pw = pw;
+      vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
+      vr.v = sv.v.v;
+      sigmoid_pair_d(-sv.v.v * c.inv_tau_pen, &vr.act, &vr.cact);
+      const int64_t row = u.env * C + r;
+      float* dst = m.contacts + row * 8;
+      dst[0] = (float)pw.x; dst[1] = (float)pw.y; dst[2] = (float)pw.z; dst[3] = (float)sv.v.v;
+      dst[4] = (float)vr.n.x; dst[5] = (float)vr.n.y; dst[6] = (float)vr.n.z; dst[7] = (float)vr.act;
+      if (m.src) {
+        m.src[row * 2] = u.prov()[r];
+        m.src[row * 2 + 1] = -1;
       }
+      u.vsdist()[r].v = sv.v.v;
     }
   }
   __syncthreads();
