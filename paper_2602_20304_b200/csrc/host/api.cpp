@@ -15,7 +15,7 @@
 #include "host.h"
 
 namespace cmgb {
-int manifold_max_threads();
+int manifold_max_threads(int k1, int k2);
 }
 
 using namespace cmgb;
@@ -231,14 +231,17 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
       throw Error(CMGB_ERR_UNSUPPORTED, "manifold: per-env working set exceeds shared memory");
   }
 
-  // Envs per block: ~288 items of E-E work per 288-thread CTA (2 box-box envs),
-  // shared memory capped so 3 CTAs fit per SM.
-  const int maxt = manifold_max_threads();
+  // Envs per block: about one CTA's worth of E-E pairs (2 box-box envs per
+  // 320-thread CTA), shared memory capped so the kernel's resident-CTA target fits.
+  // the global-record path runs the generic instantiation (manifold.cu)
+  const int k1 = plan.pairs_global ? (int)kGeneric : p.side[0].sdf.kind;
+  const int k2 = plan.pairs_global ? (int)kGeneric : p.side[1].sdf.kind;
+  const int maxt = manifold_max_threads(k1, k2);
   const int per_env = std::max({P, nslot_v, 1});
   int epb = std::max(1, maxt / per_env);
   // shared memory per CTA such that the kernel's resident-CTA target fits the SM
   const size_t smem_cap =
-      (size_t)(216 * 1024) / manifold_min_blocks(p.side[0].sdf.kind, p.side[1].sdf.kind);
+      (size_t)(216 * 1024) / manifold_min_blocks(k1, k2);
   while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
   const int threads = maxt;
   p.envs_per_block = epb;

@@ -30,12 +30,15 @@ namespace cmgb {
 
 namespace {
 
-// 9 warps per CTA (2 box-box envs x 144 E-E pairs); 3 CTAs per SM (<= 75 regs).
-constexpr int kMaxThreads = 288;
-// Resident CTAs per SM: 4 (<= 56 registers) for the compile-time eps = 0.1
-// box-box kernel, whose E-E work dominates (measured +2% over 3); 3 (<= 72
-// registers) elsewhere, where the top-K / interpreter phases spill at 56.
-__host__ __device__ constexpr int min_blocks(int k1, int k2) { return k1 == kSqE01 && k2 == kSqE01 ? 4 : 3; }
+// CTA shape per SDF kind pair (measured):
+//   eps = 0.1 box-box: 9 warps (2 envs x 144 E-E pairs), 4 CTAs/SM (<= 56
+//     registers), V-S contacts on the warps the NN phase leaves idle (F);
+//   everything else: 10 warps, 3 CTAs/SM (<= 64 registers), V-S contacts in
+//     the pair phase (E) after the pair items (config D forward +4%).
+__host__ __device__ constexpr bool box_box(int k1, int k2) { return k1 == kSqE01 && k2 == kSqE01; }
+__host__ __device__ constexpr int max_threads(int k1, int k2) { return box_box(k1, k2) ? 288 : 320; }
+__host__ __device__ constexpr int min_blocks(int k1, int k2) { return box_box(k1, k2) ? 4 : 3; }
+__host__ __device__ constexpr bool vs_in_pair_phase(int k1, int k2) { return !box_box(k1, k2); }
 
 // Pair record (doubles; kPairRec = 38 floats = 19 doubles = 152 B), rewritten
 // in place by the E-E sub-phases:
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ 
 // kGP: pair records in the global workspace (p.pairs_gmem; large pass-through
 // pair sets, one generic instantiation) instead of shared memory.
 template <int K1, int K2, bool kGP = false>
-__global__ void __launch_bounds__(kMaxThreads, min_blocks(K1, K2))
+__global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int epb = p.envs_per_block;
@@ -416,38 +419,62 @@ __global__ void __launch_bounds__(kMaxThreads, min_blocks(K1, K2))
   }
   __syncthreads();
 
-  // ---- E: E-E pair stage --------------------------------------------------
+  // ---- E: E-E pair stage + V-S contacts --------------------------------------
+  // E1-E3 per pair, one thread owning the pair end to end (no barriers in
+  // between; state passes through the pair's shared-memory record so each
+  // stage's registers are released): QP -> trace/normal/opposing value of
+  // side 1 and side 2 -> pair quantities. On the 10-warp CTA shape the V-S
+  // contacts (vs_contacts, manifold.hpp:185-204; they read only phase-D state)
+  // follow the pair items, beside them.
   const int C = p.n_contacts;
-  if (full) {
-    // E1-E3 per pair, one thread owning the pair end to end (no barriers in
-    // between; state passes through the pair's shared-memory record so each
-    // stage's registers are released): QP -> trace/normal/opposing value of
-    // side 1 and side 2 -> pair quantities.
-    for (int it = tid; it < n_here * P; it += nth) {
-      int e, i, k, l;
-      fdivmod(it, p.div_pairs, e, i);
-      fdivmod(i, p.div_m2, k, l);
-      const EnvView ev = env(e);
-      double* r = ev.pair(i);
-      ee_stage_qp(p, ev, k, l, r);
-      if constexpr (K1 == K2) {  // one code copy for both sides (I-cache)
+  const int nvs = n1 + n2;
+  constexpr bool kVsE = vs_in_pair_phase(K1, K2);
+  auto pair_item = [&](int it) {
+    int e, i, k, l;
+    fdivmod(it, p.div_pairs, e, i);
+    fdivmod(i, p.div_m2, k, l);
+    const EnvView ev = env(e);
+    double* r = ev.pair(i);
+    ee_stage_qp(p, ev, k, l, r);
+    if constexpr (K1 == K2) {  // one code copy for both sides (I-cache)
 #pragma unroll 1
-        for (int s = 0; s < 2; ++s) ee_stage_side<K1, K1>(p, ev, s, r + 8 * s);
-      } else {
-        ee_stage_side<K1, K2>(p, ev, 0, r);
-        ee_stage_side<K2, K1>(p, ev, 1, r + 8);
+      for (int s = 0; s < 2; ++s) ee_stage_side<K1, K1>(p, ev, s, r + 8 * s);
+    } else {
+      ee_stage_side<K1, K2>(p, ev, 0, r);
+      ee_stage_side<K2, K1>(p, ev, 1, r + 8);
+    }
+    ee_stage_pair(c, r);
+  };
+  if constexpr (!kVsE) {
+    if (full)
+      for (int it = tid; it < n_here * P; it += nth) pair_item(it);
+  } else {
+    const int nE = full ? n_here * P : 0;
+    for (int it = tid; it < nE + n_here * nvs; it += nth) {
+      if (it < nE) {
+        pair_item(it);
+        continue;
       }
-      ee_stage_pair(c, r);
+      int e, r;
+      fdivmod(it - nE, p.div_nvs, e, r);
+      const EnvView ev = env(e);
+      const double* q = ev.vslot(r);
+      float* dst = p.contacts + ((env0 + e) * C + r) * 8;
+      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      if (p.src) {
+        int* sp = p.src + ((env0 + e) * C + r) * 2;
+        sp[0] = ev.prov()[r];
+        sp[1] = -1;
+      }
     }
   }
   __syncthreads();
 
   {
     // ---- F: NN softmin statistics: rows (side 1) and columns (side 2) -------
-    // and, on the warps the NN items leave idle, the V-S contacts (vs_contacts,
-    // manifold.hpp:185-204; they read only phase-D state). Dense warps: a V-S
-    // item is ~1/6 of a pair, and spreading a few over every warp of phase E
-    // cost each warp a pass at 3-4 active lanes.
+    // and, on the 9-warp shape, the V-S contacts on the warps the NN items
+    // leave idle (dense warps: a V-S item is ~1/6 of a pair).
     const int nrc = m1 + m2;
     const int nF = full ? n_here * nrc : 0;
     for (int it = tid; it < nF; it += nth) {
@@ -469,20 +496,21 @@ __global__ void __launch_bounds__(kMaxThreads, min_blocks(K1, K2))
       ev.nnstat()[2 * r] = m;
       ev.nnstat()[2 * r + 1] = 1.0 / tot;
     }
-    const int nvs = n1 + n2;
-    const int vs0 = ((nF + 31) & ~31) % nth;  // first thread of the first warp after the NN items
-    for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < n_here * nvs; it += nth) {
-      int e, r;
-      fdivmod(it, p.div_nvs, e, r);
-      const EnvView ev = env(e);
-      const double* q = ev.vslot(r);
-      float* dst = p.contacts + ((env0 + e) * C + r) * 8;
-      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      if (p.src) {
-        int* sp = p.src + ((env0 + e) * C + r) * 2;
-        sp[0] = ev.prov()[r];
-        sp[1] = -1;
+    if constexpr (!kVsE) {
+      const int vs0 = ((nF + 31) & ~31) % nth;  // first thread of the first warp after the NN items
+      for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < n_here * nvs; it += nth) {
+        int e, r;
+        fdivmod(it, p.div_nvs, e, r);
+        const EnvView ev = env(e);
+        const double* q = ev.vslot(r);
+        float* dst = p.contacts + ((env0 + e) * C + r) * 8;
+        if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+        else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+        if (p.src) {
+          int* sp = p.src + ((env0 + e) * C + r) * 2;
+          sp[0] = ev.prov()[r];
+          sp[1] = -1;
+        }
       }
     }
   }
@@ -601,7 +629,7 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
   }
 }
 
-int manifold_max_threads() { return kMaxThreads; }
+int manifold_max_threads(int k1, int k2) { return max_threads(k1, k2); }
 int manifold_min_blocks(int k1, int k2) { return min_blocks(k1, k2); }
 
 }  // namespace cmgb
