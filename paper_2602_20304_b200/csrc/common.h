@@ -147,7 +147,8 @@ struct JvpParams {
   int32_t o_frames, o_scores, o_sorted, o_vslots, o_eslots, o_prov, o_pairs, o_vsdist, o_nnstat;
   int32_t o_sj, o_qp;  // per-pair side Jacobian / witness QP records (E1 -> E2)
   int32_t o_ebuf, o_aux, ebuf_stride;
-  int32_t o_vsrec, o_prec;  // V-S / E-E pair primal records (E1 -> E2)  // soft top-K row weights (FP32, stride per slot) / row totals
+  int32_t o_vsrec, o_prec;  // V-S / E-E pair primal records (E1 -> E2)
+  int32_t geom_bytes;       // per CTA after the envs: both meshes' vertices + edge endpoints (FP64)  // soft top-K row weights (FP32, stride per slot) / row totals
   int32_t bytes;  // per unit
 };
 

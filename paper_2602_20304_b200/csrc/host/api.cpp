@@ -709,7 +709,7 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   j.groups = 1;
   const ManifoldParams& m = j.m;
   const int T = 8 + 12 * 4;                  // bytes per tangent record
-  const int SJ = 32 * 8, QP = 18 * 8, AUX = 16, VS = 21 * 8, PR = 17 * 8;  // manifold_jvp.cu records
+  const int SJ = 32 * 8, QP = 18 * 8, AUX = 16, VS = 18 * 8, PR = 17 * 8;  // manifold_jvp.cu records
   const int FRAMES = 2 * 12 * 8 + 12 * 6 * 8;  // 2 x Frame + 12 x Vel
   const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2, nsl = nslot_v + nslot_e;
   const bool topk = m.side[0].topk_v || m.side[1].topk_v || m.side[0].topk_e || m.side[1].topk_e;
@@ -723,7 +723,7 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   int off = 0;
   j.o_frames = off; off = align16(off + FRAMES);
   j.o_vslots = off; off = align16(off + nslot_v * 3 * T);
-  j.o_eslots = off; off = align16(off + nslot_e * 12 * T);
+  j.o_eslots = off; off = align16(off + nslot_e * (48 + 6 * T));  // ESlot
   j.o_prov = off; off = align16(off + nsl * 4);
   j.o_pairs = off; off = align16(off + P * 4 * T);
   j.o_vsdist = off; off = align16(off + nslot_v * T);
@@ -745,8 +745,11 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   // E1 items: 2 sides + 1 QP per pair, 1 per V-S contact; as many envs per CTA
   // as its shared-memory budget holds (about 2 passes of items)
   const int per_unit = std::max(3 * P + nslot_v, 1);
+  j.geom_bytes = align16(8 * (3 * (m.side[0].nv + m.side[1].nv) + 6 * (m.side[0].ne + m.side[1].ne)));
+  if (j.bytes + j.geom_bytes > 200 * 1024)
+    throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
   int upb = std::max(1, (2 * jvp_max_threads() + per_unit - 1) / per_unit);
-  while (upb > 1 && (size_t)upb * j.bytes > (size_t)jvp_smem_cap()) --upb;
+  while (upb > 1 && (size_t)upb * j.bytes + j.geom_bytes > (size_t)jvp_smem_cap()) --upb;
   j.units_per_block = upb;
   if ((m.n_env + upb - 1) / upb > 0x7fffffffLL) invalid("manifold_jvp: n_env too large for one launch");
   return j;

@@ -19,3 +19,10 @@ int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream) {
 }
 
 }  // namespace cmgb
+
+#ifdef CMGB_PHASE_CLOCKS
+extern "C" int cmgb_debug_jvp_phase_clocks(unsigned long long* out) {
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  return cmgb::jvp_phase_clocks_sq(out) | cmgb::jvp_phase_clocks_cp(out) | cmgb::jvp_phase_clocks_gen(out);
+}
+#endif

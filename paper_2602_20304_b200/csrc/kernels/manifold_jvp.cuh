@@ -54,16 +54,35 @@ namespace {
 #define CMGB_JVP_THREADS 128
 #endif
 #ifndef CMGB_JVP_MINB
-#define CMGB_JVP_MINB 3
+#define CMGB_JVP_MINB 4
 #endif
 #ifndef CMGB_JVP_SMEM_KB
-#define CMGB_JVP_SMEM_KB 74
+#define CMGB_JVP_SMEM_KB 56
 #endif
 constexpr int kJvpThreads = CMGB_JVP_THREADS;
 constexpr int kJvpW = 3;  // tangent columns per E1 Jacobian item (Dual<3>)
 constexpr int kJvpMinBlocks = CMGB_JVP_MINB;
 
 using D3 = Dual<3>;
+
+// Developer instrumentation (-DCMGB_PHASE_CLOCKS): SM clocks per phase, summed
+// over CTAs by thread 0 at each barrier (tools/phase_clocks.py).
+#ifdef CMGB_PHASE_CLOCKS
+__device__ unsigned long long g_jvp_phase[16];
+#define JVP_PHASE_START() long long t_prev_ = clock64()
+#define JVP_PHASE_MARK(k)                                                              \
+  do {                                                                                 \
+    __syncthreads();                                                                   \
+    if (threadIdx.x == 0) {                                                            \
+      const long long t_ = clock64();                                                  \
+      atomicAdd(&g_jvp_phase[k], (unsigned long long)(t_ - t_prev_));                  \
+      t_prev_ = t_;                                                                    \
+    }                                                                                  \
+  } while (0)
+#else
+#define JVP_PHASE_START() (void)0
+#define JVP_PHASE_MARK(k) __syncthreads()
+#endif
 
 // Shared-memory tangent record: FP64 primal, 12 FP32 pose tangents (the
 // tangent outputs are FP32; every combination of tangents, differences
@@ -113,9 +132,6 @@ __device__ __forceinline__ void put3d(T12* q, double3 v, int j) {
   q[0].d[j] = v.x;
   q[1].d[j] = v.y;
   q[2].d[j] = v.z;
-}
-__device__ __forceinline__ double3 dvert(const double* v, int i) {
-  return d3(__ldg(v + 3 * i), __ldg(v + 3 * i + 1), __ldg(v + 3 * i + 2));
 }
 
 // A 3-vector of Dual<3> seeded with the identity at p (d p_r / d p_c = delta).
@@ -167,11 +183,20 @@ struct QpRec {
   double J[15];
 };
 
+// Selected edge slot: world endpoints (primal; their tangents follow from the
+// body ones and the frame) and body-frame endpoints with tangents (non-zero
+// only under soft top-K).
+struct ESlot {
+  double aw[3], bw[3];
+  T12 a[3], b[3];
+};
+__device__ __forceinline__ double3 dv3(const double* q) { return d3(q[0], q[1], q[2]); }
+
 // V-S contact (vs_contacts, manifold.hpp:185-204), direction-independent part:
 // world point / normal, the opposing field's value gradient and normal Jacobian
 // in its body frame (one column per lane), value and activity (+ complement).
 struct VsRec {
-  double3 pw, n, gb;  // gb: gradient of the opposing value in its body frame
+  double3 n, gb;  // gb: gradient of the opposing value in its body frame
   double Jb[9];       // d n_body / d x_body
   double v, act, cact;
 };
@@ -191,7 +216,7 @@ struct SlotAux {
 };
 
 static_assert(sizeof(T12) == 56 && sizeof(SideJac) == 32 * 8 && sizeof(QpRec) == 18 * 8 && sizeof(SlotAux) == 16 &&
-                  sizeof(VsRec) == 21 * 8 && sizeof(PairRec) == 17 * 8 &&
+                  sizeof(VsRec) == 18 * 8 && sizeof(ESlot) == 384 && sizeof(PairRec) == 17 * 8 &&
                   sizeof(Frame) == 12 * 8 && sizeof(Vel) == 6 * 8,
               "record sizes are mirrored by plan_jvp (host/api.cpp)");
 
@@ -212,7 +237,7 @@ struct EnvUnit {
   __device__ float* ebuf(int slot) const { return reinterpret_cast<float*>(base + p->o_ebuf) + slot * p->ebuf_stride; }
   __device__ SlotAux& aux(int slot) const { return reinterpret_cast<SlotAux*>(base + p->o_aux)[slot]; }
   __device__ T12* vslot(int i) const { return reinterpret_cast<T12*>(base + p->o_vslots) + 3 * i; }
-  __device__ T12* eslot(int i) const { return reinterpret_cast<T12*>(base + p->o_eslots) + 12 * i; }
+  __device__ ESlot& eslot(int i) const { return reinterpret_cast<ESlot*>(base + p->o_eslots)[i]; }
   __device__ int* prov() const { return reinterpret_cast<int*>(base + p->o_prov); }
   // per pair: dg, A1 = con pen1 clash cont, A2, dist1 + dist2
   __device__ T12* pair(int i) const { return reinterpret_cast<T12*>(base + p->o_pairs) + 4 * i; }
@@ -302,6 +327,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
   const ManifoldParams& m = p.m;
   const int n_here = (int)(m.n_env - u0 < upb ? m.n_env - u0 : upb);
   const int tid = threadIdx.x, nth = blockDim.x;
+  JVP_PHASE_START();
   const DevCfg& c = m.cfg;
   const DevSide& S1 = m.side[0];
   const DevSide& S2 = m.side[1];
@@ -309,6 +335,29 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
   const bool full = m1 > 0 && m2 > 0;
   const int C = m.n_contacts;
   auto unit = [&](int k) { return EnvUnit{smem + (size_t)k * p.bytes, &p, u0 + k}; };
+
+  // Mesh geometry of both sides, staged once per CTA (every env shares it):
+  // vertices [nv][3] and edge endpoints [ne][6] (the soft top-K rows walk them).
+  double* gV[2];
+  double* gE[2];
+  gV[0] = reinterpret_cast<double*>(smem + (size_t)upb * p.bytes);
+  gV[1] = gV[0] + 3 * S1.nv;
+  gE[0] = gV[1] + 3 * S2.nv;
+  gE[1] = gE[0] + 6 * S1.ne;
+  for (int i = tid; i < 3 * (S1.nv + S2.nv); i += nth)
+    gV[0][i] = i < 3 * S1.nv ? __ldg(S1.verts + i) : __ldg(S2.verts + i - 3 * S1.nv);
+  for (int i = tid; i < 6 * (S1.ne + S2.ne); i += nth) {
+    const int s = i < 6 * S1.ne ? 0 : 1;
+    const int q = s == 0 ? i : i - 6 * S1.ne;
+    const int e = q / 6, c6 = q - e * 6;
+    const DevSide& S = s == 0 ? S1 : S2;
+    gE[s][q] = __ldg(S.verts + 3 * __ldg(S.edges + 2 * e + c6 / 3) + c6 % 3);
+  }
+  auto vtx = [&](int s, int i) { return d3(gV[s][3 * i], gV[s][3 * i + 1], gV[s][3 * i + 2]); };
+  auto eend = [&](int s, int i, int end) {
+    const double* q = gE[s] + 6 * i + 3 * end;
+    return d3(q[0], q[1], q[2]);
+  };
 
   // ---- A: frames, se3_exp (pose.hpp:78-91), one Dual<1> lane per pose
   // coordinate k (seed_pose_tangents, dual.hpp:252-262); lane 0 writes R, t ----
@@ -346,7 +395,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     V.v[1] = t[1].d[0];
     V.v[2] = t[2].d[0];
   }
-  __syncthreads();
+  JVP_PHASE_MARK(0);
 
   const int off1 = S1.nv, off2 = S1.nv + S2.nv, off3 = off2 + S1.ne, off4 = off3 + S2.ne;
   const bool topk_any = S1.topk_v | S2.topk_v | S1.topk_e | S2.topk_e;
@@ -359,7 +408,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       const int vi = s == 0 ? i : i - S1.nv;
       const Frame& Fs = u.frame(s);
       const Frame& Fo = u.frame(1 - s);
-      const double3 pw = fR(Fs, dvert(s == 0 ? S1.verts : S2.verts, vi)) + ft(Fs);
+      const double3 pw = fR(Fs, vtx(s, vi)) + ft(Fs);
       const double3 q = fRt(Fo, pw - ft(Fo));
       const SdfOut o = s == 0 ? sdf_eval<kGrad, K2>(S2.sdf, q) : sdf_eval<kGrad, K1>(S1.sdf, q);
       const double3 gw = fR(Fo, o.g);
@@ -372,7 +421,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
         sc.d[j] = j / 6 == s ? -d : d;
       }
     }
-    __syncthreads();
+    JVP_PHASE_MARK(1);
     // edge scores: -(mean of endpoint penetrations) (edge_penetrations, 86-94)
     const int ne_all = S1.ne + S2.ne;
     for (int it = tid; it < n_here * ne_all * 13; it += nth) {
@@ -389,7 +438,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       if (j == 12) sc[off2 + i].v = -((-A.v + -B.v) * 0.5);
       else sc[off2 + i].d[j] = -((-A.d[j] + -B.d[j]) * 0.5);
     }
-    __syncthreads();
+    JVP_PHASE_MARK(2);
     // ---- C: descending rank sort on primals, stable on ties -------------------
     for (int it = tid; it < n_here * off4; it += nth) {
       const int k = it / off4, i = it - k * off4;
@@ -408,7 +457,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       }
       u.order()[lo + rank] = i;
     }
-    __syncthreads();
+    JVP_PHASE_MARK(3);
   }
 
   // ---- D: selected slots (pass-through or soft top-K rows) -------------------
@@ -439,10 +488,10 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     int prov = q.r;
     if (!sel) {  // K == D pass-through (manifold.hpp:135-140, 158-167): constant body points
       if (q.is_edge) {
-        a = dvert(S.verts, __ldg(S.edges + 2 * q.r));
-        b = dvert(S.verts, __ldg(S.edges + 2 * q.r + 1));
+        a = eend(q.s, q.r, 0);
+        b = eend(q.s, q.r, 1);
       } else {
-        a = dvert(S.verts, q.r);
+        a = vtx(q.s, q.r);
       }
     } else {  // soft top-K row r (smooth_ops.hpp:186-196; manifold.hpp:141-148, 168-180)
       const int lo = set_lo(q.set), D = set_hi(q.set) - lo;
@@ -467,10 +516,10 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
         eb[i] = (float)e;
         tot += e;
         if (q.is_edge) {
-          Sa = Sa + dvert(S.verts, __ldg(S.edges + 2 * i)) * e;
-          Sb = Sb + dvert(S.verts, __ldg(S.edges + 2 * i + 1)) * e;
+          Sa = Sa + eend(q.s, i, 0) * e;
+          Sb = Sb + eend(q.s, i, 1) * e;
         } else {
-          Sa = Sa + dvert(S.verts, i) * e;
+          Sa = Sa + vtx(q.s, i) * e;
         }
       }
       const double inv = rcp_d(tot);
@@ -482,16 +531,17 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     const Frame& F = u.frame(q.s);
     u.prov()[r0] = prov;
     if (q.is_edge) {
-      T12* e = u.eslot(r0 - n1 - n2);
-      put3(e, fR(F, a) + ft(F));
-      put3(e + 3, fR(F, b) + ft(F));
-      put3(e + 6, a);
-      put3(e + 9, b);
+      ESlot& e = u.eslot(r0 - n1 - n2);
+      const double3 aw = fR(F, a) + ft(F), bw = fR(F, b) + ft(F);
+      e.aw[0] = aw.x; e.aw[1] = aw.y; e.aw[2] = aw.z;
+      e.bw[0] = bw.x; e.bw[1] = bw.y; e.bw[2] = bw.z;
+      put3(e.a, a);
+      put3(e.b, b);
     } else {
       put3(u.vslot(r0), fR(F, a) + ft(F));
     }
   }
-  __syncthreads();
+  JVP_PHASE_MARK(4);
   for (int it = tid; it < n_here * nsl * 12; it += nth) {
     const int k = it / (nsl * 12), rr = it - k * nsl * 12;
     const int r0 = rr / 12, j = rr - (rr / 12) * 12;
@@ -499,7 +549,8 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     const SlotId q = slot_id(r0);
     const DevSide& S = q.s == 0 ? S1 : S2;
     const bool sel = q.is_edge ? S.topk_e : S.topk_v;
-    T12* dst = q.is_edge ? u.eslot(r0 - n1 - n2) : u.vslot(r0);
+    ESlot* es = q.is_edge ? &u.eslot(r0 - n1 - n2) : nullptr;
+    T12* vs = q.is_edge ? nullptr : u.vslot(r0);
     double3 da = d3(0, 0, 0), db = d3(0, 0, 0);
     if (sel) {
       // w_i = e_i / tot, d e_i = e_i u_i, u_i = (d m - d|s_r - x_i|) / tau:
@@ -518,29 +569,26 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
         const double eu = (double)eb[i] * (dm - sgn(sr.v - x[i].v) * (srd - x[i].d[j])) * inv_tau;
         T += eu;
         if (q.is_edge) {
-          Sua = Sua + dvert(S.verts, __ldg(S.edges + 2 * i)) * eu;
-          Sub = Sub + dvert(S.verts, __ldg(S.edges + 2 * i + 1)) * eu;
+          Sua = Sua + eend(q.s, i, 0) * eu;
+          Sub = Sub + eend(q.s, i, 1) * eu;
         } else {
-          Sua = Sua + dvert(S.verts, i) * eu;
+          Sua = Sua + vtx(q.s, i) * eu;
         }
       }
       const double inv = rcp_d(ax.tot);
-      const double3 a = q.is_edge ? val3(dst + 6) : fRt(u.frame(q.s), val3(dst) - ft(u.frame(q.s)));
+      const double3 a = q.is_edge ? val3(es->a) : fRt(u.frame(q.s), val3(vs) - ft(u.frame(q.s)));
       da = (Sua - a * T) * inv;
-      if (q.is_edge) db = (Sub - val3(dst + 9) * T) * inv;
+      if (q.is_edge) db = (Sub - val3(es->b) * T) * inv;
     }
-    const Frame& F = u.frame(q.s);
-    const bool moves = j / 6 == q.s;
-    const double3 aw = val3(dst);
-    put3d(dst, fR(F, da) + (moves ? u.uvel(j, aw) : d3(0, 0, 0)), j);
     if (q.is_edge) {
-      const double3 bw = val3(dst + 3);
-      put3d(dst + 3, fR(F, db) + (moves ? u.uvel(j, bw) : d3(0, 0, 0)), j);
-      put3d(dst + 6, da, j);
-      put3d(dst + 9, db, j);
+      put3d(es->a, da, j);
+      put3d(es->b, db, j);
+    } else {
+      const double3 aw = val3(vs);
+      put3d(vs, fR(u.frame(q.s), da) + (j / 6 == q.s ? u.uvel(j, aw) : d3(0, 0, 0)), j);
     }
   }
-  __syncthreads();
+  JVP_PHASE_MARK(5);
 
   // ---- E1: direction-independent Jacobians, one item per
   //   pair side: trace + own normal in Dual<3> (its primal alpha from the
@@ -557,15 +605,15 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       const int ku = pi / P, i = pi - ku * P;
       const EnvUnit u = unit(ku);
       const int k = i / m2, l = i - (i / m2) * m2;
-      const T12* s1 = u.eslot(k);
-      const T12* s2 = u.eslot(m1 + l);
+      const ESlot& s1 = u.eslot(k);
+      const ESlot& s2 = u.eslot(m1 + l);
       // ee_witness (witness.hpp:137-158) on the world edges: primal alpha
-      const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+      const double3 t1 = dv3(s1.bw) - dv3(s1.aw), t2n = dv3(s2.aw) - dv3(s2.bw), bv = dv3(s1.aw) - dv3(s2.aw);
       const QpSol w = solve_box_qp_2<double>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
                                              ddot(bv, t1) - 0.5 * c.lambda, ddot(bv, t2n) - 0.5 * c.lambda, c);
       // edge_point (witness.hpp:130-133) on the body-frame endpoints of this side
-      const T12* se = s == 0 ? s1 : s2;
-      const double3 pb0 = val3(se + 6) + (val3(se + 9) - val3(se + 6)) * (s == 0 ? w.a1 : w.a2);
+      const ESlot& se = s == 0 ? s1 : s2;
+      const double3 pb0 = val3(se.a) + (val3(se.b) - val3(se.a)) * (s == 0 ? w.a1 : w.a2);
       if constexpr (K1 == K2) {
         side_jac_lane<K1, K1, 3>(m.side[s].sdf, m.side[1 - s].sdf, u.frame(s), u.frame(1 - s), pb0, c, 0, u.sj(i, s));
       } else {
@@ -577,9 +625,9 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       const int ku = pi / P, i = pi - ku * P;
       const EnvUnit u = unit(ku);
       const int k = i / m2, l = i - (i / m2) * m2;
-      const T12* s1 = u.eslot(k);
-      const T12* s2 = u.eslot(m1 + l);
-      const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
+      const ESlot& s1 = u.eslot(k);
+      const ESlot& s2 = u.eslot(m1 + l);
+      const double3 t1 = dv3(s1.bw) - dv3(s1.aw), t2n = dv3(s2.aw) - dv3(s2.bw), bv = dv3(s1.aw) - dv3(s2.aw);
       Dual<5> in[5] = {Dual<5>(ddot(t1, t1) + c.lambda), Dual<5>(ddot(t1, t2n)), Dual<5>(ddot(t2n, t2n) + c.lambda),
                        Dual<5>(ddot(bv, t1) - 0.5 * c.lambda), Dual<5>(ddot(bv, t2n) - 0.5 * c.lambda)};
 #pragma unroll
@@ -617,7 +665,6 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
         vr.Jb[6 + t] = nbd.z.d[t];
       }
       vr.gb = d3(sv.v.d[0], sv.v.d[1], sv.v.d[2]);
-      vr.pw = pw;
       vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
       vr.v = sv.v.v;
       sigmoid_pair_d(-sv.v.v * c.inv_tau_pen, &vr.act, &vr.cact);
@@ -632,10 +679,36 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       u.vsdist()[r].v = sv.v.v;
     }
   }
-  __syncthreads();
+  JVP_PHASE_MARK(6);
 
-  // ---- E1b: E-E pair quantities, primal (manifold.hpp:248-266, 279-285) ----------
-  for (int it = tid; it < NP; it += nth) {
+  // ---- E1b: E-E pair quantities, primal (manifold.hpp:248-266, 279-285), and
+  // beside them the V-S tangents, one item per (contact, direction) ----------
+  for (int it = tid; it < NP + 12 * NV; it += nth) {
+    if (it >= NP) {
+      const int item = (it - NP) / 12, j = (it - NP) - item * 12;
+      const int k = item / nvs, r = item - k * nvs;
+      const EnvUnit u = unit(k);
+      const int o = r < n1 ? 1 : 0;
+      const VsRec& vr = u.vsrec(r);
+      const Frame& Fo = u.frame(o);
+      const double3 dpw = tan3(u.vslot(r), j);
+      const bool om = j / 6 == o;  // the field moves under the point
+      const double3 dxb = fRt(Fo, om ? dpw - u.uvel(j, val3(u.vslot(r))) : dpw);  // body-frame displacement
+      const double dv = ddot(vr.gb, dxb);
+      double3 dn = fR(Fo, mv3(vr.Jb, dxb));
+      if (om) dn = dn + cross3(u.omega(j), vr.n);
+      u.vsdist()[r].d[j] = dv;
+      const int64_t row = u.env * C + r;
+      put_t(p, row, 0, j, dpw.x);
+      put_t(p, row, 1, j, dpw.y);
+      put_t(p, row, 2, j, dpw.z);
+      put_t(p, row, 3, j, dv);
+      put_t(p, row, 4, j, dn.x);
+      put_t(p, row, 5, j, dn.y);
+      put_t(p, row, 6, j, dn.z);
+      put_t(p, row, 7, j, -vr.act * vr.cact * c.inv_tau_pen * dv);
+      continue;
+    }
     const int ku = it / P, i = it - ku * P;
     const EnvUnit u = unit(ku);
     const int k = i / m2, l = i - (i / m2) * m2;
@@ -676,62 +749,49 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     rec[2].v = base * pr.pen2;
     rec[3].v = pr.g1 * pr.dg + pr.g2 * pr.dg;
   }
-  __syncthreads();
+  JVP_PHASE_MARK(7);
 
-  // ---- E2: tangents, one item per (V-S contact | pair, direction); the
-  // direction is the fastest index so a warp's tangent stores are contiguous ----
-  for (int it = tid; it < 12 * (NV + NP); it += nth) {
+  // ---- E2: E-E tangents, one item per (pair, direction); the direction is the
+  // fastest index so a warp's tangent stores are contiguous -------------------
+  for (int it = tid; it < 12 * NP; it += nth) {
     const int item = it / 12, j = it - item * 12;
-    if (item < NV) {
-      const int k = item / nvs, r = item - k * nvs;
-      const EnvUnit u = unit(k);
-      const int o = r < n1 ? 1 : 0;
-      const VsRec& vr = u.vsrec(r);
-      const Frame& Fo = u.frame(o);
-      const double3 dpw = tan3(u.vslot(r), j);
-      const bool om = j / 6 == o;  // the field moves under the point
-      const double3 dxb = fRt(Fo, om ? dpw - u.uvel(j, vr.pw) : dpw);  // body-frame displacement
-      const double dv = ddot(vr.gb, dxb);
-      double3 dn = fR(Fo, mv3(vr.Jb, dxb));
-      if (om) dn = dn + cross3(u.omega(j), vr.n);
-      u.vsdist()[r].d[j] = dv;
-      const int64_t row = u.env * C + r;
-      put_t(p, row, 0, j, dpw.x);
-      put_t(p, row, 1, j, dpw.y);
-      put_t(p, row, 2, j, dpw.z);
-      put_t(p, row, 3, j, dv);
-      put_t(p, row, 4, j, dn.x);
-      put_t(p, row, 5, j, dn.y);
-      put_t(p, row, 6, j, dn.z);
-      put_t(p, row, 7, j, -vr.act * vr.cact * c.inv_tau_pen * dv);
-      continue;
-    }
-    const int pi = item - NV;
+    const int pi = item;
     const int ku = pi / P, i = pi - ku * P;
     const EnvUnit u = unit(ku);
     const int k = i / m2, l = i - (i / m2) * m2;
-    const T12* s1 = u.eslot(k);
-    const T12* s2 = u.eslot(m1 + l);
+    const ESlot& s1 = u.eslot(k);
+    const ESlot& s2 = u.eslot(m1 + l);
+    const Frame& F1 = u.frame(0);
+    const Frame& F2 = u.frame(1);
     const QpRec& qr = u.qrec(i);
     const PairRec& pr = u.prec(i);
     const SideJac& r1 = u.sj(i, 0);
     const SideJac& r2 = u.sj(i, 1);
     // QP inputs -> alpha, gamma tangents
-    const double3 t1 = val3(s1 + 3) - val3(s1), t2n = val3(s2) - val3(s2 + 3), bv = val3(s1) - val3(s2);
-    const double3 dt1 = tan3(s1 + 3, j) - tan3(s1, j), dt2n = tan3(s2, j) - tan3(s2 + 3, j);
-    const double3 dbv = tan3(s1, j) - tan3(s2, j);
+    const double3 t1 = dv3(s1.bw) - dv3(s1.aw), t2n = dv3(s2.aw) - dv3(s2.bw), bv = dv3(s1.aw) - dv3(s2.aw);
+    // world endpoint tangents: R (body tangent) + the moving body's rigid velocity
+    const double3 da1 = tan3(s1.a, j), db1 = tan3(s1.b, j), da2 = tan3(s2.a, j), db2 = tan3(s2.b, j);
+    const int mv = j / 6;
+    double3 dt1 = fR(F1, db1 - da1), dt2n = fR(F2, da2 - db2), dbv = fR(F1, da1) - fR(F2, da2);
+    if (mv == 0) {
+      dt1 = dt1 + cross3(u.omega(j), t1);
+      dbv = dbv + u.uvel(j, dv3(s1.aw));
+    } else {
+      dt2n = dt2n + cross3(u.omega(j), t2n);
+      dbv = dbv - u.uvel(j, dv3(s2.aw));
+    }
     const double dq[5] = {2.0 * ddot(t1, dt1), ddot(dt1, t2n) + ddot(t1, dt2n), 2.0 * ddot(t2n, dt2n),
                           ddot(dbv, t1) + ddot(bv, dt1), ddot(dbv, t2n) + ddot(bv, dt2n)};
-    double da1 = 0.0, da2 = 0.0, dgam = 0.0;
+    double dal1 = 0.0, dal2 = 0.0, dgam = 0.0;
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
-      da1 = fma(qr.J[q], dq[q], da1);
-      da2 = fma(qr.J[5 + q], dq[q], da2);
+      dal1 = fma(qr.J[q], dq[q], dal1);
+      dal2 = fma(qr.J[5 + q], dq[q], dal2);
       dgam = fma(qr.J[10 + q], dq[q], dgam);
     }
-    const double3 e1 = val3(s1 + 9) - val3(s1 + 6), e2 = val3(s2 + 9) - val3(s2 + 6);
-    const double3 dpb1 = tan3(s1 + 6, j) + (tan3(s1 + 9, j) - tan3(s1 + 6, j)) * qr.a1 + e1 * da1;
-    const double3 dpb2 = tan3(s2 + 6, j) + (tan3(s2 + 9, j) - tan3(s2 + 6, j)) * qr.a2 + e2 * da2;
+    const double3 e1 = val3(s1.b) - val3(s1.a), e2 = val3(s2.b) - val3(s2.a);
+    const double3 dpb1 = da1 + (db1 - da1) * qr.a1 + e1 * dal1;
+    const double3 dpb2 = da2 + (db2 - da2) * qr.a2 + e2 * dal2;
     double3 dp1, dn1, dp2, dn2;
     double dvo1, dph1, dvo2, dph2;
     side_tan(u, r1, 0, dpb1, j, dp1, dn1, dvo1, dph1);
@@ -774,7 +834,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
     put_t(p, row + 1, 5, j, dm2.y);
     put_t(p, row + 1, 6, j, dm2.z);
   }
-  __syncthreads();
+  JVP_PHASE_MARK(8);
 
   if (full) {
     // ---- F: NN softmin statistics, shift = first minimum (argmin_s 126-144) ----
@@ -808,7 +868,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
         ns[1].d[j] = -inv * inv * dtot;
       }
     }
-    __syncthreads();
+    JVP_PHASE_MARK(9);
     // ---- G: activity = con pen_b nn_b clash cont (manifold.hpp:303-330) -------
     for (int it = tid; it < 12 * NP; it += nth) {
       const int pi = it / 12, j = it - pi * 12;
@@ -832,7 +892,7 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       put_t(p, row + 1, 7, j, rec[2].d[j] * nn2 + rec[2].v * dnn2);
     }
   }
-  __syncthreads();
+  JVP_PHASE_MARK(10);
 
   // ---- H: mean contact distance (manifold.hpp:379-384), fixed order ---------
   if (m.mean_dist || p.mean_grad || p.mean_f64 || p.mean_grad_f64) {
@@ -861,7 +921,7 @@ int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
     cudaFuncSetAttribute(manifold_jvp_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const int64_t grid = (p.m.n_env + p.units_per_block - 1) / p.units_per_block;
-  manifold_jvp_kernel<K1, K2><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block, s>>>(p);
+  manifold_jvp_kernel<K1, K2><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block + p.geom_bytes, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -881,6 +941,17 @@ int launch_jvp_k2(const JvpParams& p, int threads, cudaStream_t s) {
 
 }  // namespace
 
+#ifdef CMGB_PHASE_CLOCKS
+inline int read_phase_clocks(unsigned long long* out) {
+  unsigned long long h[16];
+  if (cudaMemcpyFromSymbol(h, g_jvp_phase, sizeof(h)) != cudaSuccess) return 1;
+  for (int i = 0; i < 16; ++i) out[i] += h[i];
+  return 0;
+}
+int jvp_phase_clocks_sq(unsigned long long* out);
+int jvp_phase_clocks_cp(unsigned long long* out);
+int jvp_phase_clocks_gen(unsigned long long* out);
+#endif
 int launch_jvp_k1_sq(const JvpParams& p, int threads, cudaStream_t s);
 int launch_jvp_k1_cp(const JvpParams& p, int threads, cudaStream_t s);
 int launch_jvp_k1_gen(const JvpParams& p, int threads, cudaStream_t s);
