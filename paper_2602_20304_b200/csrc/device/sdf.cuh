@@ -92,6 +92,18 @@ __device__ __forceinline__ void pow_pair_t(const T& x, int n, double p, T& xp, T
   }
 }
 
+// Dual overload for compile-time exponents N >= 2: the primal chain is the
+// double one (bit-identical to the Dual products), the tangents take the
+// analytic derivatives N x^(N-1), (N-1) x^(N-2) -- 2 scalings instead of
+// carrying the tangents through every product of the chain.
+template <int N, int ND, std::enable_if_t<(N >= 2), int> = 0>
+__device__ __forceinline__ void pow_pair_t(const Dual<ND>& x, int, double, Dual<ND>& xp, Dual<ND>& xpm1) {
+  const double a = cpow<N - 1>(x.v);
+  const double b = N >= 3 ? cpow<(N >= 3 ? N - 2 : 1)>(x.v) : 1.0;
+  xpm1 = Dual<ND>::chain(a, (double)(N - 1) * b, x);
+  xp = Dual<ND>::chain(a * x.v, (double)N * a, x);
+}
+
 // 1 - f^p4 for f > 0, p4 < 0, cancellation-free near the surface (f -> 1).
 // When n = -1/p4 is an exact integer (eps1 = 0.1 -> 20, 0.2 -> 10, 1 -> 2),
 // f^p4 = 1/r with r = f^(1/n): an FP32 SFU seed refined by one FP64 Newton
