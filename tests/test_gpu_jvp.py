@@ -150,3 +150,35 @@ def test_manifold_reductions_and_their_tangents(cuda):
     v_ref, vg_ref = api.activity_weighted_distance(rc, rt)
     assert abs(v - v_ref) <= 1e-6 + 1e-5 * abs(v_ref)
     assert np.linalg.norm(vg - vg_ref) <= 1e-5 + 1e-4 * np.linalg.norm(vg_ref)
+
+
+@pytest.mark.parametrize("case", ["drop", "box_box", "capsule"])
+def test_jvp_batch_independence_and_determinism(case, cuda):
+    """Race / packing check (compute-sanitizer is unavailable on the pool): every
+    env's outputs are bitwise the same whether it shares its CTA with other envs
+    (odd batch, partial last CTA) or runs in a sub-batch, and across reruns."""
+    cfg = SmoothingConfig()
+    n = 257
+    if case == "drop":
+        sc = W.drop_scene(n)
+        bodies = [api.surface_from_spec(b) for b in sc.bodies]
+        i, j = api.scene_pairs(len(bodies), sc.is_static())[-1]
+        P = torch.as_tensor(sc.poses(n), device="cuda")
+        a1, a2, p1, p2 = bodies[i], bodies[j], P[:, i].contiguous(), P[:, j].contiguous()
+    else:
+        ws = W.box_box(n) if case == "box_box" else W.mixed_bucket("capsule", n)
+        a1, a2 = (api.surface_from_spec(b) for b in ws.bodies[:2])
+        q1, q2 = ws.poses(n)
+        p1, p2 = torch.as_tensor(q1, device="cuda"), torch.as_tensor(q2, device="cuda")
+        if p1.shape[0] == 1:
+            p1 = p1.expand(n, 6).contiguous()
+
+    full = api.generate_manifold_jvp_batch(a1, a2, p1, p2, cfg, want_src=True)
+    again = api.generate_manifold_jvp_batch(a1, a2, p1, p2, cfg, want_src=True)
+    lo = api.generate_manifold_jvp_batch(a1, a2, p1[:3].contiguous(), p2[:3].contiguous(), cfg, want_src=True)
+    hi = api.generate_manifold_jvp_batch(a1, a2, p1[100:].contiguous(), p2[100:].contiguous(), cfg, want_src=True)
+    torch.cuda.synchronize()
+    for k in ("contacts", "tangents", "src", "mean_dist", "mean_dist_grad"):
+        assert torch.equal(full[k], again[k]), ("rerun", k)
+        assert torch.equal(full[k][:3], lo[k]), ("sub-batch [0, 3)", k)
+        assert torch.equal(full[k][100:], hi[k]), ("sub-batch [100, n)", k)
