@@ -30,6 +30,25 @@ namespace cmgb {
 
 namespace {
 
+// Developer instrumentation (-DCMGB_PHASE_CLOCKS): SM clocks per phase,
+// summed over CTAs by thread 0 at each barrier (tools/phase_clocks.py).
+#ifdef CMGB_PHASE_CLOCKS
+__device__ unsigned long long g_mf_phase[16];
+#define MF_PHASE_START() long long t_prev_ = clock64()
+#define MF_PHASE_MARK(k)                                                    \
+  do {                                                                      \
+    __syncthreads();                                                        \
+    if (threadIdx.x == 0) {                                                 \
+      const long long t_ = clock64();                                       \
+      atomicAdd(&g_mf_phase[k], (unsigned long long)(t_ - t_prev_));       \
+      t_prev_ = t_;                                                         \
+    }                                                                       \
+  } while (0)
+#else
+#define MF_PHASE_START() (void)0
+#define MF_PHASE_MARK(k) __syncthreads()
+#endif
+
 // CTA shape per SDF kind pair (measured):
 //   eps = 0.1 box-box: 9 warps (2 envs x 144 E-E pairs), 4 CTAs/SM (<= 56
 //     registers), V-S contacts on the warps the NN phase leaves idle (F);
@@ -250,6 +269,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
   const int64_t env0 = (int64_t)blockIdx.x * epb;
   const int n_here = (int)(p.n_env - env0 < epb ? p.n_env - env0 : epb);
   const int tid = threadIdx.x, nth = blockDim.x;
+  MF_PHASE_START();
   const DevCfg& c = p.cfg;
   const DevSide& S1 = p.side[0];
   const DevSide& S2 = p.side[1];
@@ -268,7 +288,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
                              : p.frames2 + 12 * (env0 + e) * p.stride2;
     env(e).R(s)[k] = __ldg(f + k);
   }
-  __syncthreads();
+  MF_PHASE_MARK(0);
 
   const bool topk_any = S1.topk_v | S2.topk_v | S1.topk_e | S2.topk_e;
   const Sets sets(p);
@@ -286,7 +306,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       const double pen = s == 0 ? sdf_eval<kValue, K2>(S2.sdf, pb).v : sdf_eval<kValue, K1>(S1.sdf, pb).v;
       ev.scores()[i] = -pen;  // scores = negated penetrations (manifold.hpp:142-143)
     }
-    __syncthreads();
+    MF_PHASE_MARK(1);
     // edge scores: -(mean of endpoint penetrations) (edge_penetrations, 86-94)
     const int ne_all = S1.ne + S2.ne;
     for (int it = tid; it < n_here * ne_all; it += nth) {
@@ -301,7 +321,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       const double pa = -sc[voff + va], pb = -sc[voff + vb];
       sc[sets.off[2] + i] = -((pa + pb) * 0.5);
     }
-    __syncthreads();
+    MF_PHASE_MARK(2);
     // ---- C: descending rank sort (values only matter; smooth_ops.hpp:180-185)
     // 4 adjacent lanes per score split the comparisons (shuffle-summed rank)
     const int total = sets.off[4];
@@ -324,7 +344,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       rank += __shfl_xor_sync(gm, rank, 2);
       if (ql == 0) env(e).sorted()[sets.off[set] + rank] = x;
     }
-    __syncthreads();
+    MF_PHASE_MARK(3);
   }
 
   // ---- D: selected slots (pass-through or soft top-K rows) --------------
@@ -417,7 +437,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       }
     }
   }
-  __syncthreads();
+  MF_PHASE_MARK(4);
 
   // ---- E: E-E pair stage + V-S contacts --------------------------------------
   // E1-E3 per pair, one thread owning the pair end to end (no barriers in
@@ -469,7 +489,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       }
     }
   }
-  __syncthreads();
+  MF_PHASE_MARK(5);
 
   {
     // ---- F: NN softmin statistics: rows (side 1) and columns (side 2) -------
@@ -514,7 +534,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       }
     }
   }
-  __syncthreads();
+  MF_PHASE_MARK(6);
 
   if (full) {
     // ---- G: activity product + fixed-layout E-E output (303-330) -----------
@@ -630,6 +650,12 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
 }
 
 int manifold_max_threads(int k1, int k2) { return max_threads(k1, k2); }
+
+#ifdef CMGB_PHASE_CLOCKS
+int manifold_phase_clocks(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_mf_phase, 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
+}
+#endif
 int manifold_min_blocks(int k1, int k2) { return min_blocks(k1, k2); }
 
 }  // namespace cmgb

@@ -21,6 +21,10 @@ int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream) {
 }  // namespace cmgb
 
 #ifdef CMGB_PHASE_CLOCKS
+namespace cmgb {
+int manifold_phase_clocks(unsigned long long* out);
+}
+extern "C" int cmgb_debug_manifold_phase_clocks(unsigned long long* out) { return cmgb::manifold_phase_clocks(out); }
 extern "C" int cmgb_debug_jvp_phase_clocks(unsigned long long* out) {
   for (int i = 0; i < 16; ++i) out[i] = 0;
   return cmgb::jvp_phase_clocks_sq(out) | cmgb::jvp_phase_clocks_cp(out) | cmgb::jvp_phase_clocks_gen(out);

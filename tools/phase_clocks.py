@@ -1,4 +1,5 @@
-"""Per-phase SM clocks of the JVP kernel (developer tool). Needs a library
+"""Per-phase SM clocks of the JVP kernel, or of the manifold kernel with
+`box-box` as the first argument (developer tool). Needs a library
 built with `make -C paper_2602_20304_b200/csrc EXTRA_CUFLAGS=-DCMGB_PHASE_CLOCKS`
 (after `make clean`); prints each phase's share of the CTA lifetime for one
 config D forward + JVP step (python tools/phase_clocks.py [n_env])."""
@@ -15,6 +16,30 @@ from paper_2602_20304_b200 import abi, api  # noqa: E402
 from paper_2602_20304_b200 import workloads as W  # noqa: E402
 from paper_2602_20304_b200.scene import SmoothingConfig  # noqa: E402
 
+if len(sys.argv) > 1 and sys.argv[1] == "box-box":
+    n = 65536
+    ws = W.box_box(n)
+    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+    p1, p2 = ws.poses(n)
+    P1, P2 = torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda")
+    lib = abi.load()
+    out = (C.c_ulonglong * 16)()
+    api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig())
+    torch.cuda.synchronize()
+    lib.cmgb_debug_manifold_phase_clocks(out)
+    base = np.array(out[:], dtype=np.float64)
+    api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig())
+    torch.cuda.synchronize()
+    lib.cmgb_debug_manifold_phase_clocks(out)
+    d = np.array(out[:], dtype=np.float64) - base
+    names = {0: "A frames", 1: "B vertex scores", 2: "B edge scores", 3: "C rank sort", 4: "D slots",
+             5: "E pairs (+ V-S)", 6: "F NN (+ V-S)"}
+    ncta = n // 2
+    tot = d[:7].sum()
+    for k, nm in names.items():
+        print(f"{nm:20s} {100 * d[k] / tot:6.2f} %  {d[k] / ncta:9.0f} clk per CTA")
+    print(f"total {tot / ncta:.0f} clk per CTA ({ncta} CTAs)")
+    sys.exit(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 sc = W.drop_scene(n)
 bodies = [api.surface_from_spec(b) for b in sc.bodies]
