@@ -264,9 +264,148 @@ __device__ __forceinline__ V3<Dual<W>> seed_cols(double3 x, int lane) {
   return q;
 }
 
+// Value, body-frame gradient and Hessian of the eps = 0.1 superquadric leaf
+// (kSqE01: f = sum_i s_i^10, s_i = u_i^2 + 1e-30, u = diag(1/axes) x_prim,
+// phi = (1 - f^p4) / |u|; sdf.hpp:85-108), and of the normal source grad f.
+// In normalised coordinates, with f_i = df/du_i = c u_i s_i^9, k = -p4 F / f,
+// r = |u| (+1e-20 floor):
+//   g_i  = k f_i / r - phi u_i / r^2
+//   H_ij = k (p4 - 1) f_i f_j / (f r) - k (f_i u_j + u_i f_j) / r^3
+//          + 3 phi u_i u_j / r^4 + delta_ij (k f_ii / r - phi / r^2),
+//   f_ii = c s_i^8 (s_i + 18 u_i^2);
+// body frame: x = R x_prim + t, u = D R^T (x - t), so grad = R D g, Hess = R D H D R^T.
+struct SqHess {
+  double phi;
+  double3 g;    // grad phi (body)
+  double H[9];  // Hess phi (body)
+  double3 df;   // grad f (body): the normal source
+  double Hf[9]; // Hess f (body)
+};
+
+__device__ __forceinline__ void sq_e01_hess(const DevSq& q, double3 x, SqHess& o) {
+  if (q.has_frame) x = mul_Rt(q.R, x - d3(q.t[0], q.t[1], q.t[2]));
+  const double u[3] = {x.x * q.inv_ax[0], x.y * q.inv_ax[1], x.z * q.inv_ax[2]};
+  const double cc[3] = {q.c_xy, q.c_xy, q.c_z};
+  double s[3], s8[3], fi[3], fii[3];
+  double f = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    s[i] = fma(u[i], u[i], kMC.floor30);
+    s8[i] = cpow<8>(s[i]);
+    const double s9 = s8[i] * s[i];
+    f += s9 * s[i];
+    fi[i] = cc[i] * u[i] * s9;
+    fii[i] = cc[i] * s8[i] * fma(18.0 * u[i], u[i], s[i]);
+  }
+  const double r2 = fma(u[0], u[0], fma(u[1], u[1], fma(u[2], u[2], kMC.floor20)));
+  const double ri = rsqrt_d(r2), ri2 = ri * ri;
+  double F, inv_f;
+  const double phi = one_minus_pow<20>(f, q.p4, q.n4, &F, &inv_f) * ri;
+  const double k = -q.p4 * F * inv_f;
+  const double a = k * (q.p4 - 1.0) * inv_f * ri, b = k * ri * ri2, cuu = 3.0 * phi * ri2 * ri2;
+  double g[3], H[9], Hf[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g[i] = q.inv_ax[i] * (k * fi[i] * ri - phi * u[i] * ri2);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double h = a * fi[i] * fi[j] - b * (fi[i] * u[j] + u[i] * fi[j]) + cuu * u[i] * u[j];
+      if (i == j) h += k * fii[i] * ri - phi * ri2;
+      H[3 * i + j] = q.inv_ax[i] * q.inv_ax[j] * h;
+      Hf[3 * i + j] = i == j ? q.inv_ax[i] * q.inv_ax[i] * fii[i] : 0.0;
+    }
+  }
+  double3 df = d3(q.inv_ax[0] * fi[0], q.inv_ax[1] * fi[1], q.inv_ax[2] * fi[2]);
+  double3 gg = d3(g[0], g[1], g[2]);
+  if (q.has_frame) {
+    double T[9], Rt[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rt[i] = q.R[3 * (i % 3) + i / 3];
+    mm3(q.R, H, T);
+    mm3(T, Rt, H);
+    mm3(q.R, Hf, T);
+    mm3(T, Rt, Hf);
+    gg = mul_R(q.R, gg);
+    df = mul_R(q.R, df);
+  }
+  o.phi = phi;
+  o.g = gg;
+  o.df = df;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    o.H[i] = H[i];
+    o.Hf[i] = Hf[i];
+  }
+}
+
+// kSqE01 side: the trace / own-normal Jacobians from the analytic Hessians
+// (3x3 products per step instead of Dual<3> arithmetic through the field).
+// Trace step (sdf.hpp:318-326) p' = p - phi g / sqrt(tau + |g|^2):
+//   d p' / d p = I - ghat g^T - phi (H - g (g^T H) / (tau + |g|^2)) / sqrt(tau + |g|^2).
+// Primal: the value kernel's double field and update (manifold.cu trace_step).
+template <int KO>
+__device__ __forceinline__ void side_jac_sqe01(const DevSdf& own, const DevSdf& oth, const Frame& Fs, const Frame& Fo,
+                                               double3 pb0, const DevCfg& c, SideJac& r) {
+  const DevSq& q = own.nodes[0].sq;
+  double J[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  double3 p = pb0;
+  SqHess h;
+#pragma unroll 1
+  for (int it = 0; it < c.trace_iters; ++it) {
+    sq_e01_hess(q, p, h);
+    const double n2 = c.tau_normal + ddot(h.g, h.g);
+    const double inv = rsqrt_d(n2);
+    const double3 gh = h.g * inv;
+    // gT H (row vector), then Jstep = I - gh g^T - phi inv (H - g (g^T H) / n2)
+    const double3 gH = d3(h.g.x * h.H[0] + h.g.y * h.H[3] + h.g.z * h.H[6],
+                          h.g.x * h.H[1] + h.g.y * h.H[4] + h.g.z * h.H[7],
+                          h.g.x * h.H[2] + h.g.y * h.H[5] + h.g.z * h.H[8]);
+    const double pi = h.phi * inv, pin = pi / n2;
+    const double gv[3] = {h.g.x, h.g.y, h.g.z}, ghv[3] = {gh.x, gh.y, gh.z}, gHv[3] = {gH.x, gH.y, gH.z};
+    double S[9], T[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        S[3 * a + b] = (a == b ? 1.0 : 0.0) - ghv[a] * gv[b] - pi * h.H[3 * a + b] + pin * gv[a] * gHv[b];
+    mm3(S, J, T);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) J[i] = T[i];
+    const double sc = inv * h.phi;
+    p = d3(fma(-h.g.x, sc, p.x), fma(-h.g.y, sc, p.y), fma(-h.g.z, sc, p.z));
+  }
+  sq_e01_hess(q, p, h);
+  // own normal n = normalize_smooth(grad f): d n / d d = (I - n n^T) / sqrt(tau + |d|^2)
+  const double invn = rsqrt_d(c.tau_normal + ddot(h.df, h.df));
+  const double3 nb = h.df * invn;
+  const double nv[3] = {nb.x, nb.y, nb.z};
+  double Dn[9], T[9], Jn[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) Dn[3 * a + b] = invn * ((a == b ? 1.0 : 0.0) - nv[a] * nv[b]);
+  mm3(Dn, h.Hf, T);
+  mm3(T, J, Jn);
+  mm3(Fs.R, J, r.M);
+  mm3(Fs.R, Jn, r.N);
+  // own value (containment): d phi / d pb0 = g^T J
+  r.phi_own = h.phi;
+  r.gown = d3(h.g.x * J[0] + h.g.y * J[3] + h.g.z * J[6], h.g.x * J[1] + h.g.y * J[4] + h.g.z * J[7],
+              h.g.x * J[2] + h.g.y * J[5] + h.g.z * J[8]);
+  r.pw = fR(Fs, p) + ft(Fs);
+  r.nw = fR(Fs, nb);
+  const SdfOut v = sdf_eval<kGrad, KO>(oth, fRt(Fo, r.pw - ft(Fo)));
+  r.vo = v.v;
+  r.gvw = fR(Fo, v.g);
+}
+
 template <int KS, int KO, int W>
 __device__ __forceinline__ void side_jac_lane(const DevSdf& own, const DevSdf& oth, const Frame& Fs, const Frame& Fo,
                                               double3 pb0, const DevCfg& c, int lane, SideJac& r) {
+  if constexpr (KS == kSqE01 && W == 3) {
+    side_jac_sqe01<KO>(own, oth, Fs, Fo, pb0, c, r);
+    return;
+  }
   using DW = Dual<W>;
   V3<DW> p = seed_cols<W>(pb0, lane);
 #pragma unroll 1
@@ -651,32 +790,52 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       const Frame& Fo = u.frame(o);
       const double3 pw = val3(u.vslot(r));
       // vs_contacts (manifold.hpp:185-204): normal source of the opposing field
-      // in its body point
-      using DW = Dual<3>;
-      const V3<DW> xd = seed_cols<3>(fRt(Fo, pw - ft(Fo)), 0);
-      const SdfOutT<DW> sv = o == 1 ? sdf_eval<kNormalSource, K2, DW>(S2.sdf, xd)
-                                    : sdf_eval<kNormalSource, K1, DW>(S1.sdf, xd);
-      const V3<DW> nbd = normalize_smooth_t<DW>(sv.g, c.tau_normal);
+      // in its body point (analytic Hessian for kSqE01, Dual<3> otherwise)
+      const double3 xb = fRt(Fo, pw - ft(Fo));
       VsRec& vr = u.vsrec(r);
+      const int ko = o == 1 ? K2 : K1;
+      if (ko == kSqE01) {
+        SqHess h;
+        sq_e01_hess((o == 1 ? S2 : S1).sdf.nodes[0].sq, xb, h);
+        const double invn = rsqrt_d(c.tau_normal + ddot(h.df, h.df));
+        const double3 nb = h.df * invn;
+        const double nv[3] = {nb.x, nb.y, nb.z};
+        double Dn[9];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        vr.Jb[t] = nbd.x.d[t];
-        vr.Jb[3 + t] = nbd.y.d[t];
-        vr.Jb[6 + t] = nbd.z.d[t];
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) Dn[3 * a + b] = invn * ((a == b ? 1.0 : 0.0) - nv[a] * nv[b]);
+        mm3(Dn, h.Hf, vr.Jb);
+        vr.gb = h.g;
+        vr.n = fR(Fo, nb);
+        vr.v = h.phi;
+      } else {
+        using DW = Dual<3>;
+        const V3<DW> xd = seed_cols<3>(xb, 0);
+        const SdfOutT<DW> sv = o == 1 ? sdf_eval<kNormalSource, K2, DW>(S2.sdf, xd)
+                                      : sdf_eval<kNormalSource, K1, DW>(S1.sdf, xd);
+        const V3<DW> nbd = normalize_smooth_t<DW>(sv.g, c.tau_normal);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          vr.Jb[t] = nbd.x.d[t];
+          vr.Jb[3 + t] = nbd.y.d[t];
+          vr.Jb[6 + t] = nbd.z.d[t];
+        }
+        vr.gb = d3(sv.v.d[0], sv.v.d[1], sv.v.d[2]);
+        vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
+        vr.v = sv.v.v;
       }
-      vr.gb = d3(sv.v.d[0], sv.v.d[1], sv.v.d[2]);
-      vr.n = fR(Fo, d3(nbd.x.v, nbd.y.v, nbd.z.v));
-      vr.v = sv.v.v;
-      sigmoid_pair_d(-sv.v.v * c.inv_tau_pen, &vr.act, &vr.cact);
+      const double vv = vr.v;
+      sigmoid_pair_d(-vv * c.inv_tau_pen, &vr.act, &vr.cact);
       const int64_t row = u.env * C + r;
       float* dst = m.contacts + row * 8;
-      dst[0] = (float)pw.x; dst[1] = (float)pw.y; dst[2] = (float)pw.z; dst[3] = (float)sv.v.v;
+      dst[0] = (float)pw.x; dst[1] = (float)pw.y; dst[2] = (float)pw.z; dst[3] = (float)vv;
       dst[4] = (float)vr.n.x; dst[5] = (float)vr.n.y; dst[6] = (float)vr.n.z; dst[7] = (float)vr.act;
       if (m.src) {
         m.src[row * 2] = u.prov()[r];
         m.src[row * 2 + 1] = -1;
       }
-      u.vsdist()[r].v = sv.v.v;
+      u.vsdist()[r].v = vv;
     }
   }
   JVP_PHASE_MARK(6);
