@@ -338,21 +338,61 @@ __device__ __forceinline__ void sq_e01_hess(const DevSq& q, double3 x, SqHess& o
   }
 }
 
-// kSqE01 side: the trace / own-normal Jacobians from the analytic Hessians
-// (3x3 products per step instead of Dual<3> arithmetic through the field).
+// Value, gradient and Hessian of the axis-aligned box_planes leaf (kBoxCp):
+// phi = LSE_tau(d_i), d = (x - w0, -x - w1, y - w2, -y - w3, z - w4, -z - w5)
+// (sdf.hpp:110-117); grad = sum w_i n_i, Hess = (diag(w0 + w1, w2 + w3,
+// w4 + w5) - grad grad^T) / tau with the softmax weights w. Its normal source
+// is grad phi (sdf.hpp:233-288: only SQ leaves substitute grad f).
+__device__ __forceinline__ void box_cp_hess(const DevNode& nd, double3 p, SqHess& o) {
+  const SdfOut v = box_cp_leaf<kNormalSource>(nd, p);
+  const double d[6] = {p.x - nd.box_w[0], -p.x - nd.box_w[1], p.y - nd.box_w[2],
+                       -p.y - nd.box_w[3], p.z - nd.box_w[4], -p.z - nd.box_w[5]};
+  double m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) m = fmax(m, d[i]);
+  double e[6], acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    e[i] = exp_d((d[i] - m) * nd.inv_tau_d);
+    acc += e[i];
+  }
+  const double ia = rcp_d(acc);
+  const double wd[3] = {(e[0] + e[1]) * ia, (e[2] + e[3]) * ia, (e[4] + e[5]) * ia};
+  const double gv[3] = {v.g.x, v.g.y, v.g.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) o.H[3 * a + b] = ((a == b ? wd[a] : 0.0) - gv[a] * gv[b]) * nd.inv_tau_d;
+  o.phi = v.v;
+  o.g = v.g;
+  o.df = v.g;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) o.Hf[i] = o.H[i];
+}
+
+// Analytic leaf Hessians available for these kinds.
+template <int K>
+constexpr bool kHasHess = K == kSqE01 || K == kBoxCp;
+template <int K>
+__device__ __forceinline__ void leaf_hess(const DevSdf& sdf, double3 p, SqHess& h) {
+  if constexpr (K == kSqE01) sq_e01_hess(sdf.nodes[0].sq, p, h);
+  else box_cp_hess(sdf.nodes[0], p, h);
+}
+
+// Side with an analytic leaf Hessian (kSqE01 / kBoxCp): the trace / own-normal
+// Jacobians as 3x3 products per step instead of Dual<3> arithmetic.
 // Trace step (sdf.hpp:318-326) p' = p - phi g / sqrt(tau + |g|^2):
 //   d p' / d p = I - ghat g^T - phi (H - g (g^T H) / (tau + |g|^2)) / sqrt(tau + |g|^2).
 // Primal: the value kernel's double field and update (manifold.cu trace_step).
-template <int KO>
-__device__ __forceinline__ void side_jac_sqe01(const DevSdf& own, const DevSdf& oth, const Frame& Fs, const Frame& Fo,
-                                               double3 pb0, const DevCfg& c, SideJac& r) {
-  const DevSq& q = own.nodes[0].sq;
+template <int KS, int KO>
+__device__ __forceinline__ void side_jac_analytic(const DevSdf& own, const DevSdf& oth, const Frame& Fs,
+                                                  const Frame& Fo, double3 pb0, const DevCfg& c, SideJac& r) {
   double J[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   double3 p = pb0;
   SqHess h;
 #pragma unroll 1
   for (int it = 0; it < c.trace_iters; ++it) {
-    sq_e01_hess(q, p, h);
+    leaf_hess<KS>(own, p, h);
     const double n2 = c.tau_normal + ddot(h.g, h.g);
     const double inv = rsqrt_d(n2);
     const double3 gh = h.g * inv;
@@ -374,8 +414,8 @@ __device__ __forceinline__ void side_jac_sqe01(const DevSdf& own, const DevSdf& 
     const double sc = inv * h.phi;
     p = d3(fma(-h.g.x, sc, p.x), fma(-h.g.y, sc, p.y), fma(-h.g.z, sc, p.z));
   }
-  sq_e01_hess(q, p, h);
-  // own normal n = normalize_smooth(grad f): d n / d d = (I - n n^T) / sqrt(tau + |d|^2)
+  leaf_hess<KS>(own, p, h);
+  // own normal n = normalize_smooth(normal source): d n / d d = (I - n n^T) / sqrt(tau + |d|^2)
   const double invn = rsqrt_d(c.tau_normal + ddot(h.df, h.df));
   const double3 nb = h.df * invn;
   const double nv[3] = {nb.x, nb.y, nb.z};
@@ -402,8 +442,8 @@ __device__ __forceinline__ void side_jac_sqe01(const DevSdf& own, const DevSdf& 
 template <int KS, int KO, int W>
 __device__ __forceinline__ void side_jac_lane(const DevSdf& own, const DevSdf& oth, const Frame& Fs, const Frame& Fo,
                                               double3 pb0, const DevCfg& c, int lane, SideJac& r) {
-  if constexpr (KS == kSqE01 && W == 3) {
-    side_jac_sqe01<KO>(own, oth, Fs, Fo, pb0, c, r);
+  if constexpr (kHasHess<KS> && W == 3) {
+    side_jac_analytic<KS, KO>(own, oth, Fs, Fo, pb0, c, r);
     return;
   }
   using DW = Dual<W>;
@@ -793,10 +833,14 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       // in its body point (analytic Hessian for kSqE01, Dual<3> otherwise)
       const double3 xb = fRt(Fo, pw - ft(Fo));
       VsRec& vr = u.vsrec(r);
-      const int ko = o == 1 ? K2 : K1;
-      if (ko == kSqE01) {
+      const bool hess = o == 1 ? kHasHess<K2> : kHasHess<K1>;
+      if (hess) {
         SqHess h;
-        sq_e01_hess((o == 1 ? S2 : S1).sdf.nodes[0].sq, xb, h);
+        if (o == 1) {
+          if constexpr (kHasHess<K2>) leaf_hess<K2>(S2.sdf, xb, h);
+        } else {
+          if constexpr (kHasHess<K1>) leaf_hess<K1>(S1.sdf, xb, h);
+        }
         const double invn = rsqrt_d(c.tau_normal + ddot(h.df, h.df));
         const double3 nb = h.df * invn;
         const double nv[3] = {nb.x, nb.y, nb.z};
