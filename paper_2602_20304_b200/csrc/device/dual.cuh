@@ -2,9 +2,10 @@
 //
 // The reference templates every kernel on its scalar and runs it with
 // Dual<12> seeded at the two 6-D pose vectors (dual.hpp:47-130, 249-263). On
-// the device a 13-double scalar would not fit in registers, so the JVP kernel
-// carries N <= 4 tangent directions per thread and covers the 12 pose
-// directions with 12 / N direction groups (manifold_jvp.cu). Semantics follow
+// the device the JVP kernel (manifold_jvp.cuh) instead seeds Dual<N> at the
+// low-dimensional bottlenecks of the pipeline -- Dual<3> at a body point,
+// Dual<5> at the witness QP's (Q, c), Dual<1> per pose coordinate in se3_exp
+// -- and chains the 12 pose directions through the resulting Jacobians. Semantics follow
 // dual.hpp: comparisons / branches read the primal only (callers use pv()),
 // fabs has subgradient 0 at the kink (dual.hpp:236-246).
 //
