@@ -83,3 +83,30 @@ def test_cli_gradcheck_sweep_bench_sim(cuda, tmp_path):
                 str(tmp_path / "sim.csv"))
     assert r.returncode == 0, r.stderr
     assert len(open(tmp_path / "sim.csv").read().splitlines()) == 1 + 6
+
+
+@pytest.mark.parametrize("ground", ["box_planes", "sq"])
+def test_cli_gradcheck_posed_primitives(cuda, tmp_path, ground):
+    """Pose Jacobians with rotated / offset primitives inside the bodies (the
+    SQ leaf's body_from_prim frame, sdf.cpp:9): the analytic-Hessian paths of
+    the JVP kernel vs central differences of its own FP64 mean (the
+    reference's gradcheck, main.cpp:190-235)."""
+    import json
+    g = ({"type": "box_planes", "half_extents": [2.0, 2.0, 0.1]} if ground == "box_planes" else
+         {"type": "superquadric", "eps1": 0.1, "eps2": 0.1, "axes": [2.0, 2.0, 0.1],
+          "pose": [0.0, 0.01, 0.0, 0.0, 0.0, 0.3]})
+    scene = {
+        "smoothing": {"sphere_trace_iters": 5, "mode": "full"},
+        "bodies": [
+            {"name": "box", "mesh": {"box": {"half_extents": [0.5, 0.5, 0.5]}},
+             "sdf": {"type": "superquadric", "eps1": 0.1, "eps2": 0.1, "axes": [0.5, 0.5, 0.5],
+                     "pose": [0.01, -0.02, 0.005, 0.05, -0.04, 0.2]},
+             "pose": [0.01, -0.02, 0.49, 0.02, -0.01, 0.05], "edge_topk": 12},
+            {"name": "ground", "mesh": {"box": {"half_extents": [2.0, 2.0, 0.1]}}, "sdf": g,
+             "pose": [0.0, 0.0, -0.1, 0.0, 0.0, 0.0], "edge_topk": 4},
+        ],
+    }
+    path = tmp_path / "posed.json"
+    path.write_text(json.dumps(scene))
+    r = run_cli("gradcheck", "--scene", str(path))
+    assert r.returncode == 0, r.stdout + r.stderr
