@@ -8,23 +8,27 @@
 // of its arithmetic (the sphere trace, ~73%, plus the normal sources and the
 // opposing-field values) is a function of a single 3-D body-frame point, so
 // its 12-direction tangent factors through a 3x3 Jacobian: here those stages
-// run ONCE per item in Dual<3> arithmetic seeded at the point (dual.cuh), and
-// the 12 pose directions are then pushed through the small Jacobians by
-// explicit chain-rule loops. The same holds for the witness QP, a function of
-// the 5 numbers (Q, c) (witness.hpp:74-121): Dual<5>. Everything outside those
-// bottlenecks (frames, slot payloads, pair quantities, NN softmins, activity)
-// carries the 12 tangents directly (Dual<12> records in shared memory,
-// per-direction loops in registers).
+// run ONCE per item -- with analytic leaf Hessians for the eps = 0.1
+// superquadric and box_planes leaves (sq_e01_hess / box_cp_hess), in Dual<3>
+// arithmetic seeded at the point otherwise (dual.cuh) -- and the 12 pose
+// directions are pushed through the small Jacobians by explicit chain-rule
+// loops. The same holds for the witness QP, a function of the 5 numbers (Q, c)
+// (witness.hpp:74-121): Dual<5>. Pose direction j moves body j / 6 rigidly
+// (angular / linear velocity from se3_exp). Everything outside those
+// bottlenecks (slot payloads, pair quantities, NN softmins, activity) carries
+// the 12 tangents directly (records of an FP64 primal + 12 FP32 tangents in
+// shared memory, per-direction items in registers).
 //
 // Work mapping (one CTA owns `units_per_block` consecutive envs; items of all
 // its envs spread over the CTA's threads phase by phase, as manifold.cu):
-//   A  frames: se3_exp in Dual<6> per pose (pose.hpp:78-91)
+//   A  frames + rigid velocities: se3_exp, one Dual<1> lane per pose coordinate
 //   B  top-K scores: opposing field value + gradient (double), 12-direction chain
 //   C  rank sort on primals, stable on ties (smooth_ops.hpp:180-185)
-//   D  slots: soft top-K rows / pass-through, one item per (slot, direction)
-//   E  E-E pairs (QP Dual<5>, two sides' trace + normal Dual<3>, opposing
-//      value gradient) and V-S items (normal source Dual<3>); then the 12
-//      directions through the Jacobians; point / dist / normal rows out
+//   D1 slot primals (soft top-K row weights cached), D2 one item per (slot, direction)
+//   E1 Jacobians: one item per pair side (trace + own normal), per pair (QP,
+//      Dual<5>) and per V-S contact (opposing normal source)
+//   E1b pair primals + V-S tangents; E2 one item per (pair, direction), the
+//      direction fastest so a warp's FP32 tangent stores are contiguous
 //   F  NN softmin statistics (argmin_s shift carries its tangent)
 //   G  activity product + its tangents
 //   H  mean contact distance + gradient (fixed order)
@@ -60,7 +64,6 @@ namespace {
 #define CMGB_JVP_SMEM_KB 56
 #endif
 constexpr int kJvpThreads = CMGB_JVP_THREADS;
-constexpr int kJvpW = 3;  // tangent columns per E1 Jacobian item (Dual<3>)
 constexpr int kJvpMinBlocks = CMGB_JVP_MINB;
 
 using D3 = Dual<3>;
