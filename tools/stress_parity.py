@@ -1,5 +1,6 @@
 """Developer stress check: GPU vs the C oracle on large jittered batches of the
-manifold cases (python tools/stress_parity.py [n])."""
+manifold cases (python tools/stress_parity.py [n] [--jvp]); --jvp checks the
+pose-Jacobian kernel's primal contacts (smooth cases) the same way."""
 import os, sys
 import numpy as np
 import torch
@@ -11,15 +12,19 @@ from helpers import parity_report, surfaces
 from oracle import Oracle
 from paper_2602_20304_b200 import api
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+jvp = "--jvp" in sys.argv
+n = int(args[0]) if args else 16384
 for name, ws, cfg, _ in manifold_cases():
+    if jvp and cfg.hard_ops:
+        continue
     (a1, a2), (o1, o2) = surfaces(ws)
     p1, p2 = ws.poses(n)
     ref = Oracle.manifold_batch(o1, o2, p1, p2, cfg, threads=os.cpu_count())
-    r = api.generate_manifold_batch(a1, a2, torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda"),
-                                    cfg, want_src=True)
+    fn = api.generate_manifold_jvp_batch if jvp else api.generate_manifold_batch
+    r = fn(a1, a2, torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda"), cfg, want_src=True)
     torch.cuda.synchronize()
     rep, bad = parity_report(r["contacts"].cpu().numpy(), ref["contacts"])
     src_bad = int((r["src"].cpu().numpy() != ref["meta"][..., 2:]).any(axis=-1).sum())
     worst = max(v["max_ratio"] for v in rep.values())
-    print(f"{name:26s} n={n} failing contacts {int(bad.sum()):5d} / {bad.size}  worst ratio {worst:.3g}  src mismatches {src_bad}")
+    print(f"{'jvp ' if jvp else ''}{name:26s} n={n} failing contacts {int(bad.sum()):5d} / {bad.size}  worst ratio {worst:.3g}  src mismatches {src_bad}")
