@@ -889,9 +889,9 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
 
   // ---- E1b: E-E pair quantities, primal (manifold.hpp:248-266, 279-285), and
   // beside them the V-S tangents, one item per (contact, direction) ----------
-  for (int it = tid; it < NP + 12 * NV; it += nth) {
-    if (it >= NP) {
-      const int item = (it - NP) / 12, j = (it - NP) - item * 12;
+  for (int it = tid; it < 2 * NP + 12 * NV; it += nth) {
+    if (it >= 2 * NP) {
+      const int item = (it - 2 * NP) / 12, j = (it - 2 * NP) - item * 12;
       const int k = item / nvs, r = item - k * nvs;
       const EnvUnit u = unit(k);
       const int o = r < n1 ? 1 : 0;
@@ -915,45 +915,68 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       put_t(p, row, 7, j, -vr.act * vr.cact * c.inv_tau_pen * dv);
       continue;
     }
-    const int ku = it / P, i = it - ku * P;
+    // two adjacent lanes per pair: lane h owns side h's sign / penetration and
+    // contact row; lane 0 the clash, lane 1 the containment indicators
+    const int pi = it >> 1, h = it & 1;
+    const unsigned pm = 3u << ((tid & 31) & ~1);
+    const int ku = pi / P, i = pi - ku * P;
     const EnvUnit u = unit(ku);
     const int k = i / m2, l = i - (i / m2) * m2;
+    const SideJac& rs = u.sj(i, h);
+    const SideJac& ro = u.sj(i, 1 - h);
     const SideJac& r1 = u.sj(i, 0);
     const SideJac& r2 = u.sj(i, 1);
-    PairRec& pr = u.prec(i);
     const double3 de = r1.pw - r2.pw;
-    pr.dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
-    pr.idg = rcp_d(pr.dg);
-    pr.nbar = de * pr.idg;
-    pr.g1 = tanh(ddot(r2.nw, pr.nbar) * c.inv_tau_sign);
-    pr.g2 = tanh(ddot(r1.nw, pr.nbar) * c.inv_tau_sign);
-    sigmoid_pair_d(-r1.vo * c.inv_tau_pen, &pr.pen1, &pr.cpen1);
-    sigmoid_pair_d(-r2.vo * c.inv_tau_pen, &pr.pen2, &pr.cpen2);
-    sigmoid_pair_d(-ddot(r1.nw, r2.nw) * c.inv_tau_clash, &pr.cl, &pr.ccl);
-    pr.ct1 = pr.ct2 = 1.0;
-    pr.cct1 = pr.cct2 = 0.0;
-    if (c.containment) {
-      sigmoid_pair_d(-r1.phi_own * c.inv_tau_cont, &pr.ct1, &pr.cct1);
-      sigmoid_pair_d(-r2.phi_own * c.inv_tau_cont, &pr.ct2, &pr.cct2);
+    const double dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
+    const double idg = rcp_d(dg);
+    const double3 nbar = de * idg;
+    const double gh = tanh(ddot(ro.nw, nbar) * c.inv_tau_sign);  // g1 = sign_s(n2 . nbar), g2 = sign_s(n1 . nbar)
+    double pen, cpen, x0 = 1.0, x1 = 0.0, x2 = 1.0, x3 = 0.0;
+    sigmoid_pair_d(-rs.vo * c.inv_tau_pen, &pen, &cpen);
+    if (h == 0) {
+      sigmoid_pair_d(-ddot(r1.nw, r2.nw) * c.inv_tau_clash, &x0, &x1);  // clash
+    } else if (c.containment) {
+      sigmoid_pair_d(-r1.phi_own * c.inv_tau_cont, &x0, &x1);
+      sigmoid_pair_d(-r2.phi_own * c.inv_tau_cont, &x2, &x3);
     }
-    const double base = u.qrec(i).gam * pr.cl * (pr.ct1 * pr.ct2);
+    const double go = __shfl_xor_sync(pm, gh, 1);
+    const double peno = __shfl_xor_sync(pm, pen, 1), cpeno = __shfl_xor_sync(pm, cpen, 1);
+    const double y0 = __shfl_xor_sync(pm, x0, 1), y1 = __shfl_xor_sync(pm, x1, 1);
+    const double y2 = __shfl_xor_sync(pm, x2, 1), y3 = __shfl_xor_sync(pm, x3, 1);
     const int64_t row = u.env * C + n1 + n2 + 2 * i;
-    float* dst = m.contacts + row * 8;
-    const double3 o1 = pr.nbar * pr.g1, o2 = pr.nbar * pr.g2;
-    dst[0] = (float)r1.pw.x; dst[1] = (float)r1.pw.y; dst[2] = (float)r1.pw.z; dst[3] = (float)(pr.g1 * pr.dg);
-    dst[4] = (float)o1.x; dst[5] = (float)o1.y; dst[6] = (float)o1.z;
-    dst[8] = (float)r2.pw.x; dst[9] = (float)r2.pw.y; dst[10] = (float)r2.pw.z; dst[11] = (float)(pr.g2 * pr.dg);
-    dst[12] = (float)o2.x; dst[13] = (float)o2.y; dst[14] = (float)o2.z;
-    if (m.src) {
-      int* sp = m.src + row * 2;
-      const int sa = u.prov()[n1 + n2 + k], sb = u.prov()[n1 + n2 + m1 + l];
-      sp[0] = sa; sp[1] = sb; sp[2] = sa; sp[3] = sb;
+    float* dst = m.contacts + (row + h) * 8;
+    const double3 oh = nbar * gh;
+    dst[0] = (float)rs.pw.x; dst[1] = (float)rs.pw.y; dst[2] = (float)rs.pw.z; dst[3] = (float)(gh * dg);
+    dst[4] = (float)oh.x; dst[5] = (float)oh.y; dst[6] = (float)oh.z;
+    if (h == 0) {
+      PairRec& pr = u.prec(i);
+      pr.dg = dg;
+      pr.idg = idg;
+      pr.nbar = nbar;
+      pr.g1 = gh;
+      pr.g2 = go;
+      pr.pen1 = pen;
+      pr.cpen1 = cpen;
+      pr.pen2 = peno;
+      pr.cpen2 = cpeno;
+      pr.cl = x0;
+      pr.ccl = x1;
+      pr.ct1 = c.containment ? y0 : 1.0;
+      pr.cct1 = c.containment ? y1 : 0.0;
+      pr.ct2 = c.containment ? y2 : 1.0;
+      pr.cct2 = c.containment ? y3 : 0.0;
+      const double base = u.qrec(i).gam * pr.cl * (pr.ct1 * pr.ct2);
+      if (m.src) {
+        int* sp = m.src + row * 2;
+        const int sa = u.prov()[n1 + n2 + k], sb = u.prov()[n1 + n2 + m1 + l];
+        sp[0] = sa; sp[1] = sb; sp[2] = sa; sp[3] = sb;
+      }
+      T12* rec = u.pair(i);
+      rec[0].v = dg;
+      rec[1].v = base * pen;
+      rec[2].v = base * peno;
+      rec[3].v = gh * dg + go * dg;
     }
-    T12* rec = u.pair(i);
-    rec[0].v = pr.dg;
-    rec[1].v = base * pr.pen1;
-    rec[2].v = base * pr.pen2;
-    rec[3].v = pr.g1 * pr.dg + pr.g2 * pr.dg;
   }
   JVP_PHASE_MARK(7);
 
