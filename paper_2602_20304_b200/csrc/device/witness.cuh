@@ -45,6 +45,17 @@ __device__ __forceinline__ I to_ind(const T& x) {
 // a = exp(-|x|/tau), b = exp(-|x-1|/tau); hard: clamp.
 template <class T, class I = T>
 __device__ __forceinline__ T clip01(const T& x, const DevCfg& c) {
+  if constexpr (is_dual<T>::value) {
+    if (!c.hard_ops) {  // Dual: the double formula + its analytic derivative
+      const double xv = x.v;  // d clip / dx = sigma(x/tau) - sigma((x-1)/tau)
+      const double a = exp_d(-fabs(xv) * c.inv_tau_clip);
+      const double b = partner_exp(xv, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
+      const double ia = rcp_d(1.0 + a), ib = rcp_d(1.0 + b);
+      const double corr = c.tau_clip * log_d((1.0 + a) * ib);
+      const double s1 = xv >= 0.0 ? ia : a * ia, s2 = xv >= 1.0 ? ib : b * ib;
+      return T::chain((fmax(xv, 0.0) - fmax(xv - 1.0, 0.0)) + corr, s1 - s2, x);
+    }
+  }
   if (c.hard_ops) return fmin(fmax(x, T(0.0)), T(1.0));
   const I xi = to_ind<I>(x);
   const I a = exp_d(-fabs(xi) * I(c.inv_tau_clip));
@@ -67,15 +78,29 @@ __device__ __forceinline__ void within01(const T& x, double inv_tau, double C, d
     *omg = in ? 0.0 : 1.0;
     return;
   }
-  const I xi = to_ind<I>(x);
-  const I e1 = exp_d(-fabs(xi) * I(inv_tau));               // sigma(x/tau) pair
-  const I e2 = partner_exp(xi, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
-  const I i1 = rcp_d(I(1.0) + e1), i2 = rcp_d(I(1.0) + e2);
-  const bool ge0 = pv(x) >= 0.0, le1 = pv(x) <= 1.0;
-  const I s1 = ge0 ? i1 : e1 * i1, c1 = ge0 ? e1 * i1 : i1;
-  const I s2 = le1 ? i2 : e2 * i2, c2 = le1 ? e2 * i2 : i2;
-  *g = s1 * s2;
-  *omg = c1 + s1 * c2;
+  if constexpr (is_dual<T>::value && std::is_same_v<T, I>) {
+    // Dual: the double formula + d gamma / dx = gamma (c1 - c2) / tau
+    const double xv = x.v;
+    const double e1 = exp_d(-fabs(xv) * inv_tau), e2 = partner_exp(xv, e1, C, inv_C, inv_tau, pair);
+    const double i1 = rcp_d(1.0 + e1), i2 = rcp_d(1.0 + e2);
+    const double s1 = xv >= 0.0 ? i1 : e1 * i1, s2 = xv <= 1.0 ? i2 : e2 * i2;
+    const double c1 = xv >= 0.0 ? e1 * i1 : i1, c2 = xv <= 1.0 ? e2 * i2 : i2;
+    const double gv = s1 * s2, ov = c1 + s1 * c2;
+    const double dg = gv * (c1 - c2) * inv_tau;
+    *g = I::chain(gv, dg, x);
+    *omg = I::chain(ov, -dg, x);
+    return;
+  } else {
+    const I xi = to_ind<I>(x);
+    const I e1 = exp_d(-fabs(xi) * I(inv_tau));               // sigma(x/tau) pair
+    const I e2 = partner_exp(xi, e1, C, inv_C, inv_tau, pair);  // sigma((1-x)/tau) pair
+    const I i1 = rcp_d(I(1.0) + e1), i2 = rcp_d(I(1.0) + e2);
+    const bool ge0 = pv(x) >= 0.0, le1 = pv(x) <= 1.0;
+    const I s1 = ge0 ? i1 : e1 * i1, c1 = ge0 ? e1 * i1 : i1;
+    const I s2 = le1 ? i2 : e2 * i2, c2 = le1 ? e2 * i2 : i2;
+    *g = s1 * s2;
+    *omg = c1 + s1 * c2;
+  }
 }
 
 // Product of indicators and its complement: 1 - ab = (1 - a) + a (1 - b).
@@ -91,6 +116,40 @@ __device__ __forceinline__ void within_and(const I& a, const I& oma, const I& b,
 // Costs in T; weights in I from the T-exact differences m - cost_i.
 template <int N, class T, class I>
 __device__ __forceinline__ int pick_min(const T (&cost)[N], I (&w)[N], double inv_tau, int hard) {
+  if constexpr (is_dual<T>::value && std::is_same_v<T, I>) {
+    if (!hard) {  // Dual: primal softmin weights, dw_i = w_i (sum_j w_j dc_j - dc_i) / tau
+      int best = 0;
+      double m = cost[0].v;
+#pragma unroll
+      for (int i = 1; i < N; ++i)
+        if (cost[i].v < m) {
+          best = i;
+          m = cost[i].v;
+        }
+      double wv[N], total = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        wv[i] = i == best ? 1.0 : exp_d((m - cost[i].v) * inv_tau);
+        total += wv[i];
+      }
+      const double inv = rcp_d(total);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        wv[i] *= inv;
+        w[i].v = wv[i];
+      }
+      constexpr int ND = sizeof(cost[0].d) / sizeof(double);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        double avg = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) avg = fma(wv[j], cost[j].d[d], avg);
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i].d[d] = wv[i] * inv_tau * (avg - cost[i].d[d]);
+      }
+      return best;
+    }
+  }
   int best = 0;
   T m = cost[0];
 #pragma unroll
