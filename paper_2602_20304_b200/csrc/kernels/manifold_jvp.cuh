@@ -719,22 +719,48 @@ __global__ void __launch_bounds__(kJvpThreads, kJvpMinBlocks) manifold_jvp_kerne
       e.bw[0] = bw.x; e.bw[1] = bw.y; e.bw[2] = bw.z;
       put3(e.a, a);
       put3(e.b, b);
+      if (!sel)  // pass-through: constant body endpoints
+#pragma unroll 1
+        for (int j = 0; j < 12; ++j) {
+          put3d(e.a, d3(0, 0, 0), j);
+          put3d(e.b, d3(0, 0, 0), j);
+        }
     } else {
-      put3(u.vslot(r0), fR(F, a) + ft(F));
+      const double3 aw = fR(F, a) + ft(F);
+      T12* v = u.vslot(r0);
+      put3(v, aw);
+      if (!sel)  // pass-through: the vertex moves with its body
+#pragma unroll 1
+        for (int j = 0; j < 12; ++j) put3d(v, j / 6 == q.s ? u.uvel(j, aw) : d3(0, 0, 0), j);
     }
   }
   JVP_PHASE_MARK(4);
-  for (int it = tid; it < n_here * nsl * 12; it += nth) {
-    const int k = it / (nsl * 12), rr = it - k * nsl * 12;
-    const int r0 = rr / 12, j = rr - (rr / 12) * 12;
+  // D2: tangents of the soft top-K slots only, one item per (slot, direction)
+  const int nss = (S1.topk_v ? n1 : 0) + (S2.topk_v ? n2 : 0) + (S1.topk_e ? m1 : 0) + (S2.topk_e ? m2 : 0);
+  auto sel_slot = [&](int r) {  // r-th soft top-K slot -> slot index
+    if (S1.topk_v) {
+      if (r < n1) return r;
+      r -= n1;
+    }
+    if (S2.topk_v) {
+      if (r < n2) return n1 + r;
+      r -= n2;
+    }
+    if (S1.topk_e) {
+      if (r < m1) return n1 + n2 + r;
+      r -= m1;
+    }
+    return n1 + n2 + m1 + r;
+  };
+  for (int it = tid; it < n_here * nss * 12; it += nth) {
+    const int k = it / (nss * 12), rr = it - k * nss * 12;
+    const int r0 = sel_slot(rr / 12), j = rr - (rr / 12) * 12;
     const EnvUnit u = unit(k);
     const SlotId q = slot_id(r0);
-    const DevSide& S = q.s == 0 ? S1 : S2;
-    const bool sel = q.is_edge ? S.topk_e : S.topk_v;
     ESlot* es = q.is_edge ? &u.eslot(r0 - n1 - n2) : nullptr;
     T12* vs = q.is_edge ? nullptr : u.vslot(r0);
     double3 da = d3(0, 0, 0), db = d3(0, 0, 0);
-    if (sel) {
+    {
       // w_i = e_i / tot, d e_i = e_i u_i, u_i = (d m - d|s_r - x_i|) / tau:
       //   d a = (sum e_i u_i v_i - (sum e_i u_i) a) / tot
       const int lo = set_lo(q.set), D = set_hi(q.set) - lo;
