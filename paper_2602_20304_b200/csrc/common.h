@@ -127,6 +127,7 @@ struct ManifoldParams {
   int32_t* src;
   float* ee;
   float* mean_dist;
+  int32_t vs_ext;       // 1: V-S contacts (and their share of mean_dist) come from vs_kernel, launched first
   double* pairs_gmem;   // pair records in global memory ([n_env][pair_stride] doubles), or null = shared
   int64_t pair_stride;  // doubles per env in pairs_gmem
 };

@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     }
     if constexpr (!kVsE) {
       const int vs0 = ((nF + 31) & ~31) % nth;  // first thread of the first warp after the NN items
-      for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < n_here * nvs; it += nth) {
+      for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < (p.vs_ext ? 0 : n_here * nvs); it += nth) {
         int e, r;
         fdivmod(it, p.div_nvs, e, r);
         const EnvView ev = env(e);
@@ -585,7 +585,11 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     for (int e = warp; e < n_here; e += nwarps) {
       const EnvView ev = env(e);
       double acc = 0.0;
-      for (int r = lane; r < n1 + n2; r += 32) acc += (double)ev.vsdist()[r];
+      if (p.vs_ext) {  // vs_kernel left the V-S share (its fixed-order sum) in mean_dist
+        if (lane == 0) acc = (double)p.mean_dist[env0 + e];
+      } else {
+        for (int r = lane; r < n1 + n2; r += 32) acc += (double)ev.vsdist()[r];
+      }
       if (full)
         for (int i = lane; i < P; i += 32) {
           const double* rec = ev.pair(i);
@@ -596,6 +600,42 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       if (lane == 0) p.mean_dist[env0 + e] = (float)(acc / (double)C);
     }
   }
+}
+
+// V-S contacts of pass-through vertex sets as their own launch (box-box): G
+// lanes per env (a power of two >= n1 + n2), frames from the workspace, the
+// env's V-S distance sum (fixed shuffle order) left in mean_dist for the
+// manifold kernel's H phase. Keeps the ~1/6-pair V-S items off the manifold
+// CTAs, whose F phase then holds only the short NN statistics.
+template <int K1, int K2>
+__global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ ManifoldParams p, int G) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e = gt / G;
+  const int r = (int)(gt - e * G);
+  const int n1 = p.n1, nvs = p.n1 + p.n2, C = p.n_contacts;
+  const bool act = e < p.n_env && r < nvs;
+  double d = 0.0;
+  if (act) {
+    const int s = r < n1 ? 0 : 1;
+    const int vi = s == 0 ? r : r - n1;
+    const double* f1 = p.frames1 + 12 * e * p.stride1;
+    const double* f2 = p.frames2 + 12 * e * p.stride2;
+    const double* fs = s == 0 ? f1 : f2;
+    const double* fo = s == 0 ? f2 : f1;
+    const double3 pw = to_world(fs, fs + 9, ld_vert(p.side[s].verts, vi));
+    float dist;
+    float* dst = p.contacts + (e * C + r) * 8;
+    if (s == 0) vs_contact<K2>(p.side[1].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
+    else vs_contact<K1>(p.side[0].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
+    if (p.src) {
+      int* sp = p.src + (e * C + r) * 2;
+      sp[0] = vi;
+      sp[1] = -1;
+    }
+    d = (double)dist;
+  }
+  for (int o = G >> 1; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  if (act && r == 0 && p.mean_dist) p.mean_dist[e] = (float)d;
 }
 
 int launch_frames(const double* poses, int64_t stride, int64_t n, double* frames, cudaStream_t s) {
@@ -640,6 +680,18 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
     return 1;
   if (p.pairs_gmem)  // the generic interpreter evaluates every SDF kind
     return launch_kind<kGeneric, kGeneric, true>(p, block_threads, grid, smem_bytes, s);
+  const int nvs = p.n1 + p.n2;
+  if (p.side[0].sdf.kind == kSqE01 && p.side[1].sdf.kind == kSqE01 && !p.side[0].topk_v && !p.side[1].topk_v &&
+      nvs > 0 && nvs <= 32) {
+    ManifoldParams q = p;
+    q.vs_ext = 1;
+    int G = 1;
+    while (G < nvs) G <<= 1;
+    const int64_t threads = p.n_env * G;
+    vs_kernel<kSqE01, kSqE01><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(q, G);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+    return launch_k2<kSqE01>(q, block_threads, grid, smem_bytes, s);
+  }
   switch (p.side[0].sdf.kind) {
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
     case kSingleSq: return launch_k2<kSingleSq>(p, block_threads, grid, smem_bytes, s);
