@@ -280,7 +280,7 @@ struct HostScratch {
 };
 
 // Smallest env chunk worth its own pipeline stage of the host-buffer API.
-constexpr int64_t kHostChunkMin = 8192;
+constexpr int64_t kHostChunkMin = 2048;
 
 size_t workspace_doubles(int64_t n_env, int st1, int st2) {
   return 12 * (size_t)((st1 ? n_env : 1) + (st2 ? n_env : 1));
@@ -630,8 +630,20 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
       cuda_check(cudaEventCreateWithFlags(&sc.ev_start, cudaEventDisableTiming), "cudaEventCreate");
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, n_env / kHostChunkMin));
-    const int64_t per = (n_env + nchunk - 1) / nchunk;
+    // Two chunks: a small lead chunk whose pose upload is the only exposed
+    // copy, then the rest, uploaded while the lead chunk computes (equal
+    // chunks pay a wave-quantisation tail and launch gaps per chunk: measured
+    // box-box 65,536 envs, 8 equal chunks 48.8 M/s, 4 50.3; lead 1/16, 1/8,
+    // 1/4 of the envs: 51.3, 51.4, 50.9).
+    constexpr int64_t lead_div = 8;
+    int64_t bounds[3] = {0, n_env, n_env};
+    int nchunk = 1;
+    if (n_env >= 2 * kHostChunkMin) {
+      bounds[1] = std::max(kHostChunkMin, n_env / lead_div);
+      nchunk = 2;
+    }
+    int64_t per = 0;
+    for (int c = 0; c < nchunk; ++c) per = std::max(per, bounds[c + 1] - bounds[c]);
     ensure(&sc.frames, &sc.cap_frames, 2 * workspace_doubles(per, st1, st2));
     cuda_check(cudaEventRecord(sc.ev_start, s), "cudaEventRecord");
     for (int k = 0; k < 2; ++k) cuda_check(cudaStreamWaitEvent(sc.q[k], sc.ev_start, 0), "cudaStreamWaitEvent");
@@ -646,8 +658,8 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     cuda_check(cudaEventRecord(sc.ev[0], sc.q[0]), "cudaEventRecord");
     cuda_check(cudaStreamWaitEvent(sc.q[1], sc.ev[0], 0), "cudaStreamWaitEvent");
     const size_t C = (size_t)L.n_contacts;
-    for (int64_t c = 0; c < nchunk; ++c) {
-      const int64_t e0 = c * per, ne = std::min(per, n_env - e0);
+    for (int c = 0; c < nchunk; ++c) {
+      const int64_t e0 = bounds[c], ne = bounds[c + 1] - e0;
       if (ne <= 0) break;
       cudaStream_t q = sc.q[c & 1];
       double* p1 = sc.poses1 + (st1 ? 6 * e0 : 0);
