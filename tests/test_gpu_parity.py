@@ -115,10 +115,11 @@ def test_host_api_matches_device_api(cuda):
     assert np.array_equal(mean, dev["mean_dist"]) and np.array_equal(contacts, dev["contacts"])
 
 
-@pytest.mark.parametrize("n", [20001, 33333])
+@pytest.mark.parametrize("n", [4095, 4099, 20001, 33333])
 def test_host_api_pipelined_chunks(cuda, n):
-    """The host-buffer call pipelines env chunks over two streams (2 / 4 uneven
-    chunks here): results equal the device call bit for bit."""
+    """The host-buffer call pipelines a lead chunk (1/8 of the envs, at least
+    2,048) and the rest over two streams (one chunk below 4,096 envs): results
+    equal the device call bit for bit."""
     ws = W.box_box(n)
     p1, p2 = ws.poses(n)
     s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
