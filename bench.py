@@ -426,7 +426,7 @@ def main():
                 "h2d_bytes_per_step": int(h1.nbytes + h2.nbytes) * world,
                 "d2h_bytes_per_step": int(mean_h.nbytes) * world,
                 "path": "cmgb_manifold_batch_host (pinned host poses -> H2D -> kernel -> D2H mean distance)"},
-        "gpu_launches": 4 * args.steps,  # per step: frames_kernel x2 (one per body) + vs_kernel + manifold_kernel
+        "gpu_launches": 3 * args.steps,  # per step: frames_kernel (both bodies) + vs_kernel + manifold_kernel
         "roofline": roof,
         "cpu_baseline": cb,
         "clocks": clk,

@@ -243,15 +243,20 @@ __device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
 // thread each, ahead of the manifold kernel: keeps the FP64 sincos latency
 // chain off the manifold CTAs' critical path (they would otherwise idle at
 // the first barrier while 4 threads evaluate it).
-__global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ poses, int64_t stride,
-                                                     int64_t n, double* __restrict__ frames) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ poses1, int64_t stride1, int64_t n1,
+                                                     double* __restrict__ frames1, const double* __restrict__ poses2,
+                                                     int64_t stride2, int64_t n2, double* __restrict__ frames2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n1 + n2) return;
+  const bool second = i >= n1;  // both bodies' poses in one launch
+  if (second) i -= n1;
+  const double* poses = second ? poses2 : poses1;
+  const int64_t stride = second ? stride2 : stride1;
   double xi[6], R[9], t[3];
 #pragma unroll
   for (int k = 0; k < 6; ++k) xi[k] = __ldg(poses + stride * i + k);
   se3_exp_d(xi, R, t);
-  double* f = frames + 12 * i;
+  double* f = (second ? frames2 : frames1) + 12 * i;
 #pragma unroll
   for (int k = 0; k < 9; ++k) f[k] = R[k];
   f[9] = t[0];
@@ -638,9 +643,11 @@ __global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ Manifol
   if (act && r == 0 && p.mean_dist) p.mean_dist[e] = (float)d;
 }
 
-int launch_frames(const double* poses, int64_t stride, int64_t n, double* frames, cudaStream_t s) {
-  if (n <= 0) return 0;
-  frames_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(poses, stride, n, frames);
+int launch_frames(const double* poses1, int64_t stride1, int64_t n1, double* frames1, const double* poses2,
+                  int64_t stride2, int64_t n2, double* frames2, cudaStream_t s) {
+  if (n1 + n2 <= 0) return 0;
+  frames_kernel<<<(unsigned)((n1 + n2 + 255) / 256), 256, 0, s>>>(poses1, stride1, n1, frames1, poses2, stride2, n2,
+                                                                  frames2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -675,8 +682,8 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n1 = p.stride1 ? p.n_env : 1, n2 = p.stride2 ? p.n_env : 1;
-  if (launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), s) ||
-      launch_frames(p.poses2, p.pose_stride2, n2, const_cast<double*>(p.frames2), s))
+  if (launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), p.poses2, p.pose_stride2, n2,
+                    const_cast<double*>(p.frames2), s))
     return 1;
   if (p.pairs_gmem)  // the generic interpreter evaluates every SDF kind
     return launch_kind<kGeneric, kGeneric, true>(p, block_threads, grid, smem_bytes, s);
