@@ -265,8 +265,9 @@ __global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ 
 }
 
 // kGP: pair records in the global workspace (p.pairs_gmem; large pass-through
-// pair sets, one generic instantiation) instead of shared memory.
-template <int K1, int K2, bool kGP = false>
+// pair sets, one generic instantiation) instead of shared memory. kVsX: the
+// V-S contacts come from vs_kernel (box-box, pass-through vertex sets; p.vs_ext).
+template <int K1, int K2, bool kGP = false, bool kVsX = false>
 __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     manifold_kernel(const __grid_constant__ ManifoldParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     }
     if constexpr (!kVsE) {
       const int vs0 = ((nF + 31) & ~31) % nth;  // first thread of the first warp after the NN items
-      for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < (p.vs_ext ? 0 : n_here * nvs); it += nth) {
+      for (int it = tid >= vs0 ? tid - vs0 : tid - vs0 + nth; it < (kVsX ? 0 : n_here * nvs); it += nth) {
         int e, r;
         fdivmod(it, p.div_nvs, e, r);
         const EnvView ev = env(e);
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     for (int e = warp; e < n_here; e += nwarps) {
       const EnvView ev = env(e);
       double acc = 0.0;
-      if (p.vs_ext) {  // vs_kernel left the V-S share (its fixed-order sum) in mean_dist
+      if constexpr (kVsX) {  // vs_kernel left the V-S share (its fixed-order sum) in mean_dist
         if (lane == 0) acc = (double)p.mean_dist[env0 + e];
       } else {
         for (int r = lane; r < n1 + n2; r += 32) acc += (double)ev.vsdist()[r];
@@ -651,13 +652,14 @@ int launch_frames(const double* poses1, int64_t stride1, int64_t n1, double* fra
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-template <int K1, int K2, bool kGP = false>
+template <int K1, int K2, bool kGP = false, bool kVsX = false>
 int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   static PerDeviceOnce configured;
   configured([] {  // per device: the attribute does not carry across devices
-    cudaFuncSetAttribute(manifold_kernel<K1, K2, kGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(manifold_kernel<K1, K2, kGP, kVsX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
   });
-  manifold_kernel<K1, K2, kGP><<<grid, threads, smem, s>>>(p);
+  manifold_kernel<K1, K2, kGP, kVsX><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -697,7 +699,7 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
     const int64_t threads = p.n_env * G;
     vs_kernel<kSqE01, kSqE01><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(q, G);
     if (cudaGetLastError() != cudaSuccess) return 1;
-    return launch_k2<kSqE01>(q, block_threads, grid, smem_bytes, s);
+    return launch_kind<kSqE01, kSqE01, false, true>(q, block_threads, grid, smem_bytes, s);
   }
   switch (p.side[0].sdf.kind) {
     case kSqE01: return launch_k2<kSqE01>(p, block_threads, grid, smem_bytes, s);
