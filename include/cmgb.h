@@ -199,11 +199,43 @@ int cmgb_manifold_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1,
 
 /* End-to-end variant: HOST poses in, HOST mean distances (and optionally HOST
  * contacts) out; copies happen inside the call on the given stream, which is
- * synchronised before returning. Device scratch is cached per surface pair. */
+ * synchronised before returning (also when the call fails). Device scratch comes
+ * from a per-device pool: each call leases its own buffers and pipeline
+ * streams, so concurrent host threads do not serialise on each other. When
+ * contacts_host is given the batch is pipelined in equal chunks so each chunk's
+ * D2H overlaps the next chunk's kernels (host buffers should be pinned). */
 int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
                              int32_t pose1_stride, const double* poses2_host,
                              int32_t pose2_stride, int64_t n_env, const cmgb_config* cfg,
                              float* mean_dist_host, float* contacts_host, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * Active-contact compaction — an EXTRA output beside the fixed layout (which it
+ * never replaces; manifold.hpp:62-72, 303-330): the contacts of a batch with
+ * activity > activity_threshold, in fixed-layout order, packed env after env
+ * (one TMA-staged pass over the fixed layout, warp ballots, decoupled
+ * look-back scan across env tiles). All buffers are DEVICE memory.
+ * ------------------------------------------------------------------------- */
+typedef struct cmgb_compact_out {
+  float* contacts;      /* required: [capacity][8] kept contacts (px,py,pz,dist,nx,ny,nz,activity) */
+  int32_t* slot;        /* optional: [capacity] slot of each kept contact in its env's fixed layout
+                           (kind / side / static provenance: cmgb_layout_metadata)               */
+  int32_t* src;         /* optional: [capacity][2] provenance (needs the batch's src output)     */
+  int64_t* env_offset;  /* optional: [n_env + 1] first kept row of each env; [n_env] = total     */
+  int32_t* env_count;   /* optional: [n_env] kept contacts per env                               */
+  int64_t* total;       /* optional: [1] kept contacts in the batch (rows beyond capacity are
+                           counted but not written)                                               */
+  int64_t capacity;     /* rows available in contacts / slot / src (n_env * n_contacts never overflows) */
+  void* workspace;      /* optional: cmgb_compact_workspace_bytes() of device scratch, else pooled */
+  size_t workspace_bytes;
+} cmgb_compact_out;
+
+size_t cmgb_compact_workspace_bytes(int64_t n_env, int32_t n_contacts);
+
+/* contacts: DEVICE [n_env][n_contacts][8] (a cmgb_manifold_batch output, 16-byte
+ * aligned); src: optional DEVICE [n_env][n_contacts][2]. Stream-ordered. */
+int cmgb_compact_contacts(const float* contacts, const int32_t* src, int64_t n_env, int32_t n_contacts,
+                          float activity_threshold, const cmgb_compact_out* out, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * Pose Jacobians — generate_manifold<Dual12> with seed_pose_tangents

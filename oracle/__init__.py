@@ -279,6 +279,11 @@ class Ref:
             L.cmgref_so3_exp.argtypes = [_D, _D]
             L.cmgref_soft_topk.argtypes = [_D, C.c_int, C.c_int, C.c_double, _D]
             L.cmgref_config_validate.argtypes = [C.POINTER(abi.CmgbConfig)]
+            L.cmgref_opcount_manifold.argtypes = [_P, _P, _D, _D, C.POINTER(abi.CmgbConfig), C.c_int,
+                                                  C.POINTER(C.c_int64)]
+            L.cmgref_scene_bench.argtypes = [C.POINTER(_P), C.c_int, _I32, C.c_int, _D, C.c_int64,
+                                             C.POINTER(abi.CmgbConfig), C.c_int, C.c_int, C.c_int, C.c_int,
+                                             _D, _D, _D]
             cls._lib = L
         return cls._lib
 
@@ -547,6 +552,39 @@ class Ref:
                                            C.byref(med), C.byref(sd)):
             raise ValueError(Ref.err())
         return med.value, sd.value
+
+    OPCOUNT_KINDS = ("arith", "pow", "sqrt", "exp", "log", "tanh", "other")
+
+    @staticmethod
+    def opcount_manifold(s1, s2, pose1, pose2, cfg=None, jvp=False) -> dict:
+        """SURVEY Appendix B's op counter: the reference's generate_manifold<T>
+        with a counting scalar (jvp: Dual<12, counting scalar>). W = arith +
+        every transcendental, 1 op each."""
+        c = _cfg(cfg)
+        p1 = np.ascontiguousarray(pose1, dtype=np.float64).reshape(6)
+        p2 = np.ascontiguousarray(pose2, dtype=np.float64).reshape(6)
+        out = (C.c_int64 * 7)()
+        Ref.lib().cmgref_opcount_manifold(s1.h, s2.h, _dp(p1), _dp(p2), C.byref(c), int(bool(jvp)), out)
+        d = {k: int(out[i]) for i, k in enumerate(Ref.OPCOUNT_KINDS)}
+        d["transcendental"] = sum(d[k] for k in Ref.OPCOUNT_KINDS[1:])
+        d["W"] = d["arith"] + d["transcendental"]
+        return d
+
+    @staticmethod
+    def scene_bench(surfaces, pairs, poses, cfg=None, jvp=False, reps=3, warmups=1, workers=None):
+        """Config D's CPU reference: every pair of every env through
+        generate_manifold<double> / <Dual12>, std::thread chunks, time_run
+        median / std (s). poses [n_env, n_bodies, 6]."""
+        c = _cfg(cfg)
+        P = np.ascontiguousarray(poses, dtype=np.float64)
+        pr = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        hs = (_P * len(surfaces))(*[s.h for s in surfaces])
+        med, sd, cs = C.c_double(), C.c_double(), C.c_double()
+        if Ref.lib().cmgref_scene_bench(hs, len(surfaces), _ip(pr), len(pr), _dp(P), P.shape[0], C.byref(c),
+                                        int(bool(jvp)), reps, warmups, workers or os.cpu_count(),
+                                        C.byref(med), C.byref(sd), C.byref(cs)):
+            raise ValueError(Ref.err())
+        return med.value, sd.value, cs.value
 
     @staticmethod
     def bench_witness(kind, batch, variant="ours", seed=0, reps=3, workers=None):

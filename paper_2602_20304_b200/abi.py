@@ -95,6 +95,20 @@ class CmgbManifoldOut(C.Structure):
     ]
 
 
+class CmgbCompactOut(C.Structure):
+    _fields_ = [
+        ("contacts", C.c_void_p),
+        ("slot", C.c_void_p),
+        ("src", C.c_void_p),
+        ("env_offset", C.c_void_p),
+        ("env_count", C.c_void_p),
+        ("total", C.c_void_p),
+        ("capacity", C.c_int64),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
+    ]
+
+
 class CmgbManifoldJvpOut(C.Structure):
     _fields_ = [
         ("contacts", C.c_void_p),
@@ -204,6 +218,11 @@ SIGNATURES = {
          C.c_int64, _P, _P, _P, _P, _P, C.c_size_t, _P],
     ),
     "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
+    "cmgb_compact_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
+    "cmgb_compact_contacts": (
+        _I,
+        [_P, _P, C.c_int64, C.c_int32, C.c_float, C.POINTER(CmgbCompactOut), _P],
+    ),
     "cmgb_manifold_scene_batch": (
         _I,
         [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig),

@@ -156,6 +156,41 @@ def layout_metadata(s1: Surface, s2: Surface, cfg=None) -> np.ndarray:
     return meta.T.copy()
 
 
+def _pose_rows(r1: int, r2: int):
+    """(n, stride1, stride2) for pose arrays of r1 / r2 rows: each must have n
+    rows (one pose per env) or exactly 1 row (shared by every env)."""
+    n = max(r1, r2)
+    for r in (r1, r2):
+        if r != n and r != 1:
+            raise ValueError(f"pose arrays must have n_env rows or 1 row (got {r1} and {r2})")
+    if n == 1:
+        return 1, 1, 1
+    return n, int(r1 == n), int(r2 == n)
+
+
+def _cuda_tensor(t, dtypes, what: str):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype not in dtypes:
+        names = " or ".join(str(d).replace("torch.", "") for d in dtypes)
+        raise ValueError(f"{what} must be a CUDA {names} tensor")
+    return t
+
+
+def _reuse(res: dict, key: str, shape, dtype, device):
+    """res[key] if it is a tensor of exactly this shape / dtype / device, else a
+    fresh one (a buffer left from a larger batch or another surface pair must
+    never be written past its end)."""
+    import torch
+
+    t = res.get(key)
+    if not (isinstance(t, torch.Tensor) and tuple(t.shape) == tuple(shape) and t.dtype == dtype
+            and t.device == device and t.is_contiguous()):
+        t = torch.empty(shape, dtype=dtype, device=device)
+        res[key] = t
+    return t
+
+
 def _stream_ptr(stream) -> Optional[int]:
     import torch
 
@@ -173,43 +208,82 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
     import torch
 
     c = _cfg(cfg)
-    p1 = poses1.reshape(-1, 6)
-    p2 = poses2.reshape(-1, 6)
-    if p1.dtype != torch.float64 or p2.dtype != torch.float64 or not p1.is_cuda or not p2.is_cuda:
-        raise ValueError("poses must be CUDA float64 tensors")
-    p1 = p1.contiguous()
-    p2 = p2.contiguous()
-    n = max(p1.shape[0], p2.shape[0])
-    st1 = 1 if (p1.shape[0] == n and n > 1) else 0
-    st2 = 1 if (p2.shape[0] == n and n > 1) else 0
-    if n == 1:
-        st1 = st2 = 1
+    p1 = _cuda_tensor(poses1, (torch.float64,), "poses1").reshape(-1, 6).contiguous()
+    p2 = _cuda_tensor(poses2, (torch.float64,), "poses2").reshape(-1, 6).contiguous()
+    n, st1, st2 = _pose_rows(p1.shape[0], p2.shape[0])
     L = layout(s1, s2, c)
     Cn = L["n_contacts"]
     P = L["m1"] * L["m2"]
     dev = p2.device
     res = out if out is not None else {}
-    if "contacts" not in res:
-        res["contacts"] = torch.empty((n, Cn, 8), dtype=torch.float32, device=dev)
-    if want_src and "src" not in res:
-        res["src"] = torch.empty((n, Cn, 2), dtype=torch.int32, device=dev)
-    if want_ee and P > 0 and "ee" not in res:
-        res["ee"] = torch.empty((n, 9, P), dtype=torch.float32, device=dev)
-    if want_mean and "mean_dist" not in res:
-        res["mean_dist"] = torch.empty((n,), dtype=torch.float32, device=dev)
+    contacts = _reuse(res, "contacts", (n, Cn, 8), torch.float32, dev)
+    src = _reuse(res, "src", (n, Cn, 2), torch.int32, dev) if want_src else None
+    ee = _reuse(res, "ee", (n, 9, P), torch.float32, dev) if (want_ee and P > 0) else None
+    mean = _reuse(res, "mean_dist", (n,), torch.float32, dev) if want_mean else None
     ws = abi.load().cmgb_manifold_workspace_bytes(n, st1, st2)
-    if "workspace" not in res or res["workspace"].numel() < ws:
+    wsb = res.get("workspace")
+    if not (isinstance(wsb, torch.Tensor) and wsb.device == dev and wsb.dtype == torch.uint8 and wsb.numel() >= ws):
         res["workspace"] = torch.empty((max(ws, 8),), dtype=torch.uint8, device=dev)
     o = abi.CmgbManifoldOut()
-    o.contacts = res["contacts"].data_ptr()
-    o.src = res["src"].data_ptr() if "src" in res else None
-    o.ee = res["ee"].data_ptr() if "ee" in res else None
-    o.mean_dist = res["mean_dist"].data_ptr() if "mean_dist" in res else None
+    o.contacts = contacts.data_ptr()
+    o.src = src.data_ptr() if src is not None else None
+    o.ee = ee.data_ptr() if ee is not None else None
+    o.mean_dist = mean.data_ptr() if mean is not None else None
     o.workspace = res["workspace"].data_ptr()
     o.workspace_bytes = res["workspace"].numel()
     with torch.cuda.device(dev):
         _ok(abi.load().cmgb_manifold_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
                                            C.byref(c), C.byref(o), _stream_ptr(stream)))
+    return res
+
+
+def compact_contacts(contacts, activity_threshold: float, *, src=None, capacity: Optional[int] = None,
+                     out: Optional[dict] = None, stream=None) -> dict:
+    """Active-contact compaction (an extra output; the fixed layout stays as
+    it is): the contacts of a batch with activity > activity_threshold, in
+    fixed-layout order, env after env. contacts: CUDA float32 [n, C, 8] from
+    generate_manifold_batch (src: its optional [n, C, 2] provenance). Returns
+    CUDA tensors: contacts [capacity, 8] (rows >= total unused), slot
+    [capacity] (index in the env's fixed layout), src [capacity, 2] (when src is
+    given), env_offset [n + 1] (int64; env_offset[n] = total), env_count [n],
+    total [1] (int64)."""
+    import torch
+
+    c = _cuda_tensor(contacts, (torch.float32,), "contacts")
+    if c.dim() != 3 or c.shape[2] != 8 or not c.is_contiguous():
+        raise ValueError("contacts must be a contiguous [n_env, n_contacts, 8] tensor")
+    n, Cn = int(c.shape[0]), int(c.shape[1])
+    if src is not None:
+        _cuda_tensor(src, (torch.int32,), "src")
+        if tuple(src.shape) != (n, Cn, 2) or not src.is_contiguous():
+            raise ValueError("src must be a contiguous [n_env, n_contacts, 2] int32 tensor")
+    cap = n * Cn if capacity is None else int(capacity)
+    dev = c.device
+    res = out if out is not None else {}
+    oc = _reuse(res, "contacts", (cap, 8), torch.float32, dev)
+    slot = _reuse(res, "slot", (cap,), torch.int32, dev)
+    osrc = _reuse(res, "src", (cap, 2), torch.int32, dev) if src is not None else None
+    offs = _reuse(res, "env_offset", (n + 1,), torch.int64, dev)
+    cnt = _reuse(res, "env_count", (n,), torch.int32, dev)
+    tot = _reuse(res, "total", (1,), torch.int64, dev)
+    lib = abi.load()
+    ws = lib.cmgb_compact_workspace_bytes(n, Cn)
+    wsb = res.get("workspace")
+    if not (isinstance(wsb, torch.Tensor) and wsb.device == dev and wsb.numel() >= ws):
+        res["workspace"] = torch.empty((max(ws, 16),), dtype=torch.uint8, device=dev)
+    o = abi.CmgbCompactOut()
+    o.contacts = oc.data_ptr()
+    o.slot = slot.data_ptr()
+    o.src = osrc.data_ptr() if osrc is not None else None
+    o.env_offset = offs.data_ptr()
+    o.env_count = cnt.data_ptr()
+    o.total = tot.data_ptr()
+    o.capacity = cap
+    o.workspace = res["workspace"].data_ptr()
+    o.workspace_bytes = res["workspace"].numel()
+    with torch.cuda.device(dev):
+        _ok(lib.cmgb_compact_contacts(c.data_ptr(), src.data_ptr() if src is not None else None, n, Cn,
+                                      float(activity_threshold), C.byref(o), _stream_ptr(stream)))
     return res
 
 
@@ -223,17 +297,9 @@ def generate_manifold_jvp_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=No
     import torch
 
     c = _cfg(cfg)
-    p1 = poses1.reshape(-1, 6)
-    p2 = poses2.reshape(-1, 6)
-    if p1.dtype != torch.float64 or p2.dtype != torch.float64 or not p1.is_cuda or not p2.is_cuda:
-        raise ValueError("poses must be CUDA float64 tensors")
-    p1 = p1.contiguous()
-    p2 = p2.contiguous()
-    n = max(p1.shape[0], p2.shape[0])
-    st1 = 1 if (p1.shape[0] == n and n > 1) else 0
-    st2 = 1 if (p2.shape[0] == n and n > 1) else 0
-    if n == 1:
-        st1 = st2 = 1
+    p1 = _cuda_tensor(poses1, (torch.float64,), "poses1").reshape(-1, 6).contiguous()
+    p2 = _cuda_tensor(poses2, (torch.float64,), "poses2").reshape(-1, 6).contiguous()
+    n, st1, st2 = _pose_rows(p1.shape[0], p2.shape[0])
     Cn = layout(s1, s2, c)["n_contacts"]
     dev = p2.device
     res = {
@@ -267,7 +333,7 @@ def sdf_query(surface: Surface, points, flavor: int = 1, stream=None):
     source (2) or value only (0)."""
     import torch
 
-    pts = points.reshape(-1, 3).contiguous()
+    pts = _cuda_tensor(points, (torch.float64,), "points").reshape(-1, 3).contiguous()
     out = torch.empty((pts.shape[0], 4), dtype=torch.float64, device=pts.device)
     with torch.cuda.device(pts.device):
         _ok(abi.load().cmgb_sdf_query(surface._h, int(flavor), pts.data_ptr(), pts.shape[0], out.data_ptr(),
@@ -280,9 +346,9 @@ def sphere_trace(surface: Surface, pose, points, iters: int = 5, tau: float = 1e
     float64) against the surface posed by pose [6]."""
     import torch
 
-    pts = points.reshape(-1, 3).contiguous()
-    pose = np.ascontiguousarray(pose, dtype=np.float64)
-    out = torch.empty_like(pts)
+    pts = _cuda_tensor(points, (torch.float64,), "points").reshape(-1, 3).contiguous()
+    pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(6)
+    out = torch.empty(pts.shape, dtype=torch.float64, device=pts.device)
     with torch.cuda.device(pts.device):
         _ok(abi.load().cmgb_sphere_trace(surface._h, pose.ctypes.data, pts.data_ptr(), pts.shape[0], int(iters),
                                          float(tau), out.data_ptr(), _stream_ptr(stream)))
@@ -349,22 +415,20 @@ def generate_manifold_scene_batch(bodies, poses, cfg=None, *, is_static=None, pa
         L = layout(bodies[i], bodies[j], c)
         r = res[q]
         r["pair"] = (int(i), int(j))
-        if "contacts" not in r:
-            r["contacts"] = torch.empty((n_env, L["n_contacts"], 8), dtype=torch.float32, device=P.device)
-        if want_src and "src" not in r:
-            r["src"] = torch.empty((n_env, L["n_contacts"], 2), dtype=torch.int32, device=P.device)
-        if want_ee and L["m1"] * L["m2"] > 0 and "ee" not in r:
-            r["ee"] = torch.empty((n_env, 9, L["m1"] * L["m2"]), dtype=torch.float32, device=P.device)
-        if "mean_dist" not in r:
-            r["mean_dist"] = torch.empty((n_env,), dtype=torch.float32, device=P.device)
+        Pq = L["m1"] * L["m2"]
+        contacts = _reuse(r, "contacts", (n_env, L["n_contacts"], 8), torch.float32, P.device)
+        src = _reuse(r, "src", (n_env, L["n_contacts"], 2), torch.int32, P.device) if want_src else None
+        ee = _reuse(r, "ee", (n_env, 9, Pq), torch.float32, P.device) if (want_ee and Pq > 0) else None
+        mean = _reuse(r, "mean_dist", (n_env,), torch.float32, P.device)
         ws = lib.cmgb_manifold_workspace_bytes(n_env, 1, 1)
-        if "workspace" not in r or r["workspace"].numel() < ws:
+        wsb = r.get("workspace")
+        if not (isinstance(wsb, torch.Tensor) and wsb.device == P.device and wsb.numel() >= ws):
             r["workspace"] = torch.empty((max(ws, 8),), dtype=torch.uint8, device=P.device)
         o = arr[q]
-        o.contacts = r["contacts"].data_ptr()
-        o.src = r["src"].data_ptr() if "src" in r else None
-        o.ee = r["ee"].data_ptr() if "ee" in r else None
-        o.mean_dist = r["mean_dist"].data_ptr()
+        o.contacts = contacts.data_ptr()
+        o.src = src.data_ptr() if src is not None else None
+        o.ee = ee.data_ptr() if ee is not None else None
+        o.mean_dist = mean.data_ptr()
         o.workspace = r["workspace"].data_ptr()
         o.workspace_bytes = r["workspace"].numel()
     handles = (C.c_void_p * nb)(*[b._h.value if isinstance(b._h, C.c_void_p) else b._h for b in bodies])
@@ -401,14 +465,12 @@ def generate_manifold_scene_jvp_batch(bodies, poses, cfg=None, *, is_static=None
                              ("tangents", (n_env, Cn, 8, 12), torch.float32),
                              ("mean_dist", (n_env,), torch.float32),
                              ("mean_dist_grad", (n_env, 12), torch.float32)):
-            if k not in r:
-                r[k] = torch.empty(shape, dtype=dt, device=dev)
-        if want_src and "src" not in r:
-            r["src"] = torch.empty((n_env, Cn, 2), dtype=torch.int32, device=dev)
+            _reuse(r, k, shape, dt, dev)
+        src = _reuse(r, "src", (n_env, Cn, 2), torch.int32, dev) if want_src else None
         o = arr[q]
         o.contacts = r["contacts"].data_ptr()
         o.tangents = r["tangents"].data_ptr()
-        o.src = r["src"].data_ptr() if "src" in r else None
+        o.src = src.data_ptr() if src is not None else None
         o.mean_dist = r["mean_dist"].data_ptr()
         o.mean_dist_grad = r["mean_dist_grad"].data_ptr()
     handles = (C.c_void_p * nb)(*[b._h.value if isinstance(b._h, C.c_void_p) else b._h for b in bodies])
@@ -425,10 +487,14 @@ def generate_manifold_batch_host(s1: Surface, s2: Surface, poses1: np.ndarray, p
     c = _cfg(cfg)
     p1 = np.ascontiguousarray(poses1, dtype=np.float64).reshape(-1, 6)
     p2 = np.ascontiguousarray(poses2, dtype=np.float64).reshape(-1, 6)
-    n = max(len(p1), len(p2))
-    st1 = 1 if len(p1) == n and n > 1 else (1 if n == 1 else 0)
-    st2 = 1 if len(p2) == n and n > 1 else (1 if n == 1 else 0)
+    n, st1, st2 = _pose_rows(len(p1), len(p2))
     mean = mean_out if mean_out is not None else np.empty(n, np.float32)
+    if mean.dtype != np.float32 or mean.size < n or not mean.flags.c_contiguous:
+        raise ValueError("mean_out must be a contiguous float32 array of n_env elements")
+    if contacts_out is not None:
+        Cn = layout(s1, s2, c)["n_contacts"]
+        if contacts_out.dtype != np.float32 or contacts_out.size < n * Cn * 8 or not contacts_out.flags.c_contiguous:
+            raise ValueError("contacts_out must be a contiguous float32 array of n_env x n_contacts x 8")
     _ok(abi.load().cmgb_manifold_batch_host(
         s1._h, s2._h, p1.ctypes.data, st1, p2.ctypes.data, st2, n, C.byref(c), mean.ctypes.data,
         contacts_out.ctypes.data if contacts_out is not None else None, _stream_ptr(stream)))
@@ -458,7 +524,7 @@ def run_ee_batch(pairs, cfg=None, *, want_alpha: bool = False, want_labels: bool
     import torch
 
     c = _cfg(cfg)
-    pr = pairs.reshape(-1, 12).contiguous()
+    pr = _cuda_tensor(pairs, (torch.float64, torch.float32), "pairs").reshape(-1, 12).contiguous()
     n = pr.shape[0]
     res = {"out": torch.empty((n, 6), dtype=torch.float32, device=pr.device)}
     if want_alpha:
@@ -480,9 +546,7 @@ def run_ee_batch_f64(pairs, cfg=None, *, want_alpha: bool = False, want_labels: 
     import torch
 
     c = _cfg(cfg)
-    pr = pairs.reshape(-1, 12).contiguous()
-    if pr.dtype != torch.float64:
-        raise ValueError("pairs must be float64")
+    pr = _cuda_tensor(pairs, (torch.float64,), "pairs").reshape(-1, 12).contiguous()
     n = pr.shape[0]
     res = {"out": torch.empty((n, 6), dtype=torch.float64, device=pr.device)}
     if want_alpha:
@@ -515,7 +579,7 @@ def run_vf_batch(pairs, cfg=None, *, want_labels: bool = False, stream=None) -> 
     import torch
 
     c = _cfg(cfg)
-    pr = pairs.reshape(-1, 12).contiguous()
+    pr = _cuda_tensor(pairs, (torch.float64, torch.float32), "pairs").reshape(-1, 12).contiguous()
     n = pr.shape[0]
     res = {"out": torch.empty((n, 3), dtype=torch.float32, device=pr.device)}
     if want_labels:

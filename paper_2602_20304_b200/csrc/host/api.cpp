@@ -16,6 +16,10 @@
 
 namespace cmgb {
 int manifold_max_threads(int k1, int k2);
+size_t compact_workspace_bytes(int64_t n_env, int C);
+int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int C, float thr, int64_t capacity,
+                   float* out_contacts, int32_t* out_slot, int32_t* out_src, int64_t* env_offset,
+                   int32_t* env_count, int64_t* total, void* workspace, cudaStream_t s);
 }
 
 using namespace cmgb;
@@ -341,8 +345,38 @@ void ensure(T** ptr, size_t* cap, size_t n) {
   *cap = n;
 }
 
-std::mutex g_scratch_mu;
-std::unordered_map<int, HostScratch> g_scratch;
+// Host-buffer API scratch: a pool per device from which each call leases its
+// own HostScratch for its duration, so concurrent host threads never share
+// device buffers or pipeline streams (the lock covers only check-out/return).
+struct ScratchPool {
+  std::mutex mu;
+  std::unordered_map<int, std::vector<HostScratch*>> idle;
+};
+ScratchPool g_scratch_pool;
+
+struct ScratchLease {
+  int dev;
+  HostScratch* sc;
+  explicit ScratchLease(int d) : dev(d), sc(nullptr) {
+    std::lock_guard<std::mutex> lock(g_scratch_pool.mu);
+    auto& v = g_scratch_pool.idle[d];
+    if (!v.empty()) {
+      sc = v.back();
+      v.pop_back();
+    }
+    if (!sc) sc = new HostScratch();
+  }
+  // Also on the error path: copies into the caller's host buffers may already be
+  // queued on the pipeline streams; they must finish before the call returns.
+  ~ScratchLease() {
+    for (cudaStream_t q : sc->q)
+      if (q) cudaStreamSynchronize(q);
+    std::lock_guard<std::mutex> lock(g_scratch_pool.mu);
+    g_scratch_pool.idle[dev].push_back(sc);
+  }
+  ScratchLease(const ScratchLease&) = delete;
+  ScratchLease& operator=(const ScratchLease&) = delete;
+};
 
 }  // namespace
 
@@ -611,8 +645,8 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     const cmgb_layout L = layout_of(s1, s2, cfg);
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    std::lock_guard<std::mutex> lock(g_scratch_mu);
-    HostScratch& sc = g_scratch[dev];
+    ScratchLease lease(dev);
+    HostScratch& sc = *lease.sc;
     const size_t np1 = (st1 ? n_env : 1) * 6, np2 = (st2 ? n_env : 1) * 6;
     ensure(&sc.poses1, &sc.cap_poses1, np1);
     ensure(&sc.poses2, &sc.cap_poses2, np2);
@@ -635,13 +669,20 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     // chunks pay a wave-quantisation tail and launch gaps per chunk: measured
     // box-box 65,536 envs, 8 equal chunks 48.8 M/s, 4 50.3; lead 1/16, 1/8,
     // 1/4 of the envs: 51.3, 51.4, 50.9).
+    // With the full contacts coming back (9.7 KB/env box-box, D2H-bound) the
+    // batch runs as up to kHostChunksFull equal chunks alternating between the
+    // streams, so each chunk's D2H overlaps the next chunk's kernels.
     constexpr int64_t lead_div = 8;
-    int64_t bounds[3] = {0, n_env, n_env};
-    int nchunk = 1;
-    if (n_env >= 2 * kHostChunkMin) {
-      bounds[1] = std::max(kHostChunkMin, n_env / lead_div);
-      nchunk = 2;
+    constexpr int kHostChunksFull = 8;
+    std::vector<int64_t> bounds = {0, n_env};
+    if (contacts_host && n_env >= 2 * kHostChunkMin) {
+      const int64_t k = std::min<int64_t>(kHostChunksFull, n_env / kHostChunkMin);
+      bounds.clear();
+      for (int64_t c = 0; c <= k; ++c) bounds.push_back(n_env * c / k);
+    } else if (n_env >= 2 * kHostChunkMin) {
+      bounds = {0, std::max(kHostChunkMin, n_env / lead_div), n_env};
     }
+    const int nchunk = (int)bounds.size() - 1;
     int64_t per = 0;
     for (int c = 0; c < nchunk; ++c) per = std::max(per, bounds[c + 1] - bounds[c]);
     ensure(&sc.frames, &sc.cap_frames, 2 * workspace_doubles(per, st1, st2));
@@ -689,6 +730,43 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
       cuda_check(cudaStreamWaitEvent(s, sc.ev[k], 0), "cudaStreamWaitEvent");
     }
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+// ---- active-contact compaction -----------------------------------------------------
+size_t cmgb_compact_workspace_bytes(int64_t n_env, int32_t n_contacts) {
+  return n_env > 0 && n_contacts > 0 ? compact_workspace_bytes(n_env, n_contacts) : 0;
+}
+
+int cmgb_compact_contacts(const float* contacts, const int32_t* src, int64_t n_env, int32_t n_contacts,
+                          float thr, const cmgb_compact_out* out, void* stream) {
+  return guarded([&] {
+    if (!out) invalid("compact: null output descriptor");
+    if (n_env < 0 || n_contacts < 0) invalid("compact: n_env >= 0 and n_contacts >= 0");
+    if (out->capacity < 0) invalid("compact: capacity >= 0");
+    if (!(thr == thr)) invalid("compact: activity_threshold must not be NaN");
+    if (out->src && !src) invalid("compact: src output needs the batch's src input");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n_env == 0 || n_contacts == 0) {
+      if (out->total) cuda_check(cudaMemsetAsync(out->total, 0, sizeof(int64_t), s), "cudaMemsetAsync");
+      if (out->env_offset)
+        cuda_check(cudaMemsetAsync(out->env_offset, 0, sizeof(int64_t) * (n_env + 1), s), "cudaMemsetAsync");
+      if (out->env_count) cuda_check(cudaMemsetAsync(out->env_count, 0, sizeof(int32_t) * n_env, s), "cudaMemsetAsync");
+      return;
+    }
+    if (!contacts) invalid("compact: null contacts");
+    if (!out->contacts && out->capacity > 0) invalid("compact: null output contacts");
+    // the fixed layout is staged by cp.async.bulk: 16-byte aligned source
+    if (reinterpret_cast<uintptr_t>(contacts) % 16 != 0) invalid("compact: contacts must be 16-byte aligned");
+    const size_t need = compact_workspace_bytes(n_env, n_contacts);
+    void* ws = out->workspace;
+    const bool pooled = !ws || out->workspace_bytes < need;
+    if (pooled) cuda_check(cudaMallocAsync(&ws, need, s), "cudaMallocAsync(compact workspace)");
+    const int rc = launch_compact(contacts, src, n_env, n_contacts, thr, out->capacity, out->contacts, out->slot,
+                                  out->src, out->env_offset, out->env_count, out->total, ws, s);
+    if (pooled) cudaFreeAsync(ws, s);
+    if (rc != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("compact launch: ") + cudaGetErrorString(cudaGetLastError()));
   });
 }
 
@@ -856,6 +934,8 @@ int cmgb_ee_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     if (n < 0) invalid("ee_witness_batch: n >= 0");
     if (n == 0) return;
     if (!pairs || !out) invalid("ee_witness_batch: null buffer");
+    // input tiles arrive by cp.async.bulk, which needs a 16-byte aligned source
+    if (reinterpret_cast<uintptr_t>(pairs) % 16 != 0) invalid("ee_witness_batch: pairs must be 16-byte aligned");
     WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, alpha_gamma, labels, nullptr};
     if (launch_ee_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("ee_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -869,6 +949,7 @@ int cmgb_ee_witness_batch_f64(const double* pairs, int64_t n, const cmgb_config*
     if (n < 0) invalid("ee_witness_batch_f64: n >= 0");
     if (n == 0) return;
     if (!pairs || !out) invalid("ee_witness_batch_f64: null buffer");
+    if (reinterpret_cast<uintptr_t>(pairs) % 16 != 0) invalid("ee_witness_batch_f64: pairs must be 16-byte aligned");
     WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, alpha_gamma};
     if (launch_ee_witness_f64(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("ee_witness_f64 launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -940,6 +1021,8 @@ int cmgb_vf_witness_batch(const void* pairs, int32_t fp64, int64_t n, const cmgb
     if (n < 0) invalid("vf_witness_batch: n >= 0");
     if (n == 0) return;
     if (!pairs || !out) invalid("vf_witness_batch: null buffer");
+    // input tiles arrive by cp.async.bulk, which needs a 16-byte aligned source
+    if (reinterpret_cast<uintptr_t>(pairs) % 16 != 0) invalid("vf_witness_batch: pairs must be 16-byte aligned");
     WitnessParams p{pairs, fp64 ? 1 : 0, n, device_config(cfg), out, nullptr, labels, nullptr};
     if (launch_vf_witness(p, stream) != 0)
       throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));

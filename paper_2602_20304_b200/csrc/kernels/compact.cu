@@ -1,0 +1,230 @@
+// Active-contact compaction — an EXTRA output beside the reference's fixed
+// layout (include/cmg/manifold.hpp:62-72, 303-330; SURVEY.md §7 hard part 8:
+// never a replacement). For every env of a batch it keeps the contacts with
+// activity > thr, in fixed-layout order, packed back to back across the whole
+// batch, plus each kept contact's slot index and per-env offsets / counts.
+//
+// Mapping (HBM-bound: every fixed-layout byte is read once, only the kept
+// contacts are written):
+//   * one CTA per tile of `epb` consecutive envs; their fixed-layout contacts
+//     are one contiguous block of epb x C x 32 B, staged into shared memory by
+//     ONE TMA bulk copy (cp.async.bulk + mbarrier transaction count);
+//   * one warp per env: __ballot_sync(activity > thr) per 32-contact chunk,
+//     __popc -> the env's count;
+//   * tile offset: a scan of the tile's env counts, then a decoupled look-back
+//     over the preceding tiles' published aggregates / inclusive prefixes. Tiles
+//     are numbered by an atomic ticket taken at CTA start, so every tile a CTA
+//     waits on belongs to a CTA that is already running (forward progress);
+//   * each warp writes its env's kept contacts as two float4 per contact
+//     (lanes of a chunk -> consecutive 32-B slots: coalesced), their slot
+//     indices and (optionally) provenance, and the env's offset / count.
+// Envs too large to stage (C x 32 B beyond the shared-memory budget) read
+// their contacts from global memory twice instead (kStaged = false).
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../device/bulk.cuh"
+#include "launch_util.cuh"
+
+namespace cmgb {
+
+int compact_envs_per_tile(int C);
+size_t compact_workspace_bytes(int64_t n_env, int C);
+
+namespace {
+
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagIncl = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct CompactParams {
+  const float* contacts;   // [n][C][8]
+  const int32_t* src;      // optional [n][C][2]
+  int64_t n_env;
+  int32_t C;
+  int32_t epb;             // envs per tile (= warps per CTA)
+  float thr;
+  int64_t capacity;        // rows of out_contacts / out_slot / out_src
+  float* out_contacts;     // [capacity][8]
+  int32_t* out_slot;       // optional [capacity]
+  int32_t* out_src;        // optional [capacity][2]
+  int64_t* env_offset;     // optional [n + 1] (exclusive scan; [n] = total)
+  int32_t* env_count;      // optional [n]
+  int64_t* total;          // optional [1]
+  uint64_t* status;        // [n_tiles] zeroed
+  uint32_t* ticket;        // [1] zeroed
+};
+
+template <bool kStaged>
+__global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ CompactParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_tile;
+  __shared__ int64_t s_base;
+  __shared__ int32_t s_cnt[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = p.C;
+  if (threadIdx.x == 0) s_tile = atomicAdd(p.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t env0 = tile * p.epb;
+  const int64_t left = p.n_env - env0;
+  const int n_here = left < p.epb ? (int)left : p.epb;
+  const float4* gsrc = reinterpret_cast<const float4*>(p.contacts) + env0 * C * 2;
+  const float4* tile_c = gsrc;
+  if constexpr (kStaged) {
+    const uint32_t bytes = (uint32_t)n_here * (uint32_t)C * 32u;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_fence_init();
+      mbar_arrive_expect_tx(&bar, bytes);
+      bulk_g2s(smem, gsrc, bytes, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    tile_c = reinterpret_cast<const float4*>(smem);
+  }
+
+  // ---- per-env counts (one warp per env) --------------------------------------
+  int cnt = 0;
+  if (warp < n_here) {
+    const float4* ec = tile_c + (int64_t)warp * C * 2;
+    for (int j0 = 0; j0 < C; j0 += 32) {
+      const int j = j0 + lane;
+      const bool keep = j < C && ec[2 * j + 1].w > p.thr;
+      cnt += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+  }
+  __syncthreads();
+
+  // ---- tile offset: aggregate, decoupled look-back, inclusive prefix -----------
+  if (warp == 0) {
+    int64_t mine = 0;
+    for (int w = 0; w < n_here; ++w) mine += s_cnt[w];
+    if (lane == 0) st_release(p.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (uint64_t)mine);
+    int64_t excl = 0;
+    if (tile > 0) {
+      int64_t base = tile - 1;
+      while (true) {
+        const int64_t idx = base - lane;
+        uint64_t s = idx >= 0 ? ld_acquire(p.status + idx) : kFlagIncl;
+        while (__any_sync(0xffffffffu, (s >> 62) == 0)) {  // a predecessor has not published yet
+          if ((s >> 62) == 0) s = ld_acquire(p.status + idx);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest tile with an inclusive prefix
+        int64_t v = lane <= stop ? (int64_t)(s & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (incl) break;
+        base -= 32;
+      }
+      if (lane == 0) st_release(p.status + tile, kFlagIncl | (uint64_t)(excl + mine));
+    }
+    if (lane == 0) {
+      s_base = excl;
+      const int64_t ntiles = (p.n_env + p.epb - 1) / p.epb;
+      if (tile == ntiles - 1) {
+        if (p.total) *p.total = excl + mine;
+        if (p.env_offset) p.env_offset[p.n_env] = excl + mine;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- writes: env offset / count, then the kept contacts in layout order -----
+  if (warp >= n_here) return;
+  int64_t off = s_base;
+  for (int w = 0; w < warp; ++w) off += s_cnt[w];
+  const int64_t e = env0 + warp;
+  if (lane == 0) {
+    if (p.env_offset) p.env_offset[e] = off;
+    if (p.env_count) p.env_count[e] = s_cnt[warp];
+  }
+  const float4* ec = tile_c + (int64_t)warp * C * 2;
+  float4* oc = reinterpret_cast<float4*>(p.out_contacts);
+  for (int j0 = 0; j0 < C; j0 += 32) {
+    const int j = j0 + lane;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (j < C) {
+      a = ec[2 * j];
+      b = ec[2 * j + 1];
+    }
+    const bool keep = j < C && b.w > p.thr;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int64_t dst = off + __popc(m & ((1u << lane) - 1u));
+    if (keep && dst < p.capacity) {
+      oc[2 * dst] = a;
+      oc[2 * dst + 1] = b;
+      if (p.out_slot) p.out_slot[dst] = j;
+      if (p.out_src) {
+        const int2 s = reinterpret_cast<const int2*>(p.src)[e * C + j];
+        reinterpret_cast<int2*>(p.out_src)[dst] = s;
+      }
+    }
+    off += __popc(m);
+  }
+}
+
+}  // namespace
+
+size_t compact_workspace_bytes(int64_t n_env, int C) {
+  const int epb = compact_envs_per_tile(C);
+  const int64_t tiles = (n_env + epb - 1) / epb;
+  return sizeof(uint64_t) * (size_t)(tiles + 2);
+}
+
+// Envs per tile: up to 8 warps, tile staged in <= 40 KB of shared memory
+// (several CTAs per SM keep bulk copies in flight), at least one env.
+int compact_envs_per_tile(int C) {
+  const int per_env = C * 32;
+  int epb = per_env > 0 ? (40 * 1024) / per_env : 8;
+  return epb < 1 ? 1 : (epb > 8 ? 8 : epb);
+}
+
+int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int C, float thr, int64_t capacity,
+                   float* out_contacts, int32_t* out_slot, int32_t* out_src, int64_t* env_offset,
+                   int32_t* env_count, int64_t* total, void* workspace, cudaStream_t s) {
+  CompactParams p{};
+  p.contacts = contacts;
+  p.src = src;
+  p.n_env = n_env;
+  p.C = C;
+  p.epb = compact_envs_per_tile(C);
+  p.thr = thr;
+  p.capacity = capacity;
+  p.out_contacts = out_contacts;
+  p.out_slot = out_slot;
+  p.out_src = out_src;
+  p.env_offset = env_offset;
+  p.env_count = env_count;
+  p.total = total;
+  const int64_t tiles = (n_env + p.epb - 1) / p.epb;
+  p.ticket = static_cast<uint32_t*>(workspace);
+  p.status = static_cast<uint64_t*>(workspace) + 1;
+  if (cudaMemsetAsync(workspace, 0, compact_workspace_bytes(n_env, C), s) != cudaSuccess) return 1;
+  const size_t stage = (size_t)p.epb * C * 32;
+  static PerDeviceOnce configured;
+  configured([] {
+    cudaFuncSetAttribute(compact_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  if (stage <= 200 * 1024)
+    compact_kernel<true><<<(unsigned)tiles, 32 * p.epb, stage, s>>>(p);
+  else
+    compact_kernel<false><<<(unsigned)tiles, 32 * p.epb, 0, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace cmgb

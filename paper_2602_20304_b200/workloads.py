@@ -152,6 +152,19 @@ def box_box(n_env: int = 65536, edge_topk: int = 12) -> Workload:
                     notes="box-box V-S + E-E, M=12 (144 E-E pairs, 304 contacts/env)")
 
 
+def box_box_eps(eps: float, n_env: int = 65536, edge_topk: int = 12) -> Workload:
+    """Config B's scene with superquadric boxiness eps1 = eps2 = eps instead of
+    0.1 (the integer 1/eps family 0.2 / 0.25 / 0.5 runs on compile-time
+    exponent kinds; any other eps on the runtime-exponent kind)."""
+    w = box_box(n_env, edge_topk)
+    sq = Superquadric(eps, eps, (0.5, 0.5, 0.5))
+    for b in w.bodies:
+        b.sdf = sq
+    w.name = f"box-box-eps{eps:g}"
+    w.notes = f"box-box, SQ eps {eps:g}, M=12 (304 contacts/env)"
+    return w
+
+
 def box_on_plane(n_env: int = 1) -> Workload:
     """Config A (box-on-plane): box (SQ eps .1) over a 2x2x0.1 ground (box_planes
     CP, tau 1e-3); full mode = 40 contacts (n 8/8, m 12/1)."""
