@@ -1,20 +1,36 @@
 #!/usr/bin/env python
 """Benchmark: batched contact manifolds/sec (BASELINE.json metric).
 
-One step = generate_manifold over the whole env batch of config B (box-box,
-65,536 envs per GPU, 304 contacts/env) through the C ABI with poses resident
-in HBM ("value"), and the same through the host-buffer C-ABI call with the
-H2D pose copy and the D2H per-env mean contact distance inside the timed
-region ("e2e"). Multi-GPU: one process per GPU (torchrun), contiguous env
-shards, no collective on the data path (weak scaling: 65,536 envs per GPU).
+One step = generate_manifold over the whole env batch through the C ABI
+("value": poses resident in HBM), and the same through the host-buffer call
+with the H2D pose copy and a D2H of the step's result inside the timed region
+("e2e"). Workloads (one JSON line each):
+
+  box-box   config B (default): quad cube + SQ eps 0.1 per body, 304 contacts/env,
+            65,536 envs on 1 GPU; under torchrun (N > 1) config E: 1,048,576
+            envs in total, contiguous shards (strong scaling; --n-total / --n-env
+            override). --eps picks another superquadric boxiness.
+  mixed     config C: 4 buckets x 65,536 envs (rounded box / cylinder /
+            ellipsoid / capsule vs a convex mesh), soft top-K active.
+  drop      config D: 5-body drop scene, all 10 pairs, 32,768 envs, forward +
+            12-tangent pose Jacobians;  drop-fwd: the same, forward only.
+  ee | vf   the witness batches of run_ee_batch / run_vf_batch (K6), 4 M pairs.
+  demo      batched DemoSim::step (3-box scene).
+
+Every line carries roofline (algorithmic work per unit counted by the
+reference itself: profiles/work_per_unit.json, tools/count_work.py),
+cpu_baseline (the compiled reference on this host's cores, N = 1, rank 0) and
+e2e. Timing mirrors time_run (src/batch.cpp:100-120): per-step device events,
+median and population std beside the contract's mean.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload box-box|mixed|drop|drop-fwd|ee|vf|demo]
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
-import math
 import os
 import subprocess
 import sys
@@ -26,10 +42,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Algorithmic work per manifold (counted on the reference
-# formulation with an op-counting scalar: 733,352 arith + 29,811 transcendental).
-W_FLOP_PER_ENV = 763_163.0
-BYTES_PER_ENV = 48.0 + 304 * 32.0  # FP32 poses-equivalent in + fixed-layout contacts out
+WORKLOADS = ["box-box", "mixed", "drop", "drop-fwd", "ee", "vf", "demo"]
+CONFIG_E_ENVS = 1_048_576
 
 
 def parse():
@@ -38,17 +52,24 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n-env", type=int, default=65536, help="envs per GPU (weak scaling)")
-    ap.add_argument("--cpu-sample", type=int, default=16384, help="envs in the bounded CPU sample")
+    ap.add_argument("--workload", default="box-box", choices=WORKLOADS)
+    ap.add_argument("--n-env", type=int, default=None,
+                    help="envs per GPU (weak scaling); default: config size")
+    ap.add_argument("--n-total", type=int, default=None,
+                    help="envs over all GPUs (strong scaling); default 1,048,576 (config E) under torchrun")
+    ap.add_argument("--eps", type=float, default=None, help="box-box: superquadric eps1 = eps2 (default 0.1)")
+    ap.add_argument("--variant", default="ours", help="ours | ours_ns | ours_ne | ours_ne_s (config_for_variant)")
+    ap.add_argument("--compact-thr", type=float, default=0.01,
+                    help="box-box: activity threshold of the compaction extra (added-cost measurement)")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="units in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="box-box", choices=["box-box", "mixed", "drop", "drop-fwd", "demo"],
-                    help="box-box = config B (headline); mixed = config C (4 x 65,536 envs of "
-                         "primitive families vs a convex mesh); drop = config D (all 10 body pairs "
-                         "of a 5-body scene, 32,768 envs, forward + 12-tangent pose JVP); drop-fwd = "
-                         "config D forward only; demo = batched DemoSim steps of a 3-box scene")
+    ap.add_argument("--no-extras", action="store_true", help="skip the full-manifold e2e and compaction legs")
     return ap.parse_args()
 
 
+# ----------------------------------------------------------------------------------------
+# measurement plumbing
+# ----------------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -60,29 +81,23 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.n_pre = 0
 
-    def start(self):
+    def start(self, busy):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
-
-    def wait_first(self, busy, timeout=3.0):
-        """Keep the GPU loaded (busy()) until nvidia-smi has produced its first
-        sample, so the samples that follow fall inside the timed region."""
+            return
+        # keep the GPU loaded until the first sample exists, so the rest fall inside the timed region
         import torch
-
         t0 = time.time()
-        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+        while not self.lines and time.time() - t0 < 3.0:
             busy()
             torch.cuda.synchronize()
-
-    def mark(self):
-        """Samples before this point are dropped when later ones exist."""
         self.n_pre = len(self.lines)
 
     def _read(self):
@@ -98,7 +113,7 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        lines = self.lines[getattr(self, "n_pre", 0):] or self.lines
+        lines = self.lines[self.n_pre:] or self.lines
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in lines:
@@ -117,322 +132,612 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def measured_peaks():
+class Ctx:
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.args = args
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local_rank)
+        self.dev = torch.device("cuda", self.local_rank)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.stream = torch.cuda.current_stream()
+        from paper_2602_20304_b200 import abi
+        self.lib = abi.load()
+        self.lib.cmgb_kernel_launches.restype = C.c_uint64
+        self.lib.cmgb_kernel_launches.argtypes = []
+        self.lib.cmgb_probe_fma_tflops.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_void_p]
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def launches(self):
+        return int(self.lib.cmgb_kernel_launches())
+
+
+def timed(ctx, step, steps, warmup, clocks=False):
+    """W untimed warm-ups, then exactly K steps bracketed by barrier +
+    synchronize, each step between CUDA events on the launching stream.
+    Returns dict(total_ms = max over ranks, per-step median / std / mean,
+    launches per step, clocks)."""
+    import torch
+
+    for _ in range(max(3, warmup)):
+        step()
+    torch.cuda.synchronize()
+    cs = ClockSampler(ctx.local_rank) if clocks else None
+    if cs:
+        cs.start(step)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches()
+    t0.record(ctx.stream)
+    for a, b in ev:
+        a.record(ctx.stream)
+        step()
+        b.record(ctx.stream)
+    t1.record(ctx.stream)
+    l1 = ctx.launches()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    clk = cs.stop() if cs else None
+    per = np.array([a.elapsed_time(b) for a, b in ev])
+    total = ctx.max_over_ranks(t0.elapsed_time(t1))
+    return {"total_ms": total, "ms_per_step": total / steps, "median_ms": float(np.median(per)),
+            "std_ms": float(per.std()), "mean_ms": float(per.mean()), "launches_per_step": (l1 - l0) / steps,
+            "clocks": clk}
+
+
+def work_per_unit(name):
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "work_per_unit.json")) as f:
+            return json.load(f)["units"][name]["W"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def prof_json(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
 
 
-def cpu_reference_run(sample: int, reps: int = 1):
-    """The reference's own bench_manifold (oracle/_ref, unmodified reference
-    sources) on this host's cores; falls back to the C oracle port."""
+def measured_peaks():
+    return prof_json("../MEASURED_PEAKS.json")
+
+
+def fp_peaks(ctx):
+    import torch
+    f32, f64 = C.c_double(), C.c_double()
+    ctx.lib.cmgb_probe_fma_tflops(0, 8192, C.byref(f32), ctx.stream.cuda_stream)
+    ctx.lib.cmgb_probe_fma_tflops(1, 4096, C.byref(f64), ctx.stream.cuda_stream)
+    props = torch.cuda.get_device_properties(ctx.dev)
+    mhz = measured_peaks().get("sm_max_mhz") or 1965.0
+    nominal = props.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+    return f32.value, f64.value, nominal
+
+
+def compute_roofline(ctx, W, units_local, kernel_ms, extra=None):
+    """FP32 CUDA-core roofline (no dense contraction, tensor
+    cores unused): W algorithmic flop per unit (the reference formulation,
+    counted by the reference) x units / device time of the step's kernels."""
+    f32, f64, nominal = fp_peaks(ctx)
+    achieved = W * units_local / (kernel_ms * 1e-3) / 1e12 if W else None
+    roof = {"bound": "fp32", "achieved": achieved, "peak": f32, "unit": "TFLOP/s",
+            "frac": achieved / f32 if (achieved and f32) else None,
+            "frac_of_nominal": achieved / nominal if achieved else None, "nominal_peak": nominal,
+            "peak_source": "measured live on this GPU: FFMA-chain microbenchmark (cmgb_probe_fma_tflops); "
+                           "MEASURED_PEAKS.json has no FP32 CUDA-core figure. nominal_peak = SMs x 128 x 2 x "
+                           "max SM clock",
+            "work_per_unit_flop": W, "work_source": "profiles/work_per_unit.json (tools/count_work.py: the "
+                                                    "reference's generate_manifold<T> with a counting scalar)",
+            "kernel_ms": kernel_ms, "fp64_dfma_peak": f64}
+    if extra:
+        roof.update(extra)
+    return roof
+
+
+def hbm_roofline(bytes_per_unit, units_local, kernel_ms, traffic=None):
+    peak = measured_peaks().get("hbm_gbs") or 6546.2
+    achieved = bytes_per_unit * units_local / (kernel_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "bytes_per_unit": bytes_per_unit, "kernel_ms": kernel_ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
+
+
+def line(ctx, metric, unit, t, units_total, config, dtype, **extra):
+    args = ctx.args
+    out = {"metric": metric, "value": units_total / (t["ms_per_step"] * 1e-3), "unit": unit,
+           "n_gpus": ctx.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t["ms_per_step"],
+           "higher_is_better": True, "scaling": extra.pop("scaling", "weak"), "vs_baseline": None,
+           "dtype": dtype, "data": "synthetic", "config": config,
+           "timing": {"median_ms": t["median_ms"], "std_ms": t["std_ms"], "mean_ms": t["mean_ms"],
+                      "protocol": "per-step CUDA events (time_run: median + population std); value = "
+                                  "units / (max-over-ranks total / K)"},
+           "gpu_launches": int(round(t["launches_per_step"] * args.steps)),
+           "gpu_launches_per_step": t["launches_per_step"],
+           "clocks": t["clocks"]}
+    out.update(extra)
+    return out
+
+
+# ----------------------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the unmodified reference compiled from source)
+# ----------------------------------------------------------------------------------------
+def ref_surface(b):
+    from oracle import Ref
+    m = Ref.Mesh.box(b.mesh.box_half, b.mesh.subdivisions, b.mesh.quad_edges) if b.mesh.box_half is not None \
+        else Ref.Mesh.parse_obj(b.mesh.obj_text)
+    return Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk)
+
+
+def cpu_reference(workload, args, sample, reps):
+    """The reference's own implementation of the workload on all host cores:
+    (units/s, median_s, std_s, description)."""
+    from oracle import Ref
     from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
 
-    ws = W.box_box(sample)
+    if not Ref.available():
+        raise FileNotFoundError("oracle/_ref/libcmgref.so not built")
     cores = os.cpu_count() or 1
+    cfg = SmoothingConfig()
+    if workload == "box-box":
+        ws = W.box_box(sample) if args.eps is None else W.box_box_eps(args.eps, sample)
+        s = [ref_surface(b) for b in ws.bodies]
+        med, sd = Ref.bench_manifold(s[0], s[1], ws.bodies[0].pose, ws.bodies[1].pose, sample, args.variant, cfg,
+                                     seed=0, reps=reps, workers=cores)
+        return sample / med, med, sd, cores, (f"bench_manifold (src/batch.cpp:184-228), {ws.name}, {sample} envs, "
+                                              f"variant {args.variant}, time_run median of {reps} rep(s) after "
+                                              f"{min(3, reps)} warm-up(s), {cores} worker threads")
+    if workload == "mixed":
+        tot = 0.0
+        sds = []
+        for kind in W.MIXED_KINDS:
+            ws = W.mixed_bucket(kind, sample)
+            s = [ref_surface(b) for b in ws.bodies]
+            med, sd = Ref.bench_manifold(s[0], s[1], ws.bodies[0].pose, ws.bodies[1].pose, sample, args.variant,
+                                         cfg, seed=0, reps=reps, workers=cores)
+            tot += med
+            sds.append(sd)
+        units = sample * len(W.MIXED_KINDS)
+        return units / tot, tot, float(np.sqrt(np.sum(np.square(sds)))), cores, (
+            f"bench_manifold per config-C bucket (4 x {sample} envs), summed medians of {reps} rep(s), "
+            f"{cores} worker threads")
+    if workload in ("drop", "drop-fwd"):
+        sc = W.drop_scene(sample)
+        bodies = [ref_surface(b) for b in sc.bodies]
+        pairs = np.array([(i, j) for i in range(len(bodies)) for j in range(i + 1, len(bodies))
+                          if not (sc.bodies[i].is_static and sc.bodies[j].is_static)], np.int32)
+        jvp = workload == "drop"
+        med, sd, _ = Ref.scene_bench(bodies, pairs, sc.poses(sample), cfg, jvp=jvp, reps=reps, warmups=1,
+                                     workers=cores)
+        units = sample * len(pairs)
+        what = "generate_manifold<Dual12> (seed_pose_tangents; main.cpp:202-205)" if jvp else \
+            "generate_manifold<double>"
+        return units / med, med, sd, cores, (f"every pair of the drop scene ({len(pairs)} pairs x {sample} envs) "
+                                             f"through the reference's {what}, std::thread chunks, time_run "
+                                             f"median of {reps} rep(s), {cores} threads")
+    if workload in ("ee", "vf"):
+        med, sd = Ref.bench_witness(workload, sample, args.variant, seed=0, reps=reps, workers=cores)
+        return sample / med, med, sd, cores, (f"bench_witness (src/batch.cpp:152-182) kind {workload}, {sample} "
+                                              f"pairs, variant {args.variant}, make_random_{workload}_pairs seed 0, "
+                                              f"time_run median of {reps} rep(s), {cores} worker threads")
+    raise ValueError(f"no CPU reference for workload {workload}")
+
+
+def cpu_baseline(ctx, workload, unit, sample):
+    if ctx.args.no_cpu_baseline or ctx.rank != 0 or ctx.world != 1:
+        return None
     try:
-        from oracle import Ref
-        if not Ref.available():
-            raise FileNotFoundError("oracle/_ref not built")
-        from paper_2602_20304_b200.scene import SmoothingConfig
-        meshes = [Ref.Mesh.box(b.mesh.box_half) for b in ws.bodies]
-        rs = [Ref.Surface(m, b.sdf, b.vertex_topk, b.edge_topk) for m, b in zip(meshes, ws.bodies)]
-        med, _ = Ref.bench_manifold(rs[0], rs[1], ws.bodies[0].pose, ws.bodies[1].pose, sample, "ours",
-                                    SmoothingConfig(), seed=0, reps=reps, workers=cores)
-        return dict(value=sample / med, unit="manifolds/s", cores=cores, kind="reference",
-                    sample=f"bench_manifold (src/batch.cpp:184-228) box-box, {sample} envs, {reps} rep(s), "
-                           f"{cores} worker threads, -O3 build of the unmodified reference")
+        v, med, sd, cores, desc = cpu_reference(workload, ctx.args, sample, reps=2)
+        return {"value": v, "unit": unit, "cores": cores, "kind": "reference", "sample": desc,
+                "median_s": med, "std_s": sd}
     except Exception as e:  # noqa: BLE001
-        from oracle import Oracle
-        from paper_2602_20304_b200 import api
-        meshes = [api.surface_from_spec(b).mesh for b in ws.bodies]
-        s = [Oracle.Surface(m.vertices, m.edges, b.sdf, b.vertex_topk, b.edge_topk)
-             for m, b in zip(meshes, ws.bodies)]
-        p1, p2 = ws.poses(sample)
-        t = time.perf_counter()
-        Oracle.manifold_batch(s[0], s[1], p1, p2, None, threads=cores, want_meta=False)
-        dt = time.perf_counter() - t
-        return dict(value=sample / dt, unit="manifolds/s", cores=cores, kind="port",
-                    sample=f"C oracle port, box-box {sample} envs, {cores} threads ({e})")
+        return {"value": None, "unit": unit, "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
 
 
-def run_reference_arm(args, rank):
+DEFAULT_SAMPLE = {"box-box": 65536, "mixed": 16384, "drop": 1024, "drop-fwd": 8192, "ee": 4_194_304,
+                  "vf": 4_194_304}
+UNITS = {"box-box": "manifolds/s", "mixed": "manifolds/s", "drop": "manifolds/s", "drop-fwd": "manifolds/s",
+         "ee": "pairs/s", "vf": "pairs/s", "demo": "env-steps/s"}
+
+
+def run_reference_arm(args):
+    """`--impl reference`: the reference's own CPU implementation of the
+    workload (oracle/_ref, compiled from /root/reference's unmodified sources)
+    on all host cores, same metric / unit / config; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # the reference's own bench_manifold protocol: time_run(reps, warmups = min(3, reps))
+    wl = args.workload
+    if wl == "demo":
+        print(json.dumps({"impl": "reference", "unavailable": "no CPU reference timing harness for the demo "
+                                                              "integrator workload"}), flush=True)
+        return
+    sample = args.cpu_sample or DEFAULT_SAMPLE[wl]
     reps = max(1, min(args.steps, 5))
-    cb = cpu_reference_run(args.cpu_sample, reps=reps)
-    line = {
-        "impl": "reference", "metric": "contact manifolds/sec (box-box, 65,536 envs)",
-        "value": cb["value"], "unit": "manifolds/s", "n_gpus": args.gpus, "steps": reps,
-        "warmup": min(3, reps), "ms_per_step": 1e3 * args.cpu_sample / cb["value"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "box-box (config B), sampled on the host CPU", "n_env": args.cpu_sample,
-                   "contacts_per_env": 304},
-        "cpu_baseline": cb,
-        "e2e": {"value": cb["value"], "unit": "manifolds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    v, med, sd, cores, desc = cpu_reference(wl, args, sample, reps)
+    unit = UNITS[wl]
+    out = {"impl": "reference", "metric": METRICS[wl](args, args.gpus), "value": v, "unit": unit,
+           "n_gpus": args.gpus, "steps": reps, "warmup": min(3, reps), "ms_per_step": med * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{wl} on the host CPU (the reference's own code path)", "sample_units": sample,
+                      "eps": args.eps, "variant": args.variant},
+           "timing": {"median_ms": med * 1e3, "std_ms": sd * 1e3,
+                      "protocol": "the reference's time_run (src/batch.cpp:100-120)"},
+           "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "reference", "sample": desc},
+           "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
 
 
-def run_secondary(args, dev, rank, world):
-    """Configs C and D: device-resident throughput of the same path on the
-    mixed-primitive buckets / the all-pairs multi-body scene."""
+METRICS = {
+    "box-box": lambda a, n: "contact manifolds/sec (box-box, 65,536 envs)" if n == 1 and not a.eps else
+    f"contact manifolds/sec (box-box{'' if not a.eps else f' eps {a.eps:g}'}, config {'E' if n > 1 else 'B'})",
+    "mixed": lambda a, n: "contact manifolds/sec (mixed primitives vs convex mesh, 262,144 envs)",
+    "drop": lambda a, n: "pair manifolds/sec, forward + 12-tangent pose JVP (drop scene, 10 pairs, 32,768 envs)",
+    "drop-fwd": lambda a, n: "pair manifolds/sec, forward only (drop scene, 10 pairs, 32,768 envs)",
+    "ee": lambda a, n: "E-E witness pairs/sec (run_ee_batch, 4,194,304 pairs)",
+    "vf": lambda a, n: "V-F witness pairs/sec (run_vf_batch, 4,194,304 pairs)",
+    "demo": lambda a, n: "env steps/sec (DemoSim::step, 3-box scene, 32,768 envs)",
+}
+
+
+# ----------------------------------------------------------------------------------------
+# workloads
+# ----------------------------------------------------------------------------------------
+def bench_box_box(ctx):
     import torch
-    import torch.distributed as dist
+
+    from paper_2602_20304_b200 import api
+    from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
+    from paper_2602_20304_b200.sharding import shard_range
+
+    a = ctx.args
+    if a.n_env is not None:
+        n_total, scaling = a.n_env * ctx.world, "weak"
+    elif a.n_total is not None:
+        n_total, scaling = a.n_total, "strong"
+    else:
+        n_total, scaling = (65536, "weak") if ctx.world == 1 else (CONFIG_E_ENVS, "strong")
+    ws = W.box_box(n_total) if a.eps is None else W.box_box_eps(a.eps, n_total)
+    lo, hi = shard_range(n_total, ctx.rank, ctx.world)
+    n_local = hi - lo
+    p1, p2_all = ws.poses(n_total)  # global env order, then sliced: shards equal the 1-GPU result bitwise
+    p2 = np.ascontiguousarray(p2_all[lo:hi])
+    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+    cfg = SmoothingConfig().for_variant(a.variant)
+    P1 = torch.as_tensor(p1, device=ctx.dev)
+    P2 = torch.as_tensor(p2, device=ctx.dev)
+    L = api.layout(s1, s2, cfg)
+    out = {}
+
+    def step():
+        api.generate_manifold_batch(s1, s2, P1, P2, cfg, out=out)
+
+    t = timed(ctx, step, a.steps, a.warmup, clocks=True)
+
+    # e2e: host-buffer C-ABI call, pinned host poses H2D + per-env mean distance D2H
+    # (bench_manifold keeps exactly that per env: sums[i], batch.cpp:212)
+    h1 = torch.as_tensor(p1).pin_memory().numpy()
+    h2 = torch.as_tensor(p2).pin_memory().numpy()
+    mean_h = torch.empty(n_local, dtype=torch.float32).pin_memory().numpy()
+
+    def e2e_step():
+        api.generate_manifold_batch_host(s1, s2, h1, h2, cfg, mean_out=mean_h, stream=ctx.stream)
+
+    te = timed(ctx, e2e_step, a.steps, a.warmup)
+    extras = {}
+    if not a.no_extras:
+        # e2e with the WHOLE fixed-layout manifold returned to the host (what
+        # generate_manifold returns by value; 9,728 B/env box-box): D2H-bound
+        contacts_h = torch.empty((n_local, L["n_contacts"], 8), dtype=torch.float32).pin_memory().numpy()
+
+        def e2e_full():
+            api.generate_manifold_batch_host(s1, s2, h1, h2, cfg, mean_out=mean_h, contacts_out=contacts_h,
+                                             stream=ctx.stream)
+
+        kf = max(3, min(a.steps, 20))
+        tf = timed(ctx, e2e_full, kf, 2)
+        extras["e2e_full_manifold"] = {
+            "value": n_total / (tf["ms_per_step"] * 1e-3), "unit": "manifolds/s", "steps": kf,
+            "h2d_bytes_per_step": int(h1.nbytes + h2.nbytes) * ctx.world,
+            "d2h_bytes_per_step": int(mean_h.nbytes + contacts_h.nbytes) * ctx.world,
+            "path": "cmgb_manifold_batch_host with contacts_host: the whole fixed layout back to pinned host "
+                    "memory, pipelined in env chunks (D2H overlaps the next chunk's kernels)",
+            "d2h_gbs": contacts_h.nbytes / (tf["median_ms"] * 1e-3) / 1e9}
+        del contacts_h
+        # compaction extra: its added cost on top of the step
+        comp = {}
+
+        def step_compact():
+            step()
+            api.compact_contacts(out["contacts"], a.compact_thr, out=comp)
+
+        tc = timed(ctx, step_compact, a.steps, a.warmup)
+        total_kept = int(comp["total"].item())
+        n_c = n_local * L["n_contacts"]
+        added = tc["median_ms"] - t["median_ms"]
+        cbytes = n_local * L["n_contacts"] * 32 + total_kept * (32 + 4) + n_local * 12
+        extras["compaction"] = {
+            "activity_threshold": a.compact_thr, "kept": total_kept, "kept_fraction": total_kept / n_c,
+            "added_ms_per_step": added, "added_fraction": added / t["median_ms"],
+            "value_with_compaction": n_total / (tc["ms_per_step"] * 1e-3),
+            "hbm_gbs_if_added_time": cbytes / (added * 1e-3) / 1e9 if added > 0 else None,
+            "note": "step + cmgb_compact_contacts (one TMA-staged pass over the fixed layout) vs the step alone; "
+                    "median per-step device time"}
+
+    if ctx.world > 1:
+        # the optional end-of-run result gather (NCCL over NVLink), timed apart
+        # from the hot path: every rank's per-env mean distances to every rank
+        from paper_2602_20304_b200.sharding import gather_shards
+        md = out["mean_dist"]
+        g = {}
+
+        def gather():
+            g["all"] = gather_shards(md, n_total, ctx.rank, ctx.world)
+
+        tg = timed(ctx, gather, max(3, min(a.steps, 20)), 2)
+        extras["gather"] = {"what": "all-gather of the per-env mean contact distance (4 B/env)",
+                            "bytes": 4 * n_total, "median_ms": tg["median_ms"],
+                            "note": "not part of value: the hot path has no collective"}
+
+    W_env = work_per_unit("box-box" if a.eps is None else f"box-box-eps{a.eps:g}") or work_per_unit("box-box")
+    tr = prof_json("manifold_dram_bytes.json").get("dram_bytes_per_launch_per_env")
+    ops = prof_json("manifold_fp64_ops.json")
+    x64 = ops.get("fp64_flop_per_env")
+    kernel_ms = t["median_ms"]
+    f64_ach = x64 * n_local / (kernel_ms * 1e-3) / 1e12 if x64 else None
+    bytes_env = 48.0 + L["n_contacts"] * 32.0
+    hbm = bytes_env * n_local / (kernel_ms * 1e-3) / 1e9
+    peaks = measured_peaks()
+    roof = compute_roofline(ctx, W_env, n_local, kernel_ms, {
+        "traffic": tr * n_local if (tr and a.eps is None) else None,
+        "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per step (profiles/"
+                          "manifold_dram_bytes.json)",
+        "fp64_pipe": {"executed_flop_per_env": x64, "achieved": f64_ach,
+                      "ncu_pipe_active_pct": ops.get("ncu_fp64_pipe_active_pct"),
+                      "note": "the kernel computes in FP64 (DESIGN.md §4): executed DFMA x2 + DMUL + DADD per env "
+                              "from ncu (profiles/manifold_fp64_ops.json) against the live DFMA peak"},
+        "hbm": {"algorithmic_bytes_per_env": bytes_env, "achieved_gbs": hbm, "peak_gbs": peaks.get("hbm_gbs"),
+                "frac": hbm / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None}})
+    if roof.get("fp64_pipe") and f64_ach:
+        roof["fp64_pipe"]["frac"] = f64_ach / roof["fp64_dfma_peak"]
+    cb = cpu_baseline(ctx, "box-box", "manifolds/s", a.cpu_sample or n_local)
+    return line(ctx, METRICS["box-box"](a, ctx.world), "manifolds/s", t, n_total,
+                {"workload": ws.notes + (" (config B)" if ctx.world == 1 and a.eps is None else
+                                         (" (config E)" if a.eps is None else "")),
+                 "n_env_total": n_total, "n_env_per_gpu": n_local, "contacts_per_env": L["n_contacts"],
+                 "variant": a.variant, "parallelism": f"env-shard x{ctx.world}",
+                 "l2": f"per-step working set {(p2.nbytes + bytes_env * n_local) / 1e6:.0f} MB > 126 MB L2"},
+                "f64 (FP32 outputs)", scaling=scaling,
+                e2e={"value": n_total / (te["ms_per_step"] * 1e-3), "unit": "manifolds/s",
+                     "h2d_bytes_per_step": int(h1.nbytes + h2.nbytes) * ctx.world,
+                     "d2h_bytes_per_step": int(mean_h.nbytes) * ctx.world,
+                     "median_ms": te["median_ms"], "std_ms": te["std_ms"],
+                     "path": "cmgb_manifold_batch_host (pinned host poses -> H2D -> kernels -> D2H of the per-env "
+                             "mean contact distance, bench_manifold's per-env result)"},
+                roofline=roof, cpu_baseline=cb, **extras)
+
+
+def bench_mixed(ctx):
+    import torch
 
     from paper_2602_20304_b200 import api
     from paper_2602_20304_b200 import workloads as W
     from paper_2602_20304_b200.scene import SmoothingConfig
 
+    a = ctx.args
+    n = a.n_env or 65536
     cfg = SmoothingConfig()
-    if args.workload == "mixed":
-        n = 65536 if args.n_env == 65536 else args.n_env
-        calls = []
-        for kind in W.MIXED_KINDS:
-            ws = W.mixed_bucket(kind, n)
-            s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
-            p1, p2 = ws.poses(n)
-            calls.append((s1, s2, torch.as_tensor(p1, device=dev), torch.as_tensor(p2, device=dev), {}))
-        units = n * len(calls)
+    calls = []
+    for kind in W.MIXED_KINDS:
+        ws = W.mixed_bucket(kind, n)
+        s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+        p1, p2 = ws.poses(n)
+        calls.append(dict(s1=s1, s2=s2, P1=torch.as_tensor(p1, device=ctx.dev), P2=torch.as_tensor(p2, device=ctx.dev),
+                          h1=torch.as_tensor(p1).pin_memory().numpy(), h2=torch.as_tensor(p2).pin_memory().numpy(),
+                          mean=torch.empty(n, dtype=torch.float32).pin_memory().numpy(), out={},
+                          C=api.layout(s1, s2, cfg)["n_contacts"]))
+    units = n * len(calls) * ctx.world
 
-        def step():
-            for s1, s2, p1, p2, out in calls:
-                api.generate_manifold_batch(s1, s2, p1, p2, cfg, out=out)
-        metric, unit, cfgd = "contact manifolds/sec (mixed primitives vs convex mesh, 4 x %d envs)" % n, \
-            "manifolds/s", {"workload": "mixed (config C): rounded box / cylinder / ellipsoid / capsule vs "
-                            "convex mesh plate, soft top-K 16/16 vertices 8/8 edges, 160 contacts/env",
-                            "n_env_total": units}
-    elif args.workload == "demo":
-        n = 32768 if args.n_env == 65536 else args.n_env
-        sc = W.demo_scene(n)
-        bodies = [api.surface_from_spec(b) for b in sc.bodies]
-        demo = api.DemoBatch(bodies, np.ones(len(bodies)), is_static=sc.is_static(), cfg=cfg, poses=sc.poses(n),
-                             n_env=n, device=dev)
-        units = n
+    def step():
+        for c in calls:
+            api.generate_manifold_batch(c["s1"], c["s2"], c["P1"], c["P2"], cfg, out=c["out"])
 
-        def step():
-            demo.step(1e-3)
-        metric, unit, cfgd = "env steps/sec (DemoSim::step: all-pairs manifolds + penalty forces + SE(3) Euler, " \
-            "%d envs)" % n, "env-steps/s", {
-                "workload": "demo: 3 SQ boxes released over a static box_planes ground, 6 pairs x 48 contacts, "
-                            "dt 1 ms", "n_env": n, "pairs_per_env": 6}
-    else:
-        n = 32768 if args.n_env == 65536 else args.n_env
-        sc = W.drop_scene(n)
-        bodies = [api.surface_from_spec(b) for b in sc.bodies]
-        P = torch.as_tensor(sc.poses(n), device=dev)
-        outs = None
-        pairs = api.scene_pairs(len(bodies), sc.is_static())
-        units = n * len(pairs)
+    def e2e_step():
+        for c in calls:
+            api.generate_manifold_batch_host(c["s1"], c["s2"], c["h1"], c["h2"], cfg, mean_out=c["mean"],
+                                             stream=ctx.stream)
 
-        jvp = args.workload == "drop"
-        fn = api.generate_manifold_scene_jvp_batch if jvp else api.generate_manifold_scene_batch
+    t = timed(ctx, step, a.steps, a.warmup, clocks=True)
+    te = timed(ctx, e2e_step, a.steps, a.warmup)
+    roof = compute_roofline(ctx, work_per_unit("mixed"), n * len(calls), t["median_ms"], {
+        "traffic": None, "per_bucket_W": {k: work_per_unit(f"mixed-{k}") for k in W.MIXED_KINDS}})
+    cb = cpu_baseline(ctx, "mixed", "manifolds/s", a.cpu_sample or DEFAULT_SAMPLE["mixed"])
+    h2d = sum(c["h1"].nbytes + c["h2"].nbytes for c in calls)
+    return line(ctx, METRICS["mixed"](a, ctx.world), "manifolds/s", t, units,
+                {"workload": "mixed (config C): rounded box / cylinder / ellipsoid / capsule vs convex mesh plate, "
+                             "soft top-K 16/16 vertices 8/8 edges, 160 contacts/env",
+                 "n_env_total": units, "buckets": len(calls), "n_env_per_bucket": n,
+                 "parallelism": f"env-shard x{ctx.world}"},
+                "f64 (FP32 outputs)",
+                e2e={"value": units / (te["ms_per_step"] * 1e-3), "unit": "manifolds/s",
+                     "h2d_bytes_per_step": h2d * ctx.world, "d2h_bytes_per_step": 4 * n * len(calls) * ctx.world,
+                     "path": "cmgb_manifold_batch_host per bucket (pinned poses H2D, per-env mean D2H)"},
+                roofline=roof, cpu_baseline=cb)
 
-        def step():
-            nonlocal outs
-            outs = fn(bodies, P, cfg, is_static=sc.is_static(), outs=outs)
-        what = "forward + 12-tangent pose JVP" if jvp else "forward only"
-        metric, unit, cfgd = "pair manifolds/sec, %s (5-body drop scene, all %d pairs, %d envs)" % (
-            what, len(pairs), n), "manifolds/s", {
-                "workload": "drop (config D): 4 stacked SQ boxes over a static box_planes ground, edge_topk 4, "
-                            "48 contacts/pair, %s" % what, "n_env": n, "pairs_per_env": len(pairs)}
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    s = torch.cuda.current_stream()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(s)
-    for _ in range(args.steps):
-        step()
-    t1.record(s)
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / args.steps
-    if rank == 0:
-        print(json.dumps({"metric": metric, "value": units / (ms * 1e-3), "unit": unit, "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                          "dtype": "f64 (FP32 outputs)", "data": "synthetic", "config": cfgd}), flush=True)
+
+def bench_drop(ctx, jvp):
+    import torch
+
+    from paper_2602_20304_b200 import api
+    from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
+
+    a = ctx.args
+    n = a.n_env or 32768
+    cfg = SmoothingConfig()
+    sc = W.drop_scene(n)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    poses = sc.poses(n)
+    P = torch.as_tensor(poses, device=ctx.dev)
+    pairs = api.scene_pairs(len(bodies), sc.is_static())
+    units_local = n * len(pairs)
+    fn = api.generate_manifold_scene_jvp_batch if jvp else api.generate_manifold_scene_batch
+    outs = [dict() for _ in range(len(pairs))]
+
+    def step():
+        fn(bodies, P, cfg, is_static=sc.is_static(), outs=outs)
+
+    t = timed(ctx, step, a.steps, a.warmup, clocks=True)
+    # e2e through the public Python API: pinned host poses -> H2D, all pairs, D2H of
+    # every pair's per-env mean distance (+ its 12 pose tangents with the JVP)
+    hP = torch.as_tensor(poses).pin_memory()
+    Pd = torch.empty_like(P)
+    res_h = [torch.empty((n, 13 if jvp else 1), dtype=torch.float32).pin_memory() for _ in pairs]
+
+    def e2e_step():
+        Pd.copy_(hP, non_blocking=True)
+        r = fn(bodies, Pd, cfg, is_static=sc.is_static(), outs=outs)
+        for q, o in enumerate(r):
+            res_h[q][:, 0].copy_(o["mean_dist"], non_blocking=True)
+            if jvp:
+                res_h[q][:, 1:].copy_(o["mean_dist_grad"], non_blocking=True)
+        ctx.stream.synchronize()
+
+    te = timed(ctx, e2e_step, a.steps, a.warmup)
+    wname = "drop" if jvp else "drop-fwd"
+    roof = compute_roofline(ctx, work_per_unit(wname), units_local, t["median_ms"], {
+        "traffic": None,
+        "work_note": "W of the reference formulation: generate_manifold<Dual<12>> per pair (every operation "
+                     "carries 12 tangents) for the JVP workload" if jvp else "generate_manifold<double> per pair"})
+    cb = cpu_baseline(ctx, wname, "manifolds/s", a.cpu_sample or DEFAULT_SAMPLE[wname])
+    what = "forward + 12-tangent pose JVP" if jvp else "forward only"
+    return line(ctx, METRICS[wname](a, ctx.world), "manifolds/s", t, units_local * ctx.world,
+                {"workload": f"drop (config D): 4 stacked SQ boxes over a static box_planes ground, edge_topk 4, "
+                             f"48 contacts/pair, {what}", "n_env": n * ctx.world, "pairs_per_env": len(pairs),
+                 "parallelism": f"env-shard x{ctx.world}"},
+                "f64 (FP32 outputs and tangents)",
+                e2e={"value": units_local * ctx.world / (te["ms_per_step"] * 1e-3), "unit": "manifolds/s",
+                     "h2d_bytes_per_step": int(hP.numel() * 8) * ctx.world,
+                     "d2h_bytes_per_step": int(sum(r.numel() * 4 for r in res_h)) * ctx.world,
+                     "path": "api.generate_manifold_scene_%sbatch: pinned [n_env, 5, 6] poses H2D, every pair's "
+                             "per-env mean distance%s D2H" % ("jvp_" if jvp else "",
+                                                             " + its 12 pose tangents" if jvp else "")},
+                roofline=roof, cpu_baseline=cb)
+
+
+def bench_witness(ctx, kind):
+    import torch
+
+    from paper_2602_20304_b200 import api
+    from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
+
+    a = ctx.args
+    n = a.n_env or 4_194_304
+    cfg = SmoothingConfig().for_variant(a.variant)
+    pairs = W.mt19937_64_uniform(0, 12 * n, 0.0, 1.0).reshape(n, 12)  # make_random_*_pairs(n, seed 0)
+    D = torch.as_tensor(pairs, device=ctx.dev)
+    fn = api.run_ee_batch if kind == "ee" else api.run_vf_batch
+    width = 6 if kind == "ee" else 3
+
+    def step():
+        fn(D, cfg)
+
+    t = timed(ctx, step, a.steps, a.warmup, clocks=True)
+    hp = torch.as_tensor(pairs).pin_memory()
+    Dd = torch.empty_like(D)
+    oh = torch.empty((n, width), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        Dd.copy_(hp, non_blocking=True)
+        r = fn(Dd, cfg)
+        oh.copy_(r["out"], non_blocking=True)
+        ctx.stream.synchronize()
+
+    te = timed(ctx, e2e_step, max(3, min(a.steps, 20)), 2)
+    bytes_pair = 96 + 4 * width  # FP64 pair in (as the reference stores it) + FP32 witness points out
+    tr = prof_json(f"witness_{kind}_dram_bytes.json").get("dram_bytes_per_pair")
+    roof = hbm_roofline(bytes_pair, n, t["median_ms"], tr * n if tr else None)
+    cb = cpu_baseline(ctx, kind, "pairs/s", a.cpu_sample or n)
+    return line(ctx, METRICS[kind](a, ctx.world), "pairs/s", t, n * ctx.world,
+                {"workload": f"{kind} witness batch (K6): make_random_{kind}_pairs(n, seed 0), variant {a.variant}",
+                 "n_pairs": n * ctx.world, "parallelism": f"pair-shard x{ctx.world}"},
+                "f64 in (FP32 out)",
+                e2e={"value": n * ctx.world / (te["ms_per_step"] * 1e-3), "unit": "pairs/s",
+                     "h2d_bytes_per_step": int(hp.numel() * 8) * ctx.world,
+                     "d2h_bytes_per_step": int(oh.numel() * 4) * ctx.world,
+                     "path": f"api.run_{kind}_batch: pinned FP64 pairs H2D, FP32 witness points D2H (PCIe-bound)"},
+                roofline=roof, cpu_baseline=cb)
+
+
+def bench_demo(ctx):
+    from paper_2602_20304_b200 import api
+    from paper_2602_20304_b200 import workloads as W
+    from paper_2602_20304_b200.scene import SmoothingConfig
+
+    a = ctx.args
+    n = a.n_env or 32768
+    sc = W.demo_scene(n)
+    bodies = [api.surface_from_spec(b) for b in sc.bodies]
+    demo = api.DemoBatch(bodies, np.ones(len(bodies)), is_static=sc.is_static(), cfg=SmoothingConfig(),
+                         poses=sc.poses(n), n_env=n, device=ctx.dev)
+
+    def step():
+        demo.step(1e-3)
+
+    t = timed(ctx, step, a.steps, a.warmup, clocks=True)
+    return line(ctx, METRICS["demo"](a, ctx.world), "env-steps/s", t, n * ctx.world,
+                {"workload": "demo: 3 SQ boxes released over a static box_planes ground, 6 pairs x 48 contacts, "
+                             "dt 1 ms", "n_env": n * ctx.world, "pairs_per_env": 6},
+                "f64 (FP32 contacts)", roofline=None, cpu_baseline=None, e2e=None)
 
 
 def main():
     args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference_arm(args, rank)
+        run_reference_arm(args)
         return
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_2602_20304_b200 import abi, api
-    from paper_2602_20304_b200 import workloads as W
-    from paper_2602_20304_b200.scene import SmoothingConfig
-    from paper_2602_20304_b200.sharding import shard_range
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    if args.workload != "box-box":
-        run_secondary(args, dev, rank, world)
-        return
-
-    n_local = args.n_env
-    n_total = n_local * world
-    ws = W.box_box(n_total)
-    lo, hi = shard_range(n_total, rank, world)
-    p1_all, p2_all = ws.poses(n_total)  # global env order, then sliced (bitwise shard-independent)
-    p1 = p1_all
-    p2 = np.ascontiguousarray(p2_all[lo:hi])
-    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
-    cfg = SmoothingConfig()
-    P1 = torch.as_tensor(p1, device=dev)
-    P2 = torch.as_tensor(p2, device=dev)
-    L = api.layout(s1, s2, cfg)
-    out = {}
-    stream = torch.cuda.current_stream()
-
-    def step():
-        api.generate_manifold_batch(s1, s2, P1, P2, cfg, out=out)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    # ---- device-resident value ----------------------------------------------------
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
-    clocks.wait_first(step)
-    clocks.mark()
-    barrier()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for a, b in ev:
-        a.record(stream)
-        step()
-        b.record(stream)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    total_ms = max_over_ranks(t0.elapsed_time(t1))
-    kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    ms_per_step = total_ms / args.steps
-    value = n_total / (ms_per_step * 1e-3)
-
-    # ---- end-to-end through the host-buffer C-ABI call --------------------------
-    h1 = torch.as_tensor(p1).pin_memory().numpy()
-    h2 = torch.as_tensor(p2).pin_memory().numpy()
-    mean_h = torch.empty(hi - lo, dtype=torch.float32).pin_memory().numpy()
-
-    def e2e_step():
-        api.generate_manifold_batch_host(s1, s2, h1, h2, cfg, mean_out=mean_h, stream=stream)
-
-    for _ in range(max(3, args.warmup)):
-        e2e_step()
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    e2e_value = n_total / (e2e_ms * 1e-3)
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of the manifold kernel (DESIGN.md §5) ----------------------------
-    # Primary, as SURVEY §8(d) defines it: the reference formulation's algorithmic
-    # flops per env (763,163) x envs / kernel time, against the CUDA-core FP32
-    # peak (no dense contraction: tensor cores unused). Secondary: the FP64 pipe
-    # the kernel actually runs on, with its ncu-executed FP64 flops per env.
-    lib = abi.load()
-    import ctypes as C
-    f64 = C.c_double()
-    f32 = C.c_double()
-    lib.cmgb_probe_fma_tflops.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_void_p]
-    lib.cmgb_probe_fma_tflops(1, 4096, C.byref(f64), stream.cuda_stream)
-    lib.cmgb_probe_fma_tflops(0, 8192, C.byref(f32), stream.cuda_stream)
-    achieved = W_FLOP_PER_ENV * n_local / (kernel_ms * 1e-3) / 1e12
-    peaks = measured_peaks()
-
-    def prof_json(name):
-        path = os.path.join(ROOT, "profiles", name)
-        try:
-            return json.load(open(path))
-        except (OSError, ValueError):
-            return {}
-
-    tr = prof_json("manifold_dram_bytes.json").get("dram_bytes_per_launch_per_env")
-    traffic = tr * n_local if tr else None
-    ops = prof_json("manifold_fp64_ops.json")
-    x64 = ops.get("fp64_flop_per_env")
-    f64_achieved = x64 * n_local / (kernel_ms * 1e-3) / 1e12 if x64 else None
-    hbm_gbs = BYTES_PER_ENV * n_local / (kernel_ms * 1e-3) / 1e9
-    roof = {
-        "bound": "fp32", "achieved": achieved, "peak": f32.value, "unit": "TFLOP/s",
-        "frac": achieved / f32.value if f32.value else None, "traffic": traffic,
-        "peak_source": "measured live on this GPU: FFMA-chain microbenchmark (cmgb_probe_fma_tflops); "
-                       "MEASURED_PEAKS.json has no FP32/FP64 CUDA-core figure",
-        "work_per_env_flop": W_FLOP_PER_ENV,
-        "work_note": "algorithmic flops of the reference formulation (SURVEY §8(d), CUDA-core bound, tensor "
-                     "cores unused); traffic = ncu dram read+write bytes per launch (profiles/)",
-        "fp64_pipe": {"executed_flop_per_env": x64, "achieved": f64_achieved, "peak": f64.value,
-                      "unit": "TFLOP/s", "frac": f64_achieved / f64.value if (f64_achieved and f64.value) else None,
-                      "ncu_pipe_active_pct": ops.get("ncu_fp64_pipe_active_pct"),
-                      "note": "the kernel computes in FP64 (DESIGN.md §4); executed DFMA x2 + DMUL + DADD per "
-                              "env from ncu (profiles/manifold_fp64_ops.json); peak = live DFMA microbenchmark"},
-        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
-                "frac": hbm_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None},
-        "kernel_ms": kernel_ms,
-    }
-    cb = None if args.no_cpu_baseline else cpu_reference_run(args.cpu_sample, reps=3)
-    line = {
-        "metric": "contact manifolds/sec (box-box, 65,536 envs)",
-        "value": value, "unit": "manifolds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64 (FP32 outputs)", "data": "synthetic",
-        "config": {"workload": "box-box (config B): quad cube half 0.5 + SQ eps 0.1, M=12, 304 contacts/env",
-                   "n_env_per_gpu": n_local, "n_env_total": n_total, "contacts_per_env": L["n_contacts"],
-                   "variant": "ours (default SmoothingConfig)", "parallelism": f"env-shard x{world}",
-                   "l2": "per-step working set 6.3 MB poses in + 637 MB contacts out > 126 MB L2"},
-        "e2e": {"value": e2e_value, "unit": "manifolds/s",
-                "h2d_bytes_per_step": int(h1.nbytes + h2.nbytes) * world,
-                "d2h_bytes_per_step": int(mean_h.nbytes) * world,
-                "path": "cmgb_manifold_batch_host (pinned host poses -> H2D -> kernel -> D2H mean distance)"},
-        "gpu_launches": 3 * args.steps,  # per step: frames_kernel (both bodies) + vs_kernel + manifold_kernel
-        "roofline": roof,
-        "cpu_baseline": cb,
-        "clocks": clk,
-    }
-    print(json.dumps(line), flush=True)
-    if world > 1:
+    ctx = Ctx(args)
+    wl = args.workload
+    if wl == "box-box":
+        out = bench_box_box(ctx)
+    elif wl == "mixed":
+        out = bench_mixed(ctx)
+    elif wl in ("drop", "drop-fwd"):
+        out = bench_drop(ctx, wl == "drop")
+    elif wl in ("ee", "vf"):
+        out = bench_witness(ctx, wl)
+    else:
+        out = bench_demo(ctx)
+    if ctx.rank == 0:
+        print(json.dumps(out), flush=True)
+    if ctx.world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

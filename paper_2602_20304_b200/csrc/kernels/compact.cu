@@ -220,6 +220,7 @@ int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int
   configured([] {
     cudaFuncSetAttribute(compact_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
+  note_launch();
   if (stage <= 200 * 1024)
     compact_kernel<true><<<(unsigned)tiles, 32 * p.epb, stage, s>>>(p);
   else

@@ -10,6 +10,8 @@
 // FP64 throughout (the contacts arrive as the ABI's FP32 outputs).
 #include <cuda_runtime.h>
 
+#include "launch_util.cuh"
+
 #include "../common.h"
 #include "../device/dmath.cuh"
 #include "../device/pose.cuh"
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(128) integrate_kernel(const __grid_constant__ 
 int launch_penalty(const PenaltyArgs& a, void* stream) {
   if (a.n_env <= 0) return 0;
   const int64_t threads = a.n_env * kPenaltyLanes;
+  note_launch();
   penalty_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -178,6 +181,7 @@ int launch_penalty(const PenaltyArgs& a, void* stream) {
 int launch_integrate(const IntegrateArgs& a, void* stream) {
   const int64_t n = a.n_env;
   if (n <= 0) return 0;
+  note_launch();
   integrate_kernel<<<(unsigned)((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

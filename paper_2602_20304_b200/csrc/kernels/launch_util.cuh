@@ -8,6 +8,15 @@
 
 namespace cmgb {
 
+// Host-side count of this library's kernel launches (exported as
+// cmgb_kernel_launches): bench.py reads it around its timed regions, so the
+// launch count it reports is measured, not claimed.
+inline std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+
 // Runs f() once per CUDA device (function attributes such as the dynamic
 // shared-memory limit are per device); idempotent f, so a racing second call is
 // harmless.

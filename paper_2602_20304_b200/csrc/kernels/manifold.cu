@@ -647,6 +647,7 @@ __global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ Manifol
 int launch_frames(const double* poses1, int64_t stride1, int64_t n1, double* frames1, const double* poses2,
                   int64_t stride2, int64_t n2, double* frames2, cudaStream_t s) {
   if (n1 + n2 <= 0) return 0;
+  note_launch();
   frames_kernel<<<(unsigned)((n1 + n2 + 255) / 256), 256, 0, s>>>(poses1, stride1, n1, frames1, poses2, stride2, n2,
                                                                   frames2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
@@ -659,6 +660,7 @@ int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cud
     cudaFuncSetAttribute(manifold_kernel<K1, K2, kGP, kVsX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
   });
+  note_launch();
   manifold_kernel<K1, K2, kGP, kVsX><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -697,6 +699,7 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
     int G = 1;
     while (G < nvs) G <<= 1;
     const int64_t threads = p.n_env * G;
+    note_launch();
     vs_kernel<kSqE01, kSqE01><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(q, G);
     if (cudaGetLastError() != cudaSuccess) return 1;
     return launch_kind<kSqE01, kSqE01, false, true>(q, block_threads, grid, smem_bytes, s);

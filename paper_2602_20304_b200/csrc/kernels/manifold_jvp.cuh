@@ -1176,6 +1176,7 @@ int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
     cudaFuncSetAttribute(manifold_jvp_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const int64_t grid = (p.m.n_env + p.units_per_block - 1) / p.units_per_block;
+  note_launch();
   manifold_jvp_kernel<K1, K2><<<(unsigned)grid, threads, (size_t)p.bytes * p.units_per_block + p.geom_bytes, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "../../../include/cmgb_probe.h"
+#include "launch_util.cuh"
 
 namespace {
 
@@ -54,3 +55,5 @@ extern "C" int cmgb_probe_fma_tflops(int32_t fp64, int32_t iters, double* tflops
   *tflops = fp64 ? run<double>(iters, s) : run<float>(iters, s);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
+
+extern "C" uint64_t cmgb_kernel_launches(void) { return cmgb::launch_counter().load(std::memory_order_relaxed); }

@@ -5,6 +5,8 @@
 // surface's compile-time SDF kind included).
 #include <cuda_runtime.h>
 
+#include "launch_util.cuh"
+
 #include "../common.h"
 #include "../device/dmath.cuh"
 #include "../device/sdf.cuh"
@@ -49,10 +51,10 @@ template <int KIND>
 int launch_query_kind(const SdfQueryParams& q, int mode, cudaStream_t s) {
   const unsigned grid = (unsigned)((q.n + 255) / 256);
   switch (mode) {
-    case 0: sdf_query_kernel<kValue, KIND><<<grid, 256, 0, s>>>(q); break;
-    case 1: sdf_query_kernel<kGrad, KIND><<<grid, 256, 0, s>>>(q); break;
-    case 2: sdf_query_kernel<kNormalSource, KIND><<<grid, 256, 0, s>>>(q); break;
-    default: sphere_trace_kernel<KIND><<<grid, 256, 0, s>>>(q); break;
+    case 0: note_launch(); sdf_query_kernel<kValue, KIND><<<grid, 256, 0, s>>>(q); break;
+    case 1: note_launch(); sdf_query_kernel<kGrad, KIND><<<grid, 256, 0, s>>>(q); break;
+    case 2: note_launch(); sdf_query_kernel<kNormalSource, KIND><<<grid, 256, 0, s>>>(q); break;
+    default: note_launch(); sphere_trace_kernel<KIND><<<grid, 256, 0, s>>>(q); break;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -139,6 +139,7 @@ int launch_witness(const WitnessParams& p, cudaStream_t s) {
   });
   const int64_t need = (p.n + kWitnessThreads - 1) / kWitnessThreads;
   const int grid = (int)(need < cap ? (need > 0 ? need : 1) : cap);
+  note_launch();
   witness_kernel<T, Solve><<<grid, kWitnessThreads, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
