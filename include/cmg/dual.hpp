@@ -1,0 +1,5 @@
+// Drop-in forwarding header: the reference's include/cmg/dual.hpp (Dual, seed_pose_tangents) resolved
+// to the B200 path. Put <repo>/include on the include path instead of the
+// reference's; everything lives in cmgb_cmg.hpp.
+#pragma once
+#include "../cmgb_cmg.hpp"

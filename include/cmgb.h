@@ -209,6 +209,16 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
                              int32_t pose2_stride, int64_t n_env, const cmgb_config* cfg,
                              float* mean_dist_host, float* contacts_host, void* cuda_stream);
 
+/* General host-buffer form: every field of host_out is a HOST pointer (or
+ * null): contacts [n_env][n_contacts][8], src [n_env][n_contacts][2], ee
+ * [n_env][9][m1*m2] (full mode), mean_dist [n_env]; workspace fields ignored.
+ * Replaces generate_manifold<double> returning ContactManifold by value
+ * (manifold.hpp:336-377); used by the C++ drop-in header (cmgb_cmg.hpp). */
+int cmgb_manifold_batch_host_ex(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                                int32_t pose1_stride, const double* poses2_host, int32_t pose2_stride,
+                                int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_out* host_out,
+                                void* cuda_stream);
+
 /* ---------------------------------------------------------------------------
  * Active-contact compaction — an EXTRA output beside the fixed layout (which it
  * never replaces; manifold.hpp:62-72, 303-330): the contacts of a batch with
@@ -260,6 +270,13 @@ int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* pose
                             int32_t pose1_stride, const double* poses2, int32_t pose2_stride,
                             int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_jvp_out* out,
                             void* cuda_stream);
+
+/* Host-buffer form: poses and every output field of host_out are HOST memory
+ * (generate_manifold<Dual12> by value, main.cpp:202-205). Synchronous. */
+int cmgb_manifold_jvp_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                                 int32_t pose1_stride, const double* poses2_host, int32_t pose2_stride,
+                                 int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_jvp_out* host_out,
+                                 void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * Batched demo integrator — DemoSim::step (src/demosim.cpp:81-138) for every
@@ -361,6 +378,16 @@ int cmgb_rotating_edge_sweep(int32_t variant, int32_t n_samples, double* out_hos
 int cmgb_vf_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
                           const cmgb_config* cfg, float* out, int32_t* labels,
                           void* cuda_stream);
+
+/* Host-buffer witness batches with the reference's output precision
+ * (run_ee_batch / run_vf_batch write doubles, src/batch.cpp:53-98): pairs_host
+ * [n][12] FP64; out_host [n][6] (E-E: the FP64 solver of
+ * cmgb_ee_witness_batch_f64) / [n][3] (V-F: FP32 solver, widened); labels
+ * optional. Synchronous. */
+int cmgb_ee_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
+                               int32_t* labels_host, void* cuda_stream);
+int cmgb_vf_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
+                               int32_t* labels_host, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * Device info (SM count etc. queried, never hard-coded).

@@ -1,16 +1,19 @@
-// cmgb.hpp — header-only C++ wrapper over the C ABI (include/cmgb.h) that
-// mirrors the reference's C++ collision API (namespace cmg, /root/reference/
-// proj/include/cmg) so a C++ caller of the reference switches by changing
-// includes:
+// cmgb.hpp — thin RAII C++ wrapper over the C ABI (include/cmgb.h) for callers
+// that manage DEVICE buffers and streams themselves (batched calls on device
+// pointers, throwing on error). It does NOT have the reference's signatures:
+// the reference-signature drop-in (namespace cmg: generate_manifold<T>,
+// ContactManifold, run_ee_batch(problems, cfg, workers, out) -> checksum,
+// bench_manifold(scene, ...), ...) is include/cmgb_cmg.hpp, reached through the
+// forwarding headers include/cmg/*.hpp by swapping the include path.
 //
 //   cmg::make_box_mesh / parse_obj        -> cmgb::Mesh::box / Mesh::parse_obj
 //   cmg::build_surface                     -> cmgb::Surface
 //   cmg::SmoothingConfig (+ variants)      -> cmgb::SmoothingConfig
-//   cmg::generate_manifold (per env loop)  -> cmgb::generate_manifold_batch
-//   cmg::run_ee_batch / run_vf_batch       -> cmgb::run_ee_batch / run_vf_batch
+//   bench_manifold's per-env loop          -> cmgb::generate_manifold_batch (device poses / outputs)
+//   cmg::run_ee_batch / run_vf_batch       -> cmgb::run_ee_batch / run_vf_batch (device pairs / outputs)
 //
-// Errors: the reference throws std::invalid_argument / MeshParseError; this
-// wrapper throws the same exception types with the library's message.
+// Errors: std::invalid_argument / MeshParseError / std::runtime_error with the
+// library's message.
 #pragma once
 
 #include <stdexcept>

@@ -218,6 +218,17 @@ SIGNATURES = {
          C.c_int64, _P, _P, _P, _P, _P, C.c_size_t, _P],
     ),
     "cmgb_scene_pairs": (_I, [_P, C.c_int32, _P, C.POINTER(C.c_int32)]),
+    "cmgb_manifold_batch_host_ex": (
+        _I,
+        [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig), C.POINTER(CmgbManifoldOut), _P],
+    ),
+    "cmgb_manifold_jvp_batch_host": (
+        _I,
+        [_P, _P, _P, C.c_int32, _P, C.c_int32, C.c_int64, C.POINTER(CmgbConfig),
+         C.POINTER(CmgbManifoldJvpOut), _P],
+    ),
+    "cmgb_ee_witness_batch_host": (_I, [_P, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P]),
+    "cmgb_vf_witness_batch_host": (_I, [_P, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P]),
     "cmgb_compact_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
     "cmgb_compact_contacts": (
         _I,

@@ -277,7 +277,9 @@ struct HostScratch {
   float* contacts = nullptr;
   float* mean = nullptr;
   double* frames = nullptr;
-  size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0, cap_frames = 0;
+  int32_t* src = nullptr;
+  float* ee = nullptr;
+  size_t cap_poses1 = 0, cap_poses2 = 0, cap_contacts = 0, cap_mean = 0, cap_frames = 0, cap_src = 0, cap_ee = 0;
   cudaStream_t q[2] = {nullptr, nullptr};  // pipeline streams of the host-buffer API
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaEvent_t ev_start = nullptr;
@@ -632,11 +634,15 @@ int cmgb_manifold_batch(cmgb_surface s1, cmgb_surface s2, const double* poses1, 
   });
 }
 
-int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
-                             int32_t st1, const double* poses2_host, int32_t st2, int64_t n_env,
-                             const cmgb_config* cfg, float* mean_dist_host, float* contacts_host,
-                             void* stream) {
+int cmgb_manifold_batch_host_ex(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                                int32_t st1, const double* poses2_host, int32_t st2, int64_t n_env,
+                                const cmgb_config* cfg, const cmgb_manifold_out* host_out, void* stream) {
   return guarded([&] {
+    if (!host_out) invalid("manifold_batch_host: null output descriptor");
+    float* mean_dist_host = host_out->mean_dist;
+    float* contacts_host = host_out->contacts;
+    int32_t* src_host = host_out->src;
+    float* ee_host = host_out->ee;
     if (!s1 || !s2) invalid("manifold_batch_host: null surface");
     validate_config(cfg);
     if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
@@ -652,6 +658,10 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     ensure(&sc.poses2, &sc.cap_poses2, np2);
     ensure(&sc.contacts, &sc.cap_contacts, (size_t)n_env * L.n_contacts * 8);
     ensure(&sc.mean, &sc.cap_mean, (size_t)n_env);
+    const size_t P = (size_t)L.m1 * L.m2;
+    if (!(L.m1 > 0 && L.m2 > 0)) ee_host = nullptr;  // EeIndicatorMatrices exist in full mode only
+    if (src_host) ensure(&sc.src, &sc.cap_src, (size_t)n_env * L.n_contacts * 2);
+    if (ee_host) ensure(&sc.ee, &sc.cap_ee, (size_t)n_env * 9 * P);
     // Pipelined over env chunks on two internal streams: chunk c+1's pose
     // upload overlaps chunk c's kernels, and each chunk's results stream back
     // as soon as it is done. Ordered after the caller's stream and joined back
@@ -675,7 +685,7 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     constexpr int64_t lead_div = 8;
     constexpr int kHostChunksFull = 8;
     std::vector<int64_t> bounds = {0, n_env};
-    if (contacts_host && n_env >= 2 * kHostChunkMin) {
+    if ((contacts_host || src_host || ee_host) && n_env >= 2 * kHostChunkMin) {
       const int64_t k = std::min<int64_t>(kHostChunksFull, n_env / kHostChunkMin);
       bounds.clear();
       for (int64_t c = 0; c <= k; ++c) bounds.push_back(n_env * c / k);
@@ -712,7 +722,8 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
         cuda_check(cudaMemcpyAsync(p2, poses2_host + 6 * e0, sizeof(double) * 6 * ne, cudaMemcpyHostToDevice, q),
                    "H2D poses2");
       // n == 1 chunks keep stride semantics: a single-env chunk with st = 1 is one pose
-      cmgb_manifold_out out{sc.contacts + e0 * C * 8, nullptr, nullptr, sc.mean + e0,
+      cmgb_manifold_out out{sc.contacts + e0 * C * 8, src_host ? sc.src + e0 * C * 2 : nullptr,
+                            ee_host ? sc.ee + e0 * 9 * P : nullptr, sc.mean + e0,
                             sc.frames + (c & 1) * workspace_doubles(per, st1, st2),
                             workspace_doubles(per, st1, st2) * sizeof(double)};
       LaunchPlan plan = plan_manifold(s1, s2, p1, st1, p2, st2, ne, cfg, &out);
@@ -724,6 +735,14 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
         cuda_check(cudaMemcpyAsync(contacts_host + e0 * C * 8, sc.contacts + e0 * C * 8, sizeof(float) * ne * C * 8,
                                    cudaMemcpyDeviceToHost, q),
                    "D2H contacts");
+      if (src_host)
+        cuda_check(cudaMemcpyAsync(src_host + e0 * C * 2, sc.src + e0 * C * 2, sizeof(int32_t) * ne * C * 2,
+                                   cudaMemcpyDeviceToHost, q),
+                   "D2H src");
+      if (ee_host)
+        cuda_check(cudaMemcpyAsync(ee_host + e0 * 9 * P, sc.ee + e0 * 9 * P, sizeof(float) * ne * 9 * P,
+                                   cudaMemcpyDeviceToHost, q),
+                   "D2H ee");
     }
     for (int k = 0; k < 2; ++k) {
       cuda_check(cudaEventRecord(sc.ev[k], sc.q[k]), "cudaEventRecord");
@@ -731,6 +750,14 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
     }
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   });
+}
+
+int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host,
+                             int32_t st1, const double* poses2_host, int32_t st2, int64_t n_env,
+                             const cmgb_config* cfg, float* mean_dist_host, float* contacts_host,
+                             void* stream) {
+  const cmgb_manifold_out o{contacts_host, nullptr, nullptr, mean_dist_host, nullptr, 0};
+  return cmgb_manifold_batch_host_ex(s1, s2, poses1_host, st1, poses2_host, st2, n_env, cfg, &o, stream);
 }
 
 // ---- active-contact compaction -----------------------------------------------------
@@ -862,6 +889,128 @@ int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* pose
     if (n_env == 0 || plan.p.n_contacts == 0) return;
     if (!out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
     launch_jvp(plan_jvp(plan, out), static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Host-buffer form of the pose-Jacobian batch: device buffers from the stream-
+// ordered pool for the duration of the call, synchronised before returning.
+namespace {
+
+struct PoolBuffers {  // cudaMallocAsync blocks released in order on the stream (also on error)
+  cudaStream_t s;
+  std::vector<void*> bufs;
+  explicit PoolBuffers(cudaStream_t st) : s(st) {}
+  void* get(size_t bytes) {
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s), "cudaMallocAsync");
+    bufs.push_back(p);
+    return p;
+  }
+  ~PoolBuffers() {
+    for (void* p : bufs) cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+  }
+};
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+}
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (dst) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+}
+
+}  // namespace
+
+int cmgb_manifold_jvp_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host, int32_t st1,
+                                 const double* poses2_host, int32_t st2, int64_t n_env, const cmgb_config* cfg,
+                                 const cmgb_manifold_jvp_out* host_out, void* stream) {
+  return guarded([&] {
+    validate_jvp(cfg, host_out);
+    if (!s1 || !s2) invalid("manifold_jvp_batch_host: null surface");
+    if ((st1 != 0 && st1 != 1) || (st2 != 0 && st2 != 1)) invalid("manifold: pose stride must be 0 or 1");
+    if (n_env == 0) return;
+    if (n_env < 0) invalid("manifold: n_env >= 0");
+    if (!poses1_host || !poses2_host) invalid("manifold_jvp_batch_host: null poses");
+    if (!host_out->contacts || !host_out->tangents)
+      invalid("manifold_jvp: contacts and tangents outputs are required");
+    const cmgb_layout L = layout_of(s1, s2, cfg);
+    const size_t n = (size_t)n_env, C = (size_t)L.n_contacts;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PoolBuffers pb(s);
+    const size_t np1 = (st1 ? n : 1) * 6, np2 = (st2 ? n : 1) * 6;
+    double* p1 = static_cast<double*>(pb.get(sizeof(double) * (np1)));
+    double* p2 = static_cast<double*>(pb.get(sizeof(double) * (np2)));
+    h2d(p1, poses1_host, sizeof(double) * np1, s);
+    h2d(p2, poses2_host, sizeof(double) * np2, s);
+    cmgb_manifold_jvp_out d{};
+    d.contacts = static_cast<float*>(pb.get(sizeof(float) * (n * C * 8)));
+    d.tangents = static_cast<float*>(pb.get(sizeof(float) * (n * C * 96)));
+    d.src = host_out->src ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * (n * C * 2))) : nullptr;
+    d.mean_dist = host_out->mean_dist ? static_cast<float*>(pb.get(sizeof(float) * (n))) : nullptr;
+    d.mean_dist_grad = host_out->mean_dist_grad ? static_cast<float*>(pb.get(sizeof(float) * (n * 12))) : nullptr;
+    d.mean_dist_f64 = host_out->mean_dist_f64 ? static_cast<double*>(pb.get(sizeof(double) * (n))) : nullptr;
+    d.mean_dist_grad_f64 = host_out->mean_dist_grad_f64 ? static_cast<double*>(pb.get(sizeof(double) * (n * 12))) : nullptr;
+    cmgb_manifold_out mo{d.contacts, d.src, nullptr, d.mean_dist, nullptr, 0};
+    LaunchPlan plan = plan_manifold(s1, s2, p1, st1, p2, st2, n_env, cfg, &mo);
+    if (plan.p.n_contacts == 0) return;
+    launch_jvp(plan_jvp(plan, &d), s);
+    d2h(host_out->contacts, d.contacts, sizeof(float) * n * C * 8, s);
+    d2h(host_out->tangents, d.tangents, sizeof(float) * n * C * 96, s);
+    if (d.src) d2h(host_out->src, d.src, sizeof(int32_t) * n * C * 2, s);
+    if (d.mean_dist) d2h(host_out->mean_dist, d.mean_dist, sizeof(float) * n, s);
+    if (d.mean_dist_grad) d2h(host_out->mean_dist_grad, d.mean_dist_grad, sizeof(float) * n * 12, s);
+    if (d.mean_dist_f64) d2h(host_out->mean_dist_f64, d.mean_dist_f64, sizeof(double) * n, s);
+    if (d.mean_dist_grad_f64)
+      d2h(host_out->mean_dist_grad_f64, d.mean_dist_grad_f64, sizeof(double) * n * 12, s);
+  });
+}
+
+// Host-buffer witness batches with reference-precision outputs (run_ee_batch /
+// run_vf_batch, src/batch.cpp:53-98, return doubles): E-E through the FP64
+// solver; V-F through the FP32-output solver, widened.
+int cmgb_ee_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
+                               int32_t* labels_host, void* stream) {
+  return guarded([&] {
+    validate_config(cfg);
+    if (n < 0) invalid("ee_witness_batch_host: n >= 0");
+    if (n == 0) return;
+    if (!pairs_host || !out_host) invalid("ee_witness_batch_host: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PoolBuffers pb(s);
+    double* pairs = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 12)));
+    double* out = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 6)));
+    int32_t* labels = labels_host ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * ((size_t)n))) : nullptr;
+    h2d(pairs, pairs_host, sizeof(double) * 12 * n, s);
+    WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, nullptr};
+    if (launch_ee_witness_f64(p, stream) != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("ee_witness_f64 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    d2h(out_host, out, sizeof(double) * 6 * n, s);
+    if (labels) d2h(labels_host, labels, sizeof(int32_t) * n, s);
+  });
+}
+
+int cmgb_vf_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
+                               int32_t* labels_host, void* stream) {
+  return guarded([&] {
+    validate_config(cfg);
+    if (n < 0) invalid("vf_witness_batch_host: n >= 0");
+    if (n == 0) return;
+    if (!pairs_host || !out_host) invalid("vf_witness_batch_host: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<float> out32((size_t)n * 3);
+    {
+      PoolBuffers pb(s);
+      double* pairs = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 12)));
+      float* out = static_cast<float*>(pb.get(sizeof(float) * ((size_t)n * 3)));
+      int32_t* labels = labels_host ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * ((size_t)n))) : nullptr;
+      h2d(pairs, pairs_host, sizeof(double) * 12 * n, s);
+      WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, nullptr};
+      if (launch_vf_witness(p, stream) != 0)
+        throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
+      d2h(out32.data(), out, sizeof(float) * 3 * n, s);
+      if (labels) d2h(labels_host, labels, sizeof(int32_t) * n, s);
+    }  // synchronised here
+    for (size_t i = 0; i < out32.size(); ++i) out_host[i] = out32[i];
   });
 }
 
