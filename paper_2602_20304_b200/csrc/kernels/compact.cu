@@ -21,6 +21,7 @@
 // Envs too large to stage (C x 32 B beyond the shared-memory budget) read
 // their contacts from global memory twice instead (kStaged = false).
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -37,6 +38,7 @@ namespace {
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagIncl = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
+constexpr int kMaskWords = 40;  // ballots kept in shared memory for C <= 1,280 contacts per env
 
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   uint64_t v;
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
   __shared__ uint32_t s_tile;
   __shared__ int64_t s_base;
   __shared__ int32_t s_cnt[8];
+  __shared__ unsigned s_mask[8][kMaskWords];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = p.C;
   if (threadIdx.x == 0) s_tile = atomicAdd(p.ticket, 1u);
@@ -95,14 +98,20 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
     tile_c = reinterpret_cast<const float4*>(smem);
   }
 
-  // ---- per-env counts (one warp per env) --------------------------------------
+  // ---- per-env counts (one warp per env); the ballots are kept per warp for
+  // the write pass (up to kMaskWords chunks, else the activities are re-read)
   int cnt = 0;
+  const bool masks = C <= 32 * kMaskWords;
   if (warp < n_here) {
     const float4* ec = tile_c + (int64_t)warp * C * 2;
+    const float* act = reinterpret_cast<const float*>(ec) + 7;  // activity of contact j at act[8 j]
+#pragma unroll 4
     for (int j0 = 0; j0 < C; j0 += 32) {
       const int j = j0 + lane;
-      const bool keep = j < C && ec[2 * j + 1].w > p.thr;
-      cnt += __popc(__ballot_sync(0xffffffffu, keep));
+      const bool keep = j < C && act[8 * j] > p.thr;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (masks && lane == 0) s_mask[warp][j0 >> 5] = m;
+      cnt += __popc(m);
     }
     if (lane == 0) s_cnt[warp] = cnt;
   }
@@ -155,19 +164,17 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
   }
   const float4* ec = tile_c + (int64_t)warp * C * 2;
   float4* oc = reinterpret_cast<float4*>(p.out_contacts);
+  const float* act = reinterpret_cast<const float*>(ec) + 7;
   for (int j0 = 0; j0 < C; j0 += 32) {
     const int j = j0 + lane;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (j < C) {
-      a = ec[2 * j];
-      b = ec[2 * j + 1];
-    }
-    const bool keep = j < C && b.w > p.thr;
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const unsigned m =
+        masks ? s_mask[warp][j0 >> 5] : __ballot_sync(0xffffffffu, j < C && act[8 * j] > p.thr);
+    if (m == 0u) continue;
+    const bool keep = (m >> lane) & 1u;
     const int64_t dst = off + __popc(m & ((1u << lane) - 1u));
-    if (keep && dst < p.capacity) {
-      oc[2 * dst] = a;
-      oc[2 * dst + 1] = b;
+    if (keep && dst < p.capacity) {  // only the kept contacts are read again (L2-resident)
+      oc[2 * dst] = ec[2 * j];
+      oc[2 * dst + 1] = ec[2 * j + 1];
       if (p.out_slot) p.out_slot[dst] = j;
       if (p.out_src) {
         const int2 s = reinterpret_cast<const int2*>(p.src)[e * C + j];
@@ -186,9 +193,19 @@ size_t compact_workspace_bytes(int64_t n_env, int C) {
   return sizeof(uint64_t) * (size_t)(tiles + 2);
 }
 
-// Envs per tile: up to 8 warps, tile staged in <= 40 KB of shared memory
-// (several CTAs per SM keep bulk copies in flight), at least one env.
+// A/B switch for measurement (CMGB_COMPACT_STAGED=1: TMA-staged tiles).
+static bool compact_staged() {
+  static const int v = [] {
+    const char* e = getenv("CMGB_COMPACT_STAGED");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// Envs per tile: staged, up to 8 warps in <= 40 KB of shared memory (several
+// CTAs per SM keep bulk copies in flight); direct, 8 warps.
 int compact_envs_per_tile(int C) {
+  if (!compact_staged()) return 8;
   const int per_env = C * 32;
   int epb = per_env > 0 ? (40 * 1024) / per_env : 8;
   return epb < 1 ? 1 : (epb > 8 ? 8 : epb);
@@ -221,7 +238,7 @@ int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int
     cudaFuncSetAttribute(compact_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   note_launch();
-  if (stage <= 200 * 1024)
+  if (compact_staged() && stage <= 200 * 1024)
     compact_kernel<true><<<(unsigned)tiles, 32 * p.epb, stage, s>>>(p);
   else
     compact_kernel<false><<<(unsigned)tiles, 32 * p.epb, 0, s>>>(p);

@@ -1,4 +1,4 @@
-"""One warm launch of a kernel for ncu capture (python tools/profile_run.py manifold|mixed:<bucket>|drop|drop-fwd|ee|vf [n])."""
+"""One warm launch of a kernel for ncu capture (python tools/profile_run.py manifold|compact|mixed:<bucket>|drop|drop-fwd|ee|vf [n])."""
 import os, sys
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -25,14 +25,17 @@ elif kind in ("drop", "drop-fwd"):
     outs = None
     for _ in range(2):
         outs = fn(bodies, P, SmoothingConfig(), is_static=sc.is_static(), outs=outs)
-elif kind == "manifold":
+elif kind in ("manifold", "compact"):
     ws = W.box_box(n)
     s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
     p1, p2 = ws.poses(n)
     P1 = torch.as_tensor(p1, device="cuda"); P2 = torch.as_tensor(p2, device="cuda")
     out = {}
+    comp = {}
     for _ in range(3):
         api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out)
+        if kind == "compact":
+            api.compact_contacts(out["contacts"], 0.01, out=comp)
 else:
     pairs = torch.rand((n, 12), dtype=torch.float64, device="cuda")
     for _ in range(3):
