@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcmgb.so")
+# CMGB_LIBRARY: developer override (e.g. an instrumented -DCMGB_PHASE_CLOCKS build)
+LIB_PATH = os.environ.get("CMGB_LIBRARY") or os.path.join(_HERE, "libcmgb.so")
 
 CMGB_OK = 0
 STATUS_NAMES = {

@@ -23,7 +23,30 @@ constexpr int kPairRec = 38;    // floats per E-E pair record in shared memory (
 // kBoxCp: a lone convex polyhedron whose 6 planes are the axis-aligned box
 // pattern of box_planes (scene.cpp:49-62: +x, -x, +y, -y, +z, -z unit
 // normals): plane distances are +-p_i - w_i (bit-identical to the FMA dot).
-enum SdfKind : int32_t { kSingleSq = 0, kSingleCp = 1, kGeneric = 2, kSqE01 = 3, kBoxCp = 4 };
+enum SdfKind : int32_t {
+  kSingleSq = 0, kSingleCp = 1, kGeneric = 2, kSqE01 = 3, kBoxCp = 4,
+  // more lone superquadrics with compile-time exponents (n1, n2, n3, n4):
+  kSqE02 = 5,   // eps1 = eps2 = 0.2  (5, 1, 5, 10): rounded box (config C), box-box eps 0.2
+  kSqE025 = 6,  // eps1 = eps2 = 0.25 (4, 1, 4, 8)
+  kSqE05 = 7,   // eps1 = eps2 = 0.5  (2, 1, 2, 4)
+  kSqEll = 8,   // eps1 = eps2 = 1    (1, 1, 1, 2): ellipsoid / sphere
+  kSqCyl = 9    // eps1 = 0.1, eps2 = 1 (1, 10, 10, 20): cylinder (config C)
+};
+
+// Exponents of the compile-time superquadric kinds (0: not such a kind).
+struct SqExpTuple {
+  int n1, n2, n3, n4;
+};
+__host__ __device__ constexpr SqExpTuple sq_exps(int k) {
+  return k == kSqE01    ? SqExpTuple{10, 1, 10, 20}
+         : k == kSqE02  ? SqExpTuple{5, 1, 5, 10}
+         : k == kSqE025 ? SqExpTuple{4, 1, 4, 8}
+         : k == kSqE05  ? SqExpTuple{2, 1, 2, 4}
+         : k == kSqEll  ? SqExpTuple{1, 1, 1, 2}
+         : k == kSqCyl  ? SqExpTuple{1, 10, 10, 20}
+                        : SqExpTuple{0, 0, 0, 0};
+}
+__host__ __device__ constexpr bool ct_sq(int k) { return sq_exps(k).n1 > 0; }
 enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 3 };
 
 // Superquadric leaf, pre-digested on the host (sdf.hpp:85-108):
@@ -65,6 +88,7 @@ struct DevSdf {
 struct DevSide {
   const double* verts;  // [nv][3] body frame
   const int32_t* edges; // [ne][2]
+  const double* edge_body;  // [ne][6] endpoints a, b of every edge (body frame)
   int32_t nv, ne;
   int32_t n_sel;        // V-S contacts of this side (effective vertex top-K, or 0)
   int32_t m_sel;        // selected edges of this side (effective edge top-K, or 0)
@@ -99,6 +123,7 @@ struct SmemLayout {
   int32_t pairs;     // P x kPairRec floats: per E-E pair record
   int32_t vsdist;    // (n1+n2) floats
   int32_t nnstat;    // (m1+m2) x 2 floats: min, 1/sum
+  int32_t hpart;     // (warps per CTA) doubles: per-warp partial sums of the E-E distances (G)
   int32_t bytes;     // per env, 16-byte aligned
 };
 

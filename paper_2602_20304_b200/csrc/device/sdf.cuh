@@ -307,7 +307,10 @@ __device__ __forceinline__ SdfOutT<T> leaf_eval(const DevNode& nd, const double4
 template <int FL_IN, int KIND, class T = double>
 __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN, 0, 0, 0, 0, T>(s.nodes[0].sq, p);
-  if constexpr (KIND == kSqE01) return sq_leaf<FL_IN, 10, 1, 10, 20, T>(s.nodes[0].sq, p);
+  if constexpr (ct_sq(KIND)) {
+    constexpr SqExpTuple e = sq_exps(KIND);
+    return sq_leaf<FL_IN, e.n1, e.n2, e.n3, e.n4, T>(s.nodes[0].sq, p);
+  }
   // kNormalOnly skips phi only for a lone SQ leaf; compositions need the values.
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;

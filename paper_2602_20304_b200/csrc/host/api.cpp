@@ -133,6 +133,14 @@ DeviceSurface& device_image(cmgb_surface_s* s) {
   cuda_check(cudaMalloc(&d.edges, sizeof(int32_t) * s->mesh.edges.size()), "cudaMalloc");
   cuda_check(cudaMemcpy(d.edges, s->mesh.edges.data(), sizeof(int32_t) * s->mesh.edges.size(),
                         cudaMemcpyHostToDevice), "cudaMemcpy");
+  {
+    std::vector<double> eb(6 * (size_t)s->mesh.ne());
+    for (int e = 0; e < s->mesh.ne(); ++e)
+      for (int k = 0; k < 2; ++k)
+        for (int c = 0; c < 3; ++c) eb[6 * e + 3 * k + c] = s->mesh.vertices[3 * s->mesh.edges[2 * e + k] + c];
+    cuda_check(cudaMalloc(&d.edge_body, sizeof(double) * std::max<size_t>(eb.size(), 1)), "cudaMalloc");
+    cuda_check(cudaMemcpy(d.edge_body, eb.data(), sizeof(double) * eb.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
+  }
   if (!pool.empty()) {
     cuda_check(cudaMalloc(&d.pool, sizeof(double4) * pool.size()), "cudaMalloc");
     cuda_check(cudaMemcpy(d.pool, pool.data(), sizeof(double4) * pool.size(), cudaMemcpyHostToDevice),
@@ -172,6 +180,7 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     DevSide& side = p.side[k];
     side.verts = d.verts;
     side.edges = d.edges;
+    side.edge_body = d.edge_body;
     side.nv = ss[k]->mesh.nv();
     side.ne = ss[k]->mesh.ne();
     side.n_sel = nsel[k];
@@ -221,6 +230,7 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     S.pairs = off; off = align16(off + (pairs_in_smem ? P * kPairRec * 4 : 0));
     S.vsdist = off; off = align16(off + nslot_v * 4);
     S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
+    S.hpart = off; off = align16(off + 10 * 8);  // one partial per warp (<= 320-thread CTAs)
     S.bytes = off;
   };
   const size_t kSmemMax = 200 * 1024;
@@ -559,6 +569,7 @@ void cmgb_surface_destroy(cmgb_surface s) {
   for (auto& [dev, d] : s->device) {
     cudaSetDevice(dev);
     cudaFree(d.verts);
+    cudaFree(d.edge_body);
     cudaFree(d.edges);
     if (d.pool) cudaFree(d.pool);
   }

@@ -68,6 +68,7 @@ void se3_exp_host(const double xi[6], double R[9], double t[3]);
 struct DeviceSurface {
   double* verts = nullptr;
   int32_t* edges = nullptr;
+  double* edge_body = nullptr;  // [ne][6]: both endpoints of every edge (body frame), no index chase
   double4* pool = nullptr;
   DevSdf sdf{};
 };

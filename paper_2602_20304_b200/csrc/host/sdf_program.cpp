@@ -253,7 +253,10 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
   }
   if (s.kind == kSingleSq) {
     const DevSq& q = s.nodes[0].sq;
-    if (q.n1 == 10 && q.n2 == 1 && q.n3 == 10 && q.n4 == 20) s.kind = kSqE01;
+    for (int k : {kSqE01, kSqE02, kSqE025, kSqE05, kSqEll, kSqCyl}) {
+      const SqExpTuple e = sq_exps(k);
+      if (q.n1 == e.n1 && q.n2 == e.n2 && q.n3 == e.n3 && q.n4 == e.n4) s.kind = k;
+    }
   }
   if (s.kind == kSingleCp && prog.nodes[0].count == 6) {
     // the box_planes pattern: unit normals +x, -x, +y, -y, +z, -z in this order

@@ -51,7 +51,11 @@ SDF_PROGRAMS = {
 }
 
 
-JVP_ENVS = 2  # envs per case with recorded reference pose Jacobians (Dual12)
+JVP_ENVS = 16  # envs per case with recorded reference pose Jacobians (Dual12)
+JVP_FULL = 2   # the first JVP_FULL envs keep every contact's tangents; later envs every JVP_STRIDE-th contact
+JVP_STRIDE = 16
+JVP_FD_ENVS = 4  # envs per case whose reference tangents are also checked by finite differences (CPU suite)
+MANIFOLD_ENVS = 16
 DEMO_DT = 1e-3  # DemoSim golden rollouts: step and length (demo scene, envs 0 and 1)
 DEMO_STEPS = 300
 
@@ -61,24 +65,31 @@ def manifold_cases():
     base = SmoothingConfig()
     out = []
     for var in ("ours", "ours_ns", "ours_ne", "ours_ne_s"):
-        out.append((f"box_box_{var}", W.box_box(), base.for_variant(var), 8))
-    out.append(("box_on_plane_ours", W.box_on_plane(), base, 8))
-    out.append(("box_on_plane_ours_ns", W.box_on_plane(), base.for_variant("ours_ns"), 8))
+        out.append((f"box_box_{var}", W.box_box(), base.for_variant(var), MANIFOLD_ENVS))
+    out.append(("box_on_plane_ours", W.box_on_plane(), base, MANIFOLD_ENVS))
+    out.append(("box_on_plane_ours_ns", W.box_on_plane(), base.for_variant("ours_ns"), MANIFOLD_ENVS))
     ws = W.box_box()
     ws.bodies[0].vertex_topk, ws.bodies[1].vertex_topk = 4, 3
     ws.bodies[0].edge_topk, ws.bodies[1].edge_topk = 5, 4
-    out.append(("box_box_topk", ws, base, 8))
+    out.append(("box_box_topk", ws, base, MANIFOLD_ENVS))
     c = SmoothingConfig()
     c.containment_safeguard = True
-    out.append(("box_box_containment", W.box_box(), c, 8))
+    out.append(("box_box_containment", W.box_box(), c, MANIFOLD_ENVS))
     c = SmoothingConfig()
     c.sphere_trace = False
-    out.append(("box_box_notrace", W.box_box(), c, 8))
+    out.append(("box_box_notrace", W.box_box(), c, MANIFOLD_ENVS))
     for name in ("mixed_rounded_box", "mixed_cylinder", "mixed_ellipsoid", "mixed_capsule"):
-        out.append((name, W.mixed_bucket(name.split("_", 1)[1]), base, 8))
-    out.append(("opc_vs_box", opc_vs_box(), base, 8))
-    out.append(("subtraction_vs_box", subtraction_vs_box(), base, 8))
-    out.append(("octahedron_vs_box", octahedron_vs_box(), base, 8))
+        out.append((name, W.mixed_bucket(name.split("_", 1)[1]), base, MANIFOLD_ENVS))
+    out.append(("opc_vs_box", opc_vs_box(), base, MANIFOLD_ENVS))
+    out.append(("subtraction_vs_box", subtraction_vs_box(), base, MANIFOLD_ENVS))
+    out.append(("octahedron_vs_box", octahedron_vs_box(), base, MANIFOLD_ENVS))
+    # the compile-time-exponent superquadric kinds beside eps 0.1 (common.h SdfKind)
+    for eps, tag in ((0.2, "02"), (0.25, "025"), (0.5, "05"), (1.0, "1")):
+        out.append((f"box_box_eps{tag}", W.box_box_eps(eps), base, MANIFOLD_ENVS))
+    cyl = W.box_box()
+    for b in cyl.bodies:
+        b.sdf = Superquadric(0.1, 1.0, (0.5, 0.5, 0.5))
+    out.append(("cyl_cyl", cyl, base, MANIFOLD_ENVS))
     return out
 
 

@@ -139,8 +139,12 @@ def main():
         p1, p2 = ws.poses(n)
         for e in range(cases.JVP_ENVS):
             j = Ref.manifold_jvp(rs[0], rs[1], p1[min(e, len(p1) - 1)], p2[min(e, len(p2) - 1)], c)
-            jv[f"{name}_{e}_contacts"] = j["contacts"]
-            jv[f"{name}_{e}_tangents"] = j["tangents"].astype(np.float32)  # the ABI emits FP32
+            if e < cases.JVP_FULL:
+                jv[f"{name}_{e}_contacts"] = j["contacts"]
+                jv[f"{name}_{e}_tangents"] = j["tangents"].astype(np.float32)  # the ABI emits FP32
+            else:  # every JVP_STRIDE-th contact (keeps the fixture small)
+                jv[f"{name}_{e}_contacts_sub"] = j["contacts"][::cases.JVP_STRIDE]
+                jv[f"{name}_{e}_tangents_sub"] = j["tangents"][::cases.JVP_STRIDE].astype(np.float32)
             jv[f"{name}_{e}_mean"] = np.array([j["mean_dist"], *j["mean_dist_grad"]])
     # config D scene: pose Jacobians of every pair, env 0 (forward + 12-tangent JVP per pair)
     for q, (i, j) in enumerate(pairs):

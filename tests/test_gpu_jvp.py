@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 import torch
 
-from cases import JVP_ENVS, manifold_cases
+from cases import JVP_ENVS, JVP_FULL, JVP_STRIDE, manifold_cases
 from helpers import QUANTITIES, assert_parity
 from paper_2602_20304_b200 import api, abi
 from paper_2602_20304_b200 import workloads as W
@@ -54,8 +54,12 @@ def test_jvp_matches_reference(case, cuda):
     p1, p2 = ws.poses(n)
     r = run_jvp(ws, cfg, p1, p2, want_src=True)
     for e in range(JVP_ENVS):
-        assert_parity(r["contacts"][e], g[f"{name}_{e}_contacts"], what=f"{name} env {e} primal")
-        rep = jac_report(r["tangents"][e], g[f"{name}_{e}_tangents"])
+        if e < JVP_FULL:
+            assert_parity(r["contacts"][e], g[f"{name}_{e}_contacts"], what=f"{name} env {e} primal")
+            rep = jac_report(r["tangents"][e], g[f"{name}_{e}_tangents"])
+        else:  # every JVP_STRIDE-th contact recorded
+            assert_parity(r["contacts"][e][::JVP_STRIDE], g[f"{name}_{e}_contacts_sub"], what=f"{name} env {e} primal")
+            rep = jac_report(r["tangents"][e][::JVP_STRIDE], g[f"{name}_{e}_tangents_sub"])
         print(f"{name} env {e}: jacobian ratio {rep}")
         assert max(rep.values()) <= 1.0, f"{name} env {e}: jacobian outside tolerance {rep}"
         ref_mean = g[f"{name}_{e}_mean"]

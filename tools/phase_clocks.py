@@ -33,9 +33,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "box-box":
     lib.cmgb_debug_manifold_phase_clocks(out)
     d = np.array(out[:], dtype=np.float64) - base
     names = {0: "A frames", 1: "B vertex scores", 2: "B edge scores", 3: "C rank sort", 4: "D slots",
-             5: "E pairs (+ V-S)", 6: "F NN (+ V-S)"}
+             5: "E pairs (+ V-S)", 6: "F NN (+ V-S)", 7: "G activity + stores", 8: "H mean"}
     ncta = n // 2
-    tot = d[:7].sum()
+    tot = d[:9].sum()
     for k, nm in names.items():
         print(f"{nm:20s} {100 * d[k] / tot:6.2f} %  {d[k] / ncta:9.0f} clk per CTA")
     print(f"total {tot / ncta:.0f} clk per CTA ({ncta} CTAs)")

@@ -37,3 +37,27 @@ for var in ["ours", "ours_ns"]:
     ms = time_fn(lambda: api.run_vf_batch(pairs, cfg))
     nb = pairs.shape[0] * (96 + 12)
     print(f"vf_witness {var}: {ms:.3f} ms -> {pairs.shape[0]/ms*1e3/1e9:.2f} G pairs/s, {nb/ms/1e6:.0f} GB/s")
+for kind in W.MIXED_KINDS:
+    ws = W.mixed_bucket(kind, n)
+    a1 = api.surface_from_spec(ws.bodies[0]); a2 = api.surface_from_spec(ws.bodies[1])
+    q1, q2 = ws.poses(n)
+    Q1 = torch.as_tensor(q1, device="cuda"); Q2 = torch.as_tensor(q2, device="cuda")
+    out = {}
+    ms = time_fn(lambda: api.generate_manifold_batch(a1, a2, Q1, Q2, SmoothingConfig(), out=out))
+    print(f"mixed {kind} n={n}: {ms:.3f} ms -> {n/ms*1e3/1e6:.2f} M manifolds/s")
+for eps in (0.2, 0.5):
+    ws = W.box_box_eps(eps, n)
+    a1 = api.surface_from_spec(ws.bodies[0]); a2 = api.surface_from_spec(ws.bodies[1])
+    q1, q2 = ws.poses(n)
+    Q1 = torch.as_tensor(q1, device="cuda"); Q2 = torch.as_tensor(q2, device="cuda")
+    out = {}
+    ms = time_fn(lambda: api.generate_manifold_batch(a1, a2, Q1, Q2, SmoothingConfig(), out=out))
+    print(f"box-box eps {eps} n={n}: {ms:.3f} ms -> {n/ms*1e3/1e6:.2f} M manifolds/s")
+sc = W.drop_scene(32768)
+bodies = [api.surface_from_spec(b) for b in sc.bodies]
+P = torch.as_tensor(sc.poses(32768), device="cuda")
+for fn_name in ("generate_manifold_scene_batch", "generate_manifold_scene_jvp_batch"):
+    fn = getattr(api, fn_name)
+    outs = [dict() for _ in range(10)]
+    ms = time_fn(lambda: fn(bodies, P, SmoothingConfig(), is_static=sc.is_static(), outs=outs), reps=5)
+    print(f"drop {fn_name}: {ms:.3f} ms -> {327680/ms*1e3/1e6:.2f} M pair-manifolds/s")
