@@ -55,6 +55,7 @@ enum Flavor : int32_t { kValue = 0, kGrad = 1, kNormalSource = 2, kNormalOnly = 
 // (then powers are repeated products: no SFU work).
 struct DevSq {
   double inv_ax[3];
+  double ax[3];          // axes (the normalised-coordinate sphere trace maps back with them)
   double p1, p2, p3;     // 1/e2, e2/e1, 1/e1 (general-exponent path)
   double c_xy, c_z;      // 2 p1 p2, 2 p3 (grad f prefactors)
   double R[9], t[3];     // body_from_prim (sdf.cpp:9)

@@ -218,6 +218,7 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
     if (d.op == CMGB_SDF_SUPERQUADRIC) {
       DevSq& q = o.sq;
       for (int k = 0; k < 3; ++k) q.inv_ax[k] = 1.0 / d.axes[k];
+      for (int k = 0; k < 3; ++k) q.ax[k] = d.axes[k];
       const double p1 = 1.0 / d.eps2, p2 = d.eps2 / d.eps1, p3 = 1.0 / d.eps1, p4 = -d.eps1 / 2.0;
       q.p1 = p1;
       q.p2 = p2;
