@@ -8,7 +8,10 @@ FP32"): for every contact,
     |act_gpu - act_ref|       <= 1e-6 + 1e-5 |act_ref|
 Vectors are compared as vectors: "relative" is relative to the vector's
 magnitude (a per-component relative bound on a near-zero component of a unit
-normal is not a property of the normal).
+normal is not a property of the normal). The stricter per-component reading
+(|g_i - r_i| <= 1e-6 + 1e-5 |r_i| for every one of the 8 fields) is reported
+beside it (parity_report(...)["per_component"]) and asserted by
+assert_parity (per_component=True, the default).
 """
 from __future__ import annotations
 
@@ -36,6 +39,11 @@ def parity_report(got: np.ndarray, ref: np.ndarray, rtol=RTOL, atol=ATOL):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     rep = {}
+    err_c = np.abs(got - ref)
+    bound_c = atol + rtol * np.abs(ref)
+    bad_c = ~(err_c <= bound_c)
+    rep["per_component"] = dict(fails=int(bad_c.any(axis=-1).sum()), n=int(np.prod(bad_c.shape[:-1])),
+                                max_ratio=float((err_c / bound_c).max()) if err_c.size else 0.0)
     bad_any = np.zeros(got.shape[:-1], dtype=bool)
     for name, sl in QUANTITIES.items():
         err = np.linalg.norm(got[..., sl] - ref[..., sl], axis=-1)
@@ -47,13 +55,17 @@ def parity_report(got: np.ndarray, ref: np.ndarray, rtol=RTOL, atol=ATOL):
     return rep, bad_any
 
 
-def assert_parity(got, ref, what="", rtol=RTOL, atol=ATOL, allow=0):
+def assert_parity(got, ref, what="", rtol=RTOL, atol=ATOL, allow=0, per_component=True):
     rep, bad = parity_report(got, ref, rtol, atol)
+    if per_component:  # every field within 1e-6 + 1e-5 |ref| on its own
+        g = np.asarray(got, dtype=np.float64)
+        r = np.asarray(ref, dtype=np.float64)
+        bad = bad | (np.abs(g - r) > atol + rtol * np.abs(r)).any(axis=-1)
     nfail = int(bad.sum())
     if nfail > allow:
         lines = [f"{what}: {nfail} contacts outside {atol:g} + {rtol:g}|ref| (allowed {allow})"]
         for f, r in rep.items():
-            if r["fails"]:
+            if r["fails"] and f != "per_component" or (f == "per_component" and per_component and r["fails"]):
                 lines.append(f"  {f}: {r['fails']}/{r['n']} max_err={r['max_err']:.3g} max_ratio={r['max_ratio']:.3g}")
         for i in np.argwhere(bad)[:6]:
             t = tuple(int(x) for x in i)
@@ -66,3 +78,40 @@ def scalar_close(got, ref, rtol=RTOL, atol=ATOL):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     return np.abs(got - ref) <= atol + rtol * np.abs(ref)
+
+
+def assert_parity_conditioned(got, ref, reeval, what="", eps=1e-11, draws=4, max_excused_frac=1e-5):
+    """assert_parity over [n_env, C, 8] batches (per-component reading), except
+    for contacts at which the REFERENCE ITSELF is ill-conditioned: re-evaluated
+    under a pose perturbation of eps (reeval(env, delta6) -> [C, 8]), the
+    reference's own value moves by more than the tolerance. (The fixed
+    5-iteration sphere trace on a superquadric is not convergent: an iterate
+    landing near the normalised radius 2, where grad phi vanishes, amplifies
+    input differences ~1e11-fold -- sdf.hpp:318-326, SURVEY App. A. Any FP64
+    implementation with a different rounding sequence then differs.)
+    At most max_excused_frac of the contacts may be excused."""
+    g = np.asarray(got, dtype=np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    rep, bad = parity_report(g, r)
+    bad = bad | (np.abs(g - r) > ATOL + RTOL * np.abs(r)).any(axis=-1)
+    if not bad.any():
+        return 0
+    idx = np.argwhere(bad)
+    assert len(idx) <= max(1, int(max_excused_frac * bad.size)), \
+        f"{what}: {len(idx)} contacts outside tolerance ({rep})"
+    rng = np.random.default_rng(12345)
+    excused = 0
+    for e in np.unique(idx[:, 0]):
+        dev = np.zeros(r.shape[1])
+        for _ in range(draws):
+            d = rng.normal(size=6)
+            alt = np.asarray(reeval(int(e), eps * d / np.linalg.norm(d)), dtype=np.float64)
+            ratio = np.abs(alt - r[e]) / (ATOL + RTOL * np.abs(r[e]))
+            dev = np.maximum(dev, ratio.max(axis=-1))
+        for c in idx[idx[:, 0] == e][:, 1]:
+            assert dev[c] > 1.0, (f"{what}: env {e} contact {c} outside tolerance and the reference is "
+                                  f"well-conditioned there (perturbation ratio {dev[c]:.3g}): got {g[e, c]}, "
+                                  f"ref {r[e, c]}")
+            excused += 1
+    print(f"{what}: {excused} contact(s) excused as ill-conditioned in the reference itself")
+    return excused

@@ -26,5 +26,7 @@ for name, ws, cfg, _ in manifold_cases():
     torch.cuda.synchronize()
     rep, bad = parity_report(r["contacts"].cpu().numpy(), ref["contacts"])
     src_bad = int((r["src"].cpu().numpy() != ref["meta"][..., 2:]).any(axis=-1).sum())
-    worst = max(v["max_ratio"] for v in rep.values())
-    print(f"{'jvp ' if jvp else ''}{name:26s} n={n} failing contacts {int(bad.sum()):5d} / {bad.size}  worst ratio {worst:.3g}  src mismatches {src_bad}")
+    worst = max(v["max_ratio"] for k, v in rep.items() if k != "per_component")
+    pc = rep["per_component"]
+    print(f"{'jvp ' if jvp else ''}{name:26s} n={n} failing contacts {int(bad.sum()):5d} / {bad.size}  worst ratio {worst:.3g}"
+          f"  per-component: failing {pc['fails']} worst ratio {pc['max_ratio']:.3g}  src mismatches {src_bad}")
