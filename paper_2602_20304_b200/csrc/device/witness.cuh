@@ -31,7 +31,15 @@ template <class I>
 __device__ __forceinline__ I partner_exp(const I& x, const I& a, double C, double inv_C,
                                          double inv_tau, int pair) {
   if (!pair) return exp_d(-fabs(x - I(1.0)) * I(inv_tau));
-  return pv(x) < 0.0 ? a * I(C) : (pv(x) <= 1.0 ? I(C) * rcp_d(a) : a * I(inv_C));
+  if constexpr (std::is_same_v<I, float>) {
+    // branch-free (the lanes of a warp hold unrelated pairs): one reciprocal
+    // always, then selects
+    const float r = rcp_d(a);
+    const float lo = a * (float)C, mid = (float)C * r, hi = a * (float)inv_C;
+    return pv(x) < 0.0f ? lo : (pv(x) <= 1.0f ? mid : hi);
+  } else {
+    return pv(x) < 0.0 ? a * I(C) : (pv(x) <= 1.0 ? I(C) * rcp_d(a) : a * I(inv_C));
+  }
 }
 
 template <class I, class T>

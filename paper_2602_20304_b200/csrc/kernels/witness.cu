@@ -81,17 +81,20 @@ struct VfSolve {
   }
 };
 
-// Persistent grid-stride over tiles of kWitnessThreads pairs. The input tile
-// (96 B / pair FP64, 48 B FP32) arrives by one TMA bulk copy per tile into a
-// double buffer: tile t+1 streams in while the CTA solves tile t. Outputs are
-// staged in shared memory so the global stores are full lines.
+// Persistent grid-stride over tiles of kWitnessThreads pairs. The input tiles
+// (96 B / pair FP64, 48 B FP32) arrive by TMA bulk copies into a kStages-deep
+// ring: kStages - 1 tiles stream in while the CTA solves the current one.
+// Outputs are staged in shared memory so the global stores are full lines.
+constexpr int kStages = 2;  // measured: deeper rings cost resident CTAs (4 stages: 16 warps/SM, -40%)
+
 template <typename T, class Solve>
 __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_constant__ WitnessParams p) {
   constexpr int W = Solve::kOut;
   using Out = typename Solve::Out;
-  __shared__ __align__(128) T tile[2][kWitnessThreads * 12];
-  __shared__ __align__(16) Out otile[kWitnessThreads * W];
-  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(128) unsigned char dsm[];  // kStages input tiles, then the output tile
+  T(*tile)[kWitnessThreads * 12] = reinterpret_cast<T(*)[kWitnessThreads * 12]>(dsm);
+  Out* otile = reinterpret_cast<Out*>(dsm + sizeof(T) * kStages * kWitnessThreads * 12);
+  __shared__ __align__(8) uint64_t bar[kStages];
   const T* __restrict__ in = static_cast<const T*>(p.pairs);
   const int tid = threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kWitnessThreads;
@@ -103,22 +106,25 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
     bulk_g2s(tile[b], in + f * 12, bytes, &bar[b]);
   };
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int b = 0; b < kStages; ++b) mbar_init(&bar[b], 1);
     mbar_fence_init();
-    if (first < p.n) issue(first, 0);
+#pragma unroll
+    for (int k = 0; k < kStages - 1; ++k)
+      if (first + k * stride < p.n) issue(first + k * stride, k);
   }
   __syncthreads();
   for (int it = 0; first < p.n; first += stride, ++it) {
-    const int b = it & 1;
-    // prefetch the next tile into the other buffer (its readers finished at
-    // the previous iteration's first barrier)
-    if (tid == 0 && first + stride < p.n) {
+    const int b = it % kStages;
+    // refill the buffer consumed by the previous iteration (its readers
+    // finished at that iteration's first barrier)
+    const int64_t ahead = first + (int64_t)(kStages - 1) * stride;
+    if (tid == 0 && ahead < p.n) {
       fence_proxy_async_smem();
-      issue(first + stride, b ^ 1);
+      issue(ahead, (it + kStages - 1) % kStages);
     }
     const int count = (int)(p.n - first < kWitnessThreads ? p.n - first : kWitnessThreads);
-    mbar_wait(&bar[b], (it >> 1) & 1);
+    mbar_wait(&bar[b], (it / kStages) & 1);
     if (tid < count) Solve::run(p, tile[b] + 12 * tid, first + tid, otile + W * tid);
     __syncthreads();
     Out* __restrict__ out = static_cast<Out*>(p.out_any) + first * W;
@@ -129,18 +135,21 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
 
 template <typename T, class Solve>
 int launch_witness(const WitnessParams& p, cudaStream_t s) {
+  constexpr size_t smem = sizeof(T) * kStages * kWitnessThreads * 12 +
+                          sizeof(typename Solve::Out) * kWitnessThreads * Solve::kOut;
   static PerDeviceInt cap_cache;  // persistent grid: SMs x resident CTAs, per device
   const int cap = cap_cache.get([] {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
+    cudaFuncSetAttribute(witness_kernel<T, Solve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, witness_kernel<T, Solve>, kWitnessThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, witness_kernel<T, Solve>, kWitnessThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 1);
   });
   const int64_t need = (p.n + kWitnessThreads - 1) / kWitnessThreads;
   const int grid = (int)(need < cap ? (need > 0 ? need : 1) : cap);
   note_launch();
-  witness_kernel<T, Solve><<<grid, kWitnessThreads, 0, s>>>(p);
+  witness_kernel<T, Solve><<<grid, kWitnessThreads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
