@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CMGB_ABI_VERSION 1
+#define CMGB_ABI_VERSION 2  /* 2: cmgb_manifold_out gained the activity-mask fields */
 
 typedef enum cmgb_status {
   CMGB_OK = 0,
@@ -184,6 +184,12 @@ typedef struct cmgb_manifold_out {
   void* workspace;   /* optional device scratch of cmgb_manifold_workspace_bytes(); when null
                         the call takes it from the stream-ordered pool (cudaMallocAsync)     */
   size_t workspace_bytes;
+  uint32_t* active_mask;   /* optional: [n_env][ceil(n_contacts / 32)] bit c of an env's row =
+                              (activity of contact c > active_threshold), produced by the
+                              kernels beside the fixed layout (input of cmgb_compact_masked)   */
+  int32_t* active_count;   /* optional (with active_mask): [n_env] set bits per env               */
+  float active_threshold;
+  int32_t reserved;
 } cmgb_manifold_out;
 
 /* Device scratch one cmgb_manifold_batch call needs (per-env pose frames). */
@@ -241,6 +247,15 @@ typedef struct cmgb_compact_out {
 } cmgb_compact_out;
 
 size_t cmgb_compact_workspace_bytes(int64_t n_env, int32_t n_contacts);
+
+/* Compaction from the activity masks / counts a cmgb_manifold_batch call
+ * produced (cmgb_manifold_out.active_mask / active_count): a scan of the
+ * counts, then only the kept contacts are read. Same outputs as
+ * cmgb_compact_contacts with activity_threshold = the batch's active_threshold. */
+size_t cmgb_compact_masked_workspace_bytes(int64_t n_env);
+int cmgb_compact_masked(const float* contacts, const int32_t* src, int64_t n_env, int32_t n_contacts,
+                        const uint32_t* active_mask, const int32_t* active_count, const cmgb_compact_out* out,
+                        void* cuda_stream);
 
 /* contacts: DEVICE [n_env][n_contacts][8] (a cmgb_manifold_batch output, 16-byte
  * aligned); src: optional DEVICE [n_env][n_contacts][2]. Stream-ordered. */

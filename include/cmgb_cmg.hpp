@@ -817,7 +817,7 @@ std::vector<ContactManifold<T>> manifolds_f(const SurfaceModel& s1, const Surfac
   const bool ee = want_ee && P > 0 && cfg.mode == ContactMode::kFull;
   std::vector<float> contacts((size_t)n * C * 8), eem(ee ? (size_t)n * 9 * P : 0);
   std::vector<int32_t> src((size_t)n * C * 2);
-  cmgb_manifold_out o{contacts.data(), src.data(), ee ? eem.data() : nullptr, nullptr, nullptr, 0};
+  cmgb_manifold_out o{contacts.data(), src.data(), ee ? eem.data() : nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0f, 0};
   ok(cmgb_manifold_batch_host_ex(s1.handle(), s2.handle(), p1, st1, p2, st2, n, &c, &o, nullptr));
   std::vector<ContactManifold<T>> out;
   out.reserve((size_t)n);

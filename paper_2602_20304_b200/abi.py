@@ -93,6 +93,10 @@ class CmgbManifoldOut(C.Structure):
         ("mean_dist", C.c_void_p),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
+        ("active_mask", C.c_void_p),
+        ("active_count", C.c_void_p),
+        ("active_threshold", C.c_float),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -231,6 +235,8 @@ SIGNATURES = {
     "cmgb_ee_witness_batch_host": (_I, [_P, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P]),
     "cmgb_vf_witness_batch_host": (_I, [_P, C.c_int64, C.POINTER(CmgbConfig), _P, _P, _P]),
     "cmgb_compact_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
+    "cmgb_compact_masked_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "cmgb_compact_masked": (_I, [_P, _P, C.c_int64, C.c_int32, _P, _P, C.POINTER(CmgbCompactOut), _P]),
     "cmgb_compact_contacts": (
         _I,
         [_P, _P, C.c_int64, C.c_int32, C.c_float, C.POINTER(CmgbCompactOut), _P],

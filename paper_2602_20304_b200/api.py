@@ -200,11 +200,15 @@ def _stream_ptr(stream) -> Optional[int]:
 
 def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, *,
                             want_src: bool = False, want_ee: bool = False,
-                            want_mean: bool = True, out: Optional[dict] = None, stream=None) -> dict:
+                            want_mean: bool = True, active_threshold: Optional[float] = None,
+                            out: Optional[dict] = None, stream=None) -> dict:
     """Batched generate_manifold over envs: poses* are CUDA float64 tensors
     [n, 6] (or [1, 6] / [6] for a pose shared by every env). Returns CUDA
     tensors: contacts [n, C, 8] (px,py,pz,dist,nx,ny,nz,activity), and
-    optionally src [n, C, 2], ee [n, 9, m1*m2], mean_dist [n]."""
+    optionally src [n, C, 2], ee [n, 9, m1*m2], mean_dist [n]; with
+    active_threshold, the kernels also emit the compaction extra's inputs:
+    active_mask [n, ceil(C / 32)] (int32 words, bit c = activity > threshold)
+    and active_count [n] (see compact_contacts(..., mask=, count=))."""
     import torch
 
     c = _cfg(cfg)
@@ -220,6 +224,10 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
     src = _reuse(res, "src", (n, Cn, 2), torch.int32, dev) if want_src else None
     ee = _reuse(res, "ee", (n, 9, P), torch.float32, dev) if (want_ee and P > 0) else None
     mean = _reuse(res, "mean_dist", (n,), torch.float32, dev) if want_mean else None
+    amask = acount = None
+    if active_threshold is not None:
+        amask = _reuse(res, "active_mask", (n, (Cn + 31) // 32), torch.int32, dev)
+        acount = _reuse(res, "active_count", (n,), torch.int32, dev)
     ws = abi.load().cmgb_manifold_workspace_bytes(n, st1, st2)
     wsb = res.get("workspace")
     if not (isinstance(wsb, torch.Tensor) and wsb.device == dev and wsb.dtype == torch.uint8 and wsb.numel() >= ws):
@@ -231,13 +239,18 @@ def generate_manifold_batch(s1: Surface, s2: Surface, poses1, poses2, cfg=None, 
     o.mean_dist = mean.data_ptr() if mean is not None else None
     o.workspace = res["workspace"].data_ptr()
     o.workspace_bytes = res["workspace"].numel()
+    if amask is not None:
+        o.active_mask = amask.data_ptr()
+        o.active_count = acount.data_ptr()
+        o.active_threshold = float(active_threshold)
     with torch.cuda.device(dev):
         _ok(abi.load().cmgb_manifold_batch(s1._h, s2._h, p1.data_ptr(), st1, p2.data_ptr(), st2, n,
                                            C.byref(c), C.byref(o), _stream_ptr(stream)))
     return res
 
 
-def compact_contacts(contacts, activity_threshold: float, *, src=None, capacity: Optional[int] = None,
+def compact_contacts(contacts, activity_threshold: Optional[float] = None, *, src=None,
+                     capacity: Optional[int] = None, mask=None, count=None,
                      out: Optional[dict] = None, stream=None) -> dict:
     """Active-contact compaction (an extra output; the fixed layout stays as
     it is): the contacts of a batch with activity > activity_threshold, in
@@ -246,7 +259,10 @@ def compact_contacts(contacts, activity_threshold: float, *, src=None, capacity:
     CUDA tensors: contacts [capacity, 8] (rows >= total unused), slot
     [capacity] (index in the env's fixed layout), src [capacity, 2] (when src is
     given), env_offset [n + 1] (int64; env_offset[n] = total), env_count [n],
-    total [1] (int64)."""
+    total [1] (int64). With mask / count (generate_manifold_batch's
+    active_mask / active_count) the fixed layout is not scanned again: only the
+    kept contacts are read (cmgb_compact_masked); activity_threshold is then
+    the one the batch used and is not needed."""
     import torch
 
     c = _cuda_tensor(contacts, (torch.float32,), "contacts")
@@ -267,7 +283,15 @@ def compact_contacts(contacts, activity_threshold: float, *, src=None, capacity:
     cnt = _reuse(res, "env_count", (n,), torch.int32, dev)
     tot = _reuse(res, "total", (1,), torch.int64, dev)
     lib = abi.load()
-    ws = lib.cmgb_compact_workspace_bytes(n, Cn)
+    masked = mask is not None
+    if masked:
+        _cuda_tensor(mask, (torch.int32,), "mask")
+        _cuda_tensor(count, (torch.int32,), "count")
+        if tuple(mask.shape) != (n, (Cn + 31) // 32) or tuple(count.shape) != (n,):
+            raise ValueError("mask must be [n_env, ceil(n_contacts / 32)] and count [n_env]")
+    elif activity_threshold is None:
+        raise ValueError("compact_contacts needs activity_threshold or mask / count")
+    ws = lib.cmgb_compact_masked_workspace_bytes(n) if masked else lib.cmgb_compact_workspace_bytes(n, Cn)
     wsb = res.get("workspace")
     if not (isinstance(wsb, torch.Tensor) and wsb.device == dev and wsb.numel() >= ws):
         res["workspace"] = torch.empty((max(ws, 16),), dtype=torch.uint8, device=dev)
@@ -282,8 +306,12 @@ def compact_contacts(contacts, activity_threshold: float, *, src=None, capacity:
     o.workspace = res["workspace"].data_ptr()
     o.workspace_bytes = res["workspace"].numel()
     with torch.cuda.device(dev):
-        _ok(lib.cmgb_compact_contacts(c.data_ptr(), src.data_ptr() if src is not None else None, n, Cn,
-                                      float(activity_threshold), C.byref(o), _stream_ptr(stream)))
+        if masked:
+            _ok(lib.cmgb_compact_masked(c.data_ptr(), src.data_ptr() if src is not None else None, n, Cn,
+                                        mask.data_ptr(), count.data_ptr(), C.byref(o), _stream_ptr(stream)))
+        else:
+            _ok(lib.cmgb_compact_contacts(c.data_ptr(), src.data_ptr() if src is not None else None, n, Cn,
+                                          float(activity_threshold), C.byref(o), _stream_ptr(stream)))
     return res
 
 

@@ -125,6 +125,7 @@ struct SmemLayout {
   int32_t vsdist;    // (n1+n2) floats
   int32_t nnstat;    // (m1+m2) x 2 floats: min, 1/sum
   int32_t hpart;     // (warps per CTA) doubles: per-warp partial sums of the E-E distances (G)
+  int32_t amask;     // mask_words uint32: activity > threshold bit per contact (compaction extra)
   int32_t bytes;     // per env, 16-byte aligned
 };
 
@@ -156,6 +157,10 @@ struct ManifoldParams {
   int32_t vs_ext;       // 1: V-S contacts (and their share of mean_dist) come from vs_kernel, launched first
   double* pairs_gmem;   // pair records in global memory ([n_env][pair_stride] doubles), or null = shared
   int64_t pair_stride;  // doubles per env in pairs_gmem
+  uint32_t* act_mask;   // optional [n_env][mask_words]: bit c = (activity of contact c > act_thr)
+  int32_t* act_count;   // optional [n_env]: set bits
+  float act_thr;
+  int32_t mask_words;   // ceil(n_contacts / 32)
 };
 
 // Pose-Jacobian (forward-mode, Dual12) batch: the geometry / config / slot

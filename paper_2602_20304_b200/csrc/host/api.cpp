@@ -20,6 +20,11 @@ size_t compact_workspace_bytes(int64_t n_env, int C);
 int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int C, float thr, int64_t capacity,
                    float* out_contacts, int32_t* out_slot, int32_t* out_src, int64_t* env_offset,
                    int32_t* env_count, int64_t* total, void* workspace, cudaStream_t s);
+size_t compact_masked_workspace_bytes(int64_t n_env);
+int launch_compact_masked(const float* contacts, const int32_t* src, int64_t n_env, int C, const uint32_t* mask,
+                          const int32_t* count, int64_t capacity, float* out_contacts, int32_t* out_slot,
+                          int32_t* out_src, int64_t* env_offset, int32_t* env_count, int64_t* total,
+                          void* workspace, cudaStream_t s);
 }
 
 using namespace cmgb;
@@ -209,6 +214,12 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   p.src = out->src;
   p.ee = (L.m1 > 0 && L.m2 > 0) ? out->ee : nullptr;
   p.mean_dist = out->mean_dist;
+  p.act_mask = out->active_mask;
+  p.act_count = out->active_count;
+  p.act_thr = out->active_threshold;
+  p.mask_words = (L.n_contacts + 31) / 32;
+  if (p.act_mask && !p.act_count) invalid("manifold: active_mask needs active_count");
+  if (p.act_mask && !(out->active_threshold == out->active_threshold)) invalid("manifold: active_threshold is NaN");
 
   // Shared-memory carve-up per env.
   const int P = L.m1 * L.m2;
@@ -231,6 +242,7 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     S.vsdist = off; off = align16(off + nslot_v * 4);
     S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
     S.hpart = off; off = align16(off + 10 * 8);  // one partial per warp (<= 320-thread CTAs)
+    S.amask = off; off = align16(off + (out->active_mask ? 4 * ((L.n_contacts + 31) / 32) : 0));
     S.bytes = off;
   };
   const size_t kSmemMax = 200 * 1024;
@@ -337,6 +349,10 @@ void launch_with_workspace(LaunchPlan& plan, int64_t n_env, int st1, int st2, vo
       if (q.src) q.src += c0 * C * 2;
       if (q.ee) q.ee += c0 * 9 * P;
       if (q.mean_dist) q.mean_dist += c0;
+      if (q.act_mask) {
+        q.act_mask += c0 * q.mask_words;
+        q.act_count += c0;
+      }
       q.pairs_gmem = rec;
       const int grid = (int)((cn + q.envs_per_block - 1) / q.envs_per_block);
       rc = launch_manifold(q, plan.threads, grid, plan.smem, stream);
@@ -736,7 +752,7 @@ int cmgb_manifold_batch_host_ex(cmgb_surface s1, cmgb_surface s2, const double* 
       cmgb_manifold_out out{sc.contacts + e0 * C * 8, src_host ? sc.src + e0 * C * 2 : nullptr,
                             ee_host ? sc.ee + e0 * 9 * P : nullptr, sc.mean + e0,
                             sc.frames + (c & 1) * workspace_doubles(per, st1, st2),
-                            workspace_doubles(per, st1, st2) * sizeof(double)};
+                            workspace_doubles(per, st1, st2) * sizeof(double), nullptr, nullptr, 0.0f, 0};
       LaunchPlan plan = plan_manifold(s1, s2, p1, st1, p2, st2, ne, cfg, &out);
       launch_with_workspace(plan, ne, st1, st2, out.workspace, out.workspace_bytes, q);
       if (mean_dist_host)
@@ -767,7 +783,7 @@ int cmgb_manifold_batch_host(cmgb_surface s1, cmgb_surface s2, const double* pos
                              int32_t st1, const double* poses2_host, int32_t st2, int64_t n_env,
                              const cmgb_config* cfg, float* mean_dist_host, float* contacts_host,
                              void* stream) {
-  const cmgb_manifold_out o{contacts_host, nullptr, nullptr, mean_dist_host, nullptr, 0};
+  const cmgb_manifold_out o{contacts_host, nullptr, nullptr, mean_dist_host, nullptr, 0, nullptr, nullptr, 0.0f, 0};
   return cmgb_manifold_batch_host_ex(s1, s2, poses1_host, st1, poses2_host, st2, n_env, cfg, &o, stream);
 }
 
@@ -802,6 +818,40 @@ int cmgb_compact_contacts(const float* contacts, const int32_t* src, int64_t n_e
     if (pooled) cuda_check(cudaMallocAsync(&ws, need, s), "cudaMallocAsync(compact workspace)");
     const int rc = launch_compact(contacts, src, n_env, n_contacts, thr, out->capacity, out->contacts, out->slot,
                                   out->src, out->env_offset, out->env_count, out->total, ws, s);
+    if (pooled) cudaFreeAsync(ws, s);
+    if (rc != 0)
+      throw Error(CMGB_ERR_CUDA, std::string("compact launch: ") + cudaGetErrorString(cudaGetLastError()));
+  });
+}
+
+size_t cmgb_compact_masked_workspace_bytes(int64_t n_env) {
+  return n_env > 0 ? compact_masked_workspace_bytes(n_env) : 0;
+}
+
+int cmgb_compact_masked(const float* contacts, const int32_t* src, int64_t n_env, int32_t n_contacts,
+                        const uint32_t* mask, const int32_t* count, const cmgb_compact_out* out, void* stream) {
+  return guarded([&] {
+    if (!out) invalid("compact: null output descriptor");
+    if (n_env < 0 || n_contacts < 0) invalid("compact: n_env >= 0 and n_contacts >= 0");
+    if (out->capacity < 0) invalid("compact: capacity >= 0");
+    if (out->src && !src) invalid("compact: src output needs the batch's src input");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n_env == 0 || n_contacts == 0) {
+      if (out->total) cuda_check(cudaMemsetAsync(out->total, 0, sizeof(int64_t), s), "cudaMemsetAsync");
+      if (out->env_offset)
+        cuda_check(cudaMemsetAsync(out->env_offset, 0, sizeof(int64_t) * (n_env + 1), s), "cudaMemsetAsync");
+      if (out->env_count) cuda_check(cudaMemsetAsync(out->env_count, 0, sizeof(int32_t) * n_env, s), "cudaMemsetAsync");
+      return;
+    }
+    if (!contacts || !mask || !count) invalid("compact: null contacts / mask / count");
+    if (!out->contacts && out->capacity > 0) invalid("compact: null output contacts");
+    if (reinterpret_cast<uintptr_t>(contacts) % 16 != 0) invalid("compact: contacts must be 16-byte aligned");
+    const size_t need = compact_masked_workspace_bytes(n_env);
+    void* ws = out->workspace;
+    const bool pooled = !ws || out->workspace_bytes < need;
+    if (pooled) cuda_check(cudaMallocAsync(&ws, need, s), "cudaMallocAsync(compact workspace)");
+    const int rc = launch_compact_masked(contacts, src, n_env, n_contacts, mask, count, out->capacity, out->contacts,
+                                         out->slot, out->src, out->env_offset, out->env_count, out->total, ws, s);
     if (pooled) cudaFreeAsync(ws, s);
     if (rc != 0)
       throw Error(CMGB_ERR_CUDA, std::string("compact launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -895,7 +945,7 @@ int cmgb_manifold_jvp_batch(cmgb_surface s1, cmgb_surface s2, const double* pose
                             const cmgb_manifold_jvp_out* out, void* stream) {
   return guarded([&] {
     validate_jvp(cfg, out);
-    cmgb_manifold_out mo{out->contacts, out->src, nullptr, out->mean_dist, nullptr, 0};
+    cmgb_manifold_out mo{out->contacts, out->src, nullptr, out->mean_dist, nullptr, 0, nullptr, nullptr, 0.0f, 0};
     LaunchPlan plan = plan_manifold(s1, s2, poses1, st1, poses2, st2, n_env, cfg, &mo);
     if (n_env == 0 || plan.p.n_contacts == 0) return;
     if (!out->contacts || !out->tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
@@ -961,7 +1011,7 @@ int cmgb_manifold_jvp_batch_host(cmgb_surface s1, cmgb_surface s2, const double*
     d.mean_dist_grad = host_out->mean_dist_grad ? static_cast<float*>(pb.get(sizeof(float) * (n * 12))) : nullptr;
     d.mean_dist_f64 = host_out->mean_dist_f64 ? static_cast<double*>(pb.get(sizeof(double) * (n))) : nullptr;
     d.mean_dist_grad_f64 = host_out->mean_dist_grad_f64 ? static_cast<double*>(pb.get(sizeof(double) * (n * 12))) : nullptr;
-    cmgb_manifold_out mo{d.contacts, d.src, nullptr, d.mean_dist, nullptr, 0};
+    cmgb_manifold_out mo{d.contacts, d.src, nullptr, d.mean_dist, nullptr, 0, nullptr, nullptr, 0.0f, 0};
     LaunchPlan plan = plan_manifold(s1, s2, p1, st1, p2, st2, n_env, cfg, &mo);
     if (plan.p.n_contacts == 0) return;
     launch_jvp(plan_jvp(plan, &d), s);
@@ -1038,7 +1088,7 @@ int cmgb_manifold_scene_jvp_batch(const cmgb_surface* bodies, int32_t n_bodies, 
         invalid("manifold_scene_jvp_batch: pair index out of range");
       const cmgb_manifold_jvp_out& o = outs[q];
       validate_jvp(cfg, &o);
-      cmgb_manifold_out mo{o.contacts, o.src, nullptr, o.mean_dist, nullptr, 0};
+      cmgb_manifold_out mo{o.contacts, o.src, nullptr, o.mean_dist, nullptr, 0, nullptr, nullptr, 0.0f, 0};
       LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &mo);
       if (n_env == 0 || plan.p.n_contacts == 0) continue;
       if (!o.contacts || !o.tangents) invalid("manifold_jvp: contacts and tangents outputs are required");
@@ -1316,7 +1366,8 @@ int cmgb_demo_step_batch(const cmgb_demo_body* bodies, int32_t nb, const cmgb_co
       const auto [i, j] = d.pairs[q];
       float* contacts = reinterpret_cast<float*>(base + d.off_contacts[q]);
       double* frames = reinterpret_cast<double*>(base + d.off_frames[q]);
-      cmgb_manifold_out out{contacts, nullptr, nullptr, nullptr, frames, sizeof(double) * workspace_doubles(n_env, 1, 1)};
+      cmgb_manifold_out out{contacts, nullptr, nullptr, nullptr, frames, sizeof(double) * workspace_doubles(n_env, 1, 1),
+                            nullptr, nullptr, 0.0f, 0};
       LaunchPlan plan = plan_manifold(bodies[i].surface, bodies[j].surface, poses + 6 * i, 1, poses + 6 * j, 1,
                                       n_env, cfg, &out);
       if (plan.p.n_contacts == 0) {  // no contacts: zero wrench / deepest for this pair

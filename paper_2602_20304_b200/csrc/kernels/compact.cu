@@ -185,6 +185,129 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
   }
 }
 
+// ---- compaction from the manifold kernel's activity masks -------------------
+// The fixed layout is not scanned again: a tile of 256 envs per CTA scans the
+// per-env counts (warp shuffles + decoupled look-back over tiles, as above),
+// then each warp walks its 32 envs' mask words and copies only the kept
+// contacts (32 B each) to their compacted rows.
+constexpr int kMaskedTile = 256;
+
+struct MaskedParams {
+  const float* contacts;
+  const int32_t* src;
+  int64_t n_env;
+  int32_t C, mask_words;
+  const uint32_t* mask;
+  const int32_t* count;
+  int64_t capacity;
+  float* out_contacts;
+  int32_t* out_slot;
+  int32_t* out_src;
+  int64_t* env_offset;
+  int32_t* env_count;
+  int64_t* total;
+  uint64_t* status;
+  uint32_t* ticket;
+};
+
+__global__ void __launch_bounds__(kMaskedTile) compact_masked_kernel(const __grid_constant__ MaskedParams p) {
+  __shared__ uint32_t s_tile;
+  __shared__ int64_t s_wsum[kMaskedTile / 32];
+  __shared__ int64_t s_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t e = tile * kMaskedTile + tid;
+  const int64_t cnt = e < p.n_env ? p.count[e] : 0;
+  // block exclusive scan of the counts
+  int64_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int64_t wbase = 0, agg = 0;
+  for (int w = 0; w < kMaskedTile / 32; ++w) {
+    if (w < warp) wbase += s_wsum[w];
+    agg += s_wsum[w];
+  }
+  const int64_t excl_in_tile = wbase + incl - cnt;
+  if (warp == 0) {  // look-back
+    if (lane == 0) st_release(p.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (uint64_t)agg);
+    int64_t excl = 0;
+    if (tile > 0) {
+      int64_t base = tile - 1;
+      while (true) {
+        const int64_t idx = base - lane;
+        uint64_t st = idx >= 0 ? ld_acquire(p.status + idx) : kFlagIncl;
+        while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
+          if ((st >> 62) == 0) st = ld_acquire(p.status + idx);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        int64_t v = lane <= stop ? (int64_t)(st & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        base -= 32;
+      }
+      if (lane == 0) st_release(p.status + tile, kFlagIncl | (uint64_t)(excl + agg));
+    }
+    if (lane == 0) {
+      s_base = excl;
+      const int64_t ntiles = (p.n_env + kMaskedTile - 1) / kMaskedTile;
+      if (tile == ntiles - 1) {
+        if (p.total) *p.total = excl + agg;
+        if (p.env_offset) p.env_offset[p.n_env] = excl + agg;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t off = s_base + excl_in_tile;
+  if (e < p.n_env) {
+    if (p.env_offset) p.env_offset[e] = off;
+    if (p.env_count) p.env_count[e] = (int32_t)cnt;
+  }
+  // gather: warp w copies the kept contacts of its 32 envs, one env at a time
+  const float4* in = reinterpret_cast<const float4*>(p.contacts);
+  float4* oc = reinterpret_cast<float4*>(p.out_contacts);
+  for (int j = 0; j < 32; ++j) {
+    const int64_t ej = tile * kMaskedTile + warp * 32 + j;
+    const int64_t oj = __shfl_sync(0xffffffffu, off, j);
+    if (ej >= p.n_env) break;
+    int64_t run = oj;
+    for (int w0 = 0; w0 < p.mask_words; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t m = w < p.mask_words ? p.mask[ej * p.mask_words + w] : 0u;
+      int pc = __popc(m), pre = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      int64_t dst = run + pre - pc;  // this word's first kept row
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int cidx = 32 * w + b;
+        if (dst < p.capacity) {
+          const int64_t srow = ej * p.C + cidx;
+          oc[2 * dst] = in[2 * srow];
+          oc[2 * dst + 1] = in[2 * srow + 1];
+          if (p.out_slot) p.out_slot[dst] = cidx;
+          if (p.out_src) reinterpret_cast<int2*>(p.out_src)[dst] = reinterpret_cast<const int2*>(p.src)[srow];
+        }
+        ++dst;
+      }
+      run += __shfl_sync(0xffffffffu, pre, 31);
+    }
+  }
+}
+
 }  // namespace
 
 size_t compact_workspace_bytes(int64_t n_env, int C) {
@@ -242,6 +365,38 @@ int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int
     compact_kernel<true><<<(unsigned)tiles, 32 * p.epb, stage, s>>>(p);
   else
     compact_kernel<false><<<(unsigned)tiles, 32 * p.epb, 0, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+size_t compact_masked_workspace_bytes(int64_t n_env) {
+  return sizeof(uint64_t) * (size_t)((n_env + kMaskedTile - 1) / kMaskedTile + 2);
+}
+
+int launch_compact_masked(const float* contacts, const int32_t* src, int64_t n_env, int C, const uint32_t* mask,
+                          const int32_t* count, int64_t capacity, float* out_contacts, int32_t* out_slot,
+                          int32_t* out_src, int64_t* env_offset, int32_t* env_count, int64_t* total,
+                          void* workspace, cudaStream_t s) {
+  MaskedParams p{};
+  p.contacts = contacts;
+  p.src = src;
+  p.n_env = n_env;
+  p.C = C;
+  p.mask_words = (C + 31) / 32;
+  p.mask = mask;
+  p.count = count;
+  p.capacity = capacity;
+  p.out_contacts = out_contacts;
+  p.out_slot = out_slot;
+  p.out_src = out_src;
+  p.env_offset = env_offset;
+  p.env_count = env_count;
+  p.total = total;
+  p.ticket = static_cast<uint32_t*>(workspace);
+  p.status = static_cast<uint64_t*>(workspace) + 1;
+  if (cudaMemsetAsync(workspace, 0, compact_masked_workspace_bytes(n_env), s) != cudaSuccess) return 1;
+  const int64_t tiles = (n_env + kMaskedTile - 1) / kMaskedTile;
+  note_launch();
+  compact_masked_kernel<<<(unsigned)tiles, kMaskedTile, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -88,6 +88,7 @@ struct EnvView {
   __device__ float* vsdist() const { return reinterpret_cast<float*>(base + L->vsdist); }
   __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
   __device__ double* hpart() const { return reinterpret_cast<double*>(base + L->hpart); }
+  __device__ uint32_t* amask() const { return reinterpret_cast<uint32_t*>(base + L->amask); }
   __device__ double& dbar(int i) const { return pair(i)[3]; }
 };
 
@@ -137,15 +138,17 @@ __device__ __forceinline__ double3 normalize_smooth(double3 v, double tau) {
 
 // V-S contact for a selected vertex (world) against the opposing posed SDF
 // (vs_contacts, manifold.hpp:185-204).
+// Returns the stored (FP32) activity.
 template <int KO>
-__device__ __forceinline__ void vs_contact(const DevSdf& opp, const double* Ro, const double* to,
-                                           double3 pw, const DevCfg& c, float* out_dist,
-                                           float* dst) {
+__device__ __forceinline__ float vs_contact(const DevSdf& opp, const double* Ro, const double* to,
+                                            double3 pw, const DevCfg& c, float* out_dist,
+                                            float* dst) {
   const SdfOut s = sdf_eval<kNormalSource, KO>(opp, to_body(Ro, to, pw));
   const float3 n = to_f3v(mul_R(Ro, normalize_smooth(s.g, c.tau_normal)));
   const double act = sigmoid_d(-s.v * c.inv_tau_pen);  // sigma_greater(-phi, 0, tau_pen)
   *out_dist = (float)s.v;
   store_contact(dst, (float)pw.x, (float)pw.y, (float)pw.z, (float)s.v, n.x, n.y, n.z, (float)act);
+  return (float)act;
 }
 
 // sphere_trace_project (sdf.hpp:318-326) in the body frame, FP64.
@@ -348,6 +351,13 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
                              : p.frames2 + 12 * (env0 + e) * p.stride2;
     env(e).R(s)[k] = __ldg(f + k);
   }
+
+  // activity masks of the compaction extra: zero, or (kVsX) the V-S bits vs_kernel left in word 0
+  if (p.act_mask)
+    for (int i = tid; i < p.mask_words * n_here; i += nth) {
+      const int e = i / p.mask_words, w = i - e * p.mask_words;
+      env(e).amask()[w] = (kVsX && w == 0) ? p.act_mask[(env0 + e) * p.mask_words] : 0u;
+    }
 
   const bool topk_any = S1.topk_v | S2.topk_v | S1.topk_e | S2.topk_e;
   const int nsl = n1 + n2 + m1 + m2;
@@ -578,8 +588,9 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       const EnvView ev = env(e);
       const double* q = ev.vslot(r);
       float* dst = p.contacts + ((env0 + e) * C + r) * 8;
-      if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-      else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      const float act = r < n1 ? vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst)
+                               : vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+      if (p.act_mask && act > p.act_thr) atomicOr(ev.amask() + (r >> 5), 1u << (r & 31));
       if (p.src) {
         int* sp = p.src + ((env0 + e) * C + r) * 2;
         sp[0] = ev.prov()[r];
@@ -633,8 +644,9 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         const EnvView ev = env(e);
         const double* q = ev.vslot(r);
         float* dst = p.contacts + ((env0 + e) * C + r) * 8;
-        if (r < n1) vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
-        else vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+        const float act = r < n1 ? vs_contact<K2>(S2.sdf, ev.R(1), ev.t(1), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst)
+                                 : vs_contact<K1>(S1.sdf, ev.R(0), ev.t(0), d3(q[0], q[1], q[2]), c, ev.vsdist() + r, dst);
+        if (p.act_mask && act > p.act_thr) atomicOr(ev.amask() + (r >> 5), 1u << (r & 31));
         if (p.src) {
           int* sp = p.src + ((env0 + e) * C + r) * 2;
           sp[0] = ev.prov()[r];
@@ -680,6 +692,11 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
                       (float)(rec[12] * g1), (float)(rec[13] * g1), act1);
         store_contact(dst + 8, (float)rec[8], (float)rec[9], (float)rec[10], d2, (float)(rec[11] * g2),
                       (float)(rec[12] * g2), (float)(rec[13] * g2), act2);
+        if (p.act_mask) {
+          const int c0 = n1 + n2 + 2 * i;  // contact index of side 1; side 2 follows
+          if (act1 > p.act_thr) atomicOr(ev.amask() + (c0 >> 5), 1u << (c0 & 31));
+          if (act2 > p.act_thr) atomicOr(ev.amask() + ((c0 + 1) >> 5), 1u << ((c0 + 1) & 31));
+        }
         if (p.src) {
           int* sp = p.src + row * 2;
           const int sa = ev.prov()[n1 + n2 + k], sb = ev.prov()[n1 + n2 + m1 + l];
@@ -716,7 +733,23 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
   MF_PHASE_MARK(7);
 
   // ---- H: mean contact distance (manifold.hpp:379-384): one warp per env sums
-  // the V-S distances and the G partials, fixed order ------------------------
+  // the V-S distances and the G partials, fixed order; and the env's activity
+  // mask + count for the compaction extra ------------------------------------
+  if (p.act_mask) {
+    const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+    for (int e = warp; e < n_here; e += nwarps) {
+      const EnvView ev = env(e);
+      int cnt = 0;
+      for (int w = lane; w < p.mask_words; w += 32) {
+        const uint32_t m = ev.amask()[w];
+        p.act_mask[(env0 + e) * p.mask_words + w] = m;
+        cnt += __popc(m);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (lane == 0) p.act_count[env0 + e] = cnt;
+    }
+  }
   if (p.mean_dist) {
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
     for (int e = warp; e < n_here; e += nwarps) {
@@ -749,6 +782,7 @@ __global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ Manifol
   const int n1 = p.n1, nvs = p.n1 + p.n2, C = p.n_contacts;
   const bool act = e < p.n_env && r < nvs;
   double d = 0.0;
+  float act_v = 0.0f;
   if (act) {
     const int s = r < n1 ? 0 : 1;
     const int vi = s == 0 ? r : r - n1;
@@ -759,8 +793,8 @@ __global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ Manifol
     const double3 pw = to_world(fs, fs + 9, ld_vert(p.side[s].verts, vi));
     float dist;
     float* dst = p.contacts + (e * C + r) * 8;
-    if (s == 0) vs_contact<K2>(p.side[1].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
-    else vs_contact<K1>(p.side[0].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
+    if (s == 0) act_v = vs_contact<K2>(p.side[1].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
+    else act_v = vs_contact<K1>(p.side[0].sdf, fo, fo + 9, pw, p.cfg, &dist, dst);
     if (p.src) {
       int* sp = p.src + (e * C + r) * 2;
       sp[0] = vi;
@@ -770,6 +804,11 @@ __global__ void __launch_bounds__(256) vs_kernel(const __grid_constant__ Manifol
   }
   for (int o = G >> 1; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
   if (act && r == 0 && p.mean_dist) p.mean_dist[e] = (float)d;
+  if (p.act_mask) {  // the env's V-S bits (nvs <= 32: word 0), completed by the manifold kernel
+    const unsigned b = __ballot_sync(0xffffffffu, act && act_v > p.act_thr);
+    const int g0 = (threadIdx.x & 31) & ~(G - 1);
+    if (act && r == 0) p.act_mask[e * p.mask_words] = G == 32 ? b : (b >> g0) & ((1u << G) - 1u);
+  }
 }
 
 [[maybe_unused]] int launch_frames(const double* poses1, int64_t stride1, int64_t n1, double* frames1, const double* poses2,

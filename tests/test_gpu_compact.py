@@ -118,3 +118,57 @@ def test_compact_full_size_batch_independence(cuda):
     k = int(small["total"].item())
     assert np.array_equal(small["env_offset"].cpu().numpy(), res["env_offset"][:4097].cpu().numpy())
     assert torch.equal(small["contacts"][:k], res["contacts"][:k])
+
+
+def numpy_masks(contacts, thr):
+    c = np.asarray(contacts)
+    keep = c[..., 7] > thr
+    n, C = keep.shape
+    words = (C + 31) // 32
+    pad = np.zeros((n, words * 32), bool)
+    pad[:, :C] = keep
+    bits = pad.reshape(n, words, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)
+    return bits.sum(axis=2).astype(np.uint32).view(np.int32), keep.sum(axis=1).astype(np.int32)
+
+
+def masked_case(ws, n, cfg, thr):
+    s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
+    p1, p2 = ws.poses(n)
+    r = api.generate_manifold_batch(s1, s2, torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda"),
+                                    cfg, want_src=True, active_threshold=thr)
+    torch.cuda.synchronize()
+    c = r["contacts"].cpu().numpy()
+    m, k = numpy_masks(c, thr)
+    assert np.array_equal(r["active_mask"].cpu().numpy(), m), "activity masks differ from the fixed layout"
+    assert np.array_equal(r["active_count"].cpu().numpy(), k)
+    res = api.compact_contacts(r["contacts"], src=r["src"], mask=r["active_mask"], count=r["active_count"])
+    torch.cuda.synchronize()
+    check(res, c, thr, r["src"].cpu().numpy())
+
+
+@pytest.mark.parametrize("thr", [-1.0, 0.0, 0.01, 0.5, 2.0])
+def test_masks_box_box(cuda, thr):
+    """kVsX kernel pair (V-S bits from vs_kernel, E-E bits from the manifold kernel)."""
+    masked_case(W.box_box(1001), 1001, SmoothingConfig(), thr)
+
+
+@pytest.mark.parametrize("case", ["box_box_topk", "mixed_capsule", "mixed_rounded_box", "box_box_ours_ne",
+                                  "box_box_ours_ne_s", "box_on_plane_ours", "subtraction_vs_box"])
+def test_masks_every_kernel_shape(cuda, case):
+    """In-kernel V-S paths (phase E on the 10-warp shape, phase F on the
+    9-warp shape), no-EE / one-sided modes, generic interpreter."""
+    from cases import manifold_cases
+    _, ws, cfg, _ = [c for c in manifold_cases() if c[0] == case][0]
+    masked_case(ws, 777, cfg, 0.01)
+
+
+def test_masks_global_pair_records(cuda):
+    """The global-memory pair-record instantiation: two subdivided boxes with
+    all 48 edges pass-through (P = 2,304 pairs, tests/test_gpu_edges.py)."""
+    ws = W.box_box(64)
+    for b in ws.bodies:
+        b.mesh.subdivisions = 2
+    m = api.surface_from_spec(ws.bodies[0]).mesh.edges.shape[0]
+    for b in ws.bodies:
+        b.edge_topk = m
+    masked_case(ws, 16, SmoothingConfig(), 0.01)

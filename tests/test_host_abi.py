@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"libcmgb.so does not export {s}"
     assert set(syms) == set(abi.SIGNATURES), "ctypes mirror out of sync with include/cmgb.h"
-    assert lib.cmgb_abi_version() == 1
+    assert lib.cmgb_abi_version() == 2
 
 
 def test_library_is_native_cuda_for_sm100a():
