@@ -186,11 +186,13 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
 }
 
 // ---- compaction from the manifold kernel's activity masks -------------------
-// The fixed layout is not scanned again: a tile of 256 envs per CTA scans the
-// per-env counts (warp shuffles + decoupled look-back over tiles, as above),
-// then each warp walks its 32 envs' mask words and copies only the kept
-// contacts (32 B each) to their compacted rows.
-constexpr int kMaskedTile = 256;
+// The fixed layout is not scanned again. Two launches: (1) an exclusive scan
+// of the per-env counts, 1,024 envs per CTA (warp shuffles, decoupled
+// look-back over tiles as above; few tiles, so the look-back chain stays
+// short); (2) one warp per env walks the env's mask words (one lane per word)
+// and copies only the kept contacts (32 B each) to their compacted rows --
+// no dependency between envs, every warp of the grid in flight at once.
+constexpr int kScanTile = 1024;  // envs per scan CTA (one thread each)
 
 struct MaskedParams {
   const float* contacts;
@@ -203,24 +205,23 @@ struct MaskedParams {
   float* out_contacts;
   int32_t* out_slot;
   int32_t* out_src;
-  int64_t* env_offset;
+  int64_t* env_offset;  // required here: the gather reads it
   int32_t* env_count;
   int64_t* total;
   uint64_t* status;
   uint32_t* ticket;
 };
 
-__global__ void __launch_bounds__(kMaskedTile) compact_masked_kernel(const __grid_constant__ MaskedParams p) {
+__global__ void __launch_bounds__(kScanTile) compact_scan_kernel(const __grid_constant__ MaskedParams p) {
   __shared__ uint32_t s_tile;
-  __shared__ int64_t s_wsum[kMaskedTile / 32];
+  __shared__ int64_t s_wsum[kScanTile / 32];
   __shared__ int64_t s_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t e = tile * kMaskedTile + tid;
+  const int64_t e = tile * kScanTile + tid;
   const int64_t cnt = e < p.n_env ? p.count[e] : 0;
-  // block exclusive scan of the counts
   int64_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -229,13 +230,17 @@ __global__ void __launch_bounds__(kMaskedTile) compact_masked_kernel(const __gri
   }
   if (lane == 31) s_wsum[warp] = incl;
   __syncthreads();
-  int64_t wbase = 0, agg = 0;
-  for (int w = 0; w < kMaskedTile / 32; ++w) {
-    if (w < warp) wbase += s_wsum[w];
-    agg += s_wsum[w];
-  }
-  const int64_t excl_in_tile = wbase + incl - cnt;
-  if (warp == 0) {  // look-back
+  if (warp == 0) {
+    // scan of the 32 warp sums, then the look-back
+    const int64_t ws = s_wsum[lane];
+    int64_t wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    s_wsum[lane] = wi - ws;  // exclusive warp offsets
+    const int64_t agg = __shfl_sync(0xffffffffu, wi, 31);
     if (lane == 0) st_release(p.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (uint64_t)agg);
     int64_t excl = 0;
     if (tile > 0) {
@@ -259,52 +264,53 @@ __global__ void __launch_bounds__(kMaskedTile) compact_masked_kernel(const __gri
     }
     if (lane == 0) {
       s_base = excl;
-      const int64_t ntiles = (p.n_env + kMaskedTile - 1) / kMaskedTile;
+      const int64_t ntiles = (p.n_env + kScanTile - 1) / kScanTile;
       if (tile == ntiles - 1) {
         if (p.total) *p.total = excl + agg;
-        if (p.env_offset) p.env_offset[p.n_env] = excl + agg;
+        p.env_offset[p.n_env] = excl + agg;
       }
     }
   }
   __syncthreads();
-  const int64_t off = s_base + excl_in_tile;
   if (e < p.n_env) {
-    if (p.env_offset) p.env_offset[e] = off;
+    p.env_offset[e] = s_base + s_wsum[warp] + incl - cnt;
     if (p.env_count) p.env_count[e] = (int32_t)cnt;
   }
-  // gather: warp w copies the kept contacts of its 32 envs, one env at a time
+}
+
+__global__ void __launch_bounds__(256) compact_gather_kernel(const __grid_constant__ MaskedParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ej = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ej >= p.n_env) return;
+  const int mw = p.mask_words;
   const float4* in = reinterpret_cast<const float4*>(p.contacts);
   float4* oc = reinterpret_cast<float4*>(p.out_contacts);
-  for (int j = 0; j < 32; ++j) {
-    const int64_t ej = tile * kMaskedTile + warp * 32 + j;
-    const int64_t oj = __shfl_sync(0xffffffffu, off, j);
-    if (ej >= p.n_env) break;
-    int64_t run = oj;
-    for (int w0 = 0; w0 < p.mask_words; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t m = w < p.mask_words ? p.mask[ej * p.mask_words + w] : 0u;
-      int pc = __popc(m), pre = pc;
+  int64_t run = p.env_offset[ej];
+  for (int w0 = 0; w0 < mw; w0 += 32) {
+    const int w = w0 + lane;
+    uint32_t m = w < mw ? p.mask[ej * mw + w] : 0u;
+    const int pc = __popc(m);
+    int pre = pc;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += v;
-      }
-      int64_t dst = run + pre - pc;  // this word's first kept row
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        const int cidx = 32 * w + b;
-        if (dst < p.capacity) {
-          const int64_t srow = ej * p.C + cidx;
-          oc[2 * dst] = in[2 * srow];
-          oc[2 * dst + 1] = in[2 * srow + 1];
-          if (p.out_slot) p.out_slot[dst] = cidx;
-          if (p.out_src) reinterpret_cast<int2*>(p.out_src)[dst] = reinterpret_cast<const int2*>(p.src)[srow];
-        }
-        ++dst;
-      }
-      run += __shfl_sync(0xffffffffu, pre, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
     }
+    int64_t dst = run + pre - pc;  // this word's first kept row
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int cidx = 32 * w + b;
+      if (dst < p.capacity) {
+        const int64_t srow = ej * p.C + cidx;
+        oc[2 * dst] = in[2 * srow];
+        oc[2 * dst + 1] = in[2 * srow + 1];
+        if (p.out_slot) p.out_slot[dst] = cidx;
+        if (p.out_src) reinterpret_cast<int2*>(p.out_src)[dst] = reinterpret_cast<const int2*>(p.src)[srow];
+      }
+      ++dst;
+    }
+    run += __shfl_sync(0xffffffffu, pre, 31);
   }
 }
 
@@ -369,7 +375,8 @@ int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int
 }
 
 size_t compact_masked_workspace_bytes(int64_t n_env) {
-  return sizeof(uint64_t) * (size_t)((n_env + kMaskedTile - 1) / kMaskedTile + 2);
+  // ticket + scan-tile status words, then (when the caller wants no offsets) env offsets
+  return sizeof(uint64_t) * (size_t)((n_env + kScanTile - 1) / kScanTile + 2) + sizeof(int64_t) * (n_env + 1);
 }
 
 int launch_compact_masked(const float* contacts, const int32_t* src, int64_t n_env, int C, const uint32_t* mask,
@@ -388,15 +395,20 @@ int launch_compact_masked(const float* contacts, const int32_t* src, int64_t n_e
   p.out_contacts = out_contacts;
   p.out_slot = out_slot;
   p.out_src = out_src;
-  p.env_offset = env_offset;
   p.env_count = env_count;
   p.total = total;
+  const int64_t tiles = (n_env + kScanTile - 1) / kScanTile;
+  const size_t status_bytes = sizeof(uint64_t) * (size_t)(tiles + 2);
   p.ticket = static_cast<uint32_t*>(workspace);
   p.status = static_cast<uint64_t*>(workspace) + 1;
-  if (cudaMemsetAsync(workspace, 0, compact_masked_workspace_bytes(n_env), s) != cudaSuccess) return 1;
-  const int64_t tiles = (n_env + kMaskedTile - 1) / kMaskedTile;
+  p.env_offset = env_offset ? env_offset
+                            : reinterpret_cast<int64_t*>(static_cast<unsigned char*>(workspace) + status_bytes);
+  if (cudaMemsetAsync(workspace, 0, status_bytes, s) != cudaSuccess) return 1;
   note_launch();
-  compact_masked_kernel<<<(unsigned)tiles, kMaskedTile, 0, s>>>(p);
+  compact_scan_kernel<<<(unsigned)tiles, kScanTile, 0, s>>>(p);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  note_launch();
+  compact_gather_kernel<<<(unsigned)((n_env * 32 + 255) / 256), 256, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

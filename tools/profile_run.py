@@ -25,17 +25,20 @@ elif kind in ("drop", "drop-fwd"):
     outs = None
     for _ in range(2):
         outs = fn(bodies, P, SmoothingConfig(), is_static=sc.is_static(), outs=outs)
-elif kind in ("manifold", "compact"):
+elif kind in ("manifold", "compact", "compact-masked"):
     ws = W.box_box(n)
     s1 = api.surface_from_spec(ws.bodies[0]); s2 = api.surface_from_spec(ws.bodies[1])
     p1, p2 = ws.poses(n)
     P1 = torch.as_tensor(p1, device="cuda"); P2 = torch.as_tensor(p2, device="cuda")
     out = {}
     comp = {}
+    thr = 0.01 if kind == "compact-masked" else None
     for _ in range(3):
-        api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out)
+        api.generate_manifold_batch(s1, s2, P1, P2, SmoothingConfig(), out=out, active_threshold=thr)
         if kind == "compact":
             api.compact_contacts(out["contacts"], 0.01, out=comp)
+        elif kind == "compact-masked":
+            api.compact_contacts(out["contacts"], mask=out["active_mask"], count=out["active_count"], out=comp)
 else:
     pairs = torch.rand((n, 12), dtype=torch.float64, device="cuda")
     for _ in range(3):
