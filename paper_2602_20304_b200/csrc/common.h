@@ -30,7 +30,10 @@ enum SdfKind : int32_t {
   kSqE025 = 6,  // eps1 = eps2 = 0.25 (4, 1, 4, 8)
   kSqE05 = 7,   // eps1 = eps2 = 0.5  (2, 1, 2, 4)
   kSqEll = 8,   // eps1 = eps2 = 1    (1, 1, 1, 2): ellipsoid / sphere
-  kSqCyl = 9    // eps1 = 0.1, eps2 = 1 (1, 10, 10, 20): cylinder (config C)
+  kSqCyl = 9,   // eps1 = 0.1, eps2 = 1 (1, 10, 10, 20): cylinder (config C)
+  // a recognised composition: union(kSqCyl cylinder, kSqEll cap, kSqEll cap) --
+  // the capsule of config C, leaves in registers
+  kCapsule = 10
 };
 
 // Exponents of the compile-time superquadric kinds (0: not such a kind).

@@ -314,6 +314,36 @@ __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   // kNormalOnly skips phi only for a lone SQ leaf; compositions need the values.
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;
+  if constexpr (KIND == kCapsule) {
+    // union of three compile-time superquadric leaves, the interpreter's union
+    // arithmetic in the same order (bit-identical), nothing on a stack
+    constexpr SqExpTuple a = sq_exps(kSqCyl), b = sq_exps(kSqEll);
+    const SdfOutT<T> r0 = sq_leaf<FL, a.n1, a.n2, a.n3, a.n4, T>(s.nodes[0].sq, p);
+    const SdfOutT<T> r1 = sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[1].sq, p);
+    const SdfOutT<T> r2 = sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[2].sq, p);
+    const DevNode& un = s.nodes[3];
+    T m = r0.v;
+    m = fmin(m, r1.v);
+    m = fmin(m, r2.v);
+    const T e0 = exp_d((m - r0.v) * un.inv_tau_d);
+    const T e1 = exp_d((m - r1.v) * un.inv_tau_d);
+    const T e2 = exp_d((m - r2.v) * un.inv_tau_d);
+    T acc = 0.0;
+    acc += e0;
+    acc += e1;
+    acc += e2;
+    SdfOutT<T> out;
+    out.v = m - un.tau_d * log_d(acc);
+    out.g = mk3<T>(0.0, 0.0, 0.0);
+    if constexpr (kWantG) {
+      vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
+      g = g + dscale(r0.g, e0);
+      g = g + dscale(r1.g, e1);
+      g = g + dscale(r2.g, e2);
+      out.g = dscale(g, rcp_d(acc));
+    }
+    return out;
+  }
   if constexpr (KIND == kSingleCp) return cp_leaf<FL, T>(s.nodes[0], s.pool, p);
   if constexpr (KIND == kBoxCp) return box_cp_leaf<FL, T>(s.nodes[0], p);
   // Generic postfix interpreter (union: -LSE(-phi), subtraction: LSE(phi+, -phi-);

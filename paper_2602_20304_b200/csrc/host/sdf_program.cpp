@@ -259,6 +259,18 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       if (q.n1 == e.n1 && q.n2 == e.n2 && q.n3 == e.n3 && q.n4 == e.n4) s.kind = k;
     }
   }
+  if (n == 4 && prog.nodes[3].op == CMGB_SDF_UNION && prog.nodes[3].count == 3) {
+    auto sq_kind = [&](int i) {
+      if (prog.nodes[i].op != CMGB_SDF_SUPERQUADRIC) return -1;
+      const DevSq& q = s.nodes[i].sq;
+      for (int k : {kSqCyl, kSqEll}) {
+        const SqExpTuple e = sq_exps(k);
+        if (q.n1 == e.n1 && q.n2 == e.n2 && q.n3 == e.n3 && q.n4 == e.n4) return k;
+      }
+      return -1;
+    };
+    if (sq_kind(0) == kSqCyl && sq_kind(1) == kSqEll && sq_kind(2) == kSqEll) s.kind = kCapsule;
+  }
   if (s.kind == kSingleCp && prog.nodes[0].count == 6) {
     // the box_planes pattern: unit normals +x, -x, +y, -y, +z, -z in this order
     const ProgramNode& d = prog.nodes[0];

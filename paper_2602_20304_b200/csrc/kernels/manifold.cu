@@ -11,7 +11,7 @@ namespace {
 
 // Kinds without their own instantiation here run as the runtime-exponent
 // superquadric (same leaf code, exponents read from the descriptor).
-constexpr int base_kind(int k) { return ct_sq(k) && k != kSqE01 ? (int)kSingleSq : k; }
+constexpr int base_kind(int k) { return k == kCapsule ? (int)kGeneric : (ct_sq(k) && k != kSqE01 ? (int)kSingleSq : k); }
 
 template <int K1>
 int launch_k2(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {

@@ -62,8 +62,14 @@ __device__ unsigned long long g_mf_phase[16];
 //   everything else: 10 warps, 3 CTAs/SM (<= 64 registers), V-S contacts in
 //     the pair phase (E) after the pair items (config D forward +4%).
 __host__ __device__ constexpr bool box_box(int k1, int k2) { return k1 == k2 && ct_sq(k1); }
+#ifndef CMGB_CAPSULE_BLOCKS
+#define CMGB_CAPSULE_BLOCKS 3  // measured: 2 CTAs x 96 registers still spill and run 10% slower
+#endif
+constexpr int kCapsuleBlocks = CMGB_CAPSULE_BLOCKS;  // resident CTAs/SM of the capsule instantiations
 __host__ __device__ constexpr int max_threads(int k1, int k2) { return box_box(k1, k2) ? 288 : 320; }
-__host__ __device__ constexpr int min_blocks(int k1, int k2) { return box_box(k1, k2) ? 4 : 3; }
+__host__ __device__ constexpr int min_blocks(int k1, int k2) {
+  return box_box(k1, k2) ? 4 : (k1 == kCapsule || k2 == kCapsule ? kCapsuleBlocks : 3);
+}
 __host__ __device__ constexpr bool vs_in_pair_phase(int k1, int k2) { return !box_box(k1, k2); }
 
 // Pair record (doubles; kPairRec = 38 floats = 19 doubles = 152 B), rewritten
@@ -829,7 +835,7 @@ int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cud
 template <int K>
 int launch_same_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   const int nvs = p.n1 + p.n2;
-  if (!p.side[0].topk_v && !p.side[1].topk_v && nvs > 0 && nvs <= 32) {
+  if (box_box(K, K) && !p.side[0].topk_v && !p.side[1].topk_v && nvs > 0 && nvs <= 32) {
     ManifoldParams q = p;
     q.vs_ext = 1;
     int G = 1;

@@ -40,6 +40,7 @@ int launch_manifold_ct(const ManifoldParams& p, int threads, int grid, size_t sm
       case kSqE05: rc = launch_vs_cp<kSqE05>(p, threads, grid, smem, s, handled); break;
       case kSqEll: rc = launch_vs_cp<kSqEll>(p, threads, grid, smem, s, handled); break;
       case kSqCyl: rc = launch_vs_cp<kSqCyl>(p, threads, grid, smem, s, handled); break;
+      case kCapsule: rc = launch_vs_cp<kCapsule>(p, threads, grid, smem, s, handled); break;
       default: break;
     }
     if (*handled) return rc;
