@@ -58,8 +58,10 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
 int manifold_max_threads(int k1, int k2) { return max_threads(k1, k2); }
 
 #ifdef CMGB_PHASE_CLOCKS
-int manifold_phase_clocks(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_mf_phase, 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
+int manifold_ct_phase_clocks(unsigned long long* out);
+int manifold_phase_clocks(unsigned long long* out) {  // both translation units' counters
+  if (cudaMemcpyFromSymbol(out, g_mf_phase, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  return manifold_ct_phase_clocks(out);
 }
 #endif
 int manifold_min_blocks(int k1, int k2) { return min_blocks(k1, k2); }

@@ -48,4 +48,13 @@ int launch_manifold_ct(const ManifoldParams& p, int threads, int grid, size_t sm
   return 0;
 }
 
+#ifdef CMGB_PHASE_CLOCKS
+int manifold_ct_phase_clocks(unsigned long long* out) {
+  unsigned long long h[16];
+  if (cudaMemcpyFromSymbol(h, g_mf_phase, sizeof(h)) != cudaSuccess) return 1;
+  for (int i = 0; i < 16; ++i) out[i] += h[i];
+  return 0;
+}
+#endif
+
 }  // namespace cmgb

@@ -16,9 +16,9 @@ from paper_2602_20304_b200 import abi, api  # noqa: E402
 from paper_2602_20304_b200 import workloads as W  # noqa: E402
 from paper_2602_20304_b200.scene import SmoothingConfig  # noqa: E402
 
-if len(sys.argv) > 1 and sys.argv[1] == "box-box":
+if len(sys.argv) > 1 and (sys.argv[1] == "box-box" or sys.argv[1].startswith("mixed:")):
     n = 65536
-    ws = W.box_box(n)
+    ws = W.box_box(n) if sys.argv[1] == "box-box" else W.mixed_bucket(sys.argv[1].split(":", 1)[1], n)
     s1, s2 = (api.surface_from_spec(b) for b in ws.bodies)
     p1, p2 = ws.poses(n)
     P1, P2 = torch.as_tensor(p1, device="cuda"), torch.as_tensor(p2, device="cuda")
@@ -34,7 +34,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "box-box":
     d = np.array(out[:], dtype=np.float64) - base
     names = {0: "A frames", 1: "B vertex scores", 2: "B edge scores", 3: "C rank sort", 4: "D slots",
              5: "E pairs (+ V-S)", 6: "F NN (+ V-S)", 7: "G activity + stores", 8: "H mean"}
-    ncta = n // 2
+    L = api.layout(s1, s2, SmoothingConfig())
+    per_env = max(L["m1"] * L["m2"], L["n1"] + L["n2"], 1)
+    epb = max(1, (288 if sys.argv[1] == "box-box" else 320) // per_env)
+    ncta = -(-n // epb)
     tot = d[:9].sum()
     for k, nm in names.items():
         print(f"{nm:20s} {100 * d[k] / tot:6.2f} %  {d[k] / ncta:9.0f} clk per CTA")
