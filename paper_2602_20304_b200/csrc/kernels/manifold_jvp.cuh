@@ -177,6 +177,7 @@ struct SideJac {
   double M[9], N[9];
   double3 pw, nw, gvw, gown;
   double vo, phi_own;
+  double pad;  // odd 8-byte stride: lanes on consecutive records hit distinct banks
 };
 
 // Witness QP of a pair as a function of (Q11, Q12, Q22, c1, c2): primal
@@ -184,6 +185,7 @@ struct SideJac {
 struct QpRec {
   double a1, a2, gam;
   double J[15];
+  double pad;  // odd stride (bank conflicts)
 };
 
 // Selected edge slot: world endpoints (primal; their tangents follow from the
@@ -202,6 +204,7 @@ struct VsRec {
   double3 n, gb;  // gb: gradient of the opposing value in its body frame
   double Jb[9];       // d n_body / d x_body
   double v, act, cact;
+  double pad;  // odd stride (bank conflicts)
 };
 
 // E-E pair quantities (manifold.hpp:248-266, 279-285), primal, FP64.
@@ -218,8 +221,8 @@ struct SlotAux {
   int imin, pad;
 };
 
-static_assert(sizeof(T12) == 56 && sizeof(SideJac) == 32 * 8 && sizeof(QpRec) == 18 * 8 && sizeof(SlotAux) == 16 &&
-                  sizeof(VsRec) == 18 * 8 && sizeof(ESlot) == 384 && sizeof(PairRec) == 17 * 8 &&
+static_assert(sizeof(T12) == 56 && sizeof(SideJac) == 33 * 8 && sizeof(QpRec) == 19 * 8 && sizeof(SlotAux) == 16 &&
+                  sizeof(VsRec) == 19 * 8 && sizeof(ESlot) == 384 && sizeof(PairRec) == 17 * 8 &&
                   sizeof(Frame) == 12 * 8 && sizeof(Vel) == 6 * 8,
               "record sizes are mirrored by plan_jvp (host/api.cpp)");
 
@@ -243,8 +246,13 @@ struct EnvUnit {
   __device__ ESlot& eslot(int i) const { return reinterpret_cast<ESlot*>(base + p->o_eslots)[i]; }
   __device__ int* prov() const { return reinterpret_cast<int*>(base + p->o_prov); }
   // per pair: dg, A1 = con pen1 clash cont, A2, dist1 + dist2
-  __device__ T12* pair(int i) const { return reinterpret_cast<T12*>(base + p->o_pairs) + 4 * i; }
-  __device__ SideJac& sj(int i, int s) const { return reinterpret_cast<SideJac*>(base + p->o_sj)[2 * i + s]; }
+  __device__ T12* pair(int i) const {  // 4 records per pair + 8 B pad: odd 8-byte stride (bank conflicts)
+    return reinterpret_cast<T12*>(base + p->o_pairs + (size_t)i * (4 * sizeof(T12) + 8));
+  }
+  // side-major: consecutive pairs of one side are consecutive records (odd stride)
+  __device__ SideJac& sj(int i, int s) const {
+    return reinterpret_cast<SideJac*>(base + p->o_sj)[s * p->m.m1 * p->m.m2 + i];
+  }
   __device__ QpRec& qrec(int i) const { return reinterpret_cast<QpRec*>(base + p->o_qp)[i]; }
   __device__ VsRec& vsrec(int r) const { return reinterpret_cast<VsRec*>(base + p->o_vsrec)[r]; }
   __device__ PairRec& prec(int i) const { return reinterpret_cast<PairRec*>(base + p->o_prec)[i]; }
