@@ -888,7 +888,7 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   const ManifoldParams& m = j.m;
   const int T = 8 + 12 * 4;                  // bytes per tangent record
   const int SJ = 33 * 8, QP = 19 * 8, AUX = 16, VS = 19 * 8, PR = 17 * 8;  // manifold_jvp.cuh records
-  const int FRAMES = 2 * 12 * 8 + 12 * 6 * 8;  // 2 x Frame + 12 x Vel
+  const int FRAMES = 2 * 12 * 8 + 12 * 7 * 8;  // 2 x Frame + 12 x Vel
   const int P = m.m1 * m.m2, nslot_v = m.n1 + m.n2, nslot_e = m.m1 + m.m2, nsl = nslot_v + nslot_e;
   const bool topk = m.side[0].topk_v || m.side[1].topk_v || m.side[0].topk_e || m.side[1].topk_e;
   const int nscore = topk ? (m.side[0].nv + m.side[1].nv + m.side[0].ne + m.side[1].ne) : 0;
@@ -901,7 +901,7 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   int off = 0;
   j.o_frames = off; off = align16(off + FRAMES);
   j.o_vslots = off; off = align16(off + nslot_v * 3 * T);
-  j.o_eslots = off; off = align16(off + nslot_e * (48 + 6 * T));  // ESlot
+  j.o_eslots = off; off = align16(off + nslot_e * (48 + 6 * T + 8));  // ESlot
   j.o_prov = off; off = align16(off + nsl * 4);
   j.o_pairs = off; off = align16(off + P * (4 * T + 8));  // 4 records + 8 B: odd 8-byte stride per pair
   j.o_vsdist = off; off = align16(off + nslot_v * T);

@@ -106,6 +106,7 @@ struct Frame {
 struct Vel {
   double w[3];
   double v[3];
+  double pad;  // odd 8-byte stride: the 12 direction lanes read distinct banks
 };
 
 // ---- primal / tangent views ------------------------------------------------------
@@ -194,6 +195,7 @@ struct QpRec {
 struct ESlot {
   double aw[3], bw[3];
   T12 a[3], b[3];
+  double pad;  // odd 8-byte stride (bank conflicts)
 };
 __device__ __forceinline__ double3 dv3(const double* q) { return d3(q[0], q[1], q[2]); }
 
@@ -222,8 +224,8 @@ struct SlotAux {
 };
 
 static_assert(sizeof(T12) == 56 && sizeof(SideJac) == 33 * 8 && sizeof(QpRec) == 19 * 8 && sizeof(SlotAux) == 16 &&
-                  sizeof(VsRec) == 19 * 8 && sizeof(ESlot) == 384 && sizeof(PairRec) == 17 * 8 &&
-                  sizeof(Frame) == 12 * 8 && sizeof(Vel) == 6 * 8,
+                  sizeof(VsRec) == 19 * 8 && sizeof(ESlot) == 392 && sizeof(PairRec) == 17 * 8 &&
+                  sizeof(Frame) == 12 * 8 && sizeof(Vel) == 7 * 8,
               "record sizes are mirrored by plan_jvp (host/api.cpp)");
 
 struct EnvUnit {
