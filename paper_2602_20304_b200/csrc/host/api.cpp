@@ -234,13 +234,13 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     int off = 0;
     S.frames = off; off = align16(off + 24 * 8);
     S.vslots = off; off = align16(off + nslot_v * 3 * 8);
-    S.eslots = off; off = align16(off + nslot_e * 12 * 8);
+    S.eslots = off; off = align16(off + nslot_e * 13 * 8);
     S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
     S.scores = off; off = align16(off + nscore * 8);
     S.sorted = off; off = align16(off + nscore * 8);
     S.pairs = off; off = align16(off + (pairs_in_smem ? P * kPairRec * 4 : 0));
     S.vsdist = off; off = align16(off + nslot_v * 4);
-    S.nnstat = off; off = align16(off + nslot_e * 2 * 8);
+    S.nnstat = off; off = align16(off + nslot_e * 3 * 8);
     S.hpart = off; off = align16(off + 10 * 8);  // one partial per warp (<= 320-thread CTAs)
     S.amask = off; off = align16(off + (out->active_mask ? 4 * ((L.n_contacts + 31) / 32) : 0));
     S.bytes = off;

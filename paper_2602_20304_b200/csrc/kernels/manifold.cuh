@@ -86,7 +86,9 @@ struct EnvView {
   __device__ double* R(int s) const { return reinterpret_cast<double*>(base + L->frames) + 12 * s; }
   __device__ double* t(int s) const { return R(s) + 9; }
   __device__ double* vslot(int i) const { return reinterpret_cast<double*>(base + L->vslots) + 3 * i; }
-  __device__ double* eslot(int i) const { return reinterpret_cast<double*>(base + L->eslots) + 12 * i; }
+  // 12 doubles per edge slot + 1 pad: odd stride, so the lanes of a warp reading
+  // different slots hit distinct shared-memory banks
+  __device__ double* eslot(int i) const { return reinterpret_cast<double*>(base + L->eslots) + 13 * i; }
   __device__ int* prov() const { return reinterpret_cast<int*>(base + L->prov); }
   __device__ double* scores() const { return reinterpret_cast<double*>(base + L->scores); }
   __device__ double* sorted() const { return reinterpret_cast<double*>(base + L->sorted); }
@@ -638,8 +640,8 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       tot += __shfl_xor_sync(gm, tot, 1);
       tot += __shfl_xor_sync(gm, tot, 2);
       if (ql == 0) {
-        ev.nnstat()[2 * r] = m;
-        ev.nnstat()[2 * r + 1] = 1.0 / tot;
+        ev.nnstat()[3 * r] = m;  // stride 3 (odd): conflict-free reads in G
+        ev.nnstat()[3 * r + 1] = 1.0 / tot;
       }
     }
     if constexpr (!kVsE && !kVsX) {
@@ -683,8 +685,8 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         const double* rec = ev.pair(i);
         const double* ns = ev.nnstat();
         const double dg = rec[3];
-        const double nn1 = (double)expf((float)((ns[2 * k] - dg) * c.inv_tau_nn)) * ns[2 * k + 1];
-        const double nn2 = (double)expf((float)((ns[2 * (m1 + l)] - dg) * c.inv_tau_nn)) * ns[2 * (m1 + l) + 1];
+        const double nn1 = (double)expf((float)((ns[3 * k] - dg) * c.inv_tau_nn)) * ns[3 * k + 1];
+        const double nn2 = (double)expf((float)((ns[3 * (m1 + l)] - dg) * c.inv_tau_nn)) * ns[3 * (m1 + l) + 1];
         const double pen1 = rec[6], pen2 = rec[14], con = rec[16], clash = rec[15], cont = rec[7];
         const float act1 = (float)(con * pen1 * nn1 * clash * cont);
         const float act2 = (float)(con * pen2 * nn2 * clash * cont);
