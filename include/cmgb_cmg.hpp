@@ -57,7 +57,11 @@
 #include <utility>
 #include <vector>
 
+#include <filesystem>
+#include <iomanip>
+
 #include "cmgb.h"
+#include "cmgb_json.hpp"
 
 namespace cmgb {
 namespace ref {
@@ -1150,6 +1154,226 @@ inline std::vector<BenchRecord> bench_manifold(const Scene& scene, const std::ve
     }
   }
   return records;
+}
+
+// ============================================================================ scene documents (scene.hpp)
+// parse_scene / load_scene (src/scene.cpp:130-182): the same schema, defaults
+// and messages, on cmgb_json.hpp (the reference uses nlohmann::json).
+namespace detail {
+
+inline Vec3d scene_vec3(const json::Value& j, const char* what) {
+  if (!j.is_array() || j.size() != 3) throw SceneError(std::string(what) + ": expected [x, y, z]");
+  return {j[0].as_number(), j[1].as_number(), j[2].as_number()};
+}
+
+inline Pose6d scene_pose(const json::Value& j, const char* what) {
+  if (!j.is_array() || j.size() != 6)
+    throw SceneError(std::string(what) + ": expected a 6-vector [tx, ty, tz, rx, ry, rz]");
+  Pose6d p;
+  for (int i = 0; i < 6; ++i) p[i] = j[i].as_number();
+  return p;
+}
+
+inline SmoothSdf scene_sdf_node(const json::Value& j, const SmoothingConfig& defaults);
+
+inline SmoothSdf scene_sdf_primitive(const json::Value& j, const SmoothingConfig& defaults) {
+  const std::string type = j.at("type").as_string();
+  if (type == "superquadric") {
+    SuperquadricParams q;
+    q.eps1 = j.at("eps1").as_number();
+    q.eps2 = j.at("eps2").as_number();
+    q.axes = scene_vec3(j.at("axes"), "superquadric axes");
+    if (j.contains("pose")) q.pose = scene_pose(j.at("pose"), "superquadric pose");
+    return SmoothSdf::superquadric(q);
+  }
+  if (type == "convex_polyhedron" || type == "box_planes") {
+    ConvexPolyhedronParams cp;
+    cp.tau = j.value("tau", 1e-3);
+    if (type == "convex_polyhedron") {
+      for (const auto& plane : j.at("planes").arr) {
+        cp.normals.push_back(scene_vec3(plane.at("normal"), "plane normal"));
+        cp.points.push_back(scene_vec3(plane.at("point"), "plane point"));
+      }
+    } else {  // the six half-space planes of an axis-aligned box: +x, -x, +y, -y, +z, -z
+      const Vec3d h = scene_vec3(j.at("half_extents"), "box_planes half_extents");
+      for (int a = 0; a < 3; ++a)
+        for (double sg : {1.0, -1.0}) {
+          Vec3d n{0, 0, 0}, pt{0, 0, 0};
+          n[a] = sg;
+          pt[a] = sg * h[a];
+          cp.normals.push_back(n);
+          cp.points.push_back(pt);
+        }
+    }
+    return SmoothSdf::convex_polyhedron(cp);
+  }
+  if (type == "oriented_pointcloud") {
+    OrientedPointcloudParams pc;
+    for (const auto& x : j.at("points").arr) pc.points.push_back(scene_vec3(x, "pointcloud point"));
+    for (const auto& x : j.at("normals").arr) pc.normals.push_back(scene_vec3(x, "pointcloud normal"));
+    for (const auto& x : j.at("lengthscales").arr) pc.lengthscales.push_back(x.as_number());
+    return SmoothSdf::oriented_pointcloud(pc);
+  }
+  if (type == "union") {
+    std::vector<SmoothSdf> children;
+    for (const auto& c : j.at("children").arr) children.push_back(scene_sdf_node(c, defaults));
+    return SmoothSdf::smooth_union(std::move(children), j.value("tau", defaults.tau_union));
+  }
+  if (type == "subtraction")
+    return SmoothSdf::subtraction(scene_sdf_node(j.at("positive"), defaults),
+                                  scene_sdf_node(j.at("negative"), defaults), j.value("tau", defaults.tau_union));
+  throw SceneError("unknown sdf node type: " + type);
+}
+
+inline SmoothSdf scene_sdf_node(const json::Value& j, const SmoothingConfig& defaults) {
+  if (j.is_array()) {  // array shorthand: implicit union, a single child collapses
+    std::vector<SmoothSdf> children;
+    for (const auto& c : j.arr) children.push_back(scene_sdf_node(c, defaults));
+    if (children.size() == 1) return std::move(children.front());
+    return SmoothSdf::smooth_union(std::move(children), defaults.tau_union);
+  }
+  return scene_sdf_primitive(j, defaults);
+}
+
+inline CollisionMesh scene_mesh(const json::Value& j, const std::string& base_dir) {
+  if (j.contains("obj")) {
+    std::filesystem::path p = j.at("obj").as_string();
+    if (p.is_relative()) p = std::filesystem::path(base_dir) / p;
+    return load_obj(p.string());
+  }
+  if (j.contains("box")) {
+    const json::Value& b = j.at("box");
+    return make_box_mesh(scene_vec3(b.at("half_extents"), "box half_extents"), b.value("subdivisions", 1),
+                         b.value("quad_edges", true));
+  }
+  throw SceneError("mesh: expected an 'obj' path or a 'box' generator");
+}
+
+inline SmoothingConfig scene_smoothing(const json::Value& j) {
+  SmoothingConfig c;
+  if (!j.is_object()) return c;
+  c.lambda = j.value("lambda", c.lambda);
+  c.tau_clip = j.value("tau_clip", c.tau_clip);
+  c.tau_min = j.value("tau_min", c.tau_min);
+  c.tau_comp = j.value("tau_comp", c.tau_comp);
+  c.tau_sign = j.value("tau_sign", c.tau_sign);
+  c.tau_pen = j.value("tau_pen", c.tau_pen);
+  c.tau_nn = j.value("tau_nn", c.tau_nn);
+  c.tau_clash = j.value("tau_clash", c.tau_clash);
+  c.tau_cont = j.value("tau_cont", c.tau_cont);
+  c.tau_topk_verts = j.value("tau_topk_verts", c.tau_topk_verts);
+  c.tau_topk_edges = j.value("tau_topk_edges", c.tau_topk_edges);
+  c.tau_normal = j.value("tau_normal", c.tau_normal);
+  c.tau_union = j.value("tau_union", c.tau_union);
+  c.hard_ops = j.value("hard_ops", c.hard_ops);
+  c.sphere_trace = j.value("sphere_trace", c.sphere_trace);
+  c.sphere_trace_iters = j.value("sphere_trace_iters", c.sphere_trace_iters);
+  c.containment_safeguard = j.value("containment_safeguard", c.containment_safeguard);
+  if (j.contains("mode")) {
+    const std::string m = j.at("mode").as_string();
+    if (m == "full") c.mode = ContactMode::kFull;
+    else if (m == "no-ee") c.mode = ContactMode::kNoEe;
+    else if (m == "one-sided") c.mode = ContactMode::kOneSided;
+    else throw SceneError("mode must be one of: full, no-ee, one-sided");
+  }
+  c.validate();
+  return c;
+}
+
+}  // namespace detail
+
+inline Scene parse_scene(const std::string& json_text, const std::string& base_dir) {
+  json::Value doc;
+  try {
+    doc = json::parse(json_text);
+  } catch (const json::ParseError& e) {
+    throw SceneError(std::string("scene JSON parse error: ") + e.what());
+  }
+  Scene scene;
+  try {
+    scene.smoothing = detail::scene_smoothing(doc.contains("smoothing") ? doc.at("smoothing") : json::Value());
+    if (!doc.contains("bodies") || !doc.at("bodies").is_array() || doc.at("bodies").size() == 0)
+      throw SceneError("scene: needs a non-empty 'bodies' array");
+    for (const auto& jb : doc.at("bodies").arr) {
+      SceneBody body;
+      body.name = jb.value("name", std::string("body") + std::to_string(scene.bodies.size()));
+      CollisionMesh mesh = detail::scene_mesh(jb.at("mesh"), base_dir);
+      SmoothSdf sdf = detail::scene_sdf_node(jb.at("sdf"), scene.smoothing);
+      body.surface = build_surface(std::move(mesh), std::move(sdf), jb.value("vertex_topk", 0),
+                                   jb.value("edge_topk", 0));
+      body.pose = detail::scene_pose(jb.at("pose"), "body pose");
+      body.mass = jb.value("mass", 1.0);
+      if (!(body.mass > 0.0)) throw SceneError("body mass must be positive");
+      if (jb.contains("inertia")) body.inertia_diag = detail::scene_vec3(jb.at("inertia"), "inertia");
+      body.is_static = jb.value("static", false);
+      scene.bodies.push_back(std::move(body));
+    }
+  } catch (const json::KeyError& e) {  // the reference catches json::exception here
+    throw SceneError(std::string("scene schema error: ") + e.what());
+  } catch (const json::TypeError& e) {
+    throw SceneError(std::string("scene schema error: ") + e.what());
+  }
+  return scene;
+}
+
+inline Scene load_scene(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw SceneError("cannot open scene file: " + path);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  return parse_scene(ss.str(), std::filesystem::path(path).parent_path().string());
+}
+
+// ============================================================================ writers (manifold_io.hpp)
+namespace detail {
+inline const char* kind_name(ContactKind k) { return k == ContactKind::kVertexSdf ? "VS" : "EE"; }
+inline const char* mode_name(ContactMode m) {
+  return m == ContactMode::kNoEe ? "no-ee" : (m == ContactMode::kOneSided ? "one-sided" : "full");
+}
+}  // namespace detail
+
+// CSV schema v1 (src/manifold_io.cpp:24-33).
+inline void write_manifold_csv(std::ostream& os, const ContactManifold<double>& m) {
+  os << "index,kind,side,src_a,src_b,px,py,pz,dist,nx,ny,nz,activity\n";
+  const auto prec = os.precision(17);
+  for (size_t i = 0; i < m.contacts.size(); ++i) {
+    const auto& c = m.contacts[i];
+    os << i << ',' << detail::kind_name(c.kind) << ',' << c.side << ',' << c.src_a << ',' << c.src_b << ','
+       << c.point.x << ',' << c.point.y << ',' << c.point.z << ',' << c.dist << ',' << c.normal.x << ','
+       << c.normal.y << ',' << c.normal.z << ',' << c.activity << '\n';
+  }
+  os.precision(prec);
+}
+
+// JSON mirror of the same records plus the layout (src/manifold_io.cpp:35-52).
+inline std::string manifold_to_json(const ContactManifold<double>& m) {
+  using json::Value;
+  Value j = Value::object(), layout = Value::object(), rows = Value::array();
+  layout.obj["n1"] = Value::integer(m.n1);
+  layout.obj["n2"] = Value::integer(m.n2);
+  layout.obj["m1"] = Value::integer(m.m1);
+  layout.obj["m2"] = Value::integer(m.m2);
+  layout.obj["mode"] = Value::string(detail::mode_name(m.mode));
+  auto vec = [](const Vec3d& v) {
+    Value a = Value::array();
+    for (int k = 0; k < 3; ++k) a.arr.push_back(Value::number(v[k]));
+    return a;
+  };
+  for (const auto& c : m.contacts) {
+    Value r = Value::object();
+    r.obj["kind"] = Value::string(detail::kind_name(c.kind));
+    r.obj["side"] = Value::integer(c.side);
+    r.obj["src_a"] = Value::integer(c.src_a);
+    r.obj["src_b"] = Value::integer(c.src_b);
+    r.obj["point"] = vec(c.point);
+    r.obj["dist"] = Value::number(c.dist);
+    r.obj["normal"] = vec(c.normal);
+    r.obj["activity"] = Value::number(c.activity);
+    rows.arr.push_back(std::move(r));
+  }
+  j.obj["layout"] = std::move(layout);
+  j.obj["contacts"] = std::move(rows);
+  return json::dump(j, 2);
 }
 
 }  // namespace ref

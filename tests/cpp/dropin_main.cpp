@@ -11,6 +11,7 @@
 // generate_manifold<Dual12> via seed_pose_tangents + mean_contact_distance,
 // make_random_*_pairs + run_*_batch checksums, bench_manifold / write_bench_csv.
 #include <cstdio>
+#include <fstream>
 #include <random>
 #include <sstream>
 #include <string>
@@ -19,6 +20,7 @@
 #include "cmg/batch.hpp"
 #include "cmg/dual.hpp"
 #include "cmg/manifold.hpp"
+#include "cmg/manifold_io.hpp"
 #include "cmg/mesh.hpp"
 #include "cmg/scene.hpp"
 #include "cmg/surface.hpp"
@@ -41,7 +43,17 @@ static void print_manifold(const char* name, const ContactManifold<double>& m, b
   std::printf("], \"mean\": %.17g}%s\n", mean_contact_distance(m), last ? "" : ",");
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc == 4) {  // scene file -> manifold of bodies 0 and 1 -> CSV + JSON (cmd_manifold, main.cpp:124-148)
+    const Scene scene = load_scene(argv[1]);
+    const auto m = generate_manifold(scene.bodies[0].surface, scene.bodies[1].surface, scene.bodies[0].pose,
+                                     scene.bodies[1].pose, scene.smoothing);
+    std::ofstream csv(argv[2]);
+    write_manifold_csv(csv, m);
+    std::ofstream js(argv[3]);
+    js << manifold_to_json(m);
+    return 0;
+  }
   SuperquadricParams sq;
   sq.eps1 = sq.eps2 = 0.1;
   sq.axes = {0.5, 0.5, 0.5};

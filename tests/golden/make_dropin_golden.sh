@@ -11,6 +11,9 @@ g++ -std=c++20 -O2 -I/root/reference/proj/include "$ROOT/tests/cpp/dropin_main.c
     "$ROOT/oracle/_ref/libcmgref.so" -Wl,-rpath,"$ROOT/oracle/_ref" -lpthread -o /tmp/cmgb_dropin_ref
 /tmp/cmgb_dropin_ref > "$HERE/dropin_ref.json"
 echo "wrote $HERE/dropin_ref.json"
+for sc in box_on_plane capsule_vs_hollow; do
+  /tmp/cmgb_dropin_ref "$ROOT/tests/scenes/$sc.json" "$HERE/dropin_${sc}_ref.csv" "$HERE/dropin_${sc}_ref.json"
+done
 # the reference's own dev probe (proj/tests/probe.cpp) on the reference build
 g++ -std=c++20 -O2 -I/root/reference/proj/include /root/reference/proj/tests/probe.cpp \
     "$ROOT/oracle/_ref/libcmgref.so" -Wl,-rpath,"$ROOT/oracle/_ref" -lpthread -o /tmp/cmgb_probe_ref

@@ -112,3 +112,30 @@ def test_reference_probe_on_gpu(cuda, args, golden):
     assert np.abs(g - r).max() <= 0.11, np.abs(g - r).max()
     frac = [ln for ln in zip(out.splitlines(), ref.splitlines()) if ln[0] != ln[1]]
     assert len(frac) <= 2, f"more than two printed lines differ: {frac}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene", ["box_on_plane", "capsule_vs_hollow"])
+def test_dropin_scene_and_writers_on_gpu(cuda, tmp_path, scene):
+    """cmd_manifold's path through the drop-in: load_scene (the reference's
+    JSON schema) -> generate_manifold -> write_manifold_csv / manifold_to_json,
+    against the same caller built on the reference (tests/golden/
+    dropin_<scene>_ref.*): metadata columns identical, numbers within the
+    parity rule, JSON text identical once numbers are masked (key order,
+    indentation, layout block)."""
+    exe = str(tmp_path / "dropin")
+    build_ours(exe)
+    csv_p, js_p = str(tmp_path / "m.csv"), str(tmp_path / "m.json")
+    subprocess.run([exe, os.path.join(ROOT, "tests", "scenes", f"{scene}.json"), csv_p, js_p], check=True)
+    got = [ln.split(",") for ln in open(csv_p).read().splitlines()]
+    ref = [ln.split(",") for ln in open(os.path.join(GOLD, f"dropin_{scene}_ref.csv")).read().splitlines()]
+    assert got[0] == ref[0] and len(got) == len(ref)
+    for g, r in zip(got[1:], ref[1:]):
+        assert g[:5] == r[:5], (g[:5], r[:5])
+    g = np.array([[float(x) for x in row[5:]] for row in got[1:]])
+    r = np.array([[float(x) for x in row[5:]] for row in ref[1:]])
+    assert _close(g, r).all(), float((np.abs(g - r) / (1e-6 + 1e-5 * np.abs(r))).max())
+    mask = re.compile(r"-?\d+\.\d+(e[-+]?\d+)?|-?\d+e[-+]?\d+")
+    gj, rj = open(js_p).read(), open(os.path.join(GOLD, f"dropin_{scene}_ref.json")).read()
+    assert mask.sub("N", gj) == mask.sub("N", rj), "manifold_to_json layout differs from the reference's"
+    assert json.loads(gj)["layout"] == json.loads(rj)["layout"]
