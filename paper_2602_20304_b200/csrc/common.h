@@ -123,7 +123,8 @@ struct SmemLayout {
   int32_t eslots;    // (m1+m2) x 12 doubles: a_world, b_world, a_body, b_body
   int32_t prov;      // (n1+n2+m1+m2) int32 provenance
   int32_t scores;    // (V1+V2+E1+E2) floats: top-K scores (-penetration), top-K only
-  int32_t sorted;    // (V1+V2+E1+E2) floats: scores sorted descending
+  int32_t sorted;    // (V1+V2+E1+E2) int32: set-local index of the score of each rank < K (top-K rows)
+  int32_t tkw;       // (V1+V2+E1+E2) doubles: soft top-K weight factors P_i (manifold.cuh C2), top-K only
   int32_t pairs;     // P x kPairRec floats: per E-E pair record
   int32_t vsdist;    // (n1+n2) floats
   int32_t nnstat;    // (m1+m2) x 2 floats: min, 1/sum

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -237,7 +239,8 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     S.eslots = off; off = align16(off + nslot_e * 13 * 8);
     S.prov = off; off = align16(off + (nslot_v + nslot_e) * 4);
     S.scores = off; off = align16(off + nscore * 8);
-    S.sorted = off; off = align16(off + nscore * 8);
+    S.sorted = off; off = align16(off + nscore * 4);
+    S.tkw = off; off = align16(off + nscore * 8);
     S.pairs = off; off = align16(off + (pairs_in_smem ? P * kPairRec * 4 : 0));
     S.vsdist = off; off = align16(off + nslot_v * 4);
     S.nnstat = off; off = align16(off + nslot_e * 3 * 8);
@@ -289,6 +292,9 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   plan.threads = threads;
   plan.grid = static_cast<int>((n_env + epb - 1) / epb);
   plan.smem = (size_t)epb * S.bytes;
+  if (std::getenv("CMGB_DEBUG_PLAN"))  // developer instrumentation
+    std::fprintf(stderr, "cmgb plan: kinds %d/%d threads %d envs/CTA %d smem/env %d B (scores %d) P %d\n", k1, k2,
+                 threads, epb, S.bytes, nscore, P);
   return plan;
 }
 

@@ -91,7 +91,8 @@ struct EnvView {
   __device__ double* eslot(int i) const { return reinterpret_cast<double*>(base + L->eslots) + 13 * i; }
   __device__ int* prov() const { return reinterpret_cast<int*>(base + L->prov); }
   __device__ double* scores() const { return reinterpret_cast<double*>(base + L->scores); }
-  __device__ double* sorted() const { return reinterpret_cast<double*>(base + L->sorted); }
+  __device__ int* sorted() const { return reinterpret_cast<int*>(base + L->sorted); }
+  __device__ double* tkw() const { return reinterpret_cast<double*>(base + L->tkw); }
   __device__ double* pair(int i) const { return prec + (kPairRec / 2) * i; }
   __device__ float* vsdist() const { return reinterpret_cast<float*>(base + L->vsdist); }
   __device__ double* nnstat() const { return reinterpret_cast<double*>(base + L->nnstat); }
@@ -436,28 +437,52 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       sc[sets.off[2] + i] = -((pa + pb) * 0.5);
     }
     MF_PHASE_MARK(2);
-    // ---- C: descending rank sort (values only matter; smooth_ops.hpp:180-185)
-    // 4 adjacent lanes per score split the comparisons (shuffle-summed rank)
+    // ---- C: descending rank of each score in its set, ties by index (the
+    // reference's sort, smooth_ops.hpp:180-185, only matters through its
+    // values): rank_i = #{j: x_j > x_i or (x_j == x_i and j < i)}, one lane per
+    // score (the lanes of a warp read the same x_j: shared-memory broadcasts).
+    // The soft top-K rows read only ranks < K: those record the element's
+    // set-local index.
     const int total = sets.off[4];
-    for (int it = tid; it < (n_here * total) << 2; it += nth) {
-      const int ql = it & 3;
+    for (int it = tid; it < n_here * total; it += nth) {
       int e, i;
-      fdivmod(it >> 2, p.div_scores, e, i);
+      fdivmod(it, p.div_scores, e, i);
       const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
       const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
       if (!active) continue;
-      const double* sc = env(e).scores();
+      const int K = set == 0 ? S1.n_sel : set == 1 ? S2.n_sel : set == 2 ? S1.m_sel : S2.m_sel;
+      const EnvView ev = env(e);
+      const double* sc = ev.scores();
       const double x = sc[i];
+      const int lo = sets.off[set], hi = sets.off[set + 1];
       int rank = 0;
-      for (int j = sets.off[set] + ql; j < sets.off[set + 1]; j += 4) {
+#pragma unroll 4
+      for (int j = lo; j < hi; ++j) {
         const double y = sc[j];
-        rank += (y > x) || (y == x && j < i);
+        rank += y > x || (y == x && j < i);
       }
-      const unsigned gm = 0xFu << ((tid & 31) & ~3);
-      rank += __shfl_xor_sync(gm, rank, 1);
-      rank += __shfl_xor_sync(gm, rank, 2);
-      if (ql == 0) env(e).sorted()[sets.off[set] + rank] = x;
+      if (rank < K) ev.sorted()[lo + rank] = i - lo;
     }
+    MF_PHASE_MARK(3);
+    // ---- C2: soft top-K weight factors. With the set's top score c and
+    // P_i = exp((x_i - c) / tau), a row's weights exp(-|s_r - x_i| / tau) are
+    // P_i / P_r (x_i <= s_r) or P_r / P_i (x_i > s_r): one exponential per
+    // element instead of one per (row, element). Rows whose (c - s_r) / tau
+    // leaves the range where every quotient is finite evaluate their
+    // exponentials directly (D).
+    for (int it = tid; it < n_here * total; it += nth) {
+      int e, i;
+      fdivmod(it, p.div_scores, e, i);
+      const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
+      const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
+      if (!active) continue;
+      const EnvView ev = env(e);
+      const double* sc = ev.scores();
+      const int lo = sets.off[set];
+      const double top = sc[lo + min(max(ev.sorted()[lo], 0), sets.off[set + 1] - lo - 1)];
+      ev.tkw()[i] = exp_d((sc[i] - top) * (set < 2 ? c.inv_tau_topk_v : c.inv_tau_topk_e));
+    }
+    MF_PHASE_MARK(9);
     MF_PHASE_MARK(3);
   }
 
@@ -493,31 +518,48 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         }
       } else {  // soft top-K row r (smooth_ops.hpp:191-196, manifold.hpp:141-148, 168-180)
         const int set = (is_edge ? 2 : 0) + s;
-        const double* x = ev.scores() + sets.off[set];
-        const int D = sets.off[set + 1] - sets.off[set];
-        const double sr = ev.sorted()[sets.off[set] + r];
+        const int lo = sets.off[set];
+        const double* x = ev.scores() + lo;
+        const double* q = ev.tkw() + lo;
+        const int* order = ev.sorted() + lo;
+        const int D = sets.off[set + 1] - lo;
+        auto ord = [&](int k) { return min(max(order[k], 0), D - 1); };  // in range even for NaN scores
+        const int ir = ord(r);
+        const double sr = x[ir];
+        const double Pr = q[ir];
         const double inv_tau = is_edge ? c.inv_tau_topk_e : c.inv_tau_topk_v;
-        // One pass: unnormalised weights e_i = exp(-|sr - x_i| / tau) accumulate
+        // One pass: unnormalised weights w_i = exp(-|s_r - x_i| / tau) accumulate
         // the total and the payload, normalised once at the end. The row's own
-        // element has e = 1, so the total is >= 1 and a term below e^-50 moves
+        // element has w = 1, so the total is >= 1 and a term below e^-50 moves
         // neither it nor the payload at FP64 resolution: those are skipped.
         double tot = 0.0;
-        int first = 0x7fffffff;
-        for (int i = ql; i < D; i += lanes) {
-          const double dist = fabs(sr - x[i]);
-          if (first == 0x7fffffff && dist == 0.0) first = i;  // first argmax (hard_attribution, 110-121)
-          const double arg = -dist * inv_tau;
-          if (arg < -50.0) continue;
-          const double e = exp_d(arg);
-          tot += e;
-          if (is_edge) {
-            const double* eb = S.edge_body + 6 * i;
-            a = a + d3(__ldg(eb), __ldg(eb + 1), __ldg(eb + 2)) * e;
-            b = b + d3(__ldg(eb + 3), __ldg(eb + 4), __ldg(eb + 5)) * e;
+        const double* __restrict__ pay = is_edge ? S.edge_body : S.verts;  // body-frame payload rows
+        auto rows = [&](auto edge) {
+          constexpr bool kE = decltype(edge)::value;
+          auto add = [&](int i, double w) {
+            tot += w;
+            const double* pp = pay + (kE ? 6 : 3) * i;
+            a = a + d3(__ldg(pp), __ldg(pp + 1), __ldg(pp + 2)) * w;
+            if constexpr (kE) b = b + d3(__ldg(pp + 3), __ldg(pp + 4), __ldg(pp + 5)) * w;
+          };
+          if (Pr >= 1e-260) {  // (c - s_r) / tau <= 598: quotients of the C2 factors
+            const double iPr = rcp_d(Pr);
+            for (int i = ql; i < D; i += lanes) {
+              const double Pi = q[i];
+              const double w = Pi <= Pr ? Pi * iPr : Pr * rcp_d(Pi);  // Pi >= Pr >= 1e-260 in the second arm
+              if (w < 1.9287498479639178e-22) continue;  // e^-50
+              add(i, w);
+            }
           } else {
-            a = a + ld_vert(S.verts, i) * e;
+            for (int i = ql; i < D; i += lanes) {
+              const double arg = -fabs(sr - x[i]) * inv_tau;
+              if (arg < -50.0) continue;
+              add(i, exp_d(arg));
+            }
           }
-        }
+        };
+        if (is_edge) rows(std::true_type{});
+        else rows(std::false_type{});
         {  // reduce over the slot's lane group (fixed order)
           const unsigned gm = 0xFu << ((tid & 31) & ~3);
 #pragma unroll
@@ -529,11 +571,15 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
             b.x += __shfl_xor_sync(gm, b.x, o);
             b.y += __shfl_xor_sync(gm, b.y, o);
             b.z += __shfl_xor_sync(gm, b.z, o);
-            first = min(first, __shfl_xor_sync(gm, first, o));
           }
         }
-        prov = first == 0x7fffffff ? -1 : first;
-        const double inv = 1.0 / tot;
+        // provenance = first argmax of the row's weights (hard_attribution,
+        // 110-121) = the lowest index holding s_r; equal scores take
+        // consecutive ranks in index order, so it is the first rank of s_r's run
+        int rr = r;
+        while (rr > 0 && x[ord(rr - 1)] == sr) --rr;
+        prov = sr == sr ? ord(rr) : -1;
+        const double inv = rcp_d(tot);  // tot >= 1
         a = a * inv;
         b = b * inv;
       }

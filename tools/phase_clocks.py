@@ -33,12 +33,13 @@ if len(sys.argv) > 1 and (sys.argv[1] == "box-box" or sys.argv[1].startswith("mi
     lib.cmgb_debug_manifold_phase_clocks(out)
     d = np.array(out[:], dtype=np.float64) - base
     names = {0: "A frames", 1: "B vertex scores", 2: "B edge scores", 3: "C rank sort", 4: "D slots",
-             5: "E pairs (+ V-S)", 6: "F NN (+ V-S)", 7: "G activity + stores", 8: "H mean"}
+             5: "E pairs (+ V-S)", 6: "F NN (+ V-S)", 7: "G activity + stores", 8: "H mean",
+             9: "C2 top-K factors"}
     L = api.layout(s1, s2, SmoothingConfig())
     per_env = max(L["m1"] * L["m2"], L["n1"] + L["n2"], 1)
     epb = max(1, (288 if sys.argv[1] == "box-box" else 320) // per_env)
     ncta = -(-n // epb)
-    tot = d[:9].sum()
+    tot = d[:10].sum()
     for k, nm in names.items():
         print(f"{nm:20s} {100 * d[k] / tot:6.2f} %  {d[k] / ncta:9.0f} clk per CTA")
     print(f"total {tot / ncta:.0f} clk per CTA ({ncta} CTAs)")
