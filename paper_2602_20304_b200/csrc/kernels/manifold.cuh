@@ -437,20 +437,66 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       sc[sets.off[2] + i] = -((pa + pb) * 0.5);
     }
     MF_PHASE_MARK(2);
-    // ---- C: descending rank of each score in its set, ties by index (the
+    // ---- C: descending order of the scores of each set, ties by index (the
     // reference's sort, smooth_ops.hpp:180-185, only matters through its
-    // values): rank_i = #{j: x_j > x_i or (x_j == x_i and j < i)}, one lane per
-    // score (the lanes of a warp read the same x_j: shared-memory broadcasts).
-    // The soft top-K rows read only ranks < K: those record the element's
-    // set-local index.
+    // values). The soft top-K rows read only ranks < K: sorted[lo + r] holds
+    // the set-local index of the score of rank r. Two schemes:
+    //  * large sets (K x 104 < D^2, D <= 128): one warp extracts the K largest
+    //    in order -- per round, each lane's best remaining key, then warp
+    //    reductions over (key high word, key low word, lowest index);
+    //  * the others: rank_i = #{j: x_j > x_i or (x_j == x_i and j < i)}, one
+    //    lane per score (the lanes of a warp read the same x_j: broadcasts).
     const int total = sets.off[4];
+    auto set_active = [&](int set) {
+      return set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
+    };
+    auto set_K = [&](int set) { return set == 0 ? S1.n_sel : set == 1 ? S2.n_sel : set == 2 ? S1.m_sel : S2.m_sel; };
+    auto extracted = [&](int set) {
+      const int D = sets.off[set + 1] - sets.off[set];
+      return set_active(set) && D <= 128 && set_K(set) * 104 < D * D;
+    };
+    {
+      const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+      for (int task = warp; task < n_here * 4; task += nwarps) {  // warp-uniform
+        const int e = task >> 2, set = task & 3;
+        if (!extracted(set)) continue;
+        const EnvView ev = env(e);
+        const int lo = sets.off[set], D = sets.off[set + 1] - lo, K = set_K(set);
+        const double* sc = ev.scores() + lo;
+        uint64_t key[4];  // order-preserving integer images of the scores; 0 = taken / absent
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int j = lane + 32 * k;
+          const uint64_t u = j < D ? (uint64_t)__double_as_longlong(sc[j]) : 0ull;
+          key[k] = j >= D ? 0ull : ((int64_t)u < 0 ? ~u : (u | 0x8000000000000000ull));
+        }
+        int* out = ev.sorted() + lo;
+        for (int r = 0; r < K; ++r) {
+          uint64_t b = key[0];
+          int bj = lane;
+#pragma unroll
+          for (int k = 1; k < 4; ++k)
+            if (key[k] > b) {  // strict: the lowest index among equal keys
+              b = key[k];
+              bj = lane + 32 * k;
+            }
+          const unsigned bh = (unsigned)(b >> 32), bl = (unsigned)b;
+          const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
+          const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
+          const int wj = __reduce_min_sync(0xffffffffu, (bh == mh && bl == ml) ? bj : 0x7fffffff);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (lane + 32 * k == wj) key[k] = 0ull;
+          if (lane == 0) out[r] = wj;
+        }
+      }
+    }
     for (int it = tid; it < n_here * total; it += nth) {
       int e, i;
       fdivmod(it, p.div_scores, e, i);
       const int set = i < sets.off[1] ? 0 : i < sets.off[2] ? 1 : i < sets.off[3] ? 2 : 3;
-      const bool active = set == 0 ? S1.topk_v : set == 1 ? S2.topk_v : set == 2 ? S1.topk_e : S2.topk_e;
-      if (!active) continue;
-      const int K = set == 0 ? S1.n_sel : set == 1 ? S2.n_sel : set == 2 ? S1.m_sel : S2.m_sel;
+      if (!set_active(set) || extracted(set)) continue;
+      const int K = set_K(set);
       const EnvView ev = env(e);
       const double* sc = ev.scores();
       const double x = sc[i];
