@@ -677,14 +677,10 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     if (full)
       for (int it = tid; it < n_here * P; it += nth) pair_item(it);
   } else {
-    const int nE = full ? n_here * P : 0;
-    for (int it = tid; it < nE + n_here * nvs; it += nth) {
-      if (it < nE) {
-        pair_item(it);
-        continue;
-      }
+    const int nE = full ? n_here * P : 0, nV = n_here * nvs;
+    auto vs_item = [&](int v) {
       int e, r;
-      fdivmod(it - nE, p.div_nvs, e, r);
+      fdivmod(v, p.div_nvs, e, r);
       const EnvView ev = env(e);
       const double* q = ev.vslot(r);
       float* dst = p.contacts + ((env0 + e) * C + r) * 8;
@@ -696,6 +692,17 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         sp[0] = ev.prov()[r];
         sp[1] = -1;
       }
+    };
+    // Fewer pairs than threads: the V-S items (~1/6 of a pair each) go to the
+    // threads without a pair, up to 4 each, so the phase lasts one pair item
+    // (config C: 256 pairs + 128 V-S items on 320 threads); else round robin.
+    // (one call site each: the item bodies are large)
+    const int spare = nth - nE;
+    const bool spare_mode = nE > 0 && spare > 0 && nV <= 4 * spare;
+    const int step = !spare_mode ? nth : tid < nE ? nE + nV : spare;
+    for (int it = tid; it < nE + nV; it += step) {
+      if (it < nE) pair_item(it);
+      else vs_item(it - nE);
     }
   }
   MF_PHASE_MARK(5);
