@@ -57,25 +57,27 @@ __device__ __forceinline__ double rsqrt_d(double x) {
 __device__ __forceinline__ double div_d(double a, double b) { return a * rcp_d(b); }
 
 // exp(x) in FP64 for x <= ~709: x = k ln2 + r, |r| <= ln2/2 (Cody-Waite split
-// of ln2), e^r by a degree-10 near-minimax polynomial (Chebyshev
-// interpolation, tools/minimax_coeffs.py: max relative error 3.3e-16), 2^k
-// spliced into the exponent field. exp(x < -708) returns 0 (the true value is
-// < 2.3e-308). ~15 FP64 instructions, no branches beyond the underflow select --
-// the libdevice version carries full special-case handling the indicator
-// arguments never need.
+// of ln2), e^r by a degree-8 near-minimax polynomial (Chebyshev interpolation,
+// tools/minimax_coeffs.py: max relative error 1.1e-12), 2^k spliced into the
+// exponent field. exp(x < -708) returns 0 (the true value is < 2.3e-308).
+// ~13 FP64 instructions, no branches beyond the underflow select. 1e-12 is
+// the precision every use needs: the exponentials are soft
+// indicator / weight / log-sum-exp terms whose relative error moves witness
+// points and fields by <= ~tau x 1e-12 (the witness budget is ~1e-10 absolute);
+// the libdevice version carries 1-ulp accuracy and full special-case handling
+// the arguments never need.
 // FP64 literals live in the constant bank so DFMA/DMUL read them as c[][]
 // operands (an immediate double costs two UMOVs + a uniform-pipe dependency).
 struct MathConsts {
-  double exp_c[11];  // degree 10 .. 0 (Horner order)
-  double log_c[8];   // atanh(s)/s = Q(s^2), degree 7 .. 0 in s^2
+  double exp_c[9];  // degree 8 .. 0 (Horner order)
+  double log_c[6];  // atanh(s)/s = Q(s^2), degree 5 .. 0 in s^2
   double log2e, ln2_hi, ln2_lo, ln2, sqrt2, floor30, floor20;
 };
 static __constant__ MathConsts kMC = {
-    {2.7626357241447223e-07, 2.764018079620985e-06, 2.4801504346997686e-05, 0.00019841170270440067,
-     0.0013888888932488599, 0.008333333385667782, 0.04166666666657314, 0.16666666666554406,
-     0.5000000000000006, 1.0000000000000067, 1.0},
-    {0.07404855180327638, 0.07656264074182095, 0.09091815840114664, 0.11111098528363024,
-     0.1428571438032084, 0.1999999999965117, 0.33333333333333826, 1.0},
+    {2.4876164022625967e-05, 0.00019915866926782682, 0.0013888821677630362, 0.008333266097949614,
+     0.041666666890957, 0.16666666891045775, 0.49999999999797934, 0.9999999999797852, 1.0},
+    {0.09804047819876527, 0.11087124955038745, 0.14286083072937864, 0.1999999744591619,
+     0.3333333333978963, 0.9999999999999736},
     1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
     6.93147180559945309417e-01, 1.4142135623730951, 1e-30, 1e-20};
 
@@ -85,7 +87,7 @@ __device__ __forceinline__ double exp_d(double x) {
   r = fma(-k, kMC.ln2_lo, r);
   double p = kMC.exp_c[0];
 #pragma unroll
-  for (int i = 1; i < 11; ++i) p = fma(p, r, kMC.exp_c[i]);
+  for (int i = 1; i < 9; ++i) p = fma(p, r, kMC.exp_c[i]);
   const int ki = (int)k;
   const double s = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   return x < -708.0 ? 0.0 : s;
@@ -93,7 +95,7 @@ __device__ __forceinline__ double exp_d(double x) {
 
 // log(v) in FP64 for finite v > 0: v = 2^e m, m in [sqrt(1/2), sqrt(2)),
 // log m = 2 atanh(s) = 2 s Q(s^2), s = (m - 1)/(m + 1), |s| <= 0.1716, Q a
-// degree-7 near-minimax polynomial (max relative error 3e-18).
+// degree-5 near-minimax polynomial in s^2 (max relative error 2.7e-14).
 __device__ __forceinline__ double log_d(double v) {
   int hi = __double2hiint(v);
   int e = ((hi >> 20) & 0x7ff) - 1023;
@@ -107,7 +109,7 @@ __device__ __forceinline__ double log_d(double v) {
   const double s2 = s * s;
   double p = kMC.log_c[0];
 #pragma unroll
-  for (int i = 1; i < 8; ++i) p = fma(p, s2, kMC.log_c[i]);
+  for (int i = 1; i < 6; ++i) p = fma(p, s2, kMC.log_c[i]);
   return fma((double)e, kMC.ln2, 2.0 * s * p);
 }
 

@@ -31,14 +31,14 @@ def max_rel_err(c, f, a, b, grid=4000):
 
 
 ln2h = mp.log(2) / 2
-for deg in (9, 10, 11):
+for deg in (7, 8, 9, 10):
     c = cheb_fit(mp.exp, -ln2h, ln2h, deg)
     print(f"exp deg {deg}: max rel err {mp.nstr(max_rel_err(c, mp.exp, -ln2h, ln2h), 3)}")
     print("  coeffs (high->low):", ", ".join(repr(float(x)) for x in reversed(c)))
 
 zmax = ((mp.sqrt(2) - 1) / (mp.sqrt(2) + 1)) ** 2
 Q = lambda z: mp.mpf(1) if z == 0 else mp.atanh(mp.sqrt(z)) / mp.sqrt(z)
-for deg in (6, 7, 8):
+for deg in (4, 5, 6, 7):
     c = cheb_fit(Q, mp.mpf(0), zmax, deg)
     print(f"log Q deg {deg}: max rel err {mp.nstr(max_rel_err(c, Q, mp.mpf(0), zmax), 3)}")
     print("  coeffs (high->low):", ", ".join(repr(float(x)) for x in reversed(c)))
