@@ -122,8 +122,11 @@ __device__ __forceinline__ double pv(float x) { return x; }
 // witness.cuh): SFU forms. Their arguments are FP64 values rounded to FP32,
 // which already costs |x| 6e-8 relative in exp; ex2/lg2/rcp.approx stay within
 // that budget (alpha error <= tau_clip * 1e-6 on the witness points).
-__device__ __forceinline__ float exp_d(float x) { return __expf(x); }
-__device__ __forceinline__ float log_d(float x) { return __logf(x); }
+// (ftz forms without the denormal range fix-ups of __expf / __logf: the
+// arguments are <= 0 -- a result below 2^-126 is a weight that does not count
+// -- or quotients in (1/2, 2))
+__device__ __forceinline__ float exp_d(float x) { return ex2f(x * 1.44269504088896341f); }
+__device__ __forceinline__ float log_d(float x) { return lg2f(x) * 0.693147180559945309f; }
 __device__ __forceinline__ float rcp_d(float x) { return rcpf(x); }
 
 // stable_sigmoid (smooth_ops.hpp:22-35), FP64: both arms evaluate the same

@@ -48,13 +48,30 @@ __device__ __forceinline__ I to_ind(const T& x) {
   else return x;
 }
 
+// max(x, 0) as one compare + selects for double (fmax's NaN handling costs
+// five instructions; the two agree for every non-NaN x and give 0 for NaN).
+template <class T>
+__device__ __forceinline__ T pos0(const T& x) {
+  if constexpr (std::is_same_v<T, double>) return x > 0.0 ? x : 0.0;
+  else return fmax(x, T(0.0));
+}
+
+// Compile-time operator mode of the witness solvers: kH < 0 reads the
+// config's hard_ops flag at run time, 0 / 1 fix soft / hard (the K6 kernels
+// dispatch on the flag once, so the other mode's code is not issued).
+template <int kH>
+__device__ __forceinline__ bool hard_mode(const DevCfg& c) {
+  if constexpr (kH < 0) return c.hard_ops != 0;
+  else return kH == 1;
+}
+
 // clip01 (witness.hpp:45-52): clip_s(x, 0, 1, tau) = softplus(x) - softplus(x - 1)
 // (smooth_ops.hpp:66-89) = [max(x,0) - max(x-1,0)] + tau log1p((a - b) / (1 + b)),
 // a = exp(-|x|/tau), b = exp(-|x-1|/tau); hard: clamp.
-template <class T, class I = T>
+template <class T, class I = T, int kH = -1>
 __device__ __forceinline__ T clip01(const T& x, const DevCfg& c) {
   if constexpr (is_dual<T>::value) {
-    if (!c.hard_ops) {  // Dual: the double formula + its analytic derivative
+    if (!hard_mode<kH>(c)) {  // Dual: the double formula + its analytic derivative
       const double xv = x.v;  // d clip / dx = sigma(x/tau) - sigma((x-1)/tau)
       const double a = exp_d(-fabs(xv) * c.inv_tau_clip);
       const double b = partner_exp(xv, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
@@ -64,14 +81,14 @@ __device__ __forceinline__ T clip01(const T& x, const DevCfg& c) {
       return T::chain((fmax(xv, 0.0) - fmax(xv - 1.0, 0.0)) + corr, s1 - s2, x);
     }
   }
-  if (c.hard_ops) return fmin(fmax(x, T(0.0)), T(1.0));
+  if (hard_mode<kH>(c)) return fmin(fmax(x, T(0.0)), T(1.0));
   const I xi = to_ind<I>(x);
   const I a = exp_d(-fabs(xi) * I(c.inv_tau_clip));
   const I b = partner_exp(xi, a, c.clip_C, c.inv_clip_C, c.inv_tau_clip, c.pair_exp);
   // tau (log1p(a) - log1p(b)) = tau log((1 + a) / (1 + b)); the quotient is
   // formed in I (FP64 on the manifold path: absolute error ~1e-16, scaled by tau)
   const I corr = I(c.tau_clip) * log_d((I(1.0) + a) * rcp_d(I(1.0) + b));
-  return (fmax(x, T(0.0)) - fmax(x - 1.0, T(0.0))) + T(corr);
+  return (pos0(x) - pos0(x - 1.0)) + T(corr);
 }
 
 // within01 (witness.hpp:54-61): gamma = sigma(x/tau) sigma((1-x)/tau) and its
@@ -195,7 +212,7 @@ using QpSol = QpSolT<double>;
 // kIeee: IEEE quotients instead of the one-Newton reciprocals (the unconstrained
 // solve of a near-parallel pair at lambda = 1e-6 amplifies a 1e-12 quotient
 // error ~1e4-fold; the reference-precision K6 solver opts in).
-template <class T, class I = T, bool kIeee = false>
+template <class T, class I = T, bool kIeee = false, int kH = -1>
 __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, const T& q3, const T& c1,
                                                     const T& c2, const DevCfg& c) {
   T q2_over_q1, q2_over_q3, c1_over_q1, c2_over_q3, a1u, a2u;
@@ -215,10 +232,10 @@ __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, co
     a1u = div_d(q2 * c2_over_q3 - c1, q1 - q2 * q2_over_q3);
     a2u = div_d(q2 * c1_over_q1 - c2, q3 - q2 * q2_over_q1);
   }
-  const T a1_1_a2 = clip01<T, I>(-(q2_over_q3 + c2_over_q3), c);
-  const T a1_0_a2 = clip01<T, I>(-c2_over_q3, c);
-  const T a2_1_a1 = clip01<T, I>(-(q2_over_q1 + c1_over_q1), c);
-  const T a2_0_a1 = clip01<T, I>(-c1_over_q1, c);
+  const T a1_1_a2 = clip01<T, I, kH>(-(q2_over_q3 + c2_over_q3), c);
+  const T a1_0_a2 = clip01<T, I, kH>(-c2_over_q3, c);
+  const T a2_1_a1 = clip01<T, I, kH>(-(q2_over_q1 + c1_over_q1), c);
+  const T a2_0_a1 = clip01<T, I, kH>(-c1_over_q1, c);
   const T cost[4] = {
       0.5 * (q1 + 2.0 * q2 * a1_1_a2 + q3 * a1_1_a2 * a1_1_a2) + c1 + c2 * a1_1_a2,
       0.5 * q3 * a1_0_a2 * a1_0_a2 + c2 * a1_0_a2,
@@ -226,14 +243,14 @@ __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, co
       0.5 * q1 * a2_0_a1 * a2_0_a1 + c1 * a2_0_a1,
   };
   I wi[4];
-  const int best = pick_min<4>(cost, wi, c.inv_tau_min, c.hard_ops);
+  const int best = pick_min<4>(cost, wi, c.inv_tau_min, hard_mode<kH>(c));
   const T w[4] = {T(wi[0]), T(wi[1]), T(wi[2]), T(wi[3])};
   // constrained = sum_i w_i cand_i (witness.hpp:101-113)
   const T k0 = w[0] + w[2] * a2_1_a1 + w[3] * a2_0_a1;
   const T k1 = w[0] * a1_1_a2 + w[1] * a1_0_a2 + w[2];
   I g1, o1, g2, o2, in, out;
-  within01<T, I>(a1u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g1, &o1);
-  within01<T, I>(a2u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &g2, &o2);
+  within01<T, I>(a1u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, hard_mode<kH>(c), &g1, &o1);
+  within01<T, I>(a2u, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, hard_mode<kH>(c), &g2, &o2);
   within_and(g1, o1, g2, o2, &in, &out);
   QpSolT<T> s;
   s.a1 = a1u * T(in) + k0 * T(out);
@@ -245,13 +262,13 @@ __device__ __forceinline__ QpSolT<T> solve_box_qp_2(const T& q1, const T& q2, co
 
 // ee_witness Q/c construction (witness.hpp:137-158) for edges given in a
 // common frame: Q = A^T A + lambda I, c = b^T A - lambda/2, A = [t1, -t2].
-template <class T = double, class I = T, bool kIeee = false>
+template <class T = double, class I = T, bool kIeee = false, int kH = -1>
 __device__ __forceinline__ QpSolT<T> ee_qp(vec3<T> e1a, vec3<T> e1b, vec3<T> e2a, vec3<T> e2b,
                                            const DevCfg& c) {
   const vec3<T> t1 = e1b - e1a;
   const vec3<T> t2n = e2a - e2b;
   const vec3<T> b = e1a - e2a;
-  return solve_box_qp_2<T, I, kIeee>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
+  return solve_box_qp_2<T, I, kIeee, kH>(ddot(t1, t1) + c.lambda, ddot(t1, t2n), ddot(t2n, t2n) + c.lambda,
                               ddot(b, t1) - 0.5 * c.lambda, ddot(b, t2n) - 0.5 * c.lambda, c);
 }
 
@@ -260,7 +277,7 @@ __device__ __forceinline__ QpSolT<T> ee_qp(vec3<T> e1a, vec3<T> e1b, vec3<T> e2a
 // inside test, blend. Returns the closest point; label as above over 3.
 // Geometry FP64 (normalisations by the one-Newton rsqrt, 1e-12 relative);
 // indicators in I.
-template <class I = double>
+template <class I = double, int kH = -1>
 __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1, double3 t2,
                                               const DevCfg& c, int* label) {
   const double3 d10 = t1 - t0, d21 = t2 - t1, d20 = t2 - t0;
@@ -274,11 +291,11 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   // softplus(s) - softplus(s - len) = [max(s,0) - max(s-len,0)]
   //   + tau log((1 + exp(-|s|/tau)) / (1 + exp(-|s-len|/tau)))
   auto clip_len = [&](double s, double len) -> double {
-    if (c.hard_ops) return fmin(fmax(s, 0.0), len);
+    if (hard_mode<kH>(c)) return fmin(fmax(s, 0.0), len);
     const I a = exp_d(to_ind<I>(-fabs(s) * c.inv_tau_clip));
     const I b = exp_d(to_ind<I>(-fabs(s - len) * c.inv_tau_clip));
     const I corr = I(c.tau_clip) * log_d((I(1.0) + a) * rcp_d(I(1.0) + b));
-    return (fmax(s, 0.0) - fmax(s - len, 0.0)) + (double)corr;
+    return (pos0(s) - pos0(s - len)) + (double)corr;
   };
   const double3 on1 = t0 + u10 * clip_len(ddot(dv0, u10), len10);
   const double3 on2 = t1 + u21 * clip_len(ddot(dv1, u21), len21);
@@ -286,7 +303,7 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   const double3 q1 = v - on1, q2 = v - on2, q3 = v - on3;
   const double cost[3] = {sqrt(ddot(q1, q1)), sqrt(ddot(q2, q2)), sqrt(ddot(q3, q3))};
   I w[3];
-  const int best = pick_min<3>(cost, w, c.inv_tau_min, c.hard_ops);
+  const int best = pick_min<3>(cost, w, c.inv_tau_min, hard_mode<kH>(c));
   const double3 cons = on1 * (double)w[0] + on2 * (double)w[1] + on3 * (double)w[2];
   const double3 n_raw = d3(d10.y * d20.z - d10.z * d20.y, d10.z * d20.x - d10.x * d20.z,
                            d10.x * d20.y - d10.y * d20.x);
@@ -301,9 +318,9 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   const double bu = ddot(cross(dvp0, d20), n) * rn;
   const double bw = 1.0 - bu - bv;
   I gu, ou, gv, ov, gw, ow, guv, ouv, in, out;
-  within01<double, I>(bu, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gu, &ou);
-  within01<double, I>(bv, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gv, &ov);
-  within01<double, I>(bw, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, c.hard_ops, &gw, &ow);
+  within01<double, I>(bu, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, hard_mode<kH>(c), &gu, &ou);
+  within01<double, I>(bv, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, hard_mode<kH>(c), &gv, &ov);
+  within01<double, I>(bw, c.inv_tau_comp, c.comp_C, c.inv_comp_C, c.pair_exp, hard_mode<kH>(c), &gw, &ow);
   within_and(gu, ou, gv, ov, &guv, &ouv);
   within_and(guv, ouv, gw, ow, &in, &out);
   if (label) *label = best | ((pv(in) >= 0.5) << 2);

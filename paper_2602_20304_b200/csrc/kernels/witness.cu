@@ -27,10 +27,10 @@ __device__ __forceinline__ double3 load3(const T* p) {
 struct EeSolve {
   using Out = float;
   static constexpr int kOut = 6;
-  template <typename T>
+  template <int kH, typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
     const double3 e1a = load3(q), e1b = load3(q + 3), e2a = load3(q + 6), e2b = load3(q + 9);
-    const QpSol s = ee_qp<double, float>(e1a, e1b, e2a, e2b, p.cfg);  // FP32 indicators (witness.cuh)
+    const QpSol s = ee_qp<double, float, false, kH>(e1a, e1b, e2a, e2b, p.cfg);  // FP32 indicators (witness.cuh)
     const double3 p1 = e1a + (e1b - e1a) * s.a1;  // edge_point (witness.hpp:130-133)
     const double3 p2 = e2a + (e2b - e2a) * s.a2;
     o[0] = (float)p1.x; o[1] = (float)p1.y; o[2] = (float)p1.z;
@@ -51,10 +51,10 @@ struct EeSolve {
 struct EeSolve64 {
   using Out = double;
   static constexpr int kOut = 6;
-  template <typename T>
+  template <int kH, typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, double* o) {
     const double3 e1a = load3(q), e1b = load3(q + 3), e2a = load3(q + 6), e2b = load3(q + 9);
-    const QpSol s = ee_qp<double, double, true>(e1a, e1b, e2a, e2b, p.cfg);
+    const QpSol s = ee_qp<double, double, true, kH>(e1a, e1b, e2a, e2b, p.cfg);
     const double3 p1 = e1a + (e1b - e1a) * s.a1;
     const double3 p2 = e2a + (e2b - e2a) * s.a2;
     o[0] = p1.x; o[1] = p1.y; o[2] = p1.z;
@@ -72,10 +72,10 @@ struct EeSolve64 {
 struct VfSolve {
   using Out = float;
   static constexpr int kOut = 3;
-  template <typename T>
+  template <int kH, typename T>
   __device__ __forceinline__ static void run(const WitnessParams& p, const T* q, int64_t idx, float* o) {
     int label;
-    const double3 r = vf_witness<float>(load3(q), load3(q + 3), load3(q + 6), load3(q + 9), p.cfg, &label);
+    const double3 r = vf_witness<float, kH>(load3(q), load3(q + 3), load3(q + 6), load3(q + 9), p.cfg, &label);
     o[0] = (float)r.x; o[1] = (float)r.y; o[2] = (float)r.z;
     if (p.labels) p.labels[idx] = label;
   }
@@ -87,7 +87,8 @@ struct VfSolve {
 // Outputs are staged in shared memory so the global stores are full lines.
 constexpr int kStages = 2;  // measured: deeper rings cost resident CTAs (4 stages: 16 warps/SM, -40%)
 
-template <typename T, class Solve>
+// kH: the solver's operator mode (hard_ops) fixed at compile time.
+template <typename T, class Solve, int kH>
 __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_constant__ WitnessParams p) {
   constexpr int W = Solve::kOut;
   using Out = typename Solve::Out;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
     }
     const int count = (int)(p.n - first < kWitnessThreads ? p.n - first : kWitnessThreads);
     mbar_wait(&bar[b], (it / kStages) & 1);
-    if (tid < count) Solve::run(p, tile[b] + 12 * tid, first + tid, otile + W * tid);
+    if (tid < count) Solve::template run<kH>(p, tile[b] + 12 * tid, first + tid, otile + W * tid);
     __syncthreads();
     Out* __restrict__ out = static_cast<Out*>(p.out_any) + first * W;
     for (int k = tid; k < count * W; k += kWitnessThreads) out[k] = otile[k];
@@ -133,24 +134,29 @@ __global__ void __launch_bounds__(kWitnessThreads) witness_kernel(const __grid_c
   }
 }
 
-template <typename T, class Solve>
-int launch_witness(const WitnessParams& p, cudaStream_t s) {
+template <typename T, class Solve, int kH>
+int launch_witness_mode(const WitnessParams& p, cudaStream_t s) {
   constexpr size_t smem = sizeof(T) * kStages * kWitnessThreads * 12 +
                           sizeof(typename Solve::Out) * kWitnessThreads * Solve::kOut;
   static PerDeviceInt cap_cache;  // persistent grid: SMs x resident CTAs, per device
   const int cap = cap_cache.get([] {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
-    cudaFuncSetAttribute(witness_kernel<T, Solve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(witness_kernel<T, Solve, kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, witness_kernel<T, Solve>, kWitnessThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, witness_kernel<T, Solve, kH>, kWitnessThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 1);
   });
   const int64_t need = (p.n + kWitnessThreads - 1) / kWitnessThreads;
   const int grid = (int)(need < cap ? (need > 0 ? need : 1) : cap);
   note_launch();
-  witness_kernel<T, Solve><<<grid, kWitnessThreads, smem, s>>>(p);
+  witness_kernel<T, Solve, kH><<<grid, kWitnessThreads, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+template <typename T, class Solve>
+int launch_witness(const WitnessParams& p, cudaStream_t s) {
+  return p.cfg.hard_ops ? launch_witness_mode<T, Solve, 1>(p, s) : launch_witness_mode<T, Solve, 0>(p, s);
 }
 
 }  // namespace
