@@ -225,11 +225,12 @@ __device__ __forceinline__ double3 trace(const DevSdf& sdf, double3 p, const Dev
 
 // E1: witness QP of pair (k, l) (ee_witness, witness.hpp:137-158; edges in the
 // world frame), witness points written in their own body frames.
+template <int kH = -1>
 __device__ __forceinline__ void ee_stage_qp(const ManifoldParams& p, const EnvView& ev, int k, int l,
                                             double* rec) {
   const double* s1 = ev.eslot(k);
   const double* s2 = ev.eslot(p.m1 + l);
-  const QpSol w = ee_qp(d3(s1[0], s1[1], s1[2]), d3(s1[3], s1[4], s1[5]), d3(s2[0], s2[1], s2[2]),
+  const QpSol w = ee_qp<double, double, false, kH>(d3(s1[0], s1[1], s1[2]), d3(s1[3], s1[4], s1[5]), d3(s2[0], s2[1], s2[2]),
                         d3(s2[3], s2[4], s2[5]), p.cfg);
   // edge_point (witness.hpp:130-133) on the body-frame endpoints
   rec[0] = s1[6] + (s1[9] - s1[6]) * w.a1;
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     fdivmod(i, p.div_m2, k, l);
     const EnvView ev = env(e);
     double* r = ev.pair(i);
-    ee_stage_qp(p, ev, k, l, r);
+    ee_stage_qp(p, ev, k, l, r);  // (a soft / hard split of this call spills at 56 registers)
     // both sides inline (measured: a shared code copy looping over the side
     // reads the side's SDF parameters with per-thread constant loads; +2%)
     ee_stage_side<K1, K2>(p, ev, 0, r);
