@@ -27,4 +27,13 @@ ncu --set full --clock-control none --import-source on -k regex:witness_kernel -
     -o gpurun_out/${T}_ee python tools/profile_run.py ee 4194304 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'compact' --launch-skip 2 --launch-count 2 \
     -o gpurun_out/${T}_compact python tools/profile_run.py compact-masked > /dev/null 2>&1
+# summaries on the box (gpurun copies back <= 64 MiB): reports -> text, reports removed
+for n in manifold mixed jvp ee compact; do
+  if [ -f gpurun_out/${T}_${n}.ncu-rep ]; then
+    { python tools/ncu_summary.py gpurun_out/${T}_${n}.ncu-rep 30; echo; echo "--- executed SASS mix ---";
+      python tools/sass_mix.py gpurun_out/${T}_${n}.ncu-rep 25; echo; echo "--- instructions per barrier segment ---";
+      python tools/sass_phases.py gpurun_out/${T}_${n}.ncu-rep; } > gpurun_out/${T}_ncu_${n}.txt 2>&1
+    rm -f gpurun_out/${T}_${n}.ncu-rep
+  fi
+done
 echo done

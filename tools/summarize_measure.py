@@ -93,7 +93,11 @@ def main():
     # full-capture summaries
     for name in ("manifold", "mixed", "jvp", "ee", "compact"):
         rep = os.path.join(G, f"{tag}_{name}.ncu-rep")
+        txt = os.path.join(G, f"{tag}_ncu_{name}.txt")
         if not os.path.exists(rep):
+            if os.path.exists(txt):  # summarised on the GPU box (final_measure_r02.sh)
+                shutil.copy(txt, os.path.join(P, f"{rnd}_ncu_{name}.txt"))
+                print("wrote", os.path.join(P, f"{rnd}_ncu_{name}.txt"))
             continue
         a = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, "30"],
                            capture_output=True, text=True).stdout
