@@ -11,6 +11,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum \
     --clock-control none --csv -k regex:'manifold_kernel|vs_kernel' --launch-skip 4 --launch-count 2 \
     --log-file gpurun_out/${T}_fp64.csv python tools/profile_run.py manifold > gpurun_out/${T}_ncu_fp64.log 2>&1
+ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum \
+    --clock-control none --csv -k regex:manifold_jvp_kernel --launch-skip 10 --launch-count 10 \
+    --log-file gpurun_out/${T}_jvp_fp64.csv python tools/profile_run.py drop 32768 > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
     -k regex:witness_kernel --launch-skip 2 --launch-count 1 --log-file gpurun_out/${T}_ee_dram.csv \
     python tools/profile_run.py ee 4194304 > /dev/null 2>&1

@@ -81,6 +81,26 @@ def main():
                "dram_bytes_per_launch_per_env": (rd + wr) / n_env, "algorithmic_bytes_per_env": 9776,
                "source": f"ncu --metrics pass (tools/final_measure_r02.sh, {rnd})"},
               open(os.path.join(P, "manifold_dram_bytes.json"), "w"), indent=1)
+    # FP64 work of the JVP kernels (config D: one step = 10 pair launches of 32,768 envs)
+    jp = os.path.join(G, f"{tag}_jvp_fp64.csv")
+    if os.path.exists(jp):
+        per = collections.defaultdict(dict)
+        for r in ncu_csv(jp):
+            per[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+        units = 10 * 32768
+        dfma = sum(v.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0) for v in per.values())
+        dmul = sum(v.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0) for v in per.values())
+        dadd = sum(v.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0) for v in per.values())
+        pipe = [v.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") for v in per.values()]
+        json.dump({"kernels": f"manifold_jvp_kernel, the 10 pair launches of one config D step (32,768 envs), "
+                              f"ncu --metrics pass (tools/final_measure_r02.sh, {rnd})",
+                   "fp64_flop_per_unit": (2 * dfma + dmul + dadd) / units, "dfma_per_unit": dfma / units,
+                   "dmul_per_unit": dmul / units, "dadd_per_unit": dadd / units,
+                   "ncu_fp64_pipe_active_pct_mean": sum(pipe) / len(pipe) if pipe else None,
+                   "kernel_ns_sum": sum(v.get("gpu__time_duration.sum", 0) for v in per.values()),
+                   "unit": "pair manifold (one env of one body pair) with its 12 pose tangents"},
+                  open(os.path.join(P, "jvp_fp64_ops.json"), "w"), indent=1)
+        print("wrote jvp_fp64_ops.json")
     for kind in ("ee", "vf"):
         rows = ncu_csv(os.path.join(G, f"{tag}_{kind}_dram.csv"))
         m = {r["Metric Name"]: float(r["Metric Value"].replace(",", "")) for r in rows}
