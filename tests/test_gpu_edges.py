@@ -116,3 +116,39 @@ def test_config_e_size_batch(cuda):
     assert bool(torch.isfinite(big["mean_dist"]).all())
     del big
     torch.cuda.empty_cache()
+
+
+def _topk_parity(ws, n, what):
+    (a1, a2), (o1, o2) = surfaces(ws)
+    p1, p2 = ws.poses(n)
+    ref = Oracle.manifold_batch(o1, o2, p1, p2, SmoothingConfig())
+    r = api.generate_manifold_batch(a1, a2, torch.as_tensor(p1, device="cuda"),
+                                    torch.as_tensor(p2, device="cuda"), SmoothingConfig(), want_src=True)
+    torch.cuda.synchronize()
+    assert_parity(r["contacts"].cpu().numpy(), ref["contacts"], what=what)
+    assert np.array_equal(r["src"].cpu().numpy(), ref["meta"][..., 2:]), f"{what}: provenance"
+
+
+@pytest.mark.parametrize("subdiv,vk,ek", [(6, 16, 8), (6, 3, 40), (3, 50, 3)])
+def test_soft_topk_both_order_schemes(cuda, subdiv, vk, ek):
+    """Soft top-K over large candidate sets: a finely subdivided plate (218
+    vertices, 432 edges: above the warp extraction's 128, so the rank count
+    orders them) and small / large K against the primitive's sets (warp
+    extraction when K x 104 < D^2), vs the C oracle incl. provenance."""
+    ws = W.mixed_bucket("rounded_box", 64)
+    ws.bodies[0].mesh.subdivisions = subdiv
+    ws.bodies[0].vertex_topk, ws.bodies[0].edge_topk = vk, ek
+    ws.bodies[1].vertex_topk, ws.bodies[1].edge_topk = min(vk, 30), min(ek, 60)
+    _topk_parity(ws, 64, f"top-K subdiv {subdiv} K {vk}/{ek}")
+
+
+def test_soft_topk_exact_ties(cuda):
+    """Unjittered, axis-aligned box on a subdivided plate: many candidate
+    scores are exactly equal, so the order's index tie-break and the first-
+    argmax provenance are exercised (both order schemes)."""
+    ws = W.box_on_plane(8)
+    ws.jitter = 0.0
+    ws.bodies[1].mesh.subdivisions = 2
+    for b in ws.bodies:
+        b.vertex_topk, b.edge_topk = 5, 7
+    _topk_parity(ws, 8, "top-K exact ties")
