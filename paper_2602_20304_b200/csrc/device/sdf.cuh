@@ -159,7 +159,9 @@ __device__ __forceinline__ Dual<N> one_minus_pow(const Dual<N>& f, double p4, in
 // compile in the exponents (kSqE01); 0 reads them from the descriptor.
 template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0, class T = double>
 __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
-  if (q.has_frame) p = mul_Rt(q.R, p - mk3<T>(q.t[0], q.t[1], q.t[2]));  // apply_inverse
+  // apply_inverse; has_frame 2 = translation only (R = I exactly: the same result)
+  if (q.has_frame == 1) p = mul_Rt(q.R, p - mk3<T>(q.t[0], q.t[1], q.t[2]));
+  else if (q.has_frame == 2) p = p - mk3<T>(q.t[0], q.t[1], q.t[2]);
   const T xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
   const T x2 = fma(xn, xn, T(kMC.floor30)), y2 = fma(yn, yn, T(kMC.floor30)), z2 = fma(zn, zn, T(kMC.floor30));
   T A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
@@ -189,7 +191,7 @@ __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
       T F;
       out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);
     }
-    out.g = q.has_frame ? mul_R(q.R, df) : df;
+    out.g = q.has_frame == 1 ? mul_R(q.R, df) : df;
     return out;
   }
   // kGrad: grad phi = diag(1/axes) (-p4 (F/f) grad_n f - phi x~ / r) / r
@@ -206,7 +208,7 @@ __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
   const T kxy = k * cxy, kz = k * q.c_z;
   const vec3<T> gl = mk3<T>(sx * (xn * fma(kxy, Am1, -h)), sy * (yn * fma(kxy, Bm1, -h)),
                             sz * (zn * fma(kz, Czm1, -h)));
-  out.g = q.has_frame ? mul_R(q.R, gl) : gl;
+  out.g = q.has_frame == 1 ? mul_R(q.R, gl) : gl;
   return out;
 }
 

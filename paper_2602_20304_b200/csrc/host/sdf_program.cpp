@@ -230,9 +230,12 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       q.n2 = exact_int(p2);
       q.n3 = exact_int(p3);
       q.n4 = exact_int(-1.0 / p4);
-      bool ident = true;
+      bool ident = true, no_rot = true;
       for (int k = 0; k < 6; ++k) ident = ident && d.pose[k] == 0.0;
-      q.has_frame = ident ? 0 : 1;
+      for (int k = 3; k < 6; ++k) no_rot = no_rot && d.pose[k] == 0.0;
+      // 2: translation only -- se3_exp of a zero rotation is I exactly, so
+      // R^T (p - t) = p - t bit for bit (the capsule's caps)
+      q.has_frame = ident ? 0 : (no_rot ? 2 : 1);
       for (int k = 0; k < 9; ++k) q.R[k] = d.R[k];
       for (int k = 0; k < 3; ++k) q.t[k] = d.t[k];
     } else if (d.op == CMGB_SDF_CONVEX_POLYHEDRON) {
