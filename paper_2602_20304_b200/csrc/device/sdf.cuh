@@ -317,33 +317,37 @@ __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   constexpr int FL = FL_IN == kNormalOnly ? kNormalSource : FL_IN;
   constexpr bool kWantG = FL != kValue;
   if constexpr (KIND == kCapsule) {
-    // union of three compile-time superquadric leaves, the interpreter's union
-    // arithmetic in the same order (bit-identical), nothing on a stack
+    // union of three compile-time superquadric leaves (sdf.hpp smooth union:
+    // m - tau log sum exp((m - v_i) / tau), m = min v_i, gradient blended by the
+    // same weights), accumulated online so only one leaf's result is live at a
+    // time (the three-leaf form spills at the 64-register budget): the running
+    // minimum m with sum S = sum exp((m - v_i) / tau) and blended gradient G;
+    // a new leaf below m rescales both by exp((v - m) / tau). Two exponentials
+    // (the reference's exp(0) of the minimum is 1 exactly) instead of three.
     constexpr SqExpTuple a = sq_exps(kSqCyl), b = sq_exps(kSqEll);
-    const SdfOutT<T> r0 = sq_leaf<FL, a.n1, a.n2, a.n3, a.n4, T>(s.nodes[0].sq, p);
-    const SdfOutT<T> r1 = sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[1].sq, p);
-    const SdfOutT<T> r2 = sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[2].sq, p);
     const DevNode& un = s.nodes[3];
-    T m = r0.v;
-    m = fmin(m, r1.v);
-    m = fmin(m, r2.v);
-    const T e0 = exp_d((m - r0.v) * un.inv_tau_d);
-    const T e1 = exp_d((m - r1.v) * un.inv_tau_d);
-    const T e2 = exp_d((m - r2.v) * un.inv_tau_d);
-    T acc = 0.0;
-    acc += e0;
-    acc += e1;
-    acc += e2;
+    const SdfOutT<T> r0 = sq_leaf<FL, a.n1, a.n2, a.n3, a.n4, T>(s.nodes[0].sq, p);
+    T m = r0.v, acc = 1.0;
+    vec3<T> g = r0.g;
+    auto add = [&](const SdfOutT<T>& r) {
+      const T d = r.v - m;
+      const bool below = pv(d) < 0.0;
+      const T e = exp_d(-fabs(d) * un.inv_tau_d);  // exp((m - v) / tau) or exp((v - m) / tau)
+      if (below) {  // new minimum: rescale the running sums
+        acc = fma(acc, e, T(1.0));
+        if constexpr (kWantG) g = dscale(g, e) + r.g;
+        m = r.v;
+      } else {
+        acc += e;
+        if constexpr (kWantG) g = g + dscale(r.g, e);
+      }
+    };
+    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[1].sq, p));
+    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[2].sq, p));
     SdfOutT<T> out;
     out.v = m - un.tau_d * log_d(acc);
     out.g = mk3<T>(0.0, 0.0, 0.0);
-    if constexpr (kWantG) {
-      vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
-      g = g + dscale(r0.g, e0);
-      g = g + dscale(r1.g, e1);
-      g = g + dscale(r2.g, e2);
-      out.g = dscale(g, rcp_d(acc));
-    }
+    if constexpr (kWantG) out.g = dscale(g, rcp_d(acc));
     return out;
   }
   if constexpr (KIND == kSingleCp) return cp_leaf<FL, T>(s.nodes[0], s.pool, p);
