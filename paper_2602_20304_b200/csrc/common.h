@@ -64,7 +64,7 @@ struct DevSq {
   double R[9], t[3];     // body_from_prim (sdf.cpp:9)
   double p4;             // -e1/2
   int32_t n1, n2, n3;    // integer exponents (1..64) or 0
-  int32_t has_frame;     // 0 identity pose, 1 rotated, 2 translation only
+  int32_t has_frame;     // 0 identity pose, 1 rotated, 2 translation only (R = I exactly)
   int32_t n4;            // -1/p4 = 2/e1 when an exact integer (1..64): f^p4 = 1 / f^(1/n4)
 };
 

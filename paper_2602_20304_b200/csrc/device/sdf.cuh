@@ -115,6 +115,12 @@ template <int N4 = 0>
 __device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, double* F,
                                                 double* inv_f = nullptr) {
   const int n = N4 > 0 ? N4 : n_rt;
+  if constexpr (N4 == 2) {  // eps1 = 1 (ellipsoids): F = f^(-1/2) is one Newton-refined reciprocal square root
+    const double Fv = rsqrt_d(f);
+    *F = Fv;
+    if (inv_f) *inv_f = Fv * Fv;
+    return 1.0 - Fv;
+  }
   if (n > 0) {
     // F = f^(-1/n). Seed F0 = 2^(-log2(f)/n): log2 from the exponent bits +
     // SFU lg2 of the mantissa, 2^q spliced from bits (any normal f). One
@@ -157,11 +163,12 @@ __device__ __forceinline__ Dual<N> one_minus_pow(const Dual<N>& f, double p4, in
 
 // Superquadric leaf (sdf.hpp:85-108). p in the BODY frame (FP64). N1..N4 > 0
 // compile in the exponents (kSqE01); 0 reads them from the descriptor.
-template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0, class T = double>
+template <int FL, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0, class T = double, int kFrame = -1>
 __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
-  // apply_inverse; has_frame 2 = translation only (R = I exactly: the same result)
-  if (q.has_frame == 1) p = mul_Rt(q.R, p - mk3<T>(q.t[0], q.t[1], q.t[2]));
-  else if (q.has_frame == 2) p = p - mk3<T>(q.t[0], q.t[1], q.t[2]);
+  // apply_inverse; kFrame 2: the leaf is known to be translation only (R = I
+  // exactly, so p - t is the same result; the capsule's caps)
+  if constexpr (kFrame == 2) p = p - mk3<T>(q.t[0], q.t[1], q.t[2]);
+  else if (q.has_frame) p = mul_Rt(q.R, p - mk3<T>(q.t[0], q.t[1], q.t[2]));
   const T xn = p.x * q.inv_ax[0], yn = p.y * q.inv_ax[1], zn = p.z * q.inv_ax[2];
   const T x2 = fma(xn, xn, T(kMC.floor30)), y2 = fma(yn, yn, T(kMC.floor30)), z2 = fma(zn, zn, T(kMC.floor30));
   T A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
@@ -191,7 +198,7 @@ __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
       T F;
       out.v = one_minus_pow<N4>(f, q.p4, q.n4, &F) * rsqrt_d(r2);
     }
-    out.g = q.has_frame == 1 ? mul_R(q.R, df) : df;
+    out.g = (kFrame != 2 && q.has_frame) ? mul_R(q.R, df) : df;
     return out;
   }
   // kGrad: grad phi = diag(1/axes) (-p4 (F/f) grad_n f - phi x~ / r) / r
@@ -208,7 +215,7 @@ __device__ __forceinline__ SdfOutT<T> sq_leaf(const DevSq& q, vec3<T> p) {
   const T kxy = k * cxy, kz = k * q.c_z;
   const vec3<T> gl = mk3<T>(sx * (xn * fma(kxy, Am1, -h)), sy * (yn * fma(kxy, Bm1, -h)),
                             sz * (zn * fma(kz, Czm1, -h)));
-  out.g = q.has_frame == 1 ? mul_R(q.R, gl) : gl;
+  out.g = (kFrame != 2 && q.has_frame) ? mul_R(q.R, gl) : gl;
   return out;
 }
 
@@ -342,8 +349,8 @@ __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
         if constexpr (kWantG) g = g + dscale(r.g, e);
       }
     };
-    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[1].sq, p));
-    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T>(s.nodes[2].sq, p));
+    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T, 2>(s.nodes[1].sq, p));  // caps: translation only (host)
+    add(sq_leaf<FL, b.n1, b.n2, b.n3, b.n4, T, 2>(s.nodes[2].sq, p));
     SdfOutT<T> out;
     out.v = m - un.tau_d * log_d(acc);
     out.g = mk3<T>(0.0, 0.0, 0.0);

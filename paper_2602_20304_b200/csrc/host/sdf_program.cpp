@@ -272,7 +272,10 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       }
       return -1;
     };
-    if (sq_kind(0) == kSqCyl && sq_kind(1) == kSqEll && sq_kind(2) == kSqEll) s.kind = kCapsule;
+    // (the kernel evaluates the caps as translation-only leaves)
+    if (sq_kind(0) == kSqCyl && sq_kind(1) == kSqEll && sq_kind(2) == kSqEll && s.nodes[1].sq.has_frame != 1 &&
+        s.nodes[2].sq.has_frame != 1)
+      s.kind = kCapsule;
   }
   if (s.kind == kSingleCp && prog.nodes[0].count == 6) {
     // the box_planes pattern: unit normals +x, -x, +y, -y, +z, -z in this order

@@ -182,8 +182,7 @@ __device__ __forceinline__ double3 trace_step(const DevSdf& sdf, double3 p, doub
 template <int K>
 __device__ __forceinline__ double3 trace_sq(const DevSq& q, double3 p, const DevCfg& c) {
   constexpr SqExpTuple E = sq_exps(K);
-  if (q.has_frame == 1) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));
-  else if (q.has_frame == 2) p = p - d3(q.t[0], q.t[1], q.t[2]);
+  if (q.has_frame) p = mul_Rt(q.R, p - d3(q.t[0], q.t[1], q.t[2]));
   double ux = p.x * q.inv_ax[0], uy = p.y * q.inv_ax[1], uz = p.z * q.inv_ax[2];
   const double a2x = q.inv_ax[0] * q.inv_ax[0], a2y = q.inv_ax[1] * q.inv_ax[1], a2z = q.inv_ax[2] * q.inv_ax[2];
 #pragma unroll 1
@@ -209,8 +208,7 @@ __device__ __forceinline__ double3 trace_sq(const DevSq& q, double3 p, const Dev
     uz = fma(-Pz, sc, uz);
   }
   p = d3(ux * q.ax[0], uy * q.ax[1], uz * q.ax[2]);
-  if (q.has_frame == 1) p = mul_R(q.R, p) + d3(q.t[0], q.t[1], q.t[2]);
-  else if (q.has_frame == 2) p = p + d3(q.t[0], q.t[1], q.t[2]);
+  if (q.has_frame) p = mul_R(q.R, p) + d3(q.t[0], q.t[1], q.t[2]);
   return p;
 }
 

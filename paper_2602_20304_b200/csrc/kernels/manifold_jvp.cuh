@@ -296,8 +296,7 @@ struct SqHess {
 };
 
 __device__ __forceinline__ void sq_e01_hess(const DevSq& q, double3 x, SqHess& o) {
-  if (q.has_frame == 1) x = mul_Rt(q.R, x - d3(q.t[0], q.t[1], q.t[2]));
-  else if (q.has_frame == 2) x = x - d3(q.t[0], q.t[1], q.t[2]);  // translation only
+  if (q.has_frame) x = mul_Rt(q.R, x - d3(q.t[0], q.t[1], q.t[2]));
   const double u[3] = {x.x * q.inv_ax[0], x.y * q.inv_ax[1], x.z * q.inv_ax[2]};
   const double cc[3] = {q.c_xy, q.c_xy, q.c_z};
   double s[3], s8[3], fi[3], fii[3];
@@ -331,7 +330,7 @@ __device__ __forceinline__ void sq_e01_hess(const DevSq& q, double3 x, SqHess& o
   }
   double3 df = d3(q.inv_ax[0] * fi[0], q.inv_ax[1] * fi[1], q.inv_ax[2] * fi[2]);
   double3 gg = d3(g[0], g[1], g[2]);
-  if (q.has_frame == 1) {
+  if (q.has_frame) {
     double T[9], Rt[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) Rt[i] = q.R[3 * (i % 3) + i / 3];
