@@ -15,6 +15,7 @@
 #include <unordered_map>
 
 #include "host.h"
+#include "../kernels/launch_util.cuh"
 
 namespace cmgb {
 int manifold_max_threads(int k1, int k2);
@@ -248,7 +249,7 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
     S.amask = off; off = align16(off + (out->active_mask ? 4 * ((L.n_contacts + 31) / 32) : 0));
     S.bytes = off;
   };
-  const size_t kSmemMax = 200 * 1024;
+  const size_t kSmemMax = (size_t)smem_optin_per_block();  // device attribute (227 KB on B200)
   carve(true);
   p.pairs_gmem = nullptr;
   p.pair_stride = 0;
@@ -270,7 +271,7 @@ LaunchPlan plan_manifold(cmgb_surface_s* s1, cmgb_surface_s* s2, const double* p
   int epb = std::max(1, maxt / per_env);
   // shared memory per CTA such that the kernel's resident-CTA target fits the SM
   const size_t smem_cap =
-      (size_t)(216 * 1024) / manifold_min_blocks(k1, k2);
+      (size_t)(smem_per_sm() - manifold_min_blocks(k1, k2) * kSmemReservedPerCta) / manifold_min_blocks(k1, k2);
   while (epb > 1 && (size_t)epb * S.bytes > smem_cap) --epb;
   const int threads = maxt;
   p.envs_per_block = epb;
@@ -924,13 +925,13 @@ JvpParams plan_jvp(const LaunchPlan& plan, const cmgb_manifold_jvp_out* out) {
   j.o_vsrec = off; off = align16(off + nslot_v * VS);
   j.o_prec = off; off = align16(off + P * PR);
   j.bytes = std::max(off, end_topk);
-  if (j.bytes > 200 * 1024)
+  if (j.bytes > smem_optin_per_block())
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
   // E1 items: 2 sides + 1 QP per pair, 1 per V-S contact; as many envs per CTA
   // as its shared-memory budget holds (about 2 passes of items)
   const int per_unit = std::max(3 * P + nslot_v, 1);
   j.geom_bytes = align16(8 * (3 * (m.side[0].nv + m.side[1].nv) + 6 * (m.side[0].ne + m.side[1].ne)));
-  if (j.bytes + j.geom_bytes > 200 * 1024)
+  if (j.bytes + j.geom_bytes > smem_optin_per_block())
     throw Error(CMGB_ERR_UNSUPPORTED, "manifold_jvp: per-env dual working set exceeds shared memory");
   int upb = std::max(1, (2 * jvp_max_threads() + per_unit - 1) / per_unit);
   while (upb > 1 && (size_t)upb * j.bytes + j.geom_bytes > (size_t)jvp_smem_cap()) --upb;

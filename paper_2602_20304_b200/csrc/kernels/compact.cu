@@ -364,10 +364,10 @@ int launch_compact(const float* contacts, const int32_t* src, int64_t n_env, int
   const size_t stage = (size_t)p.epb * C * 32;
   static PerDeviceOnce configured;
   configured([] {
-    cudaFuncSetAttribute(compact_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    allow_max_dynamic_smem(compact_kernel<true>);
   });
   note_launch();
-  if (compact_staged() && stage <= 200 * 1024)
+  if (compact_staged() && stage <= (size_t)smem_optin_per_block())
     compact_kernel<true><<<(unsigned)tiles, 32 * p.epb, stage, s>>>(p);
   else
     compact_kernel<false><<<(unsigned)tiles, 32 * p.epb, 0, s>>>(p);

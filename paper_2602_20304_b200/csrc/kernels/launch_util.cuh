@@ -50,4 +50,38 @@ struct PerDeviceInt {
   }
 };
 
+// The current device's shared-memory budgets, cached per device: the opt-in
+// maximum per block (the dynamic-smem attribute every kernel sets, and the
+// largest per-env working set a plan may use) and the capacity per SM (what
+// the resident-CTA targets divide; the runtime reserves 1 KB per CTA).
+inline int smem_optin_per_block() {
+  static PerDeviceInt c;
+  return c.get([] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v > 0 ? v : 48 * 1024;
+  });
+}
+inline int smem_per_sm() {
+  static PerDeviceInt c;
+  return c.get([] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    return v > 0 ? v : 48 * 1024;
+  });
+}
+constexpr int kSmemReservedPerCta = 1024;
+
+// Lets kernel `fn` take the device's full opt-in shared memory as dynamic
+// shared memory (less its static shared memory: the sum may not exceed the
+// opt-in limit, or the attribute call fails).
+template <class K>
+inline void allow_max_dynamic_smem(K* fn) {
+  cudaFuncAttributes a{};
+  const int st = cudaFuncGetAttributes(&a, fn) == cudaSuccess ? (int)a.sharedSizeBytes : 0;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin_per_block() - st);
+}
+
 }  // namespace cmgb

@@ -952,8 +952,7 @@ template <int K1, int K2, bool kGP, bool kVsX>
 int launch_kind(const ManifoldParams& p, int threads, int grid, size_t smem, cudaStream_t s) {
   static PerDeviceOnce configured;
   configured([] {  // per device: the attribute does not carry across devices
-    cudaFuncSetAttribute(manifold_kernel<K1, K2, kGP, kVsX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    allow_max_dynamic_smem(manifold_kernel<K1, K2, kGP, kVsX>);
   });
   note_launch();
   manifold_kernel<K1, K2, kGP, kVsX><<<grid, threads, smem, s>>>(p);

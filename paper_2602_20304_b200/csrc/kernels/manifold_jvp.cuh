@@ -1183,7 +1183,7 @@ template <int K1, int K2>
 int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
   static PerDeviceOnce configured;
   configured([] {  // per device: the attribute does not carry across devices
-    cudaFuncSetAttribute(manifold_jvp_kernel<K1, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    allow_max_dynamic_smem(manifold_jvp_kernel<K1, K2>);
   });
   const int64_t grid = (p.m.n_env + p.units_per_block - 1) / p.units_per_block;
   note_launch();
