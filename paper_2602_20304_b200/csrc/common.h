@@ -13,8 +13,9 @@
 
 namespace cmgb {
 
-constexpr int kMaxNodes = 16;   // SDF program nodes per surface in the param block
-constexpr int kMaxStack = 8;    // generic interpreter stack depth
+constexpr int kMaxNodes = 16;      // SDF program nodes per surface held in the param block
+constexpr int kMaxNodesExt = 4096; // larger programs: the node array in device memory (DevSdf::ext)
+constexpr int kMaxStack = 8;       // generic interpreter stack depth (wide unions are chained to fit)
 constexpr int kPairRec = 38;    // floats per E-E pair record in shared memory (19 doubles:
                                  // an odd stride keeps per-lane FP64 accesses bank-conflict free)
 
@@ -86,6 +87,7 @@ struct DevSdf {
   int32_t max_stack;
   DevNode nodes[kMaxNodes];
   const double4* pool;  // CP: (n, n.p) per plane; OPC: (p, -1/2th^2), (n, 1/th^2)
+  const DevNode* ext;   // all n_nodes nodes in device memory when n_nodes > kMaxNodes (generic kind), else null
 };
 
 // One side of a surface pair as the kernel sees it.

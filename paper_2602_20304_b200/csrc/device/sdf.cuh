@@ -313,6 +313,61 @@ __device__ __forceinline__ SdfOutT<T> leaf_eval(const DevNode& nd, const double4
 // Full program evaluation in the BODY frame. KIND (SdfKind) is a compile-time
 // specialisation chosen on the host per surface: each kernel instantiation
 // carries only the field code it needs (I-cache footprint).
+// The generic postfix interpreter; Nodes = the parameter block's node array
+// (indexed in constant space, as before) or a device-memory pointer.
+template <int FL, class T, class Nodes>
+__device__ __forceinline__ SdfOutT<T> interpret(const Nodes& nodes, int n_nodes, const double4* pool, vec3<T> p) {
+  constexpr bool kWantG = FL != kValue;
+  T sv[kMaxStack];
+  vec3<T> sg[kMaxStack];
+  int sp = 0;
+#pragma unroll 1
+  for (int i = 0; i < n_nodes; ++i) {
+    const DevNode& nd = nodes[i];
+    if (nd.op <= 2) {
+      const SdfOutT<T> r = leaf_eval<FL, T>(nd, pool, p);
+      sv[sp] = r.v;
+      sg[sp] = r.g;
+      ++sp;
+    } else if (nd.op == 3) {  // union: softmin weights, first minimum
+      const int n = nd.count, base = sp - n;
+      T m = sv[base];
+#pragma unroll 1
+      for (int k = 1; k < n; ++k) m = fmin(m, sv[base + k]);
+      T acc = 0.0;
+      vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
+#pragma unroll 1
+      for (int k = 0; k < n; ++k) {
+        const T arg = (m - sv[base + k]) * nd.inv_tau_d;
+        const T e = exp_d(arg);
+        acc += e;
+        if (kWantG) g = g + dscale(sg[base + k], e);
+      }
+      sp = base;
+      sv[sp] = m - nd.tau_d * log_d(acc);
+      sg[sp] = kWantG ? dscale(g, rcp_d(acc)) : mk3<T>(0.0, 0.0, 0.0);
+      ++sp;
+    } else {  // subtraction: args (phi+, -phi-), softmax weights
+      const int a = sp - 2, b = sp - 1;
+      const T a0 = sv[a], a1 = -sv[b];
+      const T m = fmax(a0, a1);
+      const T e0 = exp_d((a0 - m) * nd.inv_tau_d);
+      const T e1 = exp_d((a1 - m) * nd.inv_tau_d);
+      const T acc = e0 + e1;
+      sv[a] = m + nd.tau_d * log_d(acc);
+      if (kWantG) {
+        const T inv = rcp_d(acc);
+        sg[a] = dscale(sg[a], e0 * inv) - dscale(sg[b], e1 * inv);
+      }
+      sp = a + 1;
+    }
+  }
+  SdfOutT<T> out;
+  out.v = sv[0];
+  out.g = sg[0];
+  return out;
+}
+
 template <int FL_IN, int KIND, class T = double>
 __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   if constexpr (KIND == kSingleSq) return sq_leaf<FL_IN, 0, 0, 0, 0, T>(s.nodes[0].sq, p);
@@ -360,55 +415,10 @@ __device__ SdfOutT<T> sdf_eval(const DevSdf& s, vec3<T> p) {
   if constexpr (KIND == kSingleCp) return cp_leaf<FL, T>(s.nodes[0], s.pool, p);
   if constexpr (KIND == kBoxCp) return box_cp_leaf<FL, T>(s.nodes[0], p);
   // Generic postfix interpreter (union: -LSE(-phi), subtraction: LSE(phi+, -phi-);
-  // sdf.hpp:222-230, 260-287). Warp-uniform control flow.
-  T sv[kMaxStack];
-  vec3<T> sg[kMaxStack];
-  int sp = 0;
-#pragma unroll 1
-  for (int i = 0; i < s.n_nodes; ++i) {
-    const DevNode& nd = s.nodes[i];
-    if (nd.op <= 2) {
-      const SdfOutT<T> r = leaf_eval<FL, T>(nd, s.pool, p);
-      sv[sp] = r.v;
-      sg[sp] = r.g;
-      ++sp;
-    } else if (nd.op == 3) {  // union: softmin weights, first minimum
-      const int n = nd.count, base = sp - n;
-      T m = sv[base];
-#pragma unroll 1
-      for (int k = 1; k < n; ++k) m = fmin(m, sv[base + k]);
-      T acc = 0.0;
-      vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
-#pragma unroll 1
-      for (int k = 0; k < n; ++k) {
-        const T arg = (m - sv[base + k]) * nd.inv_tau_d;
-        const T e = exp_d(arg);
-        acc += e;
-        if (kWantG) g = g + dscale(sg[base + k], e);
-      }
-      sp = base;
-      sv[sp] = m - nd.tau_d * log_d(acc);
-      sg[sp] = kWantG ? dscale(g, rcp_d(acc)) : mk3<T>(0.0, 0.0, 0.0);
-      ++sp;
-    } else {  // subtraction: args (phi+, -phi-), softmax weights
-      const int a = sp - 2, b = sp - 1;
-      const T a0 = sv[a], a1 = -sv[b];
-      const T m = fmax(a0, a1);
-      const T e0 = exp_d((a0 - m) * nd.inv_tau_d);
-      const T e1 = exp_d((a1 - m) * nd.inv_tau_d);
-      const T acc = e0 + e1;
-      sv[a] = m + nd.tau_d * log_d(acc);
-      if (kWantG) {
-        const T inv = rcp_d(acc);
-        sg[a] = dscale(sg[a], e0 * inv) - dscale(sg[b], e1 * inv);
-      }
-      sp = a + 1;
-    }
-  }
-  SdfOutT<T> out;
-  out.v = sv[0];
-  out.g = sg[0];
-  return out;
+  // sdf.hpp:222-230, 260-287). Warp-uniform control flow. Nodes from the
+  // parameter block, or from device memory for programs above kMaxNodes.
+  if (s.ext) return interpret<FL, T>(s.ext, s.n_nodes, s.pool, p);
+  return interpret<FL, T>(s.nodes, s.n_nodes, s.pool, p);
 }
 
 }  // namespace cmgb

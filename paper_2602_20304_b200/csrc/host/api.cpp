@@ -134,7 +134,13 @@ DeviceSurface& device_image(cmgb_surface_s* s) {
   if (it != s->device.end()) return it->second;
   DeviceSurface d;
   std::vector<double4> pool;
-  d.sdf = pack_program(s->program, &pool);
+  std::vector<DevNode> ext;
+  d.sdf = pack_program(s->program, &pool, &ext);
+  if (!ext.empty()) {  // programs above kMaxNodes: the generic interpreter reads the nodes from here
+    cuda_check(cudaMalloc(&d.ext, sizeof(DevNode) * ext.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(d.ext, ext.data(), sizeof(DevNode) * ext.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
+  }
+  d.sdf.ext = d.ext;
   cuda_check(cudaMalloc(&d.verts, sizeof(double) * s->mesh.vertices.size()), "cudaMalloc");
   cuda_check(cudaMemcpy(d.verts, s->mesh.vertices.data(), sizeof(double) * s->mesh.vertices.size(),
                         cudaMemcpyHostToDevice), "cudaMemcpy");
@@ -595,6 +601,7 @@ void cmgb_surface_destroy(cmgb_surface s) {
     cudaFree(d.edge_body);
     cudaFree(d.edges);
     if (d.pool) cudaFree(d.pool);
+    if (d.ext) cudaFree(d.ext);
   }
   if (prev >= 0) cudaSetDevice(prev);
   delete s;

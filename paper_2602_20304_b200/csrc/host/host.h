@@ -70,10 +70,13 @@ struct DeviceSurface {
   int32_t* edges = nullptr;
   double* edge_body = nullptr;  // [ne][6]: both endpoints of every edge (body frame), no index chase
   double4* pool = nullptr;
+  DevNode* ext = nullptr;  // program nodes in device memory (programs above kMaxNodes)
   DevSdf sdf{};
 };
 
-DevSdf pack_program(const Program& prog, std::vector<double4>* pool);
+// Packs a program into the kernels' image; programs above kMaxNodes nodes also
+// return every node in *ext (the caller uploads it and sets DevSdf::ext).
+DevSdf pack_program(const Program& prog, std::vector<double4>* pool, std::vector<DevNode>* ext);
 
 }  // namespace cmgb
 

@@ -193,25 +193,67 @@ int exact_int(double x) {
 
 }  // namespace
 
-DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
+namespace {
+
+// Postfix order of the device program, from the tree. Unions wider than the
+// interpreter's stack allows are emitted as left-deep chains of binary unions
+// with the same temperature: -tau log sum exp(-phi_i / tau) is associative,
+// and the blended gradient / normal source weights compose, so the chain is the
+// same smooth minimum (rounding aside). Only programs that would not otherwise
+// fit are rewritten; the others keep the reference's n-ary order exactly.
+struct Emit {
+  int src;    // program node
+  int count;  // union arity of this emission (-1: the node's own)
+};
+
+int emit(const Program& prog, int i, bool chain, std::vector<Emit>* out) {  // returns the stack depth used
+  const ProgramNode& d = prog.nodes[i];
+  if (d.op != CMGB_SDF_UNION && d.op != CMGB_SDF_SUBTRACTION) {
+    out->push_back({i, -1});
+    return 1;
+  }
+  if (d.op == CMGB_SDF_SUBTRACTION || !chain || d.children.size() <= 2) {
+    int depth = 0, k = 0;
+    for (int ch : d.children) depth = std::max(depth, k++ + emit(prog, ch, chain, out));
+    out->push_back({i, -1});
+    return depth;
+  }
+  int depth = emit(prog, d.children[0], chain, out);
+  for (size_t k = 1; k < d.children.size(); ++k) {
+    depth = std::max(depth, 1 + emit(prog, d.children[k], chain, out));
+    out->push_back({i, 2});
+  }
+  return depth;
+}
+
+}  // namespace
+
+DevSdf pack_program(const Program& prog, std::vector<double4>* pool, std::vector<DevNode>* ext) {
   DevSdf s{};
-  const int n = static_cast<int>(prog.nodes.size());
-  if (n > kMaxNodes)
-    throw Error(CMGB_ERR_UNSUPPORTED, "sdf: programs are limited to " + std::to_string(kMaxNodes) +
+  std::vector<Emit> order;
+  int depth = emit(prog, prog.root, false, &order);
+  if (depth > kMaxStack) {  // wide unions: binary chains
+    order.clear();
+    depth = emit(prog, prog.root, true, &order);
+  }
+  if (depth > kMaxStack)
+    throw Error(CMGB_ERR_UNSUPPORTED, "sdf: composition nesting exceeds " + std::to_string(kMaxStack) + " levels");
+  const int n = static_cast<int>(order.size());
+  if (n > kMaxNodesExt)
+    throw Error(CMGB_ERR_UNSUPPORTED, "sdf: programs are limited to " + std::to_string(kMaxNodesExt) +
                                           " nodes per surface");
-  if (prog.max_stack > kMaxStack)
-    throw Error(CMGB_ERR_UNSUPPORTED, "sdf: composition depth exceeds " + std::to_string(kMaxStack));
+  std::vector<DevNode> all(n);
   s.n_nodes = n;
   s.leaf_count = prog.leaf_count;
-  s.max_stack = prog.max_stack;
+  s.max_stack = depth;
   s.kind = kGeneric;
   if (n == 1 && prog.nodes[0].op == CMGB_SDF_SUPERQUADRIC) s.kind = kSingleSq;
   if (n == 1 && prog.nodes[0].op == CMGB_SDF_CONVEX_POLYHEDRON) s.kind = kSingleCp;
   for (int i = 0; i < n; ++i) {
-    const ProgramNode& d = prog.nodes[i];
-    DevNode& o = s.nodes[i];
+    const ProgramNode& d = prog.nodes[order[i].src];
+    DevNode& o = all[i];
     o.op = d.op;
-    o.count = d.count;
+    o.count = order[i].count >= 0 ? order[i].count : d.count;
     o.tau_d = d.tau;
     o.inv_tau_d = d.tau > 0.0 ? 1.0 / d.tau : 0.0;
     o.offset = static_cast<int32_t>(pool->size());
@@ -255,6 +297,9 @@ DevSdf pack_program(const Program& prog, std::vector<double4>* pool) {
       }
     }
   }
+  for (int i = 0; i < n && i < kMaxNodes; ++i) s.nodes[i] = all[i];
+  if (n > kMaxNodes) *ext = std::move(all);
+
   if (s.kind == kSingleSq) {
     const DevSq& q = s.nodes[0].sq;
     for (int k : {kSqE01, kSqE02, kSqE025, kSqE05, kSqEll, kSqCyl}) {

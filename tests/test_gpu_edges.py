@@ -152,3 +152,45 @@ def test_soft_topk_exact_ties(cuda):
     for b in ws.bodies:
         b.vertex_topk, b.edge_topk = 5, 7
     _topk_parity(ws, 8, "top-K exact ties")
+
+
+def _blob(n_leaves, seed=5):
+    """Smooth union of n small spheres (one flat union: wider than the
+    interpreter's stack, and above the parameter block's 16 nodes)."""
+    from paper_2602_20304_b200.scene import Union
+    rng = np.random.default_rng(seed)
+    leaves = [Superquadric(1.0, 1.0, (0.15, 0.15, 0.15), tuple(rng.uniform(-0.15, 0.15, 3)) + (0.0, 0.0, 0.0))
+              for _ in range(n_leaves)]
+    return Union(leaves, 0.02)
+
+
+@pytest.mark.parametrize("n_leaves", [12, 40])
+def test_large_sdf_programs(cuda, n_leaves):
+    """Programs beyond the parameter block (n_leaves + 1 > 16 nodes: the node
+    array in device memory) and unions wider than the interpreter's stack
+    (emitted as chains of binary unions, the same smooth minimum): manifold
+    and field values vs the C oracle, which evaluates the n-ary union directly."""
+    blob = W.BodySpec("blob", W.MeshSpec(obj_text=W.sq_obj_text(1.0, 1.0, (0.3, 0.3, 0.3))), _blob(n_leaves),
+                      [0.0, 0.0, 0.0, 0.0, 0.0, 0.0], 8, 6)
+    box = W.BodySpec("box", W.MeshSpec(box_half=(0.5, 0.5, 0.5)), W.BOX_SQ, [0.05, -0.02, 0.78, 0.1, 0.2, 0.3], 0, 6)
+    ws = W.Workload("blob-vs-box", [blob, box], 32)
+    _topk_parity(ws, 32, f"union of {n_leaves} spheres")
+    (a1, _), (o1, _) = surfaces(ws)
+    pts = np.random.default_rng(1).uniform(-0.5, 0.5, (512, 3))
+    ref = o1.sdf_query(1, pts)  # value + gradient
+    got = api.sdf_query(a1, torch.as_tensor(pts, device="cuda"), 1).cpu().numpy()
+    assert np.allclose(got, ref, rtol=1e-9, atol=1e-12), float(np.abs(got - ref).max())
+
+
+def test_sdf_nesting_limit_is_loud(cuda):
+    """Nesting deeper than the interpreter's stack cannot be chained: refused."""
+    from paper_2602_20304_b200.scene import Subtraction
+    s = Superquadric(1.0, 1.0, (0.3, 0.3, 0.3))
+    for _ in range(9):  # right-deep: each subtraction holds its minuend while the subtrahend nests
+        s = Subtraction(Superquadric(1.0, 1.0, (0.3, 0.3, 0.3)), s, 0.01)
+    b = W.BodySpec("deep", W.MeshSpec(box_half=(0.3, 0.3, 0.3)), s, [0.0] * 6, 0, 0)
+    with pytest.raises(Exception, match="nesting"):
+        api.surface_from_spec(b)
+        api.generate_manifold_batch(api.surface_from_spec(b), api.surface_from_spec(b),
+                                    torch.zeros((1, 6), dtype=torch.float64, device="cuda"),
+                                    torch.zeros((1, 6), dtype=torch.float64, device="cuda"), SmoothingConfig())
