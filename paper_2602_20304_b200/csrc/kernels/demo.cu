@@ -26,23 +26,32 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
   c[2] = a[0] * b[1] - a[1] * b[0];
 }
 
-// softplus_s (smooth_ops.hpp:66-81), both arms as in the reference; the
-// exponential is exp_d and below e^-40 log1p(e) = e to double precision.
+// softplus_s (smooth_ops.hpp:66-81), both arms as in the reference; below
+// e^-40 log1p(e) = e to double precision, above it log(1 + e) by log_d (the
+// absolute error of forming 1 + e, ~1e-16, is what matters: it is scaled by tau).
 __device__ __forceinline__ double softplus_ref(double x, double tau) {
   const double scaled = x / tau;
   const double e = exp_d(-fabs(scaled));
-  const double l = e < 4e-18 ? e : log1p(e);
+  const double l = e < 4e-18 ? e : log_d(1.0 + e);
   return scaled > 0.0 ? x + tau * l : tau * l;
 }
 
-// A 16-lane group per env (two envs per warp): 48-contact pair manifolds are
-// 3 contacts per lane with no idle second pass.
+// A 16-lane group per env (two envs per warp). The group first reads every
+// contact's activity and deepest-penetration term and lists the active rows
+// (activity >= 1e-12; the reference skips the others, demosim.cpp:40-41) in
+// row order in shared memory, then deals them to its lanes: inactive rows
+// leave no lane idle.
 constexpr int kPenaltyLanes = 16;
+constexpr int kPenaltyThreads = 256;
+constexpr int kPenaltyMaxC = 256;  // rows per pair the list holds (more: every row is visited)
 
-__global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ PenaltyArgs a) {
+__global__ void __launch_bounds__(kPenaltyThreads, 3) penalty_kernel(const __grid_constant__ PenaltyArgs a) {
+  __shared__ uint16_t act_list[kPenaltyThreads / kPenaltyLanes][kPenaltyMaxC];
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPenaltyLanes;
   const int lane = threadIdx.x & (kPenaltyLanes - 1);
+  const int grp = threadIdx.x / kPenaltyLanes;
   if (e >= a.n_env) return;  // a whole 16-lane group exits; the shuffles below use the group's mask
+  const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
   const DemoParamsDev& P = a.prm;
   // transforms[i].t is the COM (demosim.cpp:84, 96-97)
   const double* f1 = a.frames1 + 12 * e;
@@ -51,16 +60,45 @@ __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ Pe
   const double com2[3] = {f2[9], f2[10], f2[11]};
   const double* vel1 = a.vel + (e * a.nb + a.bi) * 6;
   const double* vel2 = a.vel + (e * a.nb + a.bj) * 6;
+  const float* rows = a.contacts + e * a.C * 8;
+  const bool listed = a.C <= kPenaltyMaxC;
+  double deep = 0.0;
+  int n_act = 0;
+  // pass 1: activity of every row; the first kPre blocks of 16 rows are loaded
+  // before any is used (independent loads in flight: the kernel is latency-bound)
+  constexpr int kPre = 4;
+  float pa[kPre], pd[kPre];
+#pragma unroll
+  for (int b = 0; b < kPre; ++b) {
+    const int r = b * kPenaltyLanes + lane;
+    pa[b] = r < a.C ? rows[r * 8 + 7] : 0.0f;
+    pd[b] = r < a.C ? rows[r * 8 + 3] : 0.0f;
+  }
+  auto take = [&](int r, double act, double dist) {
+    const bool on = r < a.C && act >= 1e-12;
+    if (r < a.C && act > 0.5) deep = fmin(deep, dist);
+    const unsigned bits = __ballot_sync(gm, on) >> (threadIdx.x & 16);
+    if (listed && on) act_list[grp][n_act + __popc(bits & ((1u << lane) - 1u))] = (uint16_t)r;
+    n_act += __popc(bits);
+  };
+#pragma unroll
+  for (int b = 0; b < kPre; ++b)
+    if (b * kPenaltyLanes < a.C) take(b * kPenaltyLanes + lane, pa[b], pd[b]);
+  for (int r0 = kPre * kPenaltyLanes; r0 < a.C; r0 += kPenaltyLanes) {
+    const int r = r0 + lane;
+    take(r, r < a.C ? rows[r * 8 + 7] : 0.0f, r < a.C ? rows[r * 8 + 3] : 0.0f);
+  }
+  __syncwarp(gm);
   double acc[12];  // force1, torque1, force2, torque2
 #pragma unroll
   for (int k = 0; k < 12; ++k) acc[k] = 0.0;
-  double deep = 0.0;
-  for (int r = lane; r < a.C; r += kPenaltyLanes) {
-    const float4* cp = reinterpret_cast<const float4*>(a.contacts + (e * a.C + r) * 8);
+  const int n_rows = listed ? n_act : a.C;
+  for (int k = lane; k < n_rows; k += kPenaltyLanes) {  // pass 2: the active rows
+    const int r = listed ? (int)act_list[grp][k] : k;
+    const float4* cp = reinterpret_cast<const float4*>(rows + r * 8);
     const float4 c0 = cp[0], c1 = cp[1];
     const double act = c1.w, dist = c0.w;
-    if (act > 0.5) deep = fmin(deep, dist);
-    if (act < 1e-12) continue;
+    if (act < 1e-12) continue;  // (unlisted path only)
     const double pt[3] = {c0.x, c0.y, c0.z};
     const double pressure = P.stiffness * softplus_ref(-dist, P.tau_force);
     const double nraw[3] = {c1.x, c1.y, c1.z};
@@ -85,24 +123,23 @@ __global__ void __launch_bounds__(256) penalty_kernel(const __grid_constant__ Pe
     const double vtg[3] = {vrel[0] - nh[0] * vn, vrel[1] - nh[1] * vn, vrel[2] - nh[2] * vn};
     const double vtn = sqrt(vtg[0] * vtg[0] + vtg[1] * vtg[1] + vtg[2] * vtg[2]);
     const double ft = fmin(P.friction * fn, P.friction_viscous * vtn);
-    const double den = vtn + 1e-12;
-    const double F[3] = {nh[0] * fn - vtg[0] / den * ft, nh[1] * fn - vtg[1] / den * ft,
-                         nh[2] * fn - vtg[2] / den * ft};
+    const double q = ft * rcp_d(vtn + 1e-12);  // (vtg / den) ft with one reciprocal
+    const double F[3] = {nh[0] * fn - vtg[0] * q, nh[1] * fn - vtg[1] * q, nh[2] * fn - vtg[2] * q};
     double to[3], tt[3];
     cross3(ro, F, to);
     cross3(rt, F, tt);
-    double* own = acc + (side1 ? 0 : 6);
-    double* oth = acc + (side1 ? 6 : 0);
+    // the own body gains (F, r_o x F), the other loses (F, r_t x F); selects,
+    // not a pointer into acc (which would put it in local memory)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      own[k] += F[k];
-      own[3 + k] += to[k];
-      oth[k] -= F[k];
-      oth[3 + k] -= tt[k];
+    for (int k2 = 0; k2 < 3; ++k2) {
+      const double sf = side1 ? F[k2] : -F[k2];
+      acc[k2] += sf;
+      acc[3 + k2] += side1 ? to[k2] : -tt[k2];
+      acc[6 + k2] -= sf;
+      acc[9 + k2] += side1 ? -tt[k2] : to[k2];
     }
   }
   // fixed-order butterfly reduction within the env's 16 lanes (deterministic)
-  const unsigned gm = 0xFFFFu << (threadIdx.x & 16);
 #pragma unroll
   for (int o = kPenaltyLanes / 2; o > 0; o >>= 1) {
 #pragma unroll
@@ -174,7 +211,8 @@ int launch_penalty(const PenaltyArgs& a, void* stream) {
   if (a.n_env <= 0) return 0;
   const int64_t threads = a.n_env * kPenaltyLanes;
   note_launch();
-  penalty_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  penalty_kernel<<<(unsigned)((threads + kPenaltyThreads - 1) / kPenaltyThreads), kPenaltyThreads, 0,
+                   static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
