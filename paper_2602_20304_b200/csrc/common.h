@@ -149,7 +149,8 @@ struct ManifoldParams {
   const double* poses2;
   const double* frames1;  // [n1][12] R (row-major), t: device workspace filled by frames_kernel
   const double* frames2;
-  int32_t stride1, stride2;            // frames: 1 = one per env, 0 = shared
+  int32_t stride1, stride2;            // frames: env e's frame at 12 e stride (1 = one per env, 0 = shared,
+                                       //   n_bodies = a scene's [env][body] frame array)
   int64_t pose_stride1, pose_stride2;  // poses: doubles between consecutive envs (0 = shared)
   int64_t n_env;
   int32_t n1, n2, m1, m2, n_contacts;
@@ -167,6 +168,7 @@ struct ManifoldParams {
   int32_t* act_count;   // optional [n_env]: set bits
   float act_thr;
   int32_t mask_words;   // ceil(n_contacts / 32)
+  int32_t frames_ready; // 1: frames1 / frames2 already hold every env's frames (a scene's shared pass)
 };
 
 // Pose-Jacobian (forward-mode, Dual12) batch: the geometry / config / slot
@@ -257,6 +259,8 @@ struct WitnessParams {
 namespace cmgb {
 int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t smem_bytes,
                     void* stream);
+// se3_exp of n_poses contiguous [6] poses into [12] frames (a scene's bodies x envs, once per call)
+int launch_scene_frames(const double* poses, int64_t n_poses, double* frames, void* stream);
 int manifold_min_blocks(int k1, int k2);  // resident CTAs / SM the kernel for this kind pair is built for
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream);
 int jvp_directions();    // tangent directions per thread of the compiled JVP kernel

@@ -34,8 +34,8 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n1 = p.stride1 ? p.n_env : 1, n2 = p.stride2 ? p.n_env : 1;
-  if (launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), p.poses2, p.pose_stride2, n2,
-                    const_cast<double*>(p.frames2), s))
+  if (!p.frames_ready && launch_frames(p.poses1, p.pose_stride1, n1, const_cast<double*>(p.frames1), p.poses2,
+                                       p.pose_stride2, n2, const_cast<double*>(p.frames2), s))
     return 1;
   if (p.pairs_gmem)  // the generic interpreter evaluates every SDF kind
     return launch_kind<kGeneric, kGeneric, true>(p, block_threads, grid, smem_bytes, s);
@@ -56,6 +56,10 @@ int launch_manifold(const ManifoldParams& p, int block_threads, int grid, size_t
 }
 
 int manifold_max_threads(int k1, int k2) { return max_threads(k1, k2); }
+
+int launch_scene_frames(const double* poses, int64_t n_poses, double* frames, void* stream) {
+  return launch_frames(poses, 6, n_poses, frames, nullptr, 0, 0, nullptr, static_cast<cudaStream_t>(stream));
+}
 
 #ifdef CMGB_PHASE_CLOCKS
 int manifold_ct_phase_clocks(unsigned long long* out);
