@@ -490,6 +490,34 @@ def bench_box_box(ctx):
         n_c = n_local * L["n_contacts"]
         added_f = tcf["median_ms"] - t["median_ms"]
         added_s = tcs["median_ms"] - t["median_ms"]
+        # e2e of the active contacts only (what a consumer of the manifold keeps):
+        # pinned poses H2D, the step with activity masks, the compaction, then the
+        # kept rows + per-env offsets D2H (the total is read first to size the copy)
+        hP2 = torch.as_tensor(p2).pin_memory()
+        P2d = torch.empty_like(P2)
+        kept_h = torch.empty((n_c, 8), dtype=torch.float32).pin_memory()
+        off_h = torch.empty((n_local + 1,), dtype=torch.int64).pin_memory()
+        oute, compe = {}, {}
+        d2h = [0]
+
+        def e2e_active():
+            P2d.copy_(hP2, non_blocking=True)
+            api.generate_manifold_batch(s1, s2, P1, P2d, cfg, out=oute, active_threshold=a.compact_thr)
+            api.compact_contacts(oute["contacts"], mask=oute["active_mask"], count=oute["active_count"], out=compe)
+            tot = int(compe["total"].item())
+            kept_h[:tot].copy_(compe["contacts"][:tot], non_blocking=True)
+            off_h.copy_(compe["env_offset"], non_blocking=True)
+            ctx.stream.synchronize()
+            d2h[0] = tot * 32 + off_h.numel() * 8 + 8
+
+        ta = timed(ctx, e2e_active, max(3, min(a.steps, 20)), 2)
+        extras["e2e_active_contacts"] = {
+            "value": n_total / (ta["ms_per_step"] * 1e-3), "unit": "manifolds/s",
+            "h2d_bytes_per_step": int(hP2.numel() * 8) * ctx.world, "d2h_bytes_per_step": d2h[0] * ctx.world,
+            "activity_threshold": a.compact_thr,
+            "path": "api.generate_manifold_batch(active_threshold) + api.compact_contacts (masked): pinned poses "
+                    "H2D, kept contacts (activity > threshold, fixed-layout order) + per-env offsets D2H"}
+        del kept_h
         extras["compaction"] = {
             "activity_threshold": a.compact_thr, "kept": total_kept, "kept_fraction": total_kept / n_c,
             "fused": {"added_ms_per_step": added_f, "added_fraction": added_f / t["median_ms"],
