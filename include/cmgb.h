@@ -83,6 +83,10 @@ int cmgb_config_for_variant(const char* variant, const cmgb_config* base, cmgb_c
  * (include/cmg/sdf.hpp:138-202). Nodes are listed in POSTFIX order: a UNION
  * node with `count` children pops the `count` most recent subtrees (in
  * order), a SUBTRACTION pops (positive, negative). The last node is the root.
+ * Device limits: up to 4,096 nodes (above 16 the node array lives in device
+ * memory); unions of any width (wide ones are evaluated as chains of binary
+ * unions with the same temperature: the same smooth minimum); nesting up to 8
+ * levels deep -- deeper programs fail with CMGB_ERR_UNSUPPORTED on first use.
  * ------------------------------------------------------------------------- */
 typedef enum cmgb_sdf_op {
   CMGB_SDF_SUPERQUADRIC = 0,        /* SuperquadricParams        sdf.hpp:35-47  */
