@@ -331,6 +331,39 @@ __global__ void __launch_bounds__(256) frames_kernel(const double* __restrict__ 
   f[11] = t[2];
 }
 
+// The K largest of a set's D <= 32 R scores in order, ties to the lowest index
+// (the soft top-K's sort, smooth_ops.hpp:180-185), by one warp: per round,
+// each lane's best remaining order-preserving 64-bit key, then warp reductions
+// over (high word, low word, lowest index); out[r] = set-local index of rank r.
+template <int R>
+__device__ __forceinline__ void extract_topk(const double* sc, int D, int K, int* out, int lane) {
+  uint64_t key[R];  // 0 = taken / absent
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int j = lane + 32 * k;
+    const uint64_t u = j < D ? (uint64_t)__double_as_longlong(sc[j]) : 0ull;
+    key[k] = j >= D ? 0ull : ((int64_t)u < 0 ? ~u : (u | 0x8000000000000000ull));
+  }
+  for (int r = 0; r < K; ++r) {
+    uint64_t b = key[0];
+    int bj = lane;
+#pragma unroll
+    for (int k = 1; k < R; ++k)
+      if (key[k] > b) {  // strict: the lowest index among equal keys
+        b = key[k];
+        bj = lane + 32 * k;
+      }
+    const unsigned bh = (unsigned)(b >> 32), bl = (unsigned)b;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
+    const int wj = __reduce_min_sync(0xffffffffu, (bh == mh && bl == ml) ? bj : 0x7fffffff);
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (lane + 32 * k == wj) key[k] = 0ull;
+    if (lane == 0) out[r] = wj;
+  }
+}
+
 // kGP: pair records in the global workspace (p.pairs_gmem; large pass-through
 // pair sets, one generic instantiation) instead of shared memory. kVsX: the
 // V-S contacts come from vs_kernel (box-box, pass-through vertex sets; p.vs_ext).
@@ -464,31 +497,12 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         const EnvView ev = env(e);
         const int lo = sets.off[set], D = sets.off[set + 1] - lo, K = set_K(set);
         const double* sc = ev.scores() + lo;
-        uint64_t key[4];  // order-preserving integer images of the scores; 0 = taken / absent
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int j = lane + 32 * k;
-          const uint64_t u = j < D ? (uint64_t)__double_as_longlong(sc[j]) : 0ull;
-          key[k] = j >= D ? 0ull : ((int64_t)u < 0 ? ~u : (u | 0x8000000000000000ull));
-        }
         int* out = ev.sorted() + lo;
-        for (int r = 0; r < K; ++r) {
-          uint64_t b = key[0];
-          int bj = lane;
-#pragma unroll
-          for (int k = 1; k < 4; ++k)
-            if (key[k] > b) {  // strict: the lowest index among equal keys
-              b = key[k];
-              bj = lane + 32 * k;
-            }
-          const unsigned bh = (unsigned)(b >> 32), bl = (unsigned)b;
-          const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
-          const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
-          const int wj = __reduce_min_sync(0xffffffffu, (bh == mh && bl == ml) ? bj : 0x7fffffff);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (lane + 32 * k == wj) key[k] = 0ull;
-          if (lane == 0) out[r] = wj;
+        switch ((D + 31) >> 5) {  // key registers per lane: the set's size, not the 128 maximum
+          case 1: extract_topk<1>(sc, D, K, out, lane); break;
+          case 2: extract_topk<2>(sc, D, K, out, lane); break;
+          case 3: extract_topk<3>(sc, D, K, out, lane); break;
+          default: extract_topk<4>(sc, D, K, out, lane); break;
         }
       }
     }
