@@ -67,13 +67,23 @@ __device__ __forceinline__ T cpow(const T& x) {
 }
 
 // (x^p, x^(p-1)) in FP64: integer chains (no SFU) or libdevice pow.
+// Runtime-exponent x^p for x > 0 (the squared-coordinate floor keeps it so):
+// exp_d(p log_d(x)), relative error ~|p log x| 3e-14 + 1e-12 -- the same
+// budget as the integer-exponent chains' Newton step, at a fifth of
+// libdevice pow's cost; Dual arguments keep their overload.
+template <class T>
+__device__ __forceinline__ T pow_rt(const T& x, double p) {
+  if constexpr (std::is_same_v<T, double>) return exp_d(p * log_d(x));
+  else return pow(x, p);
+}
+
 template <class T>
 __device__ __forceinline__ void pow_pair_d(const T& x, int n, double p, T& xp, T& xpm1) {
   if (n > 0) {
     xpm1 = n == 1 ? T(1.0) : ipow_d(x, n - 1);
     xp = xpm1 * x;
   } else {
-    xp = pow(x, p);
+    xp = pow_rt(x, p);
     xpm1 = div_d(xp, x);
   }
 }
@@ -140,9 +150,12 @@ __device__ __forceinline__ double one_minus_pow(double f, double p4, int n_rt, d
     if (inv_f) *inv_f = fma(Fn, fma(e, e, e), Fn);
     return 1.0 - Fv;
   }
-  const double d = f - 1.0;
-  const double lnf = fabs(d) < 0.5 ? log1p(d) : log(f);
-  const double em1 = expm1(p4 * lnf);
+  // ln f by log_d: forming 1 + d rounds by ~1e-16 ABSOLUTE, which is all
+  // 1 - f^p4 needs (it feeds phi additively); expm1 by a Taylor polynomial
+  // below |y| = 1e-3 (error y^5/120) and exp_d(y) - 1 above (absolute ~1e-12,
+  // the Newton-step level of the integer branch)
+  const double y = p4 * log_d(f);
+  const double em1 = fabs(y) < 1e-3 ? y * fma(y, fma(y, fma(y, 1.0 / 24.0, 1.0 / 6.0), 0.5), 1.0) : exp_d(y) - 1.0;
   *F = 1.0 + em1;
   if (inv_f) *inv_f = rcp_d(f);
   return -em1;
