@@ -189,14 +189,16 @@ __device__ __forceinline__ double3 trace_sq(const DevSq& q, double3 p, const Dev
   for (int it = 0; it < c.trace_iters; ++it) {
     const double x2 = fma(ux, ux, kMC.floor30), y2 = fma(uy, uy, kMC.floor30), z2 = fma(uz, uz, kMC.floor30);
     double A, Am1, B, Bm1, G, Gm1, Cz, Czm1;
-    pow_pair_t<E.n1>(x2, E.n1, 0.0, A, Am1);
-    pow_pair_t<E.n1>(y2, E.n1, 0.0, B, Bm1);
-    pow_pair_t<E.n2>(A + B, E.n2, 0.0, G, Gm1);
-    pow_pair_t<E.n3>(z2, E.n3, 0.0, Cz, Czm1);
+    // (compile-time exponents, or -- kSingleSq -- the descriptor's: integer
+    // chains where exact, else pow_rt)
+    pow_pair_t<E.n1>(x2, E.n1 ? E.n1 : q.n1, q.p1, A, Am1);
+    pow_pair_t<E.n1>(y2, E.n1 ? E.n1 : q.n1, q.p1, B, Bm1);
+    pow_pair_t<E.n2>(A + B, E.n2 ? E.n2 : q.n2, q.p2, G, Gm1);
+    pow_pair_t<E.n3>(z2, E.n3 ? E.n3 : q.n3, q.p3, Cz, Czm1);
     const double f = G + Cz;
     const double w = rcp_d(fma(ux, ux, fma(uy, uy, fma(uz, uz, kMC.floor20))));
     double F, inv_f;
-    const double omF = one_minus_pow<E.n4>(f, q.p4, E.n4, &F, &inv_f);
+    const double omF = one_minus_pow<E.n4>(f, q.p4, E.n4 ? E.n4 : q.n4, &F, &inv_f);
     const double k = -q.p4 * F * inv_f;
     const double kxy = k * (q.c_xy * Gm1), kz = k * q.c_z;
     const double hw = omF * w;
@@ -214,7 +216,7 @@ __device__ __forceinline__ double3 trace_sq(const DevSq& q, double3 p, const Dev
 
 template <int K>
 __device__ __forceinline__ double3 trace(const DevSdf& sdf, double3 p, const DevCfg& c) {
-  if constexpr (ct_sq(K)) {
+  if constexpr (ct_sq(K) || K == kSingleSq) {  // a lone superquadric leaf: the normalised-coordinate trace
     return trace_sq<K>(sdf.nodes[0].sq, p, c);
   } else {
 #pragma unroll 1
