@@ -138,8 +138,10 @@ struct Dual {
   }
   // pow with a constant exponent (dual.hpp:224-234)
   friend __device__ __forceinline__ Dual pow(const Dual& x, double p) {
-    const double y = ::pow(x.v, p);
-    return chain(y, p * ::pow(x.v, p - 1.0), x);
+    // x > 0 on every use (squared coordinates + floor): exp_d(p log_d x), and
+    // the derivative p x^(p-1) = p y / x from the same value (sdf.cuh pow_rt)
+    const double y = exp_d(p * log_d(x.v));
+    return chain(y, p * y * rcp_d(x.v), x);
   }
   // |x| with subgradient 0 at the kink (dual.hpp:236-246)
   friend __device__ __forceinline__ Dual fabs(const Dual& x) {
