@@ -11,9 +11,10 @@ int jvp_smem_cap() { return CMGB_JVP_SMEM_KB * 1024; }
 int launch_manifold_jvp(const JvpParams& p, int block_threads, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int threads = block_threads > 0 && block_threads <= kJvpThreads ? block_threads : kJvpThreads;
-  switch (jvp_kind(p.m.side[0].sdf.kind)) {
+  switch (jvp_kind_of(p.m.side[0].sdf)) {
     case kSqE01: return launch_jvp_k1_sq(p, threads, s);
     case kBoxCp: return launch_jvp_k1_cp(p, threads, s);
+    case kSingleSq: return launch_jvp_k1_ssq(p, threads, s);
     default: return launch_jvp_k1_gen(p, threads, s);
   }
 }
@@ -27,6 +28,7 @@ int manifold_phase_clocks(unsigned long long* out);
 extern "C" int cmgb_debug_manifold_phase_clocks(unsigned long long* out) { return cmgb::manifold_phase_clocks(out); }
 extern "C" int cmgb_debug_jvp_phase_clocks(unsigned long long* out) {
   for (int i = 0; i < 16; ++i) out[i] = 0;
-  return cmgb::jvp_phase_clocks_sq(out) | cmgb::jvp_phase_clocks_cp(out) | cmgb::jvp_phase_clocks_gen(out);
+  return cmgb::jvp_phase_clocks_sq(out) | cmgb::jvp_phase_clocks_cp(out) | cmgb::jvp_phase_clocks_gen(out) |
+         cmgb::jvp_phase_clocks_ssq(out);
 }
 #endif

@@ -295,25 +295,43 @@ struct SqHess {
   double Hf[9]; // Hess f (body)
 };
 
-__device__ __forceinline__ void sq_e01_hess(const DevSq& q, double3 x, SqHess& o) {
+// The same for the integer-exponent box family: f = sum_i s_i^n (n2 = 1,
+// n1 = n3 = n, n4 = 2n: eps1 = eps2 = 1/n... i.e. eps 0.1 / 0.2 / 0.25 / 0.5 / 1),
+// f_i = c u_i s_i^(n-1), f_ii = c s_i^(n-2) (s_i + 2 (n-1) u_i^2) (f_ii = c for
+// n = 1). N > 0: compile-time n (kSqE01, N = 10); N = 0: the descriptor's.
+template <int N>
+__device__ __forceinline__ void sq_int_hess(const DevSq& q, double3 x, SqHess& o) {
+  const int n = N > 0 ? N : q.n1;
   if (q.has_frame) x = mul_Rt(q.R, x - d3(q.t[0], q.t[1], q.t[2]));
   const double u[3] = {x.x * q.inv_ax[0], x.y * q.inv_ax[1], x.z * q.inv_ax[2]};
   const double cc[3] = {q.c_xy, q.c_xy, q.c_z};
-  double s[3], s8[3], fi[3], fii[3];
+  double s[3], fi[3], fii[3];
   double f = 0.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     s[i] = fma(u[i], u[i], kMC.floor30);
-    s8[i] = cpow<8>(s[i]);
-    const double s9 = s8[i] * s[i];
-    f += s9 * s[i];
-    fi[i] = cc[i] * u[i] * s9;
-    fii[i] = cc[i] * s8[i] * fma(18.0 * u[i], u[i], s[i]);
+    if constexpr (N >= 2) {
+      const double sm2 = cpow<(N >= 2 ? N - 2 : 1)>(s[i]);
+      const double sm1 = sm2 * s[i];
+      f += sm1 * s[i];
+      fi[i] = cc[i] * u[i] * sm1;
+      fii[i] = cc[i] * sm2 * fma((2.0 * (N - 1)) * u[i], u[i], s[i]);
+    } else if (n >= 2) {
+      const double sm2 = ipow_d(s[i], n - 2);
+      const double sm1 = sm2 * s[i];
+      f += sm1 * s[i];
+      fi[i] = cc[i] * u[i] * sm1;
+      fii[i] = cc[i] * sm2 * fma((2.0 * (n - 1)) * u[i], u[i], s[i]);
+    } else {  // n = 1 (ellipsoid): f = sum s_i
+      f += s[i];
+      fi[i] = cc[i] * u[i];
+      fii[i] = cc[i];
+    }
   }
   const double r2 = fma(u[0], u[0], fma(u[1], u[1], fma(u[2], u[2], kMC.floor20)));
   const double ri = rsqrt_d(r2), ri2 = ri * ri;
   double F, inv_f;
-  const double phi = one_minus_pow<20>(f, q.p4, q.n4, &F, &inv_f) * ri;
+  const double phi = one_minus_pow<(N > 0 ? 2 * N : 0)>(f, q.p4, q.n4, &F, &inv_f) * ri;
   const double k = -q.p4 * F * inv_f;
   const double a = k * (q.p4 - 1.0) * inv_f * ri, b = k * ri * ri2, cuu = 3.0 * phi * ri2 * ri2;
   double g[3], H[9], Hf[9];
@@ -384,11 +402,14 @@ __device__ __forceinline__ void box_cp_hess(const DevNode& nd, double3 p, SqHess
 }
 
 // Analytic leaf Hessians available for these kinds.
+// (kSingleSq here: a lone superquadric of the integer box family with the
+// descriptor's exponents -- jvp_kind_of checks the pattern)
 template <int K>
-constexpr bool kHasHess = K == kSqE01 || K == kBoxCp;
+constexpr bool kHasHess = K == kSqE01 || K == kBoxCp || K == kSingleSq;
 template <int K>
 __device__ __forceinline__ void leaf_hess(const DevSdf& sdf, double3 p, SqHess& h) {
-  if constexpr (K == kSqE01) sq_e01_hess(sdf.nodes[0].sq, p, h);
+  if constexpr (K == kSqE01) sq_int_hess<10>(sdf.nodes[0].sq, p, h);
+  else if constexpr (K == kSingleSq) sq_int_hess<0>(sdf.nodes[0].sq, p, h);
   else box_cp_hess(sdf.nodes[0], p, h);
 }
 
@@ -1194,13 +1215,26 @@ int launch_jvp_kind(const JvpParams& p, int threads, cudaStream_t s) {
 // Specialised kinds for the benchmark bodies (eps = 0.1 superquadric, box_planes
 // leaf); every other program runs through the generic interpreter (same leaf
 // code): three kinds per side keep the library small.
-constexpr int jvp_kind(int k) { return k == kSqE01 || k == kBoxCp ? k : kGeneric; }
+// kSqE01 / kBoxCp keep their kinds; a lone superquadric of the integer box
+// family (eps 0.2 / 0.25 / 0.5 / 1 ..., n2 = 1, n1 = n3, n4 = 2 n1) runs as
+// kSingleSq with the analytic Hessian; everything else as kGeneric.
+inline int jvp_kind_of(const DevSdf& s) {
+  if (s.kind == kSqE01 || s.kind == kBoxCp) return s.kind;
+  if (s.n_nodes == 1 && s.nodes[0].op == 0) {  // CMGB_SDF_SUPERQUADRIC
+    const DevSq& q = s.nodes[0].sq;
+    if (q.n2 == 1 && q.n1 > 0 && q.n1 == q.n3 && q.n4 == 2 * q.n1) return kSingleSq;
+  }
+  return kGeneric;
+}
 
 template <int K1>
 int launch_jvp_k2(const JvpParams& p, int threads, cudaStream_t s) {
-  switch (jvp_kind(p.m.side[1].sdf.kind)) {
+  switch (jvp_kind_of(p.m.side[1].sdf)) {
     case kSqE01: return launch_jvp_kind<K1, kSqE01>(p, threads, s);
     case kBoxCp: return launch_jvp_kind<K1, kBoxCp>(p, threads, s);
+    case kSingleSq:  // instantiated with itself and against box_planes
+      if constexpr (K1 == kSingleSq || K1 == kBoxCp) return launch_jvp_kind<K1, kSingleSq>(p, threads, s);
+      else return launch_jvp_kind<K1, kGeneric>(p, threads, s);
     default: return launch_jvp_kind<K1, kGeneric>(p, threads, s);
   }
 }
@@ -1217,9 +1251,11 @@ inline int read_phase_clocks(unsigned long long* out) {
 int jvp_phase_clocks_sq(unsigned long long* out);
 int jvp_phase_clocks_cp(unsigned long long* out);
 int jvp_phase_clocks_gen(unsigned long long* out);
+int jvp_phase_clocks_ssq(unsigned long long* out);
 #endif
 int launch_jvp_k1_sq(const JvpParams& p, int threads, cudaStream_t s);
 int launch_jvp_k1_cp(const JvpParams& p, int threads, cudaStream_t s);
 int launch_jvp_k1_gen(const JvpParams& p, int threads, cudaStream_t s);
+int launch_jvp_k1_ssq(const JvpParams& p, int threads, cudaStream_t s);
 
 }  // namespace cmgb
