@@ -301,7 +301,10 @@ __device__ __forceinline__ double3 vf_witness(double3 v, double3 t0, double3 t1,
   const double3 on2 = t1 + u21 * clip_len(ddot(dv1, u21), len21);
   const double3 on3 = t0 + u20 * clip_len(ddot(dv0, u20), len20);
   const double3 q1 = v - on1, q2 = v - on2, q3 = v - on3;
-  const double cost[3] = {sqrt(ddot(q1, q1)), sqrt(ddot(q2, q2)), sqrt(ddot(q3, q3))};
+  // distances as x rsqrt(x) (1.3e-12 relative: they only enter the softmin
+  // weights, scaled by 1/tau_min) instead of three IEEE square roots
+  auto dist = [](double x) { return x > 0.0 ? x * rsqrt_d(x) : 0.0; };
+  const double cost[3] = {dist(ddot(q1, q1)), dist(ddot(q2, q2)), dist(ddot(q3, q3))};
   I w[3];
   const int best = pick_min<3>(cost, w, c.inv_tau_min, hard_mode<kH>(c));
   const double3 cons = on1 * (double)w[0] + on2 * (double)w[1] + on3 * (double)w[2];
