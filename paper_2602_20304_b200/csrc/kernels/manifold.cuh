@@ -281,8 +281,12 @@ __device__ __forceinline__ void ee_stage_pair(const DevCfg& c, double* r) {
   const double3 p1w = d3(r[0], r[1], r[2]), p2w = d3(r[8], r[9], r[10]);
   const double3 n1 = d3(r[3], r[4], r[5]), n2 = d3(r[11], r[12], r[13]);
   const double3 de = p1w - p2w;
-  const double dg = sqrt(ddot(de, de) + 1e-12);  // kEdgeNormalEps
-  const double3 nb = dscale(de, rcp_d(dg));
+  // |de|_guarded and de / |de| from one refined reciprocal square root (1.3e-12
+  // relative, far below the FP32 outputs' resolution) instead of sqrt + reciprocal
+  const double dd = ddot(de, de) + 1e-12;  // kEdgeNormalEps
+  const double rs = rsqrt_d(dd);
+  const double dg = dd * rs;
+  const double3 nb = dscale(de, rs);
   const double d2 = ddot(n2, nb), d1 = ddot(n1, nb);
   double g1, g2;
   if (c.hard_ops) {  // sign_hard (smooth_ops.hpp:208)
