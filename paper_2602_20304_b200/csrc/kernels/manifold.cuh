@@ -271,7 +271,7 @@ __device__ __forceinline__ void ee_stage_side(const ManifoldParams& p, const Env
 __device__ __forceinline__ float sigmoid_acc(double xd) {
   const float x = (float)xd;
   const float e = expf(-fabsf(x));
-  const float inv = 1.0f / (1.0f + e);
+  const float inv = __frcp_rn(1.0f + e);  // correctly rounded, without the division's slow-path checks
   return x >= 0.0f ? inv : e * inv;
 }
 
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
       tot += __shfl_xor_sync(gm, tot, 2);
       if (ql == 0) {
         ev.nnstat()[3 * r] = m;  // stride 3 (odd): conflict-free reads in G
-        ev.nnstat()[3 * r + 1] = 1.0 / tot;
+        ev.nnstat()[3 * r + 1] = rcp_d(tot);  // tot >= 1
       }
     }
     if constexpr (!kVsE && !kVsX) {
