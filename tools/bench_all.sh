@@ -8,5 +8,6 @@ for w in mixed drop drop-fwd ee vf demo; do
   python bench.py --workload $w --steps 20 --warmup 3 "$@" > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err
 done
 python bench.py --eps 0.2 --steps 50 --warmup 3 --no-extras "$@" > gpurun_out/${T}_bench_eps0.2.json 2> gpurun_out/${T}_bench_eps0.2.err
+python bench.py --eps 0.3 --steps 20 --warmup 3 --no-extras "$@" > gpurun_out/${T}_bench_eps0.3.json 2> gpurun_out/${T}_bench_eps0.3.err
 python bench.py --n-total 1048576 --steps 20 --warmup 3 --no-extras --no-cpu-baseline "$@" > gpurun_out/${T}_bench_1m.json 2> gpurun_out/${T}_bench_1m.err
 echo done
