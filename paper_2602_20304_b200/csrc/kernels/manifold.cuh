@@ -266,6 +266,10 @@ __device__ __forceinline__ void ee_stage_side(const ManifoldParams& p, const Env
   r[7] = o.v;
 }
 
+// exp(x) for the NN softmin weights (x <= 0, FP64-exact argument rounded
+// once): SFU ex2 (2^-22 relative; the weights only scale FP32 activities).
+__device__ __forceinline__ float nn_weight(double x) { return ex2f((float)x * 1.44269504088896341f); }
+
 // sigma(x) in FP32 with the accurate expf (arguments are FP64-exact; the
 // indicators only scale the activity, tolerance 1e-5 relative).
 __device__ __forceinline__ float sigmoid_acc(double xd) {
@@ -730,32 +734,37 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
     // and, on the 9-warp shape, the V-S contacts on the warps the NN items
     // leave idle (dense warps: a V-S item is ~1/6 of a pair).
     for (int i = tid; i < 10 * n_here; i += nth) env(i / 10).hpart()[i % 10] = 0.0;  // G's partials
-    // 4 adjacent lanes per row / column split its elements (shuffle-reduced in
-    // a fixed order), so the serial chain is a quarter as long.
+    // 2 adjacent lanes per row / column split its elements (shuffle-reduced in
+    // a fixed order; measured: 4 lanes +0.6%, 1 lane -0.2% but serial for long rows)
+    constexpr int kNL = 2;
     const int nrc = m1 + m2;
-    const int nF = full ? 4 * n_here * nrc : 0;
+    const int nF = full ? kNL * n_here * nrc : 0;
     for (int it = tid; it < nF; it += nth) {
-      const int ql = it & 3;
+      const int ql = it & (kNL - 1);
       int e, r;
-      fdivmod(it >> 2, p.div_nrc, e, r);
+      fdivmod(it / kNL, p.div_nrc, e, r);
       const EnvView ev = env(e);
       const bool row = r < m1;
       const int n = row ? m2 : m1;
-      const unsigned gm = 0xFu << ((tid & 31) & ~3);
+      const unsigned gm = ((1u << kNL) - 1u) << ((tid & 31) & ~(kNL - 1));
       double m = INFINITY;
-      for (int j = ql; j < n; j += 4) {  // minimum shift (argmin_s, smooth_ops.hpp:130-136)
+      for (int j = ql; j < n; j += kNL) {  // minimum shift (argmin_s, smooth_ops.hpp:130-136)
         const int i = row ? r * m2 + j : j * m2 + (r - m1);
-        m = fmin(m, ev.dbar(i));
+        const double d = ev.dbar(i);
+        m = d < m ? d : m;
       }
-      m = fmin(m, __shfl_xor_sync(gm, m, 1));
-      m = fmin(m, __shfl_xor_sync(gm, m, 2));
+#pragma unroll
+      for (int o = 1; o < kNL; o <<= 1) {
+        const double mo = __shfl_xor_sync(gm, m, o);
+        m = mo < m ? mo : m;
+      }
       double tot = 0.0;
-      for (int j = ql; j < n; j += 4) {
+      for (int j = ql; j < n; j += kNL) {
         const int i = row ? r * m2 + j : j * m2 + (r - m1);
-        tot += (double)expf((float)((m - ev.dbar(i)) * c.inv_tau_nn));
+        tot += (double)nn_weight((m - ev.dbar(i)) * c.inv_tau_nn);
       }
-      tot += __shfl_xor_sync(gm, tot, 1);
-      tot += __shfl_xor_sync(gm, tot, 2);
+#pragma unroll
+      for (int o = 1; o < kNL; o <<= 1) tot += __shfl_xor_sync(gm, tot, o);
       if (ql == 0) {
         ev.nnstat()[3 * r] = m;  // stride 3 (odd): conflict-free reads in G
         ev.nnstat()[3 * r + 1] = rcp_d(tot);  // tot >= 1
@@ -802,8 +811,8 @@ __global__ void __launch_bounds__(max_threads(K1, K2), min_blocks(K1, K2))
         const double* rec = ev.pair(i);
         const double* ns = ev.nnstat();
         const double dg = rec[3];
-        const double nn1 = (double)expf((float)((ns[3 * k] - dg) * c.inv_tau_nn)) * ns[3 * k + 1];
-        const double nn2 = (double)expf((float)((ns[3 * (m1 + l)] - dg) * c.inv_tau_nn)) * ns[3 * (m1 + l) + 1];
+        const double nn1 = (double)nn_weight((ns[3 * k] - dg) * c.inv_tau_nn) * ns[3 * k + 1];
+        const double nn2 = (double)nn_weight((ns[3 * (m1 + l)] - dg) * c.inv_tau_nn) * ns[3 * (m1 + l) + 1];
         const double pen1 = rec[6], pen2 = rec[14], con = rec[16], clash = rec[15], cont = rec[7];
         const float act1 = (float)(con * pen1 * nn1 * clash * cont);
         const float act2 = (float)(con * pen2 * nn2 * clash * cont);
