@@ -66,7 +66,8 @@ def assert_parity(got, ref, what="", rtol=RTOL, atol=ATOL, allow=0, per_componen
         lines = [f"{what}: {nfail} contacts outside {atol:g} + {rtol:g}|ref| (allowed {allow})"]
         for f, r in rep.items():
             if r["fails"] and f != "per_component" or (f == "per_component" and per_component and r["fails"]):
-                lines.append(f"  {f}: {r['fails']}/{r['n']} max_err={r['max_err']:.3g} max_ratio={r['max_ratio']:.3g}")
+                err = f" max_err={r['max_err']:.3g}" if "max_err" in r else ""
+                lines.append(f"  {f}: {r['fails']}/{r['n']}{err} max_ratio={r['max_ratio']:.3g}")
         for i in np.argwhere(bad)[:6]:
             t = tuple(int(x) for x in i)
             lines.append(f"  at {t}: got={np.asarray(got)[t]!r}\n           ref={np.asarray(ref)[t]!r}")
