@@ -34,6 +34,15 @@ struct SdfOutT {
 };
 using SdfOut = SdfOutT<double>;
 
+// max(m, x) for the log-sum-exp shifts: one compare + selects for double
+// (fmax's NaN handling costs five instructions; the same value for every
+// non-NaN x); Dual keeps its fmax (the tangent of the larger arm).
+template <class T>
+__device__ __forceinline__ T max_sel(const T& m, const T& x) {
+  if constexpr (std::is_same_v<T, double>) return x > m ? x : m;
+  else return fmax(m, x);
+}
+
 // x^n for a small positive integer n (warp-uniform), FP64 products.
 template <class T>
 __device__ __forceinline__ T ipow_d(const T& x, int n) {
@@ -241,7 +250,7 @@ __device__ __forceinline__ SdfOutT<T> cp_leaf(const DevNode& nd, const double4* 
 #pragma unroll 1
   for (int i = 0; i < nd.count; ++i) {
     const double4 q = pl[i];
-    m = fmax(m, fma(T(q.x), p.x, fma(T(q.y), p.y, fma(T(q.z), p.z, T(-q.w)))));
+    m = max_sel(m, fma(T(q.x), p.x, fma(T(q.y), p.y, fma(T(q.z), p.z, T(-q.w)))));
   }
   T acc = 0.0;
   vec3<T> g = mk3<T>(0.0, 0.0, 0.0);
@@ -270,7 +279,7 @@ __device__ __forceinline__ SdfOutT<T> box_cp_leaf(const DevNode& nd, vec3<T> p) 
                   -p.y - nd.box_w[3], p.z - nd.box_w[4], -p.z - nd.box_w[5]};
   T m = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < 6; ++i) m = fmax(m, d[i]);
+  for (int i = 0; i < 6; ++i) m = max_sel(m, d[i]);
   T e[6], acc = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
