@@ -82,13 +82,16 @@ static __constant__ MathConsts kMC = {
     6.93147180559945309417e-01, 1.4142135623730951, 1e-30, 1e-20};
 
 __device__ __forceinline__ double exp_d(double x) {
-  const double k = rint(x * kMC.log2e);
+  // k = rint(x log2e) by the 1.5 * 2^52 shifter: the sum's low word is k as an
+  // integer (no FRND / F2I round trip), the difference k as a double
+  const double t = fma(x, kMC.log2e, 6755399441055744.0);
+  const double k = t - 6755399441055744.0;
   double r = fma(-k, kMC.ln2_hi, x);
   r = fma(-k, kMC.ln2_lo, r);
   double p = kMC.exp_c[0];
 #pragma unroll
   for (int i = 1; i < 9; ++i) p = fma(p, r, kMC.exp_c[i]);
-  const int ki = (int)k;
+  const int ki = __double2loint(t);
   const double s = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   return x < -708.0 ? 0.0 : s;
 }
