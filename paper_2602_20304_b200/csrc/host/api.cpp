@@ -426,6 +426,14 @@ SideStreams& side_streams() {
 }
 struct ForkEvents {  // per host thread and device: reused, so a call creates no events
   cudaEvent_t start = nullptr, done[SideStreams::kN] = {};
+  ForkEvents() = default;
+  ForkEvents(const ForkEvents&) = delete;
+  ForkEvents& operator=(const ForkEvents&) = delete;
+  ~ForkEvents() {  // at thread exit (harmless error codes if the context is already gone)
+    if (start) cudaEventDestroy(start);
+    for (auto& d : done)
+      if (d) cudaEventDestroy(d);
+  }
 };
 ForkEvents& fork_events() {
   thread_local std::unordered_map<int, ForkEvents> per_dev;
