@@ -658,15 +658,18 @@ def bench_drop(ctx, jvp):
     # every pair's per-env mean distance (+ its 12 pose tangents with the JVP)
     hP = torch.as_tensor(poses).pin_memory()
     Pd = torch.empty_like(P)
-    res_h = [torch.empty((n, 13 if jvp else 1), dtype=torch.float32).pin_memory() for _ in pairs]
+    # contiguous pinned destinations: a strided host destination would make torch
+    # stage each copy through a pageable temporary and synchronise
+    mean_h = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in pairs]
+    grad_h = [torch.empty((n, 12), dtype=torch.float32).pin_memory() for _ in pairs] if jvp else []
 
     def e2e_step():
         Pd.copy_(hP, non_blocking=True)
         r = fn(bodies, Pd, cfg, is_static=sc.is_static(), outs=outs)
         for q, o in enumerate(r):
-            res_h[q][:, 0].copy_(o["mean_dist"], non_blocking=True)
+            mean_h[q].copy_(o["mean_dist"], non_blocking=True)
             if jvp:
-                res_h[q][:, 1:].copy_(o["mean_dist_grad"], non_blocking=True)
+                grad_h[q].copy_(o["mean_dist_grad"], non_blocking=True)
         ctx.stream.synchronize()
 
     te = timed(ctx, e2e_step, a.steps, a.warmup)
@@ -701,7 +704,7 @@ def bench_drop(ctx, jvp):
                 "f64 (FP32 outputs and tangents)",
                 e2e={"value": units_local * ctx.world / (te["ms_per_step"] * 1e-3), "unit": "manifolds/s",
                      "h2d_bytes_per_step": int(hP.numel() * 8) * ctx.world,
-                     "d2h_bytes_per_step": int(sum(r.numel() * 4 for r in res_h)) * ctx.world,
+                     "d2h_bytes_per_step": int(sum(r.numel() * 4 for r in mean_h + grad_h)) * ctx.world,
                      "path": "api.generate_manifold_scene_%sbatch: pinned [n_env, 5, 6] poses H2D, every pair's "
                              "per-env mean distance%s D2H" % ("jvp_" if jvp else "",
                                                              " + its 12 pose tangents" if jvp else "")},
