@@ -730,15 +730,14 @@ def bench_witness(ctx, kind):
         fn(D, cfg)
 
     t = timed(ctx, step, a.steps, a.warmup, clocks=True)
-    hp = torch.as_tensor(pairs).pin_memory()
-    Dd = torch.empty_like(D)
-    oh = torch.empty((n, width), dtype=torch.float32).pin_memory()
+    # e2e through the reference-facing host-buffer call (run_ee_batch /
+    # run_vf_batch: host problem set in, doubles out), pinned buffers
+    hp = torch.as_tensor(pairs).pin_memory().numpy()
+    oh = torch.empty((n, width), dtype=torch.float64).pin_memory().numpy()
+    fn_host = api.run_ee_batch_host if kind == "ee" else api.run_vf_batch_host
 
     def e2e_step():
-        Dd.copy_(hp, non_blocking=True)
-        r = fn(Dd, cfg)
-        oh.copy_(r["out"], non_blocking=True)
-        ctx.stream.synchronize()
+        fn_host(hp, cfg, out=oh, stream=ctx.stream)
 
     te = timed(ctx, e2e_step, max(3, min(a.steps, 20)), 2)
     bytes_pair = 96 + 4 * width  # FP64 pair in (as the reference stores it) + FP32 witness points out
@@ -750,9 +749,12 @@ def bench_witness(ctx, kind):
                  "n_pairs": n * ctx.world, "parallelism": f"pair-shard x{ctx.world}"},
                 "f64 in (FP32 out)",
                 e2e={"value": n * ctx.world / (te["ms_per_step"] * 1e-3), "unit": "pairs/s",
-                     "h2d_bytes_per_step": int(hp.numel() * 8) * ctx.world,
-                     "d2h_bytes_per_step": int(oh.numel() * 4) * ctx.world,
-                     "path": f"api.run_{kind}_batch: pinned FP64 pairs H2D, FP32 witness points D2H (PCIe-bound)"},
+                     "h2d_bytes_per_step": int(hp.nbytes) * ctx.world,
+                     "d2h_bytes_per_step": int(oh.nbytes) * ctx.world,
+                     "path": f"api.run_{kind}_batch_host (cmgb_{kind}_witness_batch_host, the reference's "
+                             f"run_{kind}_batch signature): pinned FP64 pairs in, FP64 witness points out"
+                             f"{' (FP64 solver)' if kind == 'ee' else ' (FP32 solver, widened on the device)'}, "
+                             "pipelined over 8 pair chunks on two streams (PCIe-bound)"},
                 roofline=roof, cpu_baseline=cb)
 
 

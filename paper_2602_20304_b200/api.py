@@ -619,6 +619,39 @@ def run_vf_batch(pairs, cfg=None, *, want_labels: bool = False, stream=None) -> 
     return res
 
 
+def _witness_host(sym: str, width: int, pairs, cfg, out, labels, stream) -> np.ndarray:
+    c = _cfg(cfg)
+    pr = np.ascontiguousarray(pairs, dtype=np.float64).reshape(-1, 12)
+    n = pr.shape[0]
+    if out is None:
+        out = np.empty((n, width), np.float64)
+    if out.dtype != np.float64 or out.size < n * width or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous float64 array of n x {width} elements")
+    if labels is not None and (labels.dtype != np.int32 or labels.size < n or not labels.flags.c_contiguous):
+        raise ValueError("labels must be a contiguous int32 array of n elements")
+    _ok(getattr(abi.load(), sym)(pr.ctypes.data, n, C.byref(c), out.ctypes.data,
+                                 labels.ctypes.data if labels is not None else None, _stream_ptr(stream)))
+    return out
+
+
+def run_ee_batch_host(pairs, cfg=None, *, out: Optional[np.ndarray] = None, labels: Optional[np.ndarray] = None,
+                      stream=None) -> np.ndarray:
+    """run_ee_batch with HOST buffers (batch.cpp:53-76: the reference's problem
+    set in, doubles out): [n, 12] float64 pairs -> [n, 6] float64 witness
+    points of the FP64 solver; copies inside, pipelined over pair chunks on two
+    streams (with pinned buffers, e.g. torch's pin_memory().numpy(), the
+    downloads overlap the uploads). Synchronous."""
+    return _witness_host("cmgb_ee_witness_batch_host", 6, pairs, cfg, out, labels, stream)
+
+
+def run_vf_batch_host(pairs, cfg=None, *, out: Optional[np.ndarray] = None, labels: Optional[np.ndarray] = None,
+                      stream=None) -> np.ndarray:
+    """run_vf_batch with HOST buffers (batch.cpp:78-98): [n, 12] float64 pairs
+    -> [n, 3] witness points (the FP32-output solver, widened to float64 on
+    the device). Synchronous."""
+    return _witness_host("cmgb_vf_witness_batch_host", 3, pairs, cfg, out, labels, stream)
+
+
 def surface_from_spec(body) -> Surface:
     """Build a Surface from a workloads.BodySpec."""
     m = body.mesh

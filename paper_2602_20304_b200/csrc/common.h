@@ -272,5 +272,6 @@ int launch_penalty(const PenaltyArgs& a, void* stream);
 int launch_sdf_query(const SdfQueryParams& q, int mode, void* stream);
 int launch_integrate(const IntegrateArgs& a, void* stream);
 int launch_vf_witness(const WitnessParams& p, void* stream);
+int launch_widen(const float* src, double* dst, int64_t n, void* stream);
 const char* last_cuda_error_string();
 }  // namespace cmgb

@@ -481,6 +481,16 @@ struct ScratchPool {
 };
 ScratchPool g_scratch_pool;
 
+// The two pipeline streams (and their events) of a host scratch, created once.
+void ensure_pipeline(HostScratch& sc) {
+  if (sc.q[0]) return;
+  for (int k = 0; k < 2; ++k) {
+    cuda_check(cudaStreamCreateWithFlags(&sc.q[k], cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&sc.ev[k], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  cuda_check(cudaEventCreateWithFlags(&sc.ev_start, cudaEventDisableTiming), "cudaEventCreate");
+}
+
 struct ScratchLease {
   int dev;
   HostScratch* sc;
@@ -793,13 +803,7 @@ int cmgb_manifold_batch_host_ex(cmgb_surface s1, cmgb_surface s2, const double* 
     // upload overlaps chunk c's kernels, and each chunk's results stream back
     // as soon as it is done. Ordered after the caller's stream and joined back
     // into it (then synchronised: the outputs are host memory).
-    if (!sc.q[0]) {
-      for (int k = 0; k < 2; ++k) {
-        cuda_check(cudaStreamCreateWithFlags(&sc.q[k], cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaEventCreateWithFlags(&sc.ev[k], cudaEventDisableTiming), "cudaEventCreate");
-      }
-      cuda_check(cudaEventCreateWithFlags(&sc.ev_start, cudaEventDisableTiming), "cudaEventCreate");
-    }
+    ensure_pipeline(sc);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // Two chunks: a small lead chunk whose pose upload is the only exposed
     // copy, then the rest, uploaded while the lead chunk computes (equal
@@ -1080,6 +1084,38 @@ void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (dst) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
 }
 
+// Host-buffer witness batches with reference-precision outputs (run_ee_batch /
+// run_vf_batch, src/batch.cpp:53-98, return doubles): E-E through the FP64
+// solver; V-F through the FP32-output solver, widened on the device. Both run
+// as a two-stream pipeline over pair chunks: chunk c+1's upload overlaps chunk
+// c's kernel and download (one copy engine per direction), joined back into the
+// caller's stream. The pairs are PCIe-bound (96 B in per pair): with pinned
+// host buffers the outputs' download hides behind the uploads.
+constexpr int kWitnessChunks = 8;
+constexpr int64_t kWitnessChunkMin = 65536;
+
+extern "C++" {  // a template inside the extern "C" block
+template <class Chunk>
+void witness_pipeline(int64_t n, cudaStream_t s, Chunk&& chunk) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  ScratchLease lease(dev);
+  HostScratch& sc = *lease.sc;
+  ensure_pipeline(sc);
+  const int64_t k = std::max<int64_t>(1, std::min<int64_t>(kWitnessChunks, n / kWitnessChunkMin));
+  cuda_check(cudaEventRecord(sc.ev_start, s), "cudaEventRecord");
+  for (int q = 0; q < 2; ++q) cuda_check(cudaStreamWaitEvent(sc.q[q], sc.ev_start, 0), "cudaStreamWaitEvent");
+  for (int64_t c = 0; c < k; ++c) {
+    const int64_t e0 = n * c / k, ne = n * (c + 1) / k - e0;
+    if (ne > 0) chunk(e0, ne, sc.q[c & 1]);
+  }
+  for (int q = 0; q < 2; ++q) {
+    cuda_check(cudaEventRecord(sc.ev[q], sc.q[q]), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(s, sc.ev[q], 0), "cudaStreamWaitEvent");
+  }
+}
+}  // extern "C++"
+
 }  // namespace
 
 int cmgb_manifold_jvp_batch_host(cmgb_surface s1, cmgb_surface s2, const double* poses1_host, int32_t st1,
@@ -1126,9 +1162,6 @@ int cmgb_manifold_jvp_batch_host(cmgb_surface s1, cmgb_surface s2, const double*
   });
 }
 
-// Host-buffer witness batches with reference-precision outputs (run_ee_batch /
-// run_vf_batch, src/batch.cpp:53-98, return doubles): E-E through the FP64
-// solver; V-F through the FP32-output solver, widened.
 int cmgb_ee_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
                                int32_t* labels_host, void* stream) {
   return guarded([&] {
@@ -1137,16 +1170,19 @@ int cmgb_ee_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_c
     if (n == 0) return;
     if (!pairs_host || !out_host) invalid("ee_witness_batch_host: null buffer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    PoolBuffers pb(s);
+    PoolBuffers pb(s);  // freed after the join, then synchronised
     double* pairs = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 12)));
     double* out = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 6)));
     int32_t* labels = labels_host ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * ((size_t)n))) : nullptr;
-    h2d(pairs, pairs_host, sizeof(double) * 12 * n, s);
-    WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, nullptr};
-    if (launch_ee_witness_f64(p, stream) != 0)
-      throw Error(CMGB_ERR_CUDA, std::string("ee_witness_f64 launch: ") + cudaGetErrorString(cudaGetLastError()));
-    d2h(out_host, out, sizeof(double) * 6 * n, s);
-    if (labels) d2h(labels_host, labels, sizeof(int32_t) * n, s);
+    const DevCfg dc = device_config(cfg);
+    witness_pipeline(n, s, [&](int64_t e0, int64_t ne, cudaStream_t q) {
+      h2d(pairs + 12 * e0, pairs_host + 12 * e0, sizeof(double) * 12 * ne, q);
+      WitnessParams p{pairs + 12 * e0, 1, ne, dc, out + 6 * e0, nullptr, labels ? labels + e0 : nullptr, nullptr};
+      if (launch_ee_witness_f64(p, q) != 0)
+        throw Error(CMGB_ERR_CUDA, std::string("ee_witness_f64 launch: ") + cudaGetErrorString(cudaGetLastError()));
+      d2h(out_host + 6 * e0, out + 6 * e0, sizeof(double) * 6 * ne, q);
+      if (labels) d2h(labels_host + e0, labels + e0, sizeof(int32_t) * ne, q);
+    });
   });
 }
 
@@ -1158,20 +1194,22 @@ int cmgb_vf_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_c
     if (n == 0) return;
     if (!pairs_host || !out_host) invalid("vf_witness_batch_host: null buffer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    std::vector<float> out32((size_t)n * 3);
-    {
-      PoolBuffers pb(s);
-      double* pairs = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 12)));
-      float* out = static_cast<float*>(pb.get(sizeof(float) * ((size_t)n * 3)));
-      int32_t* labels = labels_host ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * ((size_t)n))) : nullptr;
-      h2d(pairs, pairs_host, sizeof(double) * 12 * n, s);
-      WitnessParams p{pairs, 1, n, device_config(cfg), out, nullptr, labels, nullptr};
-      if (launch_vf_witness(p, stream) != 0)
+    PoolBuffers pb(s);
+    double* pairs = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 12)));
+    float* out = static_cast<float*>(pb.get(sizeof(float) * ((size_t)n * 3)));
+    double* wide = static_cast<double*>(pb.get(sizeof(double) * ((size_t)n * 3)));
+    int32_t* labels = labels_host ? static_cast<int32_t*>(pb.get(sizeof(int32_t) * ((size_t)n))) : nullptr;
+    const DevCfg dc = device_config(cfg);
+    witness_pipeline(n, s, [&](int64_t e0, int64_t ne, cudaStream_t q) {
+      h2d(pairs + 12 * e0, pairs_host + 12 * e0, sizeof(double) * 12 * ne, q);
+      WitnessParams p{pairs + 12 * e0, 1, ne, dc, out + 3 * e0, nullptr, labels ? labels + e0 : nullptr, nullptr};
+      if (launch_vf_witness(p, q) != 0)
         throw Error(CMGB_ERR_CUDA, std::string("vf_witness launch: ") + cudaGetErrorString(cudaGetLastError()));
-      d2h(out32.data(), out, sizeof(float) * 3 * n, s);
-      if (labels) d2h(labels_host, labels, sizeof(int32_t) * n, s);
-    }  // synchronised here
-    for (size_t i = 0; i < out32.size(); ++i) out_host[i] = out32[i];
+      if (launch_widen(out + 3 * e0, wide + 3 * e0, 3 * ne, q) != 0)
+        throw Error(CMGB_ERR_CUDA, std::string("widen launch: ") + cudaGetErrorString(cudaGetLastError()));
+      d2h(out_host + 3 * e0, wide + 3 * e0, sizeof(double) * 3 * ne, q);
+      if (labels) d2h(labels_host + e0, labels + e0, sizeof(int32_t) * ne, q);
+    });
   });
 }
 

@@ -159,7 +159,24 @@ int launch_witness(const WitnessParams& p, cudaStream_t s) {
   return p.cfg.hard_ops ? launch_witness_mode<T, Solve, 1>(p, s) : launch_witness_mode<T, Solve, 0>(p, s);
 }
 
+// FP32 -> FP64 widening of the V-F outputs for the host-buffer call (the
+// reference's run_vf_batch writes doubles): on the device, so the D2H of a
+// pipeline chunk lands in the caller's buffer directly.
+__global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i];
+}
+
 }  // namespace
+
+int launch_widen(const float* src, double* dst, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  const int64_t need = (n + 255) / 256;
+  const int grid = (int)(need < 148 * 8 ? need : 148 * 8);
+  note_launch();
+  widen_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
 
 int launch_ee_witness(const WitnessParams& p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
