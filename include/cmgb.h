@@ -401,8 +401,12 @@ int cmgb_vf_witness_batch(const void* pairs, int32_t pairs_fp64, int64_t n,
 /* Host-buffer witness batches with the reference's output precision
  * (run_ee_batch / run_vf_batch write doubles, src/batch.cpp:53-98): pairs_host
  * [n][12] FP64; out_host [n][6] (E-E: the FP64 solver of
- * cmgb_ee_witness_batch_f64) / [n][3] (V-F: FP32 solver, widened); labels
- * optional. Synchronous. */
+ * cmgb_ee_witness_batch_f64) / [n][3] (V-F: FP32 solver, widened on the
+ * device); labels optional. Synchronous. Batches of >= 131,072 pairs run as a
+ * two-stream pipeline over up to 8 pair chunks (a chunk's upload overlaps the
+ * previous chunk's kernel and download); page-locked host buffers let the
+ * copies run asynchronously. Results are bit-identical to the device-buffer
+ * calls. */
 int cmgb_ee_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
                                int32_t* labels_host, void* cuda_stream);
 int cmgb_vf_witness_batch_host(const double* pairs_host, int64_t n, const cmgb_config* cfg, double* out_host,
