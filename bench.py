@@ -663,13 +663,19 @@ def bench_drop(ctx, jvp):
     mean_h = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in pairs]
     grad_h = [torch.empty((n, 12), dtype=torch.float32).pin_memory() for _ in pairs] if jvp else []
 
+    mean_all = torch.empty((len(pairs), n), dtype=torch.float32).pin_memory().numpy()
+    hPn = hP.numpy()
+
     def e2e_step():
+        if not jvp:  # the host-buffer C-ABI scene call (pipelined upload, means back)
+            api.generate_manifold_scene_batch_host(bodies, hPn, cfg, is_static=sc.is_static(), mean_out=mean_all,
+                                                   stream=ctx.stream)
+            return
         Pd.copy_(hP, non_blocking=True)
         r = fn(bodies, Pd, cfg, is_static=sc.is_static(), outs=outs)
         for q, o in enumerate(r):
             mean_h[q].copy_(o["mean_dist"], non_blocking=True)
-            if jvp:
-                grad_h[q].copy_(o["mean_dist_grad"], non_blocking=True)
+            grad_h[q].copy_(o["mean_dist_grad"], non_blocking=True)
         ctx.stream.synchronize()
 
     te = timed(ctx, e2e_step, a.steps, a.warmup)
@@ -705,9 +711,10 @@ def bench_drop(ctx, jvp):
                 e2e={"value": units_local * ctx.world / (te["ms_per_step"] * 1e-3), "unit": "manifolds/s",
                      "h2d_bytes_per_step": int(hP.numel() * 8) * ctx.world,
                      "d2h_bytes_per_step": int(sum(r.numel() * 4 for r in mean_h + grad_h)) * ctx.world,
-                     "path": "api.generate_manifold_scene_%sbatch: pinned [n_env, 5, 6] poses H2D, every pair's "
-                             "per-env mean distance%s D2H" % ("jvp_" if jvp else "",
-                                                             " + its 12 pose tangents" if jvp else "")},
+                     "path": ("api.generate_manifold_scene_jvp_batch: pinned [n_env, 5, 6] poses H2D, every pair's "
+                              "per-env mean distance + its 12 pose tangents D2H") if jvp else
+                             ("api.generate_manifold_scene_batch_host (cmgb_manifold_scene_batch_host): pinned "
+                              "[n_env, 5, 6] host poses in, every pair's per-env mean distance out")},
                 roofline=roof, cpu_baseline=cb)
 
 

@@ -349,6 +349,13 @@ int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, cons
                               int32_t n_pairs, const double* poses, int64_t n_env,
                               const cmgb_config* cfg, const cmgb_manifold_out* outs,
                               void* cuda_stream);
+/* The same with HOST buffers: poses_host [n_env][n_bodies][6] in, each pair's
+ * per-env mean contact distance mean_dist_host [n_pairs][n_env] out (copies
+ * inside; a lead env chunk, then the rest, so the rest's upload overlaps the
+ * lead chunk's kernels). Synchronous. */
+int cmgb_manifold_scene_batch_host(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                                   int32_t n_pairs, const double* poses_host, int64_t n_env,
+                                   const cmgb_config* cfg, float* mean_dist_host, void* cuda_stream);
 /* Config D's "forward + 12-tangent JVP per pair": pair q's primal contacts and
  * pose Jacobians (w.r.t. the poses of bodies[pairs[2q]] and bodies[pairs[2q+1]])
  * into outs[q], as cmgb_manifold_jvp_batch. */

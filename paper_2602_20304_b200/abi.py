@@ -246,6 +246,10 @@ SIGNATURES = {
         [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig),
          C.POINTER(CmgbManifoldOut), _P],
     ),
+    "cmgb_manifold_scene_batch_host": (
+        _I,
+        [C.POINTER(_P), C.c_int32, _P, C.c_int32, _P, C.c_int64, C.POINTER(CmgbConfig), _P, _P],
+    ),
 }
 
 _lib = None

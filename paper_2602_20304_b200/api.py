@@ -466,6 +466,29 @@ def generate_manifold_scene_batch(bodies, poses, cfg=None, *, is_static=None, pa
     return res
 
 
+def generate_manifold_scene_batch_host(bodies, poses, cfg=None, *, is_static=None, pairs=None,
+                                       mean_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+    """End-to-end C-ABI scene path (cmgb_manifold_scene_batch_host): HOST
+    float64 poses [n_env, n_bodies, 6] in, each pair's per-env mean contact
+    distance [n_pairs, n_env] float32 out (copies inside, synchronous). Pairs
+    in scene_pairs order unless given."""
+    c = _cfg(cfg)
+    P = np.ascontiguousarray(poses, dtype=np.float64)
+    if P.ndim != 3 or P.shape[2] != 6:
+        raise ValueError("poses must be [n_env, n_bodies, 6]")
+    n_env, nb = P.shape[0], P.shape[1]
+    if len(bodies) != nb:
+        raise ValueError("one surface per body")
+    pr = scene_pairs(nb, is_static) if pairs is None else np.ascontiguousarray(pairs, dtype=np.int32)
+    mean = mean_out if mean_out is not None else np.empty((len(pr), n_env), np.float32)
+    if mean.dtype != np.float32 or mean.size < len(pr) * n_env or not mean.flags.c_contiguous:
+        raise ValueError("mean_out must be a contiguous float32 array of n_pairs x n_env elements")
+    handles = (C.c_void_p * nb)(*[b._h.value if isinstance(b._h, C.c_void_p) else b._h for b in bodies])
+    _ok(abi.load().cmgb_manifold_scene_batch_host(handles, nb, pr.ctypes.data, len(pr), P.ctypes.data, n_env,
+                                                   C.byref(c), mean.ctypes.data, _stream_ptr(stream)))
+    return mean
+
+
 def generate_manifold_scene_jvp_batch(bodies, poses, cfg=None, *, is_static=None, pairs=None,
                                       want_src: bool = False, outs: Optional[list] = None,
                                       stream=None) -> list:

@@ -1095,24 +1095,32 @@ constexpr int kWitnessChunks = 8;
 constexpr int64_t kWitnessChunkMin = 65536;
 
 extern "C++" {  // a template inside the extern "C" block
+// chunk(e0, ne, stream) for each [bounds[c], bounds[c + 1]) on the two
+// pipeline streams alternately, ordered after s and joined back into it
 template <class Chunk>
-void witness_pipeline(int64_t n, cudaStream_t s, Chunk&& chunk) {
+void host_pipeline(const std::vector<int64_t>& bounds, cudaStream_t s, Chunk&& chunk) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   ScratchLease lease(dev);
   HostScratch& sc = *lease.sc;
   ensure_pipeline(sc);
-  const int64_t k = std::max<int64_t>(1, std::min<int64_t>(kWitnessChunks, n / kWitnessChunkMin));
   cuda_check(cudaEventRecord(sc.ev_start, s), "cudaEventRecord");
   for (int q = 0; q < 2; ++q) cuda_check(cudaStreamWaitEvent(sc.q[q], sc.ev_start, 0), "cudaStreamWaitEvent");
-  for (int64_t c = 0; c < k; ++c) {
-    const int64_t e0 = n * c / k, ne = n * (c + 1) / k - e0;
+  for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+    const int64_t e0 = bounds[c], ne = bounds[c + 1] - e0;
     if (ne > 0) chunk(e0, ne, sc.q[c & 1]);
   }
   for (int q = 0; q < 2; ++q) {
     cuda_check(cudaEventRecord(sc.ev[q], sc.q[q]), "cudaEventRecord");
     cuda_check(cudaStreamWaitEvent(s, sc.ev[q], 0), "cudaStreamWaitEvent");
   }
+}
+template <class Chunk>
+void witness_pipeline(int64_t n, cudaStream_t s, Chunk&& chunk) {
+  const int64_t k = std::max<int64_t>(1, std::min<int64_t>(kWitnessChunks, n / kWitnessChunkMin));
+  std::vector<int64_t> bounds;
+  for (int64_t c = 0; c <= k; ++c) bounds.push_back(n * c / k);
+  host_pipeline(bounds, s, chunk);
 }
 }  // extern "C++"
 
@@ -1397,51 +1405,104 @@ int cmgb_scene_pairs(const int32_t* is_static, int32_t n_bodies, int32_t* pairs,
   });
 }
 
+namespace {
+
+// every (env, body) frame once (the pairs share bodies), then the pairs on the
+// device's side streams, joined back into s (throws)
+void scene_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs, int32_t n_pairs,
+                 const double* poses, int64_t n_env, const cmgb_config* cfg, const cmgb_manifold_out* outs,
+                 cudaStream_t s) {
+  if (!bodies || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0 || (n_pairs > 0 && !pairs) ||
+      (n_env > 0 && !poses))
+    invalid("manifold_scene_batch: bad argument");
+  std::vector<LaunchPlan> plans;
+  std::vector<std::pair<int, int>> ij;
+  for (int q = 0; q < n_pairs; ++q) {
+    const int i = pairs[2 * q], j = pairs[2 * q + 1];
+    if (i < 0 || j < 0 || i >= n_bodies || j >= n_bodies || i == j)
+      invalid("manifold_scene_batch: pair index out of range");
+    LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &outs[q]);
+    if (n_env == 0 || plan.p.n_contacts == 0) continue;
+    plans.push_back(plan);
+    ij.emplace_back(i, j);
+  }
+  if (plans.empty()) return;
+  double* frames = nullptr;
+  cuda_check(scratch_alloc(reinterpret_cast<void**>(&frames), sizeof(double) * 12 * (size_t)n_env * n_bodies, s),
+             "cudaMallocAsync(scene frames)");
+  if (launch_scene_frames(poses, n_env * n_bodies, frames, s) != 0) {
+    cudaFreeAsync(frames, s);
+    throw Error(CMGB_ERR_CUDA, std::string("frames launch: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  try {
+    StreamFork fork(s, (int)plans.size());  // the pairs overlap each other's tails
+    for (size_t k = 0; k < plans.size(); ++k) {
+      LaunchPlan& plan = plans[k];
+      plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)n_bodies;
+      plan.p.frames1 = frames + 12 * ij[k].first;
+      plan.p.frames2 = frames + 12 * ij[k].second;
+      plan.p.stride1 = plan.p.stride2 = n_bodies;
+      plan.p.frames_ready = 1;
+      launch_planned(plan, n_env, fork.stream((int)k));
+    }
+  } catch (...) {
+    cudaFreeAsync(frames, s);
+    throw;
+  }
+  cudaFreeAsync(frames, s);  // after the fork's join
+}
+
+}  // namespace
+
 int cmgb_manifold_scene_batch(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
                               int32_t n_pairs, const double* poses, int64_t n_env,
                               const cmgb_config* cfg, const cmgb_manifold_out* outs, void* stream) {
   return guarded([&] {
-    if (!bodies || !outs || n_bodies < 1 || n_pairs < 0 || n_env < 0 || (n_pairs > 0 && !pairs) ||
-        (n_env > 0 && !poses))
-      invalid("manifold_scene_batch: bad argument");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    std::vector<LaunchPlan> plans;
-    std::vector<std::pair<int, int>> ij;
+    scene_batch(bodies, n_bodies, pairs, n_pairs, poses, n_env, cfg, outs, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Host-buffer scene batch: HOST poses [n_env][n_bodies][6] in, each pair's
+// per-env mean distance [n_pairs][n_env] out. A lead chunk of the envs, then
+// the rest, on the two pipeline streams: the rest's pose upload overlaps the
+// lead chunk's kernels (as cmgb_manifold_batch_host).
+int cmgb_manifold_scene_batch_host(const cmgb_surface* bodies, int32_t n_bodies, const int32_t* pairs,
+                                   int32_t n_pairs, const double* poses_host, int64_t n_env,
+                                   const cmgb_config* cfg, float* mean_dist_host, void* stream) {
+  return guarded([&] {
+    if (!bodies || n_bodies < 1 || n_pairs < 0 || n_env < 0 || (n_pairs > 0 && !pairs) ||
+        (n_env > 0 && n_pairs > 0 && (!poses_host || !mean_dist_host)))
+      invalid("manifold_scene_batch_host: bad argument");
+    if (n_env == 0 || n_pairs == 0) return;
+    validate_config(cfg);
+    std::vector<size_t> C(n_pairs);
     for (int q = 0; q < n_pairs; ++q) {
       const int i = pairs[2 * q], j = pairs[2 * q + 1];
-      if (i < 0 || j < 0 || i >= n_bodies || j >= n_bodies || i == j)
+      if (i < 0 || j < 0 || i >= n_bodies || j >= n_bodies || i == j || !bodies[i] || !bodies[j])
         invalid("manifold_scene_batch: pair index out of range");
-      LaunchPlan plan = plan_manifold(bodies[i], bodies[j], poses + 6 * i, 1, poses + 6 * j, 1, n_env, cfg, &outs[q]);
-      if (n_env == 0 || plan.p.n_contacts == 0) continue;
-      plans.push_back(plan);
-      ij.emplace_back(i, j);
+      C[q] = (size_t)layout_of(bodies[i], bodies[j], cfg).n_contacts;
     }
-    if (plans.empty()) return;
-    // every (env, body) frame once (the pairs share bodies), then the pairs on
-    // the device's side streams
-    double* frames = nullptr;
-    cuda_check(scratch_alloc(reinterpret_cast<void**>(&frames), sizeof(double) * 12 * (size_t)n_env * n_bodies, s),
-               "cudaMallocAsync(scene frames)");
-    if (launch_scene_frames(poses, n_env * n_bodies, frames, s) != 0) {
-      cudaFreeAsync(frames, s);
-      throw Error(CMGB_ERR_CUDA, std::string("frames launch: ") + cudaGetErrorString(cudaGetLastError()));
-    }
-    try {
-      StreamFork fork(s, (int)plans.size());  // the pairs overlap each other's tails
-      for (size_t k = 0; k < plans.size(); ++k) {
-        LaunchPlan& plan = plans[k];
-        plan.p.pose_stride1 = plan.p.pose_stride2 = 6 * (int64_t)n_bodies;
-        plan.p.frames1 = frames + 12 * ij[k].first;
-        plan.p.frames2 = frames + 12 * ij[k].second;
-        plan.p.stride1 = plan.p.stride2 = n_bodies;
-        plan.p.frames_ready = 1;
-        launch_planned(plan, n_env, fork.stream((int)k));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PoolBuffers pb(s);  // freed after the join, then synchronised
+    const size_t row = 6 * (size_t)n_bodies, n = (size_t)n_env;
+    double* P = static_cast<double*>(pb.get(sizeof(double) * row * n));
+    float* mean = static_cast<float*>(pb.get(sizeof(float) * n * n_pairs));
+    std::vector<float*> contacts(n_pairs);
+    for (int q = 0; q < n_pairs; ++q) contacts[q] = static_cast<float*>(pb.get(sizeof(float) * n * C[q] * 8));
+    std::vector<int64_t> bounds = {0, n_env};
+    if (n_env >= 2 * kHostChunkMin) bounds = {0, std::max(kHostChunkMin, n_env / 8), n_env};
+    std::vector<cmgb_manifold_out> outs(n_pairs);
+    host_pipeline(bounds, s, [&](int64_t e0, int64_t ne, cudaStream_t st) {
+      h2d(P + row * e0, poses_host + row * e0, sizeof(double) * row * ne, st);
+      for (int q = 0; q < n_pairs; ++q) {
+        outs[q] = cmgb_manifold_out{};
+        outs[q].contacts = contacts[q] + (size_t)e0 * C[q] * 8;
+        outs[q].mean_dist = mean + (size_t)q * n + e0;
       }
-    } catch (...) {
-      cudaFreeAsync(frames, s);
-      throw;
-    }
-    cudaFreeAsync(frames, s);  // after the fork's join
+      scene_batch(bodies, n_bodies, pairs, n_pairs, P + row * e0, ne, cfg, outs.data(), st);
+      for (int q = 0; q < n_pairs; ++q)
+        d2h(mean_dist_host + (size_t)q * n + e0, mean + (size_t)q * n + e0, sizeof(float) * ne, st);
+    });
   });
 }
 
