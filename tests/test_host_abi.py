@@ -147,3 +147,34 @@ def test_effective_budgets():
     assert s.effective_vertex_topk() == 8 and s.effective_edge_topk() == 1
     s = api.Surface(box, Union([Superquadric(), Superquadric(), box_planes((0.5, 0.5, 0.5))], 0.01))
     assert s.info["leaf_count"] == 3 and s.effective_edge_topk() == 3
+
+
+def test_host_buffer_calls_validate_before_touching_the_device():
+    """The pipelined host-buffer calls (witness batches, scene batch) reject bad
+    arguments with the library's messages before any CUDA work; empty batches
+    are no-ops."""
+    lib = abi.load()
+    good = SmoothingConfig().to_c()
+    pairs = np.zeros((4, 12))
+    out = np.zeros((4, 6))
+    for fn, name in ((lib.cmgb_ee_witness_batch_host, "ee"), (lib.cmgb_vf_witness_batch_host, "vf")):
+        assert fn(pairs.ctypes.data, -1, C.byref(good), out.ctypes.data, None, None) != 0
+        assert lib.cmgb_last_error().decode() == f"{name}_witness_batch_host: n >= 0"
+        assert fn(None, 4, C.byref(good), out.ctypes.data, None, None) != 0
+        assert lib.cmgb_last_error().decode() == f"{name}_witness_batch_host: null buffer"
+        bad = SmoothingConfig(tau_nn=0.0).to_c()
+        assert fn(pairs.ctypes.data, 4, C.byref(bad), out.ctypes.data, None, None) != 0
+        assert lib.cmgb_last_error().decode() == "smoothing: tau_nn must be > 0"
+        assert fn(None, 0, C.byref(good), None, None, None) == 0
+    mean = np.zeros((1, 4), np.float32)
+    pr = np.array([[0, 1]], np.int32)
+    poses = np.zeros((4, 2, 6))
+    assert lib.cmgb_manifold_scene_batch_host(None, 2, pr.ctypes.data, 1, poses.ctypes.data, 4, C.byref(good),
+                                              mean.ctypes.data, None) != 0
+    assert lib.cmgb_last_error().decode() == "manifold_scene_batch_host: bad argument"
+    handles = (C.c_void_p * 2)(None, None)
+    assert lib.cmgb_manifold_scene_batch_host(handles, 2, pr.ctypes.data, 1, poses.ctypes.data, 0, C.byref(good),
+                                              mean.ctypes.data, None) == 0
+    assert lib.cmgb_manifold_scene_batch_host(handles, 2, pr.ctypes.data, 1, poses.ctypes.data, 4, C.byref(good),
+                                              mean.ctypes.data, None) != 0
+    assert lib.cmgb_last_error().decode() == "manifold_scene_batch: pair index out of range"
