@@ -1491,6 +1491,9 @@ int cmgb_manifold_scene_batch_host(const cmgb_surface* bodies, int32_t n_bodies,
     for (int q = 0; q < n_pairs; ++q) contacts[q] = static_cast<float*>(pb.get(sizeof(float) * n * C[q] * 8));
     std::vector<int64_t> bounds = {0, n_env};
     if (n_env >= 2 * kHostChunkMin) bounds = {0, std::max(kHostChunkMin, n_env / 8), n_env};
+    for (int q = 0; q < n_pairs; ++q)  // an empty layout's mean is 0 / 0 in the reference (manifold.hpp:379-384)
+      if (C[q] == 0)
+        cuda_check(cudaMemsetAsync(mean + (size_t)q * n, 0xFF, sizeof(float) * n, s), "cudaMemsetAsync");
     std::vector<cmgb_manifold_out> outs(n_pairs);
     host_pipeline(bounds, s, [&](int64_t e0, int64_t ne, cudaStream_t st) {
       h2d(P + row * e0, poses_host + row * e0, sizeof(double) * row * ne, st);
